@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the collaborative texture filtering hot path on B200.
+
+Workload (BASELINE.json configs[4], "config 5"): a batch of 64 4K (3840x2160)
+frames of the animated camera path over the perspective ground plane
+(synthetic.camera_path_frame: magnification ~0.5-9.4), BC1-style 4096^2
+texture, CTF_MODE_COLLAB with the C+ fallback, per-pixel uv + fp16 Jacobian
+in, RGBA fp32 + per-wave records out.  One step = one ctf_filter_batch call
+(one persistent-kernel launch) over the rank's 64 frames.  Inputs are resident
+in HBM before timing; the batch (17 GB of I/O) is far larger than L2, so no
+L2 flush is needed between steps.  Multi-GPU: weak scaling — every rank
+filters its own 64 frames (distinct RNG frame indices); NCCL is used only to
+gather statistics and the max-over-ranks time.
+
+  python bench.py [--gpus N --steps K --warmup W]          # our CUDA path
+  python bench.py --impl reference ...                      # CPU oracle arm
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+METRIC = "4K filtered Gpix/s per B200 (1/2/4/8 GPUs); texel evals/pixel; error vs bilinear"
+UNIT = "Gpix/s"
+MODES = {"collab": 3, "4tap": 0, "stf": 1, "wc": 2}
+FALLBACKS = {"stf": 0, "wc": 1, "c": 2, "cplus": 3}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--frames", type=int, default=64, help="frames per rank per step")
+    ap.add_argument("--width", type=int, default=3840)
+    ap.add_argument("--height", type=int, default=2160)
+    ap.add_argument("--tex", type=int, default=4096)
+    ap.add_argument("--mode", choices=list(MODES), default="collab")
+    ap.add_argument("--fallback", choices=list(FALLBACKS), default="cplus")
+    ap.add_argument("--no-grad", action="store_true")
+    ap.add_argument("--e2e-frames", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--profile-launches", type=int, default=0,
+                    help="(for ncu) run this many launches after warmup, no timing/json")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.idx)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "samples": len(sm),
+                "power_w_max": max(power) if power else None, "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(frames: int, wf: int, hf: int):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        per_px = d["dram_bytes_per_launch"] / (d["frames"] * d["width"] * d["height"])
+        return per_px * frames * wf * hf
+    except Exception:
+        return None
+
+
+def make_texture(args):
+    import synthetic
+    return synthetic.bc1_texture(args.tex, args.tex, args.seed, "image")
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(blocks, tex_size, frames_np, mode, fb, seed, frame_base, budget_s):
+    """Time the oracle on whole frames until the budget is spent; returns (pixels, seconds, nframes)."""
+    import oracle
+    tex = {"format": 1, "width": tex_size, "height": tex_size, "bc1": blocks}
+    px, t_total, n = 0, 0.0, 0
+    for i, (f, uv, g) in enumerate(frames_np):
+        t0 = time.perf_counter()
+        oracle.filter_frame(tex, uv, g, mode, fb, 0, seed, frame_base + f, debug=False)
+        t_total += time.perf_counter() - t0
+        px += uv.shape[0] * uv.shape[1]
+        n += 1
+        if t_total >= budget_s:
+            break
+    return px, t_total, n
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    import synthetic
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
+    oracle.build_oracle()
+    blocks = make_texture(args)
+    mode, fb = MODES[args.mode], FALLBACKS[args.fallback]
+    tex = {"format": 1, "width": args.tex, "height": args.tex, "bc1": blocks}
+    # each step: one full 4K frame of the camera path (a bounded sample of the 64-frame batch)
+    times = []
+    nsteps = args.warmup + args.steps
+    for s in range(nsteps):
+        f = (s * 7) % 64
+        uv, g = synthetic.camera_path_frame(f, args.width, args.height, args.tex, args.tex)
+        if args.no_grad:
+            g = None
+        t0 = time.perf_counter()
+        oracle.filter_frame(tex, uv, g, mode, fb, 0, args.seed, f, debug=False)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    value = args.width * args.height / (ms / 1000.0) / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", cpu_cores()))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config5: camera-path 4K frames, BC1 4096^2, COLLAB(C+)",
+                       "frames_per_step": 1, "width": args.width, "height": args.height, "tex": args.tex,
+                       "mode": args.mode, "fallback": args.fallback, "grad": not args.no_grad},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": "one full 4K camera-path frame per step (frames 7s mod 64)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import synthetic
+    from paper_2506_17770_b200 import build as pbuild
+    import paper_2506_17770_b200.ctf as ctf
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    pbuild.build()
+    ctf.load_library()
+
+    F, Wf, Hf, T = args.frames, args.width, args.height, args.tex
+    mode, fb = MODES[args.mode], FALLBACKS[args.fallback]
+    blocks = make_texture(args)
+    tex = ctf.Texture.bc1(blocks, T, T, device=dev)
+    frame_base = rank * F
+    uv = torch.empty((F, Hf, Wf, 2), dtype=torch.float32, device=dev)
+    grad = None if args.no_grad else torch.empty((F, Hf, Wf, 4), dtype=torch.float16, device=dev)
+    for f in range(F):
+        u, g = synthetic.camera_path_frame_torch((frame_base + f) % 64, Wf, Hf, T, T, device=dev)
+        uv[f].copy_(u)
+        if grad is not None:
+            grad[f].copy_(g)
+        del u, g
+    out = torch.empty((F, Hf, Wf, 4), dtype=torch.float32, device=dev)
+    nwy, nwx = (Hf + 3) // 4, (Wf + 7) // 8
+    rec = torch.empty((F, nwy, nwx), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ctf.filter_batch(tex, uv, grad, mode, fb, 0, args.seed, frame_base, out=out, rec=rec, stream=stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if args.profile_launches:
+        for _ in range(args.profile_launches):
+            step()
+        torch.cuda.synchronize()
+        return 0
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = t0.elapsed_time(t1)
+    kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    if ws > 1:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    pixels_per_step = ws * F * Wf * Hf
+    value = pixels_per_step / (ms_per_step / 1e3) / 1e9
+
+    # roofline of the dominant (only) kernel: algorithmic bytes per launch / mean launch time
+    nwaves = nwy * nwx
+    bytes_per_launch = F * (Wf * Hf * (8 + (0 if grad is None else 8) + 16) + nwaves * 4)
+    k_ms = statistics.mean(kernel_ms)
+    achieved = bytes_per_launch / (k_ms / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    traffic = ncu_traffic(F, Wf, Hf)
+
+    # quality + statistics (off the timed path): 4-tap reference, ctf_stats, NCCL gather
+    ref = torch.empty_like(out)
+    out2 = torch.empty_like(out)
+    ctf.filter_batch(tex, uv, grad, mode, fb, 0, args.seed, frame_base, out=out2, rec=rec, stream=stream)
+    ctf.filter_batch(tex, uv, grad, 0, 0, 0, args.seed, frame_base, out=ref, rec=torch.empty_like(rec),
+                     stream=stream)
+    st = ctf.stats(rec, Wf, Hf, F, out2, ref, stream=stream)
+    del ref, out2
+    keys = ["waves_live", "waves_exact", "waves_fallback", "waves_magnified", "pixels_active",
+            "pixels_in_magnified_waves", "texel_evals", "texel_evals_in_magnified_waves", "err_pixels"]
+    vec = torch.tensor([st[k] for k in keys], dtype=torch.float64, device=dev)
+    fvec = torch.tensor([st["sum_sq_err"], st["max_abs_err"]], dtype=torch.float64, device=dev)
+    if ws > 1:
+        gv = [torch.zeros_like(vec) for _ in range(ws)]
+        gf = [torch.zeros_like(fvec) for _ in range(ws)]
+        dist.all_gather(gv, vec)
+        dist.all_gather(gf, fvec)
+        vec = torch.stack(gv).sum(0)     # rank order: deterministic
+        ssum = sum(float(x[0]) for x in gf)
+        smax = max(float(x[1]) for x in gf)
+    else:
+        ssum, smax = float(fvec[0]), float(fvec[1])
+    tot = dict(zip(keys, [int(x) for x in vec.tolist()]))
+    mse = ssum / max(1, 4 * tot["pixels_active"])
+    quality = {
+        "texel_evals_per_px": tot["texel_evals"] / max(1, tot["pixels_active"]),
+        "texel_evals_per_px_magnified_waves": tot["texel_evals_in_magnified_waves"] / max(1, tot["pixels_in_magnified_waves"]),
+        "exact_wave_frac": tot["waves_exact"] / max(1, tot["waves_live"]),
+        "magnified_wave_frac": tot["waves_magnified"] / max(1, tot["waves_live"]),
+        "psnr_vs_bilinear_db": (10.0 * np.log10(1.0 / mse)) if mse > 0 else float("inf"),
+        "max_abs_err_vs_bilinear": smax,
+    }
+
+    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        E = min(args.e2e_frames, F)
+        uv_h = uv[:E].cpu().pin_memory()
+        g_h = None if grad is None else grad[:E].cpu().pin_memory()
+        out_h = torch.empty((E, Hf, Wf, 4), dtype=torch.float32).pin_memory()
+        rec_h = torch.empty((E, nwy, nwx), dtype=torch.int32).pin_memory()
+        pipe = ctf.HostPipeline(Wf, Hf, max(1, E // 4), grad is not None, device=dev)
+        pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream)  # warm
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.e2e_steps):
+            pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a0.elapsed_time(a1) / args.e2e_steps
+        if ws > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": ws * E * Wf * Hf / (e_ms / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": E * Wf * Hf * (8 + (0 if grad is None else 8)),
+               "d2h_bytes_per_step": E * (Wf * Hf * 16 + nwaves * 4), "frames_per_step": E,
+               "ms_per_step": e_ms, "api": "ctf_filter_frames_host (pinned host buffers)"}
+        del uv_h, g_h, out_h, rec_h, pipe
+
+    # CPU oracle baseline on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
+        import oracle
+        oracle.build_oracle()
+        sample = []
+        for f in (0, 16, 32, 48, 8, 24, 40, 56):
+            sample.append((f, uv[f].cpu().numpy(), None if grad is None else grad[f].cpu().numpy()))
+        px, secs, nfr = oracle_sample(blocks, T, sample, mode, fb, args.seed, frame_base, args.cpu_seconds)
+        cpu = {"value": px / secs / 1e9, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
+               "sample": f"{nfr} full 4K frames of the batch (frames 0,16,32,...), {secs:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config5: 64-frame 4K camera path over a perspective plane, BC1 4096^2, "
+                                   "COLLAB + C+ fallback, uv f32x2 + grad f16x4 in, RGBA f32 out",
+                       "frames_per_rank_per_step": F, "width": Wf, "height": Hf, "tex": T, "mode": args.mode,
+                       "fallback": args.fallback, "grad": grad is not None,
+                       "l2": "inputs (17 GB/step) >> L2, no flush needed", "parallelism": f"frames x{ws} (weak)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "ctf_filter_kernel<BC1,COLLAB>", "kernel_ms": k_ms,
+                         "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src},
+            "quality": quality,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

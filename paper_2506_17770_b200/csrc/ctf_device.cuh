@@ -1,0 +1,237 @@
+// ctf_device.cuh — device building blocks of the CTF hot path (sm_100a).
+//
+// Independent of the CPU oracle: nothing here is shared with oracle/.
+// P:n = PAPER.md line; R-n = DESIGN.md reading.
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+
+namespace ctf {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t INVALID_ID = 0xffffffffu;
+
+enum { FMT_BC1 = 1, FMT_MLP = 2 };
+enum { MODE_4TAP = 0, MODE_STF = 1, MODE_WC = 2, MODE_COLLAB = 3 };
+enum { FB_STF = 0, FB_WC = 1, FB_C = 2, FB_CPLUS = 3 };
+enum { FLAG_DEBUG = 1u, FLAG_FORCE_FALLBACK = 2u };
+enum { PATH_EXACT = 0, PATH_FB_STF = 1, PATH_FB_WC = 2, PATH_FB_C = 3, PATH_FB_CPLUS = 4,
+       PATH_4TAP = 5, PATH_STF = 6, PATH_WC = 7 };
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---------------------------------------------------------------- streaming I/O
+__device__ __forceinline__ float2 ld_stream_f2(const float2 *p) {
+    float2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];"
+                 : "=f"(r.x), "=f"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2 *p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream_f4(float4 *p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+// ---------------------------------------------------------- Philox4x32-10 (R-11)
+// Salmon et al. SC'11; counter (x, y, frame, 0), key (seed_lo, seed_hi).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+    return c;
+}
+// uniform in [0,1) on the 2^-24 grid: exact in fp32 (R-11)
+__device__ __forceinline__ float unit24(uint32_t r) { return __uint2float_rn(r >> 8) * 5.9604644775390625e-08f; }
+
+// ------------------------------------------------------------------ texels
+// A produced texel and how lanes exchange it (step 3 "gather"; WaveReadLaneAt).
+template <int FMT> struct Texel;
+
+template <> struct Texel<FMT_BC1> {
+    uint32_t v;  // RGBA8 packed: one 32-bit shuffle per texel
+    __device__ __forceinline__ static Texel shfl(Texel t, int src) { return {__shfl_sync(FULL, t.v, src)}; }
+    __device__ __forceinline__ float ch(int c) const { return (float)((v >> (8 * c)) & 255u); }
+    __device__ __forceinline__ static Texel zero() { return {0u}; }
+    static constexpr float kScale = 1.0f / 255.0f;  // bytes -> [0,1] (R-9)
+};
+
+template <> struct Texel<FMT_MLP> {
+    float4 v;
+    __device__ __forceinline__ static Texel shfl(Texel t, int src) {
+        return {make_float4(__shfl_sync(FULL, t.v.x, src), __shfl_sync(FULL, t.v.y, src),
+                            __shfl_sync(FULL, t.v.z, src), __shfl_sync(FULL, t.v.w, src))};
+    }
+    __device__ __forceinline__ float ch(int c) const { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
+    __device__ __forceinline__ static Texel zero() { return {make_float4(0.f, 0.f, 0.f, 0.f)}; }
+    static constexpr float kScale = 1.0f;
+};
+
+struct TexArgs {
+    int W, H;
+    const uint2 *bc1;       // BC1 blocks
+    const uint4 *latent;    // 8 x fp16 per latent texel
+    const float *mlp;       // packed weights (global)
+};
+
+// Synthetic BC1-style decode of texel (x, y) (R-9).  Integer only; /3 as (v*683)>>11,
+// exact for v <= 765 (checked exhaustively in DESIGN.md).
+__device__ __forceinline__ uint32_t bc1_decode(const TexArgs &t, int x, int y) {
+    const uint2 b = __ldg(t.bc1 + (size_t)(y >> 2) * (size_t)(t.W >> 2) + (size_t)(x >> 2));
+    const uint32_t c0 = b.x & 0xffffu, c1 = b.x >> 16;
+    const uint32_t code = (b.y >> (2u * ((((unsigned)y & 3u) << 2) | ((unsigned)x & 3u)))) & 3u;
+    // RGB565 -> 888 by bit replication: (r5*33)>>2, (g6*65)>>4, (b5*33)>>2
+    const uint32_t r0 = ((c0 >> 11) * 33u) >> 2, g0 = (((c0 >> 5) & 63u) * 65u) >> 4, b0 = ((c0 & 31u) * 33u) >> 2;
+    const uint32_t r1 = ((c1 >> 11) * 33u) >> 2, g1 = (((c1 >> 5) & 63u) * 65u) >> 4, b1 = ((c1 & 31u) * 33u) >> 2;
+    const bool four = c0 > c1;
+    // value = ((wa*e0 + wb*e1) * mul) >> 11 with (wa, wb, mul) picked by the code
+    uint32_t wa, wb, mul;
+    if (code == 0) { wa = 1; wb = 0; mul = 2048; }
+    else if (code == 1) { wa = 0; wb = 1; mul = 2048; }
+    else if (code == 2) { wa = four ? 2u : 1u; wb = 1; mul = four ? 683u : 1024u; }
+    else { wa = four ? 1u : 0u; wb = four ? 2u : 0u; mul = 683u; }
+    const uint32_t r = ((wa * r0 + wb * r1) * mul) >> 11;
+    const uint32_t g = ((wa * g0 + wb * g1) * mul) >> 11;
+    const uint32_t bb = ((wa * b0 + wb * b1) * mul) >> 11;
+    const uint32_t a = (four || code != 3u) ? 255u : 0u;
+    return r | (g << 8) | (bb << 16) | (a << 24);
+}
+
+// Latent + MLP decode (R-10; NTC-style inference-on-sample).  fp32 FFMA.
+// `w` points at the packed weights staged in shared memory.
+__device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const float *__restrict__ w, int x, int y) {
+    const int lw = t.W >> 2, lh = t.H >> 2;
+    // sample point ((x-1.5)/4, (y-1.5)/4): integer part and phase in eighths (exact weights)
+    const int gx8 = 2 * x - 3, gy8 = 2 * y - 3;                 // 8 * position
+    const int ix = gx8 >> 3, iy = gy8 >> 3;                      // floor
+    const float fx = (float)(gx8 & 7) * 0.125f, fy = (float)(gy8 & 7) * 0.125f;
+    const int x0 = min(max(ix, 0), lw - 1), x1 = min(max(ix + 1, 0), lw - 1);
+    const int y0 = min(max(iy, 0), lh - 1), y1 = min(max(iy + 1, 0), lh - 1);
+    const uint4 q00 = __ldg(t.latent + (size_t)y0 * lw + x0), q01 = __ldg(t.latent + (size_t)y0 * lw + x1);
+    const uint4 q10 = __ldg(t.latent + (size_t)y1 * lw + x0), q11 = __ldg(t.latent + (size_t)y1 * lw + x1);
+    const float w00 = (1.f - fx) * (1.f - fy), w01 = fx * (1.f - fy), w10 = (1.f - fx) * fy, w11 = fx * fy;
+    float in[12];
+    const uint32_t *a0 = &q00.x, *a1 = &q01.x, *a2 = &q10.x, *a3 = &q11.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 v0 = __half22float2(*reinterpret_cast<const __half2 *>(a0 + k));
+        const float2 v1 = __half22float2(*reinterpret_cast<const __half2 *>(a1 + k));
+        const float2 v2 = __half22float2(*reinterpret_cast<const __half2 *>(a2 + k));
+        const float2 v3 = __half22float2(*reinterpret_cast<const __half2 *>(a3 + k));
+        in[2 * k] = fmaf(w11, v3.x, fmaf(w10, v2.x, fmaf(w01, v1.x, w00 * v0.x)));
+        in[2 * k + 1] = fmaf(w11, v3.y, fmaf(w10, v2.y, fmaf(w01, v1.y, w00 * v0.y)));
+    }
+    in[8] = (float)((x & 3) * 2 - 3) * 0.25f;
+    in[9] = (float)((y & 3) * 2 - 3) * 0.25f;
+    in[10] = ((x >> 2) & 1) ? 0.5f : -0.5f;
+    in[11] = ((y >> 2) & 1) ? 0.5f : -0.5f;
+    const float *W1 = w, *b1 = W1 + 32 * 12, *W2 = b1 + 32, *b2 = W2 + 32 * 32, *W3 = b2 + 32, *b3 = W3 + 4 * 32;
+    float h1[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        float acc = b1[j];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) acc = fmaf(W1[j * 12 + k], in[k], acc);
+        h1[j] = fmaxf(acc, 0.f);
+    }
+    float h2[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        float acc = b2[j];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc = fmaf(W2[j * 32 + k], h1[k], acc);
+        h2[j] = fmaxf(acc, 0.f);
+    }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float acc = b3[j];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc = fmaf(W3[j * 32 + k], h2[k], acc);
+        o[j] = fminf(fmaxf(acc, 0.f), 1.f);
+    }
+    return make_float4(o[0], o[1], o[2], o[3]);
+}
+
+template <int FMT> __device__ __forceinline__ Texel<FMT> produce(const TexArgs &t, const float *w, uint32_t x, uint32_t y);
+template <> __device__ __forceinline__ Texel<FMT_BC1> produce<FMT_BC1>(const TexArgs &t, const float *, uint32_t x, uint32_t y) {
+    return {bc1_decode(t, (int)x, (int)y)};
+}
+template <> __device__ __forceinline__ Texel<FMT_MLP> produce<FMT_MLP>(const TexArgs &t, const float *w, uint32_t x, uint32_t y) {
+    return {mlp_decode(t, w, (int)x, (int)y)};
+}
+
+// ------------------------------------------------------------- warp sorting
+// Bitonic sort of one 32-bit key per lane, ascending by lane (shfl_xor network).
+__device__ __forceinline__ uint32_t warp_sort32(uint32_t key) {
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint32_t other = __shfl_xor_sync(FULL, key, j);
+            const bool asc = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            key = (lower == asc) ? min(key, other) : max(key, other);
+        }
+    }
+    return key;
+}
+
+// Bitonic sort of 128 keys held 4 per lane (element e = 4*lane + r), ascending in e.
+__device__ __forceinline__ void warp_sort128(uint32_t (&k)[4]) {
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 128; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            if (j >= 4) {
+                const int lj = j >> 2;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t other = __shfl_xor_sync(FULL, k[r], lj);
+                    const unsigned e = 4u * lane + r;
+                    const bool asc = (e & size) == 0;
+                    const bool lower = (lane & lj) == 0;
+                    k[r] = (lower == asc) ? min(k[r], other) : max(k[r], other);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    if (r & j) continue;
+                    const unsigned e = 4u * lane + r;
+                    const bool asc = (e & size) == 0;
+                    const uint32_t a = k[r], b = k[r | j];
+                    k[r] = asc ? min(a, b) : max(a, b);
+                    k[r | j] = asc ? max(a, b) : min(a, b);
+                }
+            }
+        }
+    }
+}
+
+// lower_bound of `q` in a sorted shared array of 32 keys; returns index in [0, 32].
+__device__ __forceinline__ int lower_bound32(const uint32_t *s, uint32_t q) {
+    int pos = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+        if (s[pos + step - 1] < q) pos += step;
+    return (pos < 31 || s[31] >= q) ? pos : 32;
+}
+
+}  // namespace ctf

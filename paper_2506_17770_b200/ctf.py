@@ -1,0 +1,231 @@
+"""Thin ctypes binding of libctf.so (include/ctf.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI.  Tensors
+are torch CUDA tensors (PyTorch supplies device memory and streams only); this
+module never computes any part of the method and has no CPU fallback: if the
+shared library is missing or a CUDA device is absent, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import torch
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libctf.so"
+
+CTF_OK, CTF_EINVAL, CTF_EUNSUPPORTED, CTF_EALIGN, CTF_ECUDA = 0, -1, -2, -3, -4
+FMT_BC1, FMT_LATENT_MLP = 1, 2
+MODE_4TAP, MODE_STF, MODE_WAVECOMM, MODE_COLLAB = 0, 1, 2, 3
+FB_STF, FB_WAVECOMM, FB_C, FB_CPLUS = 0, 1, 2, 3
+FLAG_DEBUG, FLAG_FORCE_FALLBACK = 1, 2
+_STATUS = {0: "CTF_OK", -1: "CTF_EINVAL", -2: "CTF_EUNSUPPORTED", -3: "CTF_EALIGN", -4: "CTF_ECUDA"}
+
+
+class CtfError(RuntimeError):
+    def __init__(self, fn: str, code: int):
+        super().__init__(f"{fn} failed: {_STATUS.get(code, code)}")
+        self.code = code
+
+
+class ctf_texture(ctypes.Structure):
+    _fields_ = [("format", ctypes.c_int32), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("addr", ctypes.c_int32), ("data_dev", ctypes.c_void_p), ("mlp_dev", ctypes.c_void_p)]
+
+
+class ctf_params(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("fallback", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("frame_index", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
+
+
+class ctf_debug(ctypes.Structure):
+    _fields_ = [("produced_id_dev", ctypes.c_void_p), ("selection_dev", ctypes.c_void_p),
+                ("unread_dev", ctypes.c_void_p)]
+
+
+class ctf_frame_stats(ctypes.Structure):
+    _fields_ = [("waves_live", ctypes.c_uint64), ("waves_partial", ctypes.c_uint64),
+                ("waves_exact", ctypes.c_uint64), ("waves_fallback", ctypes.c_uint64),
+                ("waves_magnified", ctypes.c_uint64), ("pixels_active", ctypes.c_uint64),
+                ("pixels_in_magnified_waves", ctypes.c_uint64), ("texel_evals", ctypes.c_uint64),
+                ("texel_evals_in_magnified_waves", ctypes.c_uint64), ("max_evals_per_lane", ctypes.c_uint32),
+                ("max_unique_per_wave", ctypes.c_uint32), ("unique_hist", ctypes.c_uint64 * 129),
+                ("sum_sq_err", ctypes.c_double), ("max_abs_err", ctypes.c_float), ("pad_", ctypes.c_uint32),
+                ("err_pixels", ctypes.c_uint64)]
+
+    def to_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("unique_hist", "pad_")}
+        d["unique_hist"] = list(self.unique_hist)
+        return d
+
+
+EXPORTS = ["ctf_filter_frame", "ctf_filter_batch", "ctf_stats", "ctf_host_workspace_bytes",
+           "ctf_filter_frames_host", "ctf_launches_per_call", "ctf_abi_version"]
+
+_lib = None
+
+
+def load_library(path: Path | str | None = None):
+    """Load libctf.so and declare the ABI.  Raises if the library is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(str(p))
+    V, I32, U32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32
+    PT, PP, PD = ctypes.POINTER(ctf_texture), ctypes.POINTER(ctf_params), ctypes.POINTER(ctf_debug)
+    lib.ctf_filter_frame.argtypes = [PT, V, V, I32, I32, PP, V, V, PD, V]
+    lib.ctf_filter_batch.argtypes = [PT, V, V, I32, I32, I32, PP, V, V, PD, V]
+    lib.ctf_stats.argtypes = [V, I32, I32, I32, V, V, ctypes.POINTER(ctf_frame_stats), V]
+    lib.ctf_host_workspace_bytes.argtypes = [I32, I32, I32, ctypes.c_int]
+    lib.ctf_host_workspace_bytes.restype = ctypes.c_size_t
+    lib.ctf_filter_frames_host.argtypes = [PT, V, V, I32, I32, I32, I32, PP, V, V, V, ctypes.c_size_t, V]
+    lib.ctf_launches_per_call.argtypes = [I32, ctypes.c_int]
+    for fn in ("ctf_filter_frame", "ctf_filter_batch", "ctf_stats", "ctf_filter_frames_host",
+               "ctf_launches_per_call", "ctf_abi_version"):
+        getattr(lib, fn).restype = ctypes.c_int
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(fn: str, rc: int):
+    if rc != CTF_OK:
+        raise CtfError(fn, rc)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (the hot path has no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream: torch.cuda.Stream | None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Texture:
+    """Device-resident texture (keeps the tensors alive) + its ctf_texture descriptor."""
+
+    def __init__(self, fmt: int, width: int, height: int, data: torch.Tensor, mlp: torch.Tensor | None = None):
+        self.fmt, self.width, self.height = fmt, width, height
+        self.data, self.mlp = data, mlp
+        self.desc = ctf_texture(fmt, width, height, 0, data.data_ptr(), mlp.data_ptr() if mlp is not None else None)
+
+    @staticmethod
+    def bc1(blocks, width: int, height: int, device="cuda") -> "Texture":
+        t = torch.as_tensor(blocks).to(device=device, dtype=torch.uint8).contiguous()
+        return Texture(FMT_BC1, width, height, t)
+
+    @staticmethod
+    def latent_mlp(latent, mlp, width: int, height: int, device="cuda") -> "Texture":
+        lat = torch.as_tensor(latent).to(device=device).contiguous()
+        if lat.dtype != torch.float16:
+            raise ValueError("latent grid must be float16")
+        w = torch.as_tensor(mlp).to(device=device, dtype=torch.float32).contiguous()
+        return Texture(FMT_LATENT_MLP, width, height, lat, w)
+
+
+def num_waves(wf: int, hf: int) -> int:
+    return ((wf + 7) // 8) * ((hf + 3) // 4)
+
+
+def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS,
+                 flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
+                 rec: torch.Tensor | None = None, debug: dict | None = None,
+                 stream: torch.cuda.Stream | None = None):
+    """uv: float32 [F][Hf][Wf][2] (or [Hf][Wf][2]); grad: float16 [..][4] or None.
+    Returns (out float32 [..][4], rec int32 [F][nwy][nwx]).  `debug` may hold tensors
+    'produced_id', 'selection' (int32, pixel-shaped) and 'unread' (int32 [1])."""
+    lib = load_library()
+    single = uv.dim() == 3
+    uv4 = uv.unsqueeze(0) if single else uv
+    frames, hf, wf = uv4.shape[0], uv4.shape[1], uv4.shape[2]
+    if uv4.dtype != torch.float32 or uv4.shape[3] != 2:
+        raise ValueError("uv must be float32 [..., 2]")
+    if grad is not None and (grad.dtype != torch.float16 or grad.shape[-1] != 4):
+        raise ValueError("grad must be float16 [..., 4]")
+    if out is None:
+        out = torch.empty((frames, hf, wf, 4), device=uv.device, dtype=torch.float32)
+    if rec is None:
+        rec = torch.empty((frames, (hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
+    p = ctf_params(mode, fallback, flags, frame_index, seed)
+    dbg = None
+    if debug is not None:
+        dbg = ctf_debug(_ptr(debug.get("produced_id")), _ptr(debug.get("selection")), _ptr(debug.get("unread")))
+        p.flags |= FLAG_DEBUG
+    rc = lib.ctf_filter_batch(ctypes.byref(tex.desc), _ptr(uv4), _ptr(grad), wf, hf, frames, ctypes.byref(p),
+                              _ptr(out), _ptr(rec), ctypes.byref(dbg) if dbg is not None else None,
+                              _stream(stream))
+    _check("ctf_filter_batch", rc)
+    if single:
+        return out[0], rec[0]
+    return out, rec
+
+
+def filter_frame(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS,
+                 flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
+                 rec: torch.Tensor | None = None, debug: dict | None = None,
+                 stream: torch.cuda.Stream | None = None):
+    """One frame through ctf_filter_frame.  uv float32 [Hf][Wf][2]."""
+    lib = load_library()
+    hf, wf = uv.shape[0], uv.shape[1]
+    if out is None:
+        out = torch.empty((hf, wf, 4), device=uv.device, dtype=torch.float32)
+    if rec is None:
+        rec = torch.empty(((hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
+    p = ctf_params(mode, fallback, flags, frame_index, seed)
+    dbg = None
+    if debug is not None:
+        dbg = ctf_debug(_ptr(debug.get("produced_id")), _ptr(debug.get("selection")), _ptr(debug.get("unread")))
+        p.flags |= FLAG_DEBUG
+    rc = lib.ctf_filter_frame(ctypes.byref(tex.desc), _ptr(uv), _ptr(grad), wf, hf, ctypes.byref(p), _ptr(out),
+                              _ptr(rec), ctypes.byref(dbg) if dbg is not None else None, _stream(stream))
+    _check("ctf_filter_frame", rc)
+    return out, rec
+
+
+def stats(rec: torch.Tensor, wf: int, hf: int, frames: int = 1, out: torch.Tensor | None = None,
+          ref: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> dict:
+    """ctf_stats: totals of `frames` frames of records (+ error of out vs ref).  Synchronises."""
+    lib = load_library()
+    st = ctf_frame_stats()
+    rc = lib.ctf_stats(_ptr(rec), wf, hf, frames, _ptr(out), _ptr(ref), ctypes.byref(st), _stream(stream))
+    _check("ctf_stats", rc)
+    return st.to_dict()
+
+
+class HostPipeline:
+    """ctf_filter_frames_host: host buffers in, host buffers out (copies inside the call)."""
+
+    def __init__(self, wf: int, hf: int, chunk_frames: int, with_grad: bool, device="cuda"):
+        lib = load_library()
+        self.wf, self.hf, self.chunk = wf, hf, chunk_frames
+        nbytes = lib.ctf_host_workspace_bytes(wf, hf, chunk_frames, int(with_grad))
+        if nbytes == 0:
+            raise ValueError("bad pipeline geometry")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+    def run(self, tex: Texture, uv_host: torch.Tensor, grad_host: torch.Tensor | None, out_host: torch.Tensor,
+            rec_host: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS, flags: int = 0, seed: int = 0,
+            frame_index: int = 0, stream: torch.cuda.Stream | None = None):
+        lib = load_library()
+        for t in (uv_host, grad_host, out_host, rec_host):
+            if t is not None and (t.is_cuda or not t.is_contiguous()):
+                raise ValueError("host pipeline expects contiguous CPU (ideally pinned) tensors")
+        frames = uv_host.shape[0]
+        p = ctf_params(mode, fallback, flags, frame_index, seed)
+        hp = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        rc = lib.ctf_filter_frames_host(ctypes.byref(tex.desc), hp(uv_host), hp(grad_host), self.wf, self.hf,
+                                        frames, self.chunk, ctypes.byref(p), hp(out_host), hp(rec_host),
+                                        ctypes.c_void_p(self.workspace.data_ptr()), self.workspace.numel(),
+                                        _stream(stream))
+        _check("ctf_filter_frames_host", rc)

@@ -162,3 +162,62 @@ def scene_magnification(grad: np.ndarray) -> np.ndarray:
     r = np.sqrt(np.maximum(jx, jy))
     with np.errstate(divide="ignore"):
         return 1.0 / r
+
+
+# ----------------------------------------------------------------------------------------------
+# Device-side generation of the same scenes (torch, float64), used by bench.py to build large
+# batches quickly.  Same formulas as the numpy versions above; bytes may differ in the last ulp
+# of the float64 trig, so anything compared against the oracle takes host copies of these
+# tensors (never regenerates them with numpy).
+# ----------------------------------------------------------------------------------------------
+def _plane_uv_torch(torch, px, py, wf, hf, p: PlaneParams, cam_height: float):
+    import math
+    t_half = math.tan(math.radians(p.fov_deg) / 2.0)
+    aspect = wf / hf
+    xc = (2.0 * px / wf - 1.0) * t_half * aspect
+    yc = (1.0 - 2.0 * py / hf) * t_half
+    ph = math.radians(p.pitch_deg)
+    dir_y = math.cos(ph) + yc * math.sin(ph)
+    dir_z = -math.sin(ph) + yc * math.cos(ph)
+    dir_x = xc
+    hit = dir_z < -1e-12
+    tt = torch.where(hit, cam_height / torch.where(hit, -dir_z, torch.ones_like(dir_z)), torch.zeros_like(dir_z))
+    gx = tt * dir_x
+    gy = tt * dir_y
+    gyc = cam_height / math.tan(ph)
+    yaw = math.radians(p.yaw_deg)
+    cy_, sy_ = math.cos(yaw), math.sin(yaw)
+    rx = cy_ * gx - sy_ * (gy - gyc)
+    ry = sy_ * gx + cy_ * (gy - gyc)
+    return 0.5 + rx / p.scale, 0.5 - ry / p.scale, hit
+
+
+def perspective_plane_torch(wf: int, hf: int, tex_w: int, tex_h: int, params: PlaneParams = PLANE_C2,
+                            cam_height: float | None = None, device="cuda"):
+    """Device twin of `perspective_plane`: returns (uv float32 [Hf][Wf][2], grad float16 [Hf][Wf][4])."""
+    import torch
+    h = params.height if cam_height is None else cam_height
+    py, px = torch.meshgrid(torch.arange(hf, dtype=torch.float64, device=device),
+                            torch.arange(wf, dtype=torch.float64, device=device), indexing="ij")
+    cxp, cyp = px + 0.5, py + 0.5
+    u, v, hit = _plane_uv_torch(torch, cxp, cyp, wf, hf, params, h)
+    ux1, vx1, hx1 = _plane_uv_torch(torch, cxp + 0.5, cyp, wf, hf, params, h)
+    ux0, vx0, hx0 = _plane_uv_torch(torch, cxp - 0.5, cyp, wf, hf, params, h)
+    uy1, vy1, hy1 = _plane_uv_torch(torch, cxp, cyp + 0.5, wf, hf, params, h)
+    uy0, vy0, hy0 = _plane_uv_torch(torch, cxp, cyp - 0.5, wf, hf, params, h)
+    cov = hit & hx1 & hx0 & hy1 & hy0 & (u >= 0) & (u <= 1) & (v >= 0) & (v <= 1)
+    nan = torch.full_like(u, float("nan"))
+    uv = torch.stack([torch.where(cov, u, nan), torch.where(cov, v, nan)], -1).to(torch.float32)
+    z = torch.zeros_like(u)
+    grad = torch.stack([torch.where(cov, (ux1 - ux0) * tex_w, z), torch.where(cov, (vx1 - vx0) * tex_h, z),
+                        torch.where(cov, (uy1 - uy0) * tex_w, z), torch.where(cov, (vy1 - vy0) * tex_h, z)],
+                       -1).to(torch.float16)
+    return uv.contiguous(), grad.contiguous()
+
+
+def camera_path_frame_torch(f: int, wf: int, hf: int, tex_w: int, tex_h: int, nframes: int = 64,
+                            base: PlaneParams = PLANE_C2, device="cuda"):
+    """Device twin of `camera_path_frame`."""
+    hcam = 1.0 + 0.5 * (1.0 + np.cos(2.0 * np.pi * f / nframes))
+    p = PlaneParams(base.pitch_deg, hcam, base.scale, 45.0 * f / nframes, base.fov_deg)
+    return perspective_plane_torch(wf, hf, tex_w, tex_h, p, device=device)

@@ -1,0 +1,76 @@
+"""CPU checks of the boundary: libctf.so loads, exports every symbol include/ctf.h
+declares, the product path never touches the oracle, and there is no CPU fallback."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_functions():
+    text = (ROOT / "include" / "ctf.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ctf_[a-z_0-9]+)\s*\(", text)) - {"ctf_status"})
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2506_17770_b200 import build
+    lib_path = build.build()
+    lib = ctypes.CDLL(str(lib_path))
+    names = header_functions()
+    assert {"ctf_filter_frame", "ctf_stats", "ctf_filter_batch"} <= set(names)
+    for n in names:
+        assert hasattr(lib, n), n
+    lib.ctf_abi_version.restype = ctypes.c_int
+    assert lib.ctf_abi_version() == 1
+
+
+def test_binding_declares_all_exports():
+    import paper_2506_17770_b200.ctf as c
+    assert sorted(c.EXPORTS) == header_functions()
+
+
+def test_product_never_imports_oracle():
+    pkg = ROOT / "paper_2506_17770_b200"
+    for p in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + list(pkg.rglob("*.h")):
+        src = p.read_text()
+        assert not re.search(r"^\s*(import|from)\s+oracle", src, re.M), p
+        assert "ctf_oracle" not in src, p
+
+
+def test_oracle_never_includes_product():
+    src = (ROOT / "oracle" / "ctf_oracle.c").read_text()
+    assert "#include \"" not in src and "ctf.h" not in src
+    py = (ROOT / "oracle" / "oracle.py").read_text()
+    assert "paper_2506_17770_b200" not in py
+
+
+def test_no_cpu_fallback():
+    torch = pytest.importorskip("torch")
+    import paper_2506_17770_b200.ctf as c
+    with pytest.raises((ValueError, RuntimeError)):
+        c._ptr(torch.zeros(4))
+
+
+def test_validation_errors_without_gpu():
+    """Host-side validation runs before any CUDA call, so it is testable on CPU."""
+    import paper_2506_17770_b200.ctf as c
+    lib = c.load_library()
+    tex = c.ctf_texture(1, 32, 32, 0, 0x1000, None)
+    p = c.ctf_params(3, 3, 0, 0, 0)
+    V = ctypes.c_void_p
+    # null uv
+    assert lib.ctf_filter_frame(ctypes.byref(tex), None, None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EINVAL
+    # misaligned out
+    assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1008), V(0x1000), None, None) == c.CTF_EALIGN
+    # bad mode / dims / unsupported size
+    p.mode = 9
+    assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EINVAL
+    p.mode = 3
+    tex.width = 30
+    assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EINVAL
+    tex.width, tex.height = 8192, 8192
+    assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EUNSUPPORTED
+    assert lib.ctf_launches_per_call(64, 1) == 1 and lib.ctf_launches_per_call(64, 0) == 64

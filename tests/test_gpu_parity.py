@@ -1,0 +1,246 @@
+"""GPU (CUDA path through the C ABI) vs CPU oracle parity — run with -m gpu on a B200.
+
+Bar (BASELINE.json north_star): bit-exact unique counts, producer lanes/ids,
+evaluation counts, per-wave records and RNG-driven selections; |colour| error
+<= 1e-5 absolute per fp32 channel.
+"""
+import numpy as np
+import pytest
+
+import synthetic
+from tests.helpers import bc1_tex, mlp_tex
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ATOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ctf():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2506_17770_b200.ctf as c
+    c.load_library()
+    return c
+
+
+def to_dev_tex(ctf, t):
+    if t["format"] == 1:
+        return ctf.Texture.bc1(t["bc1"], t["width"], t["height"])
+    return ctf.Texture.latent_mlp(t["latent"], t["mlp"], t["width"], t["height"])
+
+
+def run_gpu(ctf, tex, uv, grad, mode, fb=3, flags=0, seed=0, frame_index=0, batch=False):
+    dt = to_dev_tex(ctf, tex)
+    uvd = torch.from_numpy(np.ascontiguousarray(uv)).cuda()
+    gd = None if grad is None else torch.from_numpy(np.ascontiguousarray(grad)).cuda()
+    hf, wf = uv.shape[-3], uv.shape[-2]
+    shape = uv.shape[:-1]
+    dbg = {"produced_id": torch.zeros(shape, dtype=torch.int32, device="cuda"),
+           "selection": torch.zeros(shape, dtype=torch.int32, device="cuda"),
+           "unread": torch.zeros(1, dtype=torch.int32, device="cuda")}
+    if batch or uv.ndim == 4:
+        out, rec = ctf.filter_batch(dt, uvd, gd, mode, fb, flags, seed, frame_index, debug=dbg)
+    else:
+        out, rec = ctf.filter_frame(dt, uvd, gd, mode, fb, flags, seed, frame_index, debug=dbg)
+    torch.cuda.synchronize()
+    return {"out": out.cpu().numpy(), "rec": rec.cpu().numpy().view(np.uint32),
+            "produced_id": dbg["produced_id"].cpu().numpy().view(np.uint32),
+            "selection": dbg["selection"].cpu().numpy().view(np.uint32),
+            "unread": int(dbg["unread"].item())}
+
+
+def run_oracle(tex, uv, grad, mode, fb=3, flags=0, seed=0, frame_index=0):
+    import oracle
+    return oracle.filter_frame(tex, uv, grad, mode, fb, flags, seed, frame_index)
+
+
+def assert_parity(g, o, what=""):
+    np.testing.assert_array_equal(g["rec"], o["rec"], err_msg=f"records {what}")
+    np.testing.assert_array_equal(g["produced_id"], o["produced_id"], err_msg=f"produced ids {what}")
+    np.testing.assert_array_equal(g["selection"], o["selection"], err_msg=f"selections {what}")
+    err = np.abs(g["out"].astype(np.float64) - o["out"])
+    assert err.max() <= ATOL, f"colour error {err.max()} {what}"
+
+
+MODES = [(0, 0, 0), (1, 0, 0), (2, 0, 0), (3, 0, 0), (3, 1, 0), (3, 2, 0), (3, 3, 0),
+         (3, 0, 2), (3, 1, 2), (3, 2, 2), (3, 3, 2)]
+
+
+@pytest.mark.parametrize("theta", [0.0, 30.0, 45.0])
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config1_uniform_4x(ctf, theta, seed):
+    """Config 1: 64x64 frame of a 32x32 BC1 texture at 4x magnification, every mode."""
+    tex = bc1_tex(32, 32, seed, "image")
+    uv, g = synthetic.rotated_quad(64, 64, 32, 32, 4.0, theta, jitter_seed=seed)
+    for mode, fb, fl in MODES:
+        o = run_oracle(tex, uv, g, mode, fb, fl, seed=seed)
+        gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=seed)
+        assert_parity(gg, o, f"mode={mode} fb={fb} flags={fl}")
+        assert gg["unread"] == 0
+
+
+@pytest.mark.parametrize("mag,theta,cov", [(1.3, 33.0, "circle"), (1.05, 61.0, "halfplane"), (2.2, 45.0, None),
+                                           (0.7, 12.0, "circle"), (0.3, 80.0, None)])
+def test_ragged_mixed_frames(ctf, mag, theta, cov):
+    """Partial waves (61x37 frame, coverage masks), exact + fallback waves, slow-path collect."""
+    tex = bc1_tex(128, 128, 7, "image")
+    uv, g = synthetic.rotated_quad(61, 37, 128, 128, mag, theta, coverage=cov, radius=16.0, jitter_seed=4)
+    for mode, fb, fl in MODES:
+        o = run_oracle(tex, uv, g, mode, fb, fl, seed=77, frame_index=5)
+        gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=77, frame_index=5)
+        assert_parity(gg, o, f"m={mag} mode={mode} fb={fb} flags={fl}")
+        assert gg["unread"] == 0
+
+
+def test_random_uv_stress(ctf):
+    """Uniform random uv: huge AABBs (sort path), random BC1 blocks (both modes)."""
+    rng = np.random.default_rng(3)
+    tex = bc1_tex(256, 128, 5, "random")
+    uv = rng.random((45, 83, 2)).astype(np.float32)
+    uv[rng.random((45, 83)) < 0.1, 0] = np.nan
+    uv[0, :5] = [[-100.0, 3.0], [np.inf, 0.5], [0.5, -np.inf], [1.0, 1.0], [0.0, 0.0]]
+    for mode, fb, fl in MODES:
+        o = run_oracle(tex, uv, None, mode, fb, fl, seed=2**40 + 17)
+        gg = run_gpu(ctf, tex, uv, None, mode, fb, fl, seed=2**40 + 17)
+        assert_parity(gg, o, f"mode={mode} fb={fb}")
+
+
+def test_clustered_uv_edge_cases(ctf):
+    """Waves whose lanes share footprints, single active lanes, clamp duplicates at borders."""
+    W = H = 16
+    tex = bc1_tex(W, H, 2, "image")
+    uv = np.full((8, 24, 2), np.nan, np.float32)
+    uv[0:4, 0:8] = (5.3 / W, 7.6 / H)                   # all lanes share one footprint
+    for l in (1, 3, 5, 6, 7):
+        uv[l // 8, 8 + l % 8] = (0.2, 0.9)               # edge-remap example lanes
+    uv[2, 19] = (1.0, 7.6 / H)                           # single lane, clamped x: n=2 > a=1
+    uv[4:8, 0:8] = (1.0, 1.0)                            # corner clamp: n = 1
+    uv[5, 9] = (0.0, 0.0)
+    uv[6, 17:20] = [(0.999, 0.001), (0.001, 0.999), (0.5, 0.5)]
+    for mode, fb, fl in MODES:
+        o = run_oracle(tex, uv, None, mode, fb, fl, seed=1)
+        gg = run_gpu(ctf, tex, uv, None, mode, fb, fl, seed=1)
+        assert_parity(gg, o, f"mode={mode} fb={fb}")
+
+
+@pytest.mark.parametrize("wf,hf", [(1, 1), (8, 4), (9, 5), (7, 3)])
+def test_tiny_frames(ctf, wf, hf):
+    tex = bc1_tex(32, 32, 1, "image")
+    uv, g = synthetic.rotated_quad(wf, hf, 32, 32, 3.0, 20.0)
+    for mode, fb, fl in MODES:
+        assert_parity(run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=4), run_oracle(tex, uv, g, mode, fb, fl, seed=4))
+
+
+def test_all_uncovered(ctf):
+    tex = bc1_tex(32, 32, 1, "image")
+    uv = np.full((12, 20, 2), np.nan, np.float32)
+    for mode, fb, fl in MODES:
+        assert_parity(run_gpu(ctf, tex, uv, None, mode, fb, fl), run_oracle(tex, uv, None, mode, fb, fl))
+
+
+def test_perspective_mixed_minification(ctf):
+    """Config-4 shape at small size: grazing plane with horizon, minified + magnified waves."""
+    tex = bc1_tex(512, 512, 11, "image")
+    uv, g = synthetic.perspective_plane(256, 144, 512, 512, synthetic.PLANE_C4)
+    for mode, fb, fl in MODES:
+        o = run_oracle(tex, uv, g, mode, fb, fl, seed=3)
+        gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=3)
+        assert_parity(gg, o, f"mode={mode} fb={fb} flags={fl}")
+
+
+@pytest.mark.parametrize("mode,fb,fl", [(0, 0, 0), (3, 3, 0), (3, 2, 2), (3, 3, 2), (1, 0, 0)])
+def test_latent_mlp_texture(ctf, mode, fb, fl):
+    """Config-3 format at small size: latent grid + MLP decode."""
+    tex = mlp_tex(64, 64, 3)
+    uv, g = synthetic.rotated_quad(45, 22, 64, 64, 2.5, 17.0, coverage="circle", radius=14.0)
+    assert_parity(run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=6), run_oracle(tex, uv, g, mode, fb, fl, seed=6))
+
+
+def test_batch_equals_frames(ctf):
+    """ctf_filter_batch over 3 frames == per-frame oracle with frame_index + f."""
+    tex = bc1_tex(128, 128, 3, "image")
+    frames = [synthetic.rotated_quad(40, 20, 128, 128, 1.2 + 0.5 * f, 10.0 * f) for f in range(3)]
+    uv = np.stack([f[0] for f in frames])
+    g = np.stack([f[1] for f in frames])
+    gg = run_gpu(ctf, tex, uv, g, 3, 3, 0, seed=9, frame_index=100, batch=True)
+    for f in range(3):
+        o = run_oracle(tex, uv[f], g[f], 3, 3, 0, seed=9, frame_index=100 + f)
+        assert_parity({k: (v[f] if isinstance(v, np.ndarray) else v) for k, v in gg.items()}, o, f"frame {f}")
+
+
+def test_exact_waves_bitwise_equal_4tap(ctf):
+    """T3: on every exact wave the collaborative result equals 4-tap bilinear bit for bit."""
+    tex = bc1_tex(512, 512, 2, "image")
+    uv, g = synthetic.perspective_plane(320, 180, 512, 512, synthetic.PLANE_C2)
+    c = run_gpu(ctf, tex, uv, g, 3, 3)
+    f = run_gpu(ctf, tex, uv, g, 0, 0)
+    exact = ((c["rec"] >> 22) & 7) == 0
+    px = np.repeat(np.repeat(exact, 4, 0), 8, 1)[:180, :320]
+    assert px.mean() > 0.9
+    assert np.array_equal(c["out"][px].view(np.uint32), f["out"][px].view(np.uint32))
+
+
+def test_determinism(ctf):
+    tex = bc1_tex(256, 256, 2, "image")
+    uv, g = synthetic.perspective_plane(160, 90, 256, 256, synthetic.PLANE_C4)
+    a = run_gpu(ctf, tex, uv, g, 3, 3, 0, seed=5)
+    b = run_gpu(ctf, tex, uv, g, 3, 3, 0, seed=5)
+    for k in ("out", "rec", "produced_id", "selection"):
+        assert np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32))
+
+
+def test_stats_match_oracle(ctf):
+    import oracle
+    tex = bc1_tex(512, 512, 2, "image")
+    uv, g = synthetic.perspective_plane(256, 144, 512, 512, synthetic.PLANE_C4)
+    dt = to_dev_tex(ctf, tex)
+    uvd, gd = torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda()
+    out, rec = ctf.filter_frame(dt, uvd, gd, 3, 3, seed=1)
+    ref, _ = ctf.filter_frame(dt, uvd, gd, 0, 0)
+    st = ctf.stats(rec, 256, 144, 1, out, ref)
+    o = oracle.frame_stats(rec.cpu().numpy().view(np.uint32), out.cpu().numpy(), ref.cpu().numpy())
+    for k in ("waves_live", "waves_partial", "waves_exact", "waves_fallback", "waves_magnified", "pixels_active",
+              "pixels_in_magnified_waves", "texel_evals", "texel_evals_in_magnified_waves", "max_evals_per_lane",
+              "max_unique_per_wave"):
+        assert st[k] == o[k], k
+    assert st["unique_hist"] == o["unique_hist"].tolist()
+    assert st["err_pixels"] == 256 * 144
+    np.testing.assert_allclose(st["sum_sq_err"], o["sum_sq_err"], rtol=1e-9)
+    np.testing.assert_allclose(st["max_abs_err"], o["max_abs_err"], rtol=1e-6)
+    # the records themselves match the oracle's
+    orc = oracle.filter_frame(tex, uv, g, 3, 3, 0, seed=1)
+    np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), orc["rec"])
+
+
+def test_host_pipeline_matches_device(ctf):
+    tex = bc1_tex(256, 256, 4, "image")
+    fr = [synthetic.perspective_plane(96, 52, 256, 256, synthetic.PLANE_C4) for _ in range(5)]
+    uv = torch.from_numpy(np.stack([f[0] for f in fr])).pin_memory()
+    g = torch.from_numpy(np.stack([f[1] for f in fr])).pin_memory()
+    dt = to_dev_tex(ctf, tex)
+    out_h = torch.empty((5, 52, 96, 4), dtype=torch.float32).pin_memory()
+    rec_h = torch.empty((5, 13, 12), dtype=torch.int32).pin_memory()
+    pipe = ctf.HostPipeline(96, 52, 2, True)
+    pipe.run(dt, uv, g, out_h, rec_h, 3, 3, seed=8, frame_index=3)
+    out_d, rec_d = ctf.filter_batch(dt, uv.cuda(), g.cuda(), 3, 3, seed=8, frame_index=3)
+    assert torch.equal(out_h, out_d.cpu()) and torch.equal(rec_h, rec_d.cpu())
+
+
+def test_abi_errors(ctf):
+    tex = bc1_tex(32, 32, 1, "image")
+    dt = to_dev_tex(ctf, tex)
+    uv = torch.zeros((4, 8, 2), device="cuda")
+    with pytest.raises(ctf.CtfError) as e:
+        ctf.filter_frame(dt, uv, None, 7)
+    assert e.value.code == ctf.CTF_EINVAL
+    big = torch.zeros(16, dtype=torch.float32, device="cuda")
+    with pytest.raises(ctf.CtfError) as e:
+        ctf.filter_frame(dt, big[1:].view(-1)[:8].view(4, 1, 2) if False else uv, None, 3,
+                         out=torch.zeros(4 * 8 * 4 + 1, device="cuda")[1:].view(4, 8, 4))
+    assert e.value.code == ctf.CTF_EALIGN
+    bad = ctf.Texture(ctf.FMT_BC1, 30, 32, dt.data)
+    with pytest.raises(ctf.CtfError) as e:
+        ctf.filter_frame(bad, uv, None, 3)
+    assert e.value.code == ctf.CTF_EINVAL
