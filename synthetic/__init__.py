@@ -11,6 +11,8 @@ from .scenes import (  # noqa: F401
     rotated_quad,
     perspective_plane,
     camera_path_frame,
+    camera_path_frame_torch,
+    perspective_plane_torch,
     scene_magnification,
     PLANE_C2,
     PLANE_C4,
