@@ -207,13 +207,12 @@ static int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v
 /* exported for the pins: footprint of one uv -> ids, s, t */
 void oracle_footprint(float u, float v, int W, int H, uint32_t id[4], float st[2])
 {
-    /* R-2: u, v clamped to [-16, 16]; fx = u*W - 0.5 with two fp32 roundings;
-     * x0 = floor(fx); s = fx - x0 (exact in fp32).                            */
-    float uc = fminf(fmaxf(u, -16.0f), 16.0f);
-    float vc = fminf(fmaxf(v, -16.0f), 16.0f);
-    volatile float mx = uc * (float)W;    /* volatile: keep the two roundings separate */
-    volatile float my = vc * (float)H;
-    float fx = mx - 0.5f, fy = my - 0.5f;
+    /* R-2: u, v clamped to [0, 1] (clamp-to-edge addressing; a NaN v maps to 0);
+     * fx = fma(u, W, -0.5) with ONE fp32 rounding (the listing's uv * txDim - 0.5 as a
+     * fused multiply-add); x0 = floor(fx); s = fx - x0 (exact in fp32).              */
+    float uc = fminf(fmaxf(u, 0.0f), 1.0f);
+    float vc = fminf(fmaxf(v, 0.0f), 1.0f);
+    float fx = fmaf(uc, (float)W, -0.5f), fy = fmaf(vc, (float)H, -0.5f);
     float flx = floorf(fx), fly = floorf(fy);
     int x0 = (int)flx, y0 = (int)fly;
     st[0] = fx - flx;
@@ -244,7 +243,8 @@ static void make_lane(lane_t *L, const float *uv, const uint16_t *grad, int W, i
     L->w32[1] = L->s * b;
     L->w32[2] = a * L->t;
     L->w32[3] = L->s * L->t;
-    /* R-20: rho^2 = max(Jxx^2 + Jyx^2, Jxy^2 + Jyy^2) in fp32; magnified <=> rho^2 <= 1 */
+    /* R-20: rho^2 = max(Jxx^2 + Jyx^2, Jxy^2 + Jyy^2) in fp32; magnified <=> rho^2 <= 1.
+     * The squares of fp16 values are exact in fp32, so each sum has one rounding. */
     L->magnified = 0;
     if (grad) {
         float g0 = half_to_float(grad[0]), g1 = half_to_float(grad[1]);

@@ -25,7 +25,10 @@ int validate(const ctf_texture *tex, const float *uv, const uint16_t *grad, int3
     // texel ids y*W+x must fit 24 bits (sort keys) and coordinates 16 bits
     if ((int64_t)tex->width * tex->height > (1LL << 24) || tex->width > 65535 || tex->height > 65535)
         return CTF_EUNSUPPORTED;
-    if ((int64_t)Wf * Hf * frames > (1LL << 40)) return CTF_EUNSUPPORTED;
+    // wave indices are 32-bit in the kernel
+    if ((int64_t)((Wf + 7) / 8) * ((Hf + 3) / 4) * frames >= (1LL << 31)) return CTF_EUNSUPPORTED;
+    // pixel indices are 32-bit in the kernel
+    if ((int64_t)Wf * Hf * frames + 4LL * Wf + 8 >= (1LL << 32)) return CTF_EUNSUPPORTED;
     if (!aligned(uv, 8) || (grad && !aligned(grad, 8)) || !aligned(out, 16) || !aligned(rec, 4)) return CTF_EALIGN;
     if (!aligned(tex->data_dev, tex->format == CTF_FMT_BC1 ? 8 : 16)) return CTF_EALIGN;
     if (tex->mlp_dev && !aligned(tex->mlp_dev, 4)) return CTF_EALIGN;

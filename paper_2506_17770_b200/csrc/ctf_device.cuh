@@ -67,8 +67,11 @@ template <> struct Texel<FMT_BC1> {
     uint32_t v;  // RGBA8 packed: one 32-bit shuffle per texel
     __device__ __forceinline__ static Texel shfl(Texel t, int src) { return {__shfl_sync(FULL, t.v, src)}; }
     __device__ __forceinline__ float ch(int c) const { return (float)((v >> (8 * c)) & 255u); }
+    __device__ __forceinline__ void expand(float (&c)[4]) const;         // exact v in [0, 255]
+    __device__ __forceinline__ void expand_biased(float (&c)[4]) const;  // 1024 + v (no constant operand)
     __device__ __forceinline__ static Texel zero() { return {0u}; }
     static constexpr float kScale = 1.0f / 255.0f;  // bytes -> [0,1] (R-9)
+    static constexpr float kBias = 1024.0f;
 };
 
 template <> struct Texel<FMT_MLP> {
@@ -78,8 +81,11 @@ template <> struct Texel<FMT_MLP> {
                             __shfl_sync(FULL, t.v.z, src), __shfl_sync(FULL, t.v.w, src))};
     }
     __device__ __forceinline__ float ch(int c) const { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
+    __device__ __forceinline__ void expand(float (&c)[4]) const { c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w; }
+    __device__ __forceinline__ void expand_biased(float (&c)[4]) const { expand(c); }
     __device__ __forceinline__ static Texel zero() { return {make_float4(0.f, 0.f, 0.f, 0.f)}; }
     static constexpr float kScale = 1.0f;
+    static constexpr float kBias = 0.0f;
 };
 
 struct TexArgs {
@@ -89,27 +95,56 @@ struct TexArgs {
     const float *mlp;       // packed weights (global)
 };
 
-// Synthetic BC1-style decode of texel (x, y) (R-9).  Integer only; /3 as (v*683)>>11,
-// exact for v <= 765 (checked exhaustively in DESIGN.md).
+// Synthetic BC1-style decode of texel (x, y) (R-9).  Integer only and branch-free.
+// Both endpoints are expanded at once in 16-bit lanes (e0 low, e1 high); the palette
+// entry wa*e0 + wb*e1 is one IMAD against M = (wa << 16) | wb (bits 16-31 of the
+// product), then /1, /2 or /3 as (v * {2048, 1024, 683}) >> 11 — exact for v <= 765
+// (checked exhaustively, R-9).
 __device__ __forceinline__ uint32_t bc1_decode(const TexArgs &t, int x, int y) {
-    const uint2 b = __ldg(t.bc1 + (size_t)(y >> 2) * (size_t)(t.W >> 2) + (size_t)(x >> 2));
-    const uint32_t c0 = b.x & 0xffffu, c1 = b.x >> 16;
-    const uint32_t code = (b.y >> (2u * ((((unsigned)y & 3u) << 2) | ((unsigned)x & 3u)))) & 3u;
-    // RGB565 -> 888 by bit replication: (r5*33)>>2, (g6*65)>>4, (b5*33)>>2
-    const uint32_t r0 = ((c0 >> 11) * 33u) >> 2, g0 = (((c0 >> 5) & 63u) * 65u) >> 4, b0 = ((c0 & 31u) * 33u) >> 2;
-    const uint32_t r1 = ((c1 >> 11) * 33u) >> 2, g1 = (((c1 >> 5) & 63u) * 65u) >> 4, b1 = ((c1 & 31u) * 33u) >> 2;
-    const bool four = c0 > c1;
-    // value = ((wa*e0 + wb*e1) * mul) >> 11 with (wa, wb, mul) picked by the code
-    uint32_t wa, wb, mul;
-    if (code == 0) { wa = 1; wb = 0; mul = 2048; }
-    else if (code == 1) { wa = 0; wb = 1; mul = 2048; }
-    else if (code == 2) { wa = four ? 2u : 1u; wb = 1; mul = four ? 683u : 1024u; }
-    else { wa = four ? 1u : 0u; wb = four ? 2u : 0u; mul = 683u; }
-    const uint32_t r = ((wa * r0 + wb * r1) * mul) >> 11;
-    const uint32_t g = ((wa * g0 + wb * g1) * mul) >> 11;
-    const uint32_t bb = ((wa * b0 + wb * b1) * mul) >> 11;
-    const uint32_t a = (four || code != 3u) ? 255u : 0u;
-    return r | (g << 8) | (bb << 16) | (a << 24);
+    const uint2 b = __ldg(t.bc1 + ((unsigned)(y >> 2) * (unsigned)(t.W >> 2) + (unsigned)(x >> 2)));
+    const uint32_t shift = 2u * ((((unsigned)y & 3u) << 2) | ((unsigned)x & 3u));
+    const uint32_t code = (b.y >> shift) & 3u;
+    const bool four = (b.x & 0xffffu) > (b.x >> 16);
+    uint32_t rp = (b.x >> 11) & 0x001F001Fu;
+    rp = ((rp << 3) | (rp >> 2)) & 0x00FF00FFu;
+    uint32_t gp = (b.x >> 5) & 0x003F003Fu;
+    gp = ((gp << 2) | (gp >> 4)) & 0x00FF00FFu;
+    uint32_t bp = b.x & 0x001F001Fu;
+    bp = ((bp << 3) | (bp >> 2)) & 0x00FF00FFu;
+    // (wa, wb) for index code | four << 2, 4 bits each: wa in bits 0-1, wb in bits 2-3
+    //   4-colour: {c0, c1, (2c0+c1)/3, (c0+2c1)/3}; 3-colour: {c0, c1, (c0+c1)/2, 0}
+    const uint32_t i = code | (four ? 4u : 0u);
+    const uint32_t nib = (0x96410541u >> (4u * i)) & 15u;
+    const uint32_t M = ((nib & 3u) << 16) | (nib >> 2);
+    const uint32_t mul = code < 2u ? 2048u : (four ? 683u : 1024u);
+    const uint32_t r = (((rp * M) >> 16) * mul) >> 11;
+    const uint32_t g = (((gp * M) >> 16) * mul) >> 11;
+    const uint32_t bb = (((bp * M) >> 16) * mul) >> 11;
+    const uint32_t a = (four || code != 3u) ? 0xff000000u : 0u;
+    return r | (g << 8) | (bb << 16) | a;
+}
+
+// fp16 -> fp32 convert-and-add in one instruction (PTX 8.6 mixed precision, sm_100+).
+__device__ __forceinline__ float f16_add_f32(unsigned short h, float c) {
+    float d;
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(d) : "h"(h), "f"(c));
+    return d;
+}
+// fp32 = fp16 * fp16 + fp32 with one rounding (PTX 8.6 mixed precision, sm_100+).
+__device__ __forceinline__ float fma_f32_f16(unsigned short a, unsigned short b, float c) {
+    float d;
+    asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+    return d;
+}
+// RGBA8 -> 4 exact floats in [0,255]: two byte permutes build half2 (1024 + v) pairs
+// (0x64xx), then each half is converted while subtracting 1024 (no slow I2F).
+__device__ __forceinline__ void rgba8_to_float(uint32_t v, float (&c)[4]) {
+    const uint32_t rg = __byte_perm(v, 0x64646464u, 0x4140);
+    const uint32_t ba = __byte_perm(v, 0x64646464u, 0x4342);
+    c[0] = f16_add_f32((unsigned short)(rg & 0xffffu), -1024.0f);
+    c[1] = f16_add_f32((unsigned short)(rg >> 16), -1024.0f);
+    c[2] = f16_add_f32((unsigned short)(ba & 0xffffu), -1024.0f);
+    c[3] = f16_add_f32((unsigned short)(ba >> 16), -1024.0f);
 }
 
 // Latent + MLP decode (R-10; NTC-style inference-on-sample).  fp32 FFMA.
@@ -166,6 +201,16 @@ __device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const float *__re
         o[j] = fminf(fmaxf(acc, 0.f), 1.f);
     }
     return make_float4(o[0], o[1], o[2], o[3]);
+}
+
+__device__ __forceinline__ void Texel<FMT_BC1>::expand(float (&c)[4]) const { rgba8_to_float(v, c); }
+__device__ __forceinline__ void Texel<FMT_BC1>::expand_biased(float (&c)[4]) const {
+    const uint32_t rg = __byte_perm(v, 0x64646464u, 0x4140);
+    const uint32_t ba = __byte_perm(v, 0x64646464u, 0x4342);
+    c[0] = f16_add_f32((unsigned short)(rg & 0xffffu), 0.0f);
+    c[1] = f16_add_f32((unsigned short)(rg >> 16), 0.0f);
+    c[2] = f16_add_f32((unsigned short)(ba & 0xffffu), 0.0f);
+    c[3] = f16_add_f32((unsigned short)(ba >> 16), 0.0f);
 }
 
 template <int FMT> __device__ __forceinline__ Texel<FMT> produce(const TexArgs &t, const float *w, uint32_t x, uint32_t y);

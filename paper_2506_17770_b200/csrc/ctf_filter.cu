@@ -1,19 +1,22 @@
 // ctf_filter.cu — the collaborative texture filtering kernel (sm_100a).
 //
 // One 8x4-pixel wave = one warp.  Persistent grid: each warp walks
-// waves w = gwarp, gwarp + nwarps, ... over all frames of the batch.  Per wave:
+// waves w = gwarp, gwarp + S, ... over all frames of the batch (S = warps in the
+// grid); the wave coordinates are advanced incrementally (no divisions).
+// Per wave:
 //   a1 load uv/grad (coalesced 64-B row segments), active mask A = ballot
-//   a2 footprint: fx = u*W - 0.5, floor, clamp, 4 texel ids
+//   a2 footprint: fx = u*W - 0.5, floor (magic-number, no F2I), clamp, weights
 //   a3 collect: exact unique set U of the wave's footprint texels (List
 //      semantics) in canonical ascending-id order (Mask h-order,
-//      P:389-399).  Fast path: AABB by 4 redux.sync, then a row-major bitmask
-//      of the AABB with power-of-two pitch (<= 128 bits) OR-reduced by
-//      redux.sync (the WaveActiveBitOr of P:377) and popc ranks
-//      (h^-1).  Slow path: bitonic sort of the 128 footprint keys.
+//      P:389-399).  Fast path: AABB by 4 redux.sync, then a row-major bitmask of
+//      the AABB with power-of-two pitch (32/64/128 bits, specialised) OR-reduced
+//      by redux.sync (WaveActiveBitOr) and popc ranks (h^-1).
+//      Slow path: bitonic sort of the 128 footprint keys.
 //   a4 decide: exact iff n <= popc(A)
 //   a5 produce: active rank r < n produces texel U[r] (lane h(r,A))
-//   a6 gather + blend: 4 __shfl_sync (WaveReadLaneAt) + fma chain
-//   a7 fallback (n > a): STF / WC stand-in / C (Eq. 1) / C+ (Eq. 2)
+//   a6 gather + blend: 4 __shfl_sync of packed RGBA8 (WaveReadLaneAt)
+//   a7 fallback (n > a): STF / WC stand-in / C (Eq. 1) / C+ (Eq. 2); membership of
+//      produced texels by AABB bitmask when it fits, else sorted keys
 //   a8 per-wave record
 #include <climits>
 #include <cmath>
@@ -32,26 +35,30 @@ struct KArgs {
     float4 *out;
     uint32_t *rec;
     uint32_t *dbg_pid, *dbg_sel, *dbg_unread;
-    long long total_waves;
-    int Wf, Hf, nwx, wpf;  // waves per frame
+    unsigned fpx;                   // pixels per frame
+    unsigned total_waves;           // < 2^31 (validated on the host; all pixel indices < 2^32)
+    int Wf, Hf, nwx, nwy, wpf;
+    unsigned S;                     // grid stride in waves
+    int S_fr, S_wy, S_wx;           // S = S_fr*wpf + S_wy*nwx + S_wx
+    unsigned S_base;                // pixel-index increment for S (mod 2^32)
     float Wflt, Hflt;
     int fallback;
     uint32_t flags, frame_index, seed_lo, seed_hi;
 };
 
 struct WarpSmem {
-    uint32_t tbl[32];       // rank -> texel (exact path) / sorted planned ids P (C+)
-    uint32_t sorted[32];    // sorted (id << 5 | lane) of produced texels (fallback gather)
+    uint32_t tbl[32];       // rank -> packed (y << 16 | x) of U[rank] (exact) / planned P (C+, sort path)
+    uint32_t sorted[32];    // sorted (id << 5 | lane) of produced texels (fallback, sort path)
     uint8_t lane_of_rank[32];
-    uint8_t rank_of[128];   // slow-path collect: (lane*4 + corner) -> rank
+    uint8_t lane_of_t[128]; // AABB position -> a lane that produced it (fallback, mask path)
+    uint8_t rank_of[128];   // slow collect: (lane*4 + corner) -> rank
 };
 
 // Per-lane footprint of one pixel (a2).
 struct Foot {
     int xa, xb, ya, yb;     // clamped texel columns / rows
-    uint32_t id[4];         // UL, UR, LL, LR
     float s, t;             // fp32 fractional position (decides coordinates)
-    float w[4];             // fp32 weights, each product rounded once (R-3)
+    float w[4];             // fp32 weights UL, UR, LL, LR, each product rounded once (R-3)
 };
 
 __device__ __forceinline__ void make_weights(Foot &f) {
@@ -62,55 +69,74 @@ __device__ __forceinline__ void make_weights(Foot &f) {
     f.w[3] = __fmul_rn(f.s, f.t);
 }
 
-__device__ __forceinline__ void make_ids(Foot &f, int W) {
-    f.id[0] = (uint32_t)(f.ya * W + f.xa);
-    f.id[1] = (uint32_t)(f.ya * W + f.xb);
-    f.id[2] = (uint32_t)(f.yb * W + f.xa);
-    f.id[3] = (uint32_t)(f.yb * W + f.xb);
+// floor(v) for |v| < 2^22 without F2I/FRND: v + 1.5*2^23 rounded toward -inf lands
+// on the integer grid, so its bits hold floor(v) and subtracting the magic is exact.
+__device__ __forceinline__ int floor_split(float v, float &flo) {
+    const float r = __fadd_rd(v, 12582912.0f);
+    flo = __fsub_rn(r, 12582912.0f);
+    return __float_as_int(r) - 0x4B400000;
 }
 
 __device__ __forceinline__ Foot footprint(float2 uv, const KArgs &a) {
     Foot f;
-    // R-2: clamp to [-16, 16] (NaN v -> -16), two fp32 roundings, floor, exact s
-    const float uc = fminf(fmaxf(uv.x, -16.0f), 16.0f), vc = fminf(fmaxf(uv.y, -16.0f), 16.0f);
-    const float fx = __fsub_rn(__fmul_rn(uc, a.Wflt), 0.5f), fy = __fsub_rn(__fmul_rn(vc, a.Hflt), 0.5f);
-    const float flx = floorf(fx), fly = floorf(fy);
-    const int x0 = (int)flx, y0 = (int)fly;
+    // R-2: u, v clamped to [0, 1] (NaN -> 0), fx = fma(u, W, -0.5) (one rounding),
+    // floor, exact s.  fx lies in [-0.5, W - 0.5], so x0 in [-1, W - 1]: only the
+    // lower corner can fall below 0 and only the upper one above W - 1.
+    const float fx = fmaf(__saturatef(uv.x), a.Wflt, -0.5f), fy = fmaf(__saturatef(uv.y), a.Hflt, -0.5f);
+    float flx, fly;
+    const int x0 = floor_split(fx, flx), y0 = floor_split(fy, fly);
     f.s = __fsub_rn(fx, flx);
     f.t = __fsub_rn(fy, fly);
-    const int W = a.tex.W, H = a.tex.H;
-    f.xa = min(max(x0, 0), W - 1);
-    f.xb = min(max(x0 + 1, 0), W - 1);
-    f.ya = min(max(y0, 0), H - 1);
-    f.yb = min(max(y0 + 1, 0), H - 1);
-    make_ids(f, W);
+    f.xa = max(x0, 0);
+    f.xb = min(x0 + 1, a.tex.W - 1);
+    f.ya = max(y0, 0);
+    f.yb = min(y0 + 1, a.tex.H - 1);
     make_weights(f);
     return f;
 }
 
 __device__ __forceinline__ int corner_x(const Foot &f, int k) { return (k & 1) ? f.xb : f.xa; }
-// runtime-indexed corner id without local-memory indexing
-__device__ __forceinline__ uint32_t corner_id(const Foot &f, int k) {
-    return k == 0 ? f.id[0] : k == 1 ? f.id[1] : k == 2 ? f.id[2] : f.id[3];
-}
 __device__ __forceinline__ int corner_y(const Foot &f, int k) { return (k & 2) ? f.yb : f.ya; }
+__device__ __forceinline__ uint32_t corner_id(const Foot &f, int k, int W) {
+    return (uint32_t)(corner_y(f, k) * W + corner_x(f, k));
+}
 
-// Exact bilinear of 4 gathered texels (c8): same code in 4TAP and COLLAB-exact,
-// so the two are bit-identical on exact waves.
+// Exact bilinear of 4 gathered texels (c8).  The same code runs in 4TAP and in
+// COLLAB-exact, so the two are bit-identical on exact waves.
 template <int FMT>
 __device__ __forceinline__ float4 blend4(const Texel<FMT> (&p)[4], const float (&w)[4]) {
-    float c[4];
-#pragma unroll
-    for (int ch = 0; ch < 4; ++ch)
-        c[ch] = fmaf(w[3], p[3].ch(ch), fmaf(w[2], p[2].ch(ch), fmaf(w[1], p[1].ch(ch), w[0] * p[0].ch(ch))));
+    // c = sum_k (w_k * scale) * v_k.  BC1 texels expand to (1024 + v) without a
+    // constant operand (FHADD with RZ); the bias is removed by starting the fma
+    // chain at -1024 * sum_k w_k * scale (|error| <= ~2e-6).
     const float sc = Texel<FMT>::kScale;
-    return make_float4(c[0] * sc, c[1] * sc, c[2] * sc, c[3] * sc);
+    float ws[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ws[k] = w[k] * sc;
+    float c[4], v[4];
+    p[0].expand_biased(v);
+    if constexpr (Texel<FMT>::kBias != 0.0f) {
+        const float nb = -Texel<FMT>::kBias * ((ws[0] + ws[1]) + (ws[2] + ws[3]));
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(ws[0], v[ch], nb);
+    } else {
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) c[ch] = ws[0] * v[ch];
+    }
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+        p[k].expand_biased(v);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(ws[k], v[ch], c[ch]);
+    }
+    return make_float4(c[0], c[1], c[2], c[3]);
 }
 
 template <int FMT>
 __device__ __forceinline__ float4 scaled(const Texel<FMT> &p) {
     const float sc = Texel<FMT>::kScale;
-    return make_float4(p.ch(0) * sc, p.ch(1) * sc, p.ch(2) * sc, p.ch(3) * sc);
+    float v[4];
+    p.expand(v);
+    return make_float4(v[0] * sc, v[1] * sc, v[2] * sc, v[3] * sc);
 }
 
 // Eq. 2 generalised to a active lanes (R-18 iv), round half up.
@@ -126,57 +152,116 @@ __device__ __forceinline__ int stf_corner(const Foot &f, uint4 r) {
     return (unit24(r.x) < f.s ? 1 : 0) + (unit24(r.y) < f.t ? 2 : 0);
 }
 
-// Fallback gather + combine (c14-c16, c19).  Every lane holds its produced texel
-// (`val`, id `prod` or INVALID).  Each lane looks up its distinct nonzero-weight
-// footprint texels among the produced ones (sorted keys + binary search in smem),
-// shuffles the values in and applies Eq. 1 (wc = false) or the WC stand-in.
-template <int FMT>
-__device__ __forceinline__ float4 fallback_gather(const Foot &f, bool active, uint32_t prod, const Texel<FMT> &val,
-                                                  bool wc, WarpSmem &s) {
-    const unsigned lane = lane_id();
-    const uint32_t key = (active && prod != INVALID_ID) ? ((prod << 5) | lane) : INVALID_ID;
-    s.sorted[lane] = warp_sort32(key);
-    __syncwarp();
-    // distinct corners in first-occurrence order with merged fp32 weights
-    bool first[4];
-    float dw[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        first[k] = true;
-        dw[k] = f.w[k];
+// ------------------------------------------------------------------ AABB bitmask
+// Wave AABB and a bit position t = (y - miny) * 2^lgP + (x - minx) per texel.
+struct Box {
+    int minx, miny, lgP, area;
+    bool fits;      // area <= 128 with width <= 32: usable as a register bitmask
+};
+
+__device__ __forceinline__ Box wave_box(const Foot &f, bool active) {
+    Box b;
+    b.minx = __reduce_min_sync(FULL, active ? f.xa : INT_MAX);
+    const int maxx = __reduce_max_sync(FULL, active ? f.xb : INT_MIN);
+    b.miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
+    const int maxy = __reduce_max_sync(FULL, active ? f.yb : INT_MIN);
+    const int bw = maxx - b.minx + 1, bh = maxy - b.miny + 1;
+    b.lgP = bw <= 1 ? 0 : 32 - __clz(bw - 1);
+    const bool small = bw <= 32 && bh <= 128;
+    b.area = small ? (bh << b.lgP) : INT_MAX;
+    b.fits = small && b.area <= 128;
+    return b;
+}
+__device__ __forceinline__ uint32_t box_t(const Box &b, int x, int y) {
+    return ((uint32_t)(y - b.miny) << b.lgP) + (uint32_t)(x - b.minx);
+}
+__device__ __forceinline__ uint32_t box_xy(const Box &b, uint32_t t) {  // t -> packed (y << 16 | x)
+    return ((uint32_t)(b.miny + (int)(t >> b.lgP)) << 16) | (uint32_t)(b.minx + (int)(t & ((1u << b.lgP) - 1u)));
+}
+
+// K-word (K*32-bit) wave mask, OR-reduced across the warp.
+template <int K>
+struct WMask {
+    uint32_t w[K];
+    int pre[K];
+    int n;
+    __device__ __forceinline__ uint32_t word(uint32_t k) const {
+        if constexpr (K == 1) return w[0];
+        else if constexpr (K == 2) return k == 0 ? w[0] : w[1];
+        else return k == 0 ? w[0] : k == 1 ? w[1] : k == 2 ? w[2] : w[3];
     }
+    __device__ __forceinline__ int prefix(uint32_t k) const {
+        if constexpr (K == 1) return 0;
+        else if constexpr (K == 2) return k == 0 ? 0 : pre[1];
+        else return k == 0 ? 0 : k == 1 ? pre[1] : k == 2 ? pre[2] : pre[3];
+    }
+    __device__ __forceinline__ void finish() {
+        n = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) { pre[k] = n; n += __popc(w[k]); }
+    }
+    // OR of a 2-bit pattern at t0 and t2 (a lane's 2x2 footprint; rows never straddle words)
+    __device__ __forceinline__ void reduce_2x2(uint32_t t0, uint32_t t2, uint32_t pat, bool on) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            uint32_t m = 0u;
+            if (on) {
+                if (K == 1 || (t0 >> 5) == (uint32_t)k) m |= pat << (t0 & 31u);
+                if (K == 1 || (t2 >> 5) == (uint32_t)k) m |= pat << (t2 & 31u);
+            }
+            w[k] = __reduce_or_sync(FULL, m);
+        }
+        finish();
+    }
+    __device__ __forceinline__ void reduce_bit(uint32_t t, bool on) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            w[k] = __reduce_or_sync(FULL, (on && (t >> 5) == (uint32_t)k) ? (1u << (t & 31u)) : 0u);
+        finish();
+    }
+    __device__ __forceinline__ int rank(uint32_t t) const {
+        return prefix(t >> 5) + __popc(word(t >> 5) & ((1u << (t & 31u)) - 1u));
+    }
+    __device__ __forceinline__ bool test(uint32_t t) const { return (word(t >> 5) >> (t & 31u)) & 1u; }
+    // lane j owns bit j of every word: write rank -> packed (y,x) for ranks < 32
+    __device__ __forceinline__ void push(uint32_t *tbl, const Box &b, unsigned lane, unsigned lt) const {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if ((w[k] >> lane) & 1u) {
+                const int r = pre[k] + __popc(w[k] & lt);
+                if (r < 32) tbl[r] = box_xy(b, ((uint32_t)k << 5) | lane);
+            }
+        }
+    }
+};
+
+// ------------------------------------------------------------- fallback gather
+// distinct corners in first-occurrence order + merged fp32 weights; dup[k] = first corner
+// holding the same texel (texel identity by packed (y << 16 | x)).
+__device__ __forceinline__ void distinct_corners(const Foot &f, bool (&first)[4], float (&dw)[4], int (&dup)[4]) {
+    const uint32_t key[4] = {((uint32_t)f.ya << 16) | (uint32_t)f.xa, ((uint32_t)f.ya << 16) | (uint32_t)f.xb,
+                             ((uint32_t)f.yb << 16) | (uint32_t)f.xa, ((uint32_t)f.yb << 16) | (uint32_t)f.xb};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { first[k] = true; dw[k] = f.w[k]; dup[k] = k; }
 #pragma unroll
     for (int k = 1; k < 4; ++k)
 #pragma unroll
         for (int j = 0; j < k; ++j)
-            if (first[j] && first[k] && f.id[j] == f.id[k]) {
+            if (first[j] && first[k] && key[j] == key[k]) {
                 first[k] = false;
+                dup[k] = j;
                 dw[j] = __fadd_rn(dw[j], f.w[k]);
             }
-    int src[4];
-    bool known[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        known[k] = false;
-        src[k] = (int)lane;
-        if (active && first[k] && dw[k] != 0.0f) {
-            const uint32_t q = f.id[k] << 5;
-            const int pos = lower_bound32(s.sorted, q);
-            if (pos < 32) {
-                const uint32_t hit = s.sorted[pos];
-                if ((hit >> 5) == f.id[k]) { known[k] = true; src[k] = (int)(hit & 31u); }
-            }
-        }
-    }
-    Texel<FMT> p[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
-    __syncwarp();
-    if (!active) return make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Eq. 1 / WC combine from the gathered values of the lane's distinct corners (c14-c16).
+template <int FMT>
+__device__ __forceinline__ float4 combine_eq1(const Foot &f, const bool (&first)[4], const float (&dw)[4],
+                                              const bool (&known)[4], const int (&dup)[4], const Texel<FMT> (&p)[4],
+                                              bool wc) {
     bool all_known = true;
-    int N = 0;
+    int N = 0, last = 0;
     float Sw = 0.f, Swp[4] = {0.f, 0.f, 0.f, 0.f}, Sp[4] = {0.f, 0.f, 0.f, 0.f};
-    int last = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if (!first[k] || dw[k] == 0.0f) continue;
@@ -184,28 +269,26 @@ __device__ __forceinline__ float4 fallback_gather(const Foot &f, bool active, ui
         ++N;
         last = k;
         Sw += dw[k];
+        float v[4];
+        p[k].expand(v);
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
-            Swp[ch] = fmaf(dw[k], p[k].ch(ch), Swp[ch]);
-            Sp[ch] += p[k].ch(ch);
+            Swp[ch] = fmaf(dw[k], v[ch], Swp[ch]);
+            Sp[ch] += v[ch];
         }
     }
-    if (all_known) {
-        // duplicates take their first occurrence's value; unknown corners have weight 0
+    if (all_known) {  // every nonzero-weight texel known -> exact bilinear
         Texel<FMT> q[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            q[k] = known[k] ? p[k] : Texel<FMT>::zero();
-#pragma unroll
-            for (int j = 0; j < k; ++j)
-                if (f.id[j] == f.id[k] && known[j]) { q[k] = p[j]; break; }
+            const int d = dup[k];
+            const Texel<FMT> src = d == 0 ? p[0] : d == 1 ? p[1] : d == 2 ? p[2] : p[3];
+            const bool kd = d == 0 ? known[0] : d == 1 ? known[1] : d == 2 ? known[2] : known[3];
+            q[k] = kd ? src : Texel<FMT>::zero();
         }
         return blend4<FMT>(q, f.w);
     }
-    Texel<FMT> pl = p[0];
-#pragma unroll
-    for (int k = 1; k < 4; ++k) if (k == last) pl = p[k];
-    if (N == 1) return scaled<FMT>(pl);
+    if (N == 1) return scaled<FMT>(last == 0 ? p[0] : last == 1 ? p[1] : last == 2 ? p[2] : p[3]);
     const float sc = Texel<FMT>::kScale;
     float c[4];
     if (wc) {
@@ -219,8 +302,285 @@ __device__ __forceinline__ float4 fallback_gather(const Foot &f, bool active, ui
     return make_float4(c[0], c[1], c[2], c[3]);
 }
 
+// Gather via sorted (id << 5 | lane) keys + binary search (any AABB size).
+template <int FMT>
+__device__ __forceinline__ float4 gather_sorted(const Foot &f, bool active, uint32_t prod, const Texel<FMT> &val,
+                                                bool wc, WarpSmem &s, int W) {
+    const unsigned lane = lane_id();
+    const uint32_t key = (active && prod != INVALID_ID) ? ((prod << 5) | lane) : INVALID_ID;
+    s.sorted[lane] = warp_sort32(key);
+    __syncwarp();
+    bool first[4], known[4];
+    float dw[4];
+    int dup[4], src[4];
+    distinct_corners(f, first, dw, dup);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        known[k] = false;
+        src[k] = (int)lane;
+        if (active && first[k] && dw[k] != 0.0f) {
+            const uint32_t id = corner_id(f, k, W);
+            const int pos = lower_bound32(s.sorted, id << 5);
+            if (pos < 32) {
+                const uint32_t hit = s.sorted[pos];
+                if ((hit >> 5) == id) { known[k] = true; src[k] = (int)(hit & 31u); }
+            }
+        }
+    }
+    Texel<FMT> p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
+    __syncwarp();
+    if (!active) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return combine_eq1<FMT>(f, first, dw, known, dup, p, wc);
+}
+
+// Gather via the AABB bitmask of produced texels + a position -> lane table.
+template <int FMT>
+__device__ __forceinline__ float4 gather_mask(const Foot &f, const Box &b, bool active, bool produced,
+                                              uint32_t prod_t, const Texel<FMT> &val, bool wc, WarpSmem &s) {
+    const unsigned lane = lane_id();
+    WMask<4> D;
+    D.reduce_bit(prod_t, active && produced);
+    if (active && produced) s.lane_of_t[prod_t] = (uint8_t)lane;  // any producer of t will do
+    __syncwarp();
+    bool first[4], known[4];
+    float dw[4];
+    int dup[4], src[4];
+    distinct_corners(f, first, dw, dup);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        known[k] = false;
+        src[k] = (int)lane;
+        if (active && first[k] && dw[k] != 0.0f) {
+            const uint32_t t = box_t(b, corner_x(f, k), corner_y(f, k));
+            if (D.test(t)) { known[k] = true; src[k] = s.lane_of_t[t]; }
+        }
+    }
+    Texel<FMT> p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
+    __syncwarp();
+    if (!active) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return combine_eq1<FMT>(f, first, dw, known, dup, p, wc);
+}
+
+// ------------------------------------------------------------------ fallbacks
+struct FbOut {
+    float4 color;
+    uint32_t prod;     // texel id produced by this lane (or INVALID)
+    uint32_t selbits;
+    int evals;
+};
+
+// C+ spare lane: candidate pick from served lane l's footprint g (R-18 v): distinct
+// nonzero-weight texels not in the plan, chosen with probability ~ merged weight.
+template <typename Planned>
+__device__ __forceinline__ int cplus_pick(const Foot &g, float u2, Planned planned) {
+    bool first[4];
+    float cw[4];
+    int dup[4];
+    distinct_corners(g, first, cw, dup);
+    bool cand[4];
+    float wsum = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cand[k] = first[k] && cw[k] != 0.0f && !planned(corner_x(g, k), corner_y(g, k));
+        if (cand[k]) wsum = __fadd_rn(wsum, cw[k]);
+    }
+    if (!(cand[0] || cand[1] || cand[2] || cand[3])) return -1;
+    const float target = __fmul_rn(u2, wsum);
+    float cum = 0.0f;
+    int pick = -1, lastc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!cand[k]) continue;
+        lastc = k;
+        cum = __fadd_rn(cum, cw[k]);
+        if (pick < 0 && cum > target) pick = k;
+    }
+    return pick < 0 ? lastc : pick;
+}
+
+template <int FMT>
+__device__ __noinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bool active, unsigned A, int na,
+                                           int px, int py, uint32_t frame, const KArgs &a, const float *mlpw,
+                                           WarpSmem &s) {
+    const unsigned lane = lane_id();
+    const unsigned lt = lanemask_lt();
+    const int W = a.tex.W;
+    FbOut o;
+    o.prod = INVALID_ID;
+    o.color = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint4 rr = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo, a.seed_hi);
+    const int ksel = stf_corner(f, rr);
+    o.selbits = active ? (uint32_t)ksel : 0u;
+    Texel<FMT> val = Texel<FMT>::zero();
+    if (fb == FB_STF) {  // one-tap STF
+        o.evals = na;
+        if (active) {
+            o.prod = corner_id(f, ksel, W);
+            val = produce<FMT>(a.tex, mlpw, corner_x(f, ksel), corner_y(f, ksel));
+            o.color = scaled<FMT>(val);
+        }
+        return o;
+    }
+    if (fb == FB_WC || fb == FB_C) {  // every lane produces its STF texel
+        o.evals = na;
+        if (active) {
+            o.prod = corner_id(f, ksel, W);
+            val = produce<FMT>(a.tex, mlpw, corner_x(f, ksel), corner_y(f, ksel));
+        }
+        if (b.fits)
+            o.color = gather_mask<FMT>(f, b, active, true, box_t(b, corner_x(f, ksel), corner_y(f, ksel)), val,
+                                       fb == FB_WC, s);
+        else
+            o.color = gather_sorted<FMT>(f, active, o.prod, val, fb == FB_WC, s, W);
+        return o;
+    }
+    // ---- C+ 
+    const int ar = __popc(A & lt);
+    if (active) s.lane_of_rank[ar] = (uint8_t)lane;
+    const int sx = corner_x(f, ksel), sy = corner_y(f, ksel);
+    int np;
+    WMask<4> P;
+    if (b.fits) {
+        // (1) planned STF texels as a bitmask (one bit per lane)
+        P.reduce_bit(box_t(b, sx, sy), active);
+        np = P.n;
+        P.push(s.tbl, b, lane, lt);
+    } else {
+        const uint32_t pid = (uint32_t)(sy * W + sx);
+        const uint32_t sk = warp_sort32(active ? ((pid << 5) | lane) : INVALID_ID);
+        const uint32_t skp = __shfl_up_sync(FULL, sk, 1);
+        const bool firstp = sk != INVALID_ID && (lane == 0 || (sk >> 5) != (skp >> 5));
+        const unsigned F = __ballot_sync(FULL, firstp);
+        np = __popc(F);
+        if (firstp) s.tbl[__popc(F & lt)] = sk >> 5;   // sorted planned ids
+        if ((int)lane >= np) s.tbl[lane] = INVALID_ID;
+    }
+    __syncwarp();
+    // (2) active ranks < n_p produce the planned texels; (3) the rest are spare lanes (Eq. 2)
+    bool spare = false, produced = false;
+    int l = (int)lane;
+    int qx = 0, qy = 0;
+    if (active) {
+        if (ar < np) {
+            const uint32_t e = s.tbl[ar];
+            if (b.fits) { qx = (int)(e & 0xffffu); qy = (int)(e >> 16); }
+            else { qy = (int)(e / (uint32_t)W); qx = (int)(e - (uint32_t)qy * (uint32_t)W); }
+            produced = true;
+        } else {
+            spare = true;
+            l = (int)s.lane_of_rank[eq2_lane_rank(ar, np, na)];
+            o.selbits |= (1u << 5) | ((uint32_t)l << 8);
+        }
+    }
+    Foot g;
+    g.xa = __shfl_sync(FULL, f.xa, l);
+    g.xb = __shfl_sync(FULL, f.xb, l);
+    g.ya = __shfl_sync(FULL, f.ya, l);
+    g.yb = __shfl_sync(FULL, f.yb, l);
+    g.s = __shfl_sync(FULL, f.s, l);
+    g.t = __shfl_sync(FULL, f.t, l);
+    if (spare) {
+        make_weights(g);
+        int pick;
+        if (b.fits) {
+            pick = cplus_pick(g, unit24(rr.z), [&](int x, int y) { return P.test(box_t(b, x, y)); });
+        } else {
+            pick = cplus_pick(g, unit24(rr.z), [&](int x, int y) {
+                const uint32_t id = (uint32_t)(y * W + x);
+                const int pos = lower_bound32(s.tbl, id);
+                return pos < 32 && s.tbl[pos] == id;
+            });
+        }
+        if (pick >= 0) {
+            qx = corner_x(g, pick);
+            qy = corner_y(g, pick);
+            produced = true;
+            o.selbits |= ((uint32_t)pick << 2) | (1u << 4);
+        }
+    }
+    if (produced) {
+        val = produce<FMT>(a.tex, mlpw, qx, qy);
+        o.prod = (uint32_t)(qy * W + qx);
+    }
+    __syncwarp();
+    o.evals = __popc(__ballot_sync(FULL, active && produced));
+    // (4) every lane filters with Eq. 1 over the produced set
+    if (b.fits)
+        o.color = gather_mask<FMT>(f, b, active, produced, box_t(b, qx, qy), val, false, s);
+    else
+        o.color = gather_sorted<FMT>(f, active, o.prod, val, false, s, W);
+    return o;
+}
+
+// --------------------------------------------------------------- exact collect
+template <int K>
+__device__ __forceinline__ int collect_mask(const Foot &f, const Box &b, bool active, int (&rho)[4], WarpSmem &s,
+                                            unsigned lane) {
+    const uint32_t t0 = box_t(b, f.xa, f.ya);
+    const uint32_t t2 = t0 + ((uint32_t)(f.yb - f.ya) << b.lgP);
+    const uint32_t dxs = (uint32_t)(f.xb - f.xa);
+    WMask<K> B;
+    B.reduce_2x2(t0, t2, 1u | (dxs << 1), active);
+    rho[0] = B.rank(t0);
+    rho[1] = rho[0] + (int)dxs;
+    rho[2] = B.rank(t2);
+    rho[3] = rho[2] + (int)dxs;
+    if (B.n <= 32) B.push(s.tbl, b, lane, lanemask_lt());
+    return B.n;
+}
+
+struct Collected {
+    int n;
+    int rho[4];
+};
+
+static __device__ __noinline__ Collected collect_sort(const Foot f, bool active, WarpSmem &s, unsigned lane, int W) {
+    Collected c;
+    uint32_t key[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        key[k] = active ? ((corner_id(f, k, W) << 7) | (lane << 2) | (uint32_t)k) : INVALID_ID;
+    warp_sort128(key);
+    const uint32_t prev = __shfl_up_sync(FULL, key[3], 1);
+    int fl[4];
+    fl[0] = key[0] != INVALID_ID && (lane == 0 || (key[0] >> 7) != (prev >> 7));
+#pragma unroll
+    for (int k = 1; k < 4; ++k) fl[k] = key[k] != INVALID_ID && (key[k] >> 7) != (key[k - 1] >> 7);
+    const int cnt = fl[0] + fl[1] + fl[2] + fl[3];
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(FULL, incl, d);
+        if ((int)lane >= d) incl += o;
+    }
+    c.n = __shfl_sync(FULL, incl, 31);
+    int run = incl - cnt;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        run += fl[k];
+        if (key[k] != INVALID_ID) {
+            const int r = run - 1;
+            s.rank_of[key[k] & 127u] = (uint8_t)r;
+            if (fl[k] && r < 32) {
+                const uint32_t id = key[k] >> 7;
+                const uint32_t y = id / (uint32_t)W;
+                s.tbl[r] = (y << 16) | (id - y * (uint32_t)W);
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c.rho[k] = active ? (int)s.rank_of[lane * 4 + k] : 0;
+    return c;
+}
+
+// ----------------------------------------------------------------------- kernel
 template <int FMT, int MODE>
-__global__ void __launch_bounds__(kWarps * 32) ctf_filter_kernel(const KArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_filter_kernel(const KArgs a) {
     __shared__ WarpSmem smem[kWarps];
     __shared__ __align__(16) float mlpw[FMT == FMT_MLP ? kMlpParams : 4];
     if constexpr (FMT == FMT_MLP) {
@@ -230,15 +590,22 @@ __global__ void __launch_bounds__(kWarps * 32) ctf_filter_kernel(const KArgs a) 
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     WarpSmem &s = smem[warp];
     const bool debug = (a.flags & FLAG_DEBUG) != 0;
-    const long long nwarps = (long long)gridDim.x * kWarps;
+    const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
+    const unsigned laneoff = (unsigned)(ly * a.Wf + lx);
+    const unsigned lt = lanemask_lt();
 
-    for (long long w = (long long)blockIdx.x * kWarps + warp; w < a.total_waves; w += nwarps) {
-        const int fr = (int)(w / a.wpf);
-        const int rw = (int)(w - (long long)fr * a.wpf);
-        const int wy = rw / a.nwx, wx = rw - wy * a.nwx;
-        const int px = wx * 8 + (int)(lane & 7), py = wy * 4 + (int)(lane >> 3);
+    unsigned w = blockIdx.x * kWarps + warp;
+    if (w >= a.total_waves) return;
+    int fr = (int)(w / (unsigned)a.wpf);
+    const int rw = (int)(w - (unsigned)fr * (unsigned)a.wpf);
+    int wy = rw / a.nwx, wx = rw - wy * a.nwx;
+    unsigned base = (unsigned)fr * a.fpx + (unsigned)(wy * 4) * (unsigned)a.Wf + (unsigned)(wx * 8);
+
+    for (; w < a.total_waves; w += a.S) {
+        const int px = wx * 8 + lx, py = wy * 4 + ly;
         const bool inframe = px < a.Wf && py < a.Hf;
-        const size_t pix = (size_t)fr * (size_t)a.Wf * (size_t)a.Hf + (size_t)py * (size_t)a.Wf + (size_t)px;
+        const unsigned pix = base + laneoff;
+        const uint32_t frame = a.frame_index + (uint32_t)fr;
 
         // ---- a1: load + classify
         float2 uv = make_float2(__int_as_float(0x7fc00000), 0.f);
@@ -250,6 +617,7 @@ __global__ void __launch_bounds__(kWarps * 32) ctf_filter_kernel(const KArgs a) 
         const bool active = inframe && !isnan(uv.x);
         const unsigned A = __ballot_sync(FULL, active);
         const int na = __popc(A);
+
         if (na == 0) {
             if (inframe) st_stream_f4(a.out + pix, make_float4(0.f, 0.f, 0.f, 0.f));
             if (debug && inframe) {
@@ -257,299 +625,134 @@ __global__ void __launch_bounds__(kWarps * 32) ctf_filter_kernel(const KArgs a) 
                 if (a.dbg_sel) a.dbg_sel[pix] = 0u;
             }
             if (lane == 0) a.rec[w] = ((MODE == MODE_COLLAB ? 0u : 0xFFu) << 8) | (1u << 26);
-            continue;
-        }
-        bool mag_lane = true;
-        if (a.grad) {
-            const float2 g01 = __half22float2(*reinterpret_cast<const __half2 *>(&gr.x));
-            const float2 g23 = __half22float2(*reinterpret_cast<const __half2 *>(&gr.y));
-            const float rx = __fadd_rn(__fmul_rn(g01.x, g01.x), __fmul_rn(g01.y, g01.y));
-            const float ry = __fadd_rn(__fmul_rn(g23.x, g23.x), __fmul_rn(g23.y, g23.y));
-            mag_lane = (rx > ry ? rx : ry) <= 1.0f;  // R-20
-        }
-        const bool wave_mag = a.grad != nullptr && __all_sync(FULL, !active || mag_lane);
-
-        // ---- a2: footprint
-        const Foot f = footprint(uv, a);
-
-        Texel<FMT> val = Texel<FMT>::zero();
-        uint32_t prod = INVALID_ID;   // texel id this lane produced
-        uint32_t selbits = 0u;
-        float4 color = make_float4(0.f, 0.f, 0.f, 0.f);
-        int n = 0xFF, evals = 0, path = 0;
-        int run_fb = -1;
-
-        if constexpr (MODE == MODE_4TAP) {
-            path = PATH_4TAP;
-            evals = 4 * na;
-            if (active) {
-                Texel<FMT> p[4];
-                p[0] = produce<FMT>(a.tex, mlpw, f.xa, f.ya);
-                p[1] = produce<FMT>(a.tex, mlpw, f.xb, f.ya);
-                p[2] = produce<FMT>(a.tex, mlpw, f.xa, f.yb);
-                p[3] = produce<FMT>(a.tex, mlpw, f.xb, f.yb);
-                color = blend4<FMT>(p, f.w);
-            }
-        } else if constexpr (MODE == MODE_STF) {
-            path = PATH_STF;
-            run_fb = FB_STF;
-        } else if constexpr (MODE == MODE_WC) {
-            path = PATH_WC;
-            run_fb = FB_WC;
         } else {
-            // ---- a3: collect the exact unique set U and the canonical ranks
-            const int minx = __reduce_min_sync(FULL, active ? f.xa : INT_MAX);
-            const int maxx = __reduce_max_sync(FULL, active ? f.xb : INT_MIN);
-            const int miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
-            const int maxy = __reduce_max_sync(FULL, active ? f.yb : INT_MIN);
-            const int bw = maxx - minx + 1, bh = maxy - miny + 1;
-            const int lgP = bw <= 1 ? 0 : 32 - __clz(bw - 1);
-            const bool fast = bw <= 32 && bh <= 128 && (bh << lgP) <= 128;
-            int rho[4];
-            if (fast) {
-                // bit t = (y - miny) * P + (x - minx) of a <=128-bit AABB mask (rows never straddle words)
-                const int t0 = ((f.ya - miny) << lgP) + (f.xa - minx);
-                const int t2 = t0 + ((f.yb - f.ya) << lgP);
-                const uint32_t dxs = (uint32_t)(f.xb - f.xa);
-                const uint32_t pat = 1u | (dxs << 1);
-                const int nwords = ((bh << lgP) + 31) >> 5;
-                uint32_t B[4] = {0u, 0u, 0u, 0u};
-                int pre[4] = {0, 0, 0, 0};
-                n = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (k < nwords) {
-                        uint32_t m = 0u;
-                        if (active) {
-                            if ((t0 >> 5) == k) m |= pat << (t0 & 31);
-                            if ((t2 >> 5) == k) m |= pat << (t2 & 31);
-                        }
-                        B[k] = __reduce_or_sync(FULL, m);
-                        pre[k] = n;
-                        n += __popc(B[k]);
-                    }
-                }
-                auto rank = [&](int t) {
-                    const int k = t >> 5;
-                    const uint32_t bk = k == 0 ? B[0] : k == 1 ? B[1] : k == 2 ? B[2] : B[3];
-                    const int pk = k == 0 ? pre[0] : k == 1 ? pre[1] : k == 2 ? pre[2] : pre[3];
-                    return pk + __popc(bk & ((1u << (t & 31)) - 1u));
-                };
-                rho[0] = rank(t0);
-                rho[1] = rho[0] + (int)dxs;
-                rho[2] = rank(t2);
-                rho[3] = rho[2] + (int)dxs;
-                // producer table: rank -> (x, y) packed; lane j owns bit j of every word
-                const unsigned lt = lanemask_lt();
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (k < nwords && ((B[k] >> lane) & 1u)) {
-                        const int r = pre[k] + __popc(B[k] & lt);
-                        const uint32_t t = ((uint32_t)k << 5) | lane;
-                        if (r < 32)
-                            s.tbl[r] = ((uint32_t)(miny + (int)(t >> lgP)) << 16) |
-                                       (uint32_t)(minx + (int)(t & ((1u << lgP) - 1u)));
-                    }
-                }
-            } else {
-                // slow path: sort the 128 (id << 7 | lane << 2 | corner) keys
-                uint32_t key[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) key[k] = active ? ((f.id[k] << 7) | (lane << 2) | (uint32_t)k) : INVALID_ID;
-                warp_sort128(key);
-                const uint32_t prev = __shfl_up_sync(FULL, key[3], 1);
-                int fl[4];
-                fl[0] = key[0] != INVALID_ID && (lane == 0 || (key[0] >> 7) != (prev >> 7));
-#pragma unroll
-                for (int k = 1; k < 4; ++k) fl[k] = key[k] != INVALID_ID && (key[k] >> 7) != (key[k - 1] >> 7);
-                const int cnt = fl[0] + fl[1] + fl[2] + fl[3];
-                int incl = cnt;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int o = __shfl_up_sync(FULL, incl, d);
-                    if ((int)lane >= d) incl += o;
-                }
-                n = __shfl_sync(FULL, incl, 31);
-                int run = incl - cnt;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    run += fl[k];
-                    if (key[k] != INVALID_ID) {
-                        const int r = run - 1;
-                        s.rank_of[key[k] & 127u] = (uint8_t)r;
-                        if (fl[k] && r < 32) {
-                            const uint32_t id = key[k] >> 7;
-                            const uint32_t y = id / (uint32_t)a.tex.W;
-                            s.tbl[r] = (y << 16) | (id - y * (uint32_t)a.tex.W);
-                        }
-                    }
-                }
-                __syncwarp();
-#pragma unroll
-                for (int k = 0; k < 4; ++k) rho[k] = active ? (int)s.rank_of[lane * 4 + k] : 0;
+            bool mag_lane = true;
+            if (a.grad) {
+                // R-20: squares of fp16 values are exact in fp32, so fma(g0, g0, g1*g1)
+                // rounds once exactly like the fp32 sum of the two products
+                const float rx = fma_f32_f16((unsigned short)(gr.x & 0xffffu), (unsigned short)(gr.x & 0xffffu),
+                                             fma_f32_f16((unsigned short)(gr.x >> 16), (unsigned short)(gr.x >> 16), 0.0f));
+                const float ry = fma_f32_f16((unsigned short)(gr.y & 0xffffu), (unsigned short)(gr.y & 0xffffu),
+                                             fma_f32_f16((unsigned short)(gr.y >> 16), (unsigned short)(gr.y >> 16), 0.0f));
+                mag_lane = rx <= 1.0f && ry <= 1.0f;  // max(rx, ry) <= 1
             }
-            __syncwarp();
-            // ---- a4: decide
-            const bool exact = n <= na && !(a.flags & FLAG_FORCE_FALLBACK);
-            if (exact) {
-                path = PATH_EXACT;
-                evals = n;
-                const bool full = A == FULL;
-                const int ar = __popc(A & lanemask_lt());
-                if (!full) {
-                    if (active) s.lane_of_rank[ar] = (uint8_t)lane;
-                    __syncwarp();
-                }
-                // ---- a5: active rank r < n produces U[r] (lane h(r, A))
-                const bool producer = active && ar < n;
-                if (producer) {
-                    const uint32_t xy = s.tbl[ar];
-                    val = produce<FMT>(a.tex, mlpw, xy & 0xffffu, xy >> 16);
-                    prod = (xy >> 16) * (uint32_t)a.tex.W + (xy & 0xffffu);
-                }
-                // ---- a6: gather from lanes h(rho_k, A) and blend
-                int src[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    src[k] = active ? (full ? rho[k] : (int)s.lane_of_rank[rho[k]]) : (int)lane;
-                }
-                Texel<FMT> p[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
-                if (active) color = blend4<FMT>(p, f.w);
-                if (debug && a.dbg_unread) {
-                    int bad = 0;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) bad += (active && !__shfl_sync(FULL, producer, src[k])) ? 1 : 0;
-                    if (bad) atomicAdd(a.dbg_unread, (unsigned)bad);
-                }
-            } else {
-                run_fb = a.fallback;
-                path = PATH_FB_STF + a.fallback;
-            }
-        }
+            const bool wave_mag = a.grad != nullptr && __all_sync(FULL, !active || mag_lane);
 
-        // ---- a7: fallbacks (and the pure STF / WC modes)
-        if (MODE != MODE_4TAP && run_fb >= 0) {
-            const uint4 rr = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, a.frame_index + (uint32_t)fr, 0u),
-                                           a.seed_lo, a.seed_hi);
-            const int ksel = stf_corner(f, rr);
-            selbits = active ? (uint32_t)ksel : 0u;
-            if (run_fb == FB_STF) {
-                evals = na;
+            // ---- a2: footprint
+            const Foot f = footprint(uv, a);
+
+            uint32_t prod = INVALID_ID, selbits = 0u;
+            float4 color = make_float4(0.f, 0.f, 0.f, 0.f);
+            int n = 0xFF, evals = 0, path = 0;
+
+            if constexpr (MODE == MODE_4TAP) {
+                path = PATH_4TAP;
+                evals = 4 * na;
                 if (active) {
-                    prod = corner_id(f, ksel);
-                    val = produce<FMT>(a.tex, mlpw, corner_x(f, ksel), corner_y(f, ksel));
-                    color = scaled<FMT>(val);
+                    Texel<FMT> p[4];
+                    p[0] = produce<FMT>(a.tex, mlpw, f.xa, f.ya);
+                    p[1] = produce<FMT>(a.tex, mlpw, f.xb, f.ya);
+                    p[2] = produce<FMT>(a.tex, mlpw, f.xa, f.yb);
+                    p[3] = produce<FMT>(a.tex, mlpw, f.xb, f.yb);
+                    color = blend4<FMT>(p, f.w);
                 }
-            } else if (run_fb == FB_WC || run_fb == FB_C) {
-                evals = na;
-                if (active) {
-                    prod = corner_id(f, ksel);
-                    val = produce<FMT>(a.tex, mlpw, corner_x(f, ksel), corner_y(f, ksel));
-                }
-                color = fallback_gather<FMT>(f, active, prod, val, run_fb == FB_WC, s);
+            } else if constexpr (MODE == MODE_STF || MODE == MODE_WC) {
+                path = MODE == MODE_STF ? PATH_STF : PATH_WC;
+                Box b;
+                b.fits = false;
+                if constexpr (MODE == MODE_WC) b = wave_box(f, active);
+                const FbOut o = run_fallback<FMT>(MODE == MODE_STF ? FB_STF : FB_WC, f, b, active, A, na, px, py,
+                                                  frame, a, mlpw, s);
+                color = o.color;
+                prod = o.prod;
+                selbits = o.selbits;
+                evals = o.evals;
             } else {
-                // C+ (P:485-518): (1) planned STF texels, deduplicated and ranked ascending
-                const uint32_t pid = corner_id(f, ksel);
-                const uint32_t sk = warp_sort32(active ? ((pid << 5) | lane) : INVALID_ID);
-                const uint32_t skp = __shfl_up_sync(FULL, sk, 1);
-                const bool firstp = sk != INVALID_ID && (lane == 0 || (sk >> 5) != (skp >> 5));
-                const unsigned F = __ballot_sync(FULL, firstp);
-                const int np = __popc(F);
-                if (firstp) s.tbl[__popc(F & lanemask_lt())] = sk >> 5;
-                if ((int)lane >= np) s.tbl[lane] = INVALID_ID;
-                const int ar = __popc(A & lanemask_lt());
-                if (active) s.lane_of_rank[ar] = (uint8_t)lane;
+                // ---- a3: collect the exact unique set U and canonical ranks
+                const Box b = wave_box(f, active);
+                int rho[4];
+                if (b.area <= 32) n = collect_mask<1>(f, b, active, rho, s, lane);
+                else if (b.area <= 64) n = collect_mask<2>(f, b, active, rho, s, lane);
+                else if (b.area <= 128) n = collect_mask<4>(f, b, active, rho, s, lane);
+                else {
+                    const Collected c = collect_sort(f, active, s, lane, a.tex.W);
+                    n = c.n;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) rho[k] = c.rho[k];
+                }
                 __syncwarp();
-                // (2) active ranks < n_p produce the planned texels
-                bool spare = false;
-                int l = (int)lane;
-                if (active) {
-                    if (ar < np) {
-                        prod = s.tbl[ar];
-                        const uint32_t y = prod / (uint32_t)a.tex.W;
-                        val = produce<FMT>(a.tex, mlpw, prod - y * (uint32_t)a.tex.W, y);
+                // ---- a4: decide
+                if (n <= na && !(a.flags & FLAG_FORCE_FALLBACK)) {
+                    path = PATH_EXACT;
+                    evals = n;
+                    const bool full = A == FULL;
+                    const int ar = __popc(A & lt);
+                    if (!full) {
+                        if (active) s.lane_of_rank[ar] = (uint8_t)lane;
+                        __syncwarp();
+                    }
+                    // ---- a5: active rank r < n produces U[r] on lane h(r, A)
+                    const bool producer = active && ar < n;
+                    Texel<FMT> val = Texel<FMT>::zero();
+                    if (producer) {
+                        const uint32_t xy = s.tbl[ar];
+                        val = produce<FMT>(a.tex, mlpw, xy & 0xffffu, xy >> 16);
+                        if (debug) prod = (xy >> 16) * (uint32_t)a.tex.W + (xy & 0xffffu);
+                    }
+                    // ---- a6: gather from lanes h(rho_k, A) and blend
+                    int src[4];
+                    if (full) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) src[k] = rho[k] & 31;
                     } else {
-                        spare = true;
-                        l = (int)s.lane_of_rank[eq2_lane_rank(ar, np, na)];  // (3) Eq. 2
-                        selbits |= (1u << 5) | ((uint32_t)l << 8);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) src[k] = active ? (int)s.lane_of_rank[rho[k] & 31] : (int)lane;
                     }
+                    Texel<FMT> p[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
+                    if (active) color = blend4<FMT>(p, f.w);
+                    if (debug && a.dbg_unread) {
+                        int bad = 0;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) bad += (active && !__shfl_sync(FULL, producer, src[k])) ? 1 : 0;
+                        if (bad) atomicAdd(a.dbg_unread, (unsigned)bad);
+                    }
+                } else {
+                    path = PATH_FB_STF + a.fallback;
+                    const FbOut o = run_fallback<FMT>(a.fallback, f, b, active, A, na, px, py, frame, a, mlpw, s);
+                    color = o.color;
+                    prod = o.prod;
+                    selbits = o.selbits;
+                    evals = o.evals;
                 }
-                // spare lanes fetch the served lane's footprint
-                Foot g;
-                g.xa = __shfl_sync(FULL, f.xa, l);
-                g.xb = __shfl_sync(FULL, f.xb, l);
-                g.ya = __shfl_sync(FULL, f.ya, l);
-                g.yb = __shfl_sync(FULL, f.yb, l);
-                g.s = __shfl_sync(FULL, f.s, l);
-                g.t = __shfl_sync(FULL, f.t, l);
-                if (spare) {
-                    make_ids(g, a.tex.W);
-                    make_weights(g);
-                    // candidates: distinct nonzero-weight texels of l's footprint not in P (R-18 v)
-                    bool cand[4];
-                    float cw[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) { cand[k] = true; cw[k] = g.w[k]; }
-#pragma unroll
-                    for (int k = 1; k < 4; ++k)
-#pragma unroll
-                        for (int j = 0; j < k; ++j)
-                            if (cand[j] && cand[k] && g.id[j] == g.id[k]) {
-                                cand[k] = false;
-                                cw[j] = __fadd_rn(cw[j], g.w[k]);
-                            }
-                    float wsum = 0.0f;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (cand[k] && cw[k] != 0.0f) {
-                            const int pos = lower_bound32(s.tbl, g.id[k]);
-                            if (pos < 32 && s.tbl[pos] == g.id[k]) cand[k] = false;
-                        } else {
-                            cand[k] = false;
-                        }
-                        if (cand[k]) wsum = __fadd_rn(wsum, cw[k]);
-                    }
-                    if (cand[0] || cand[1] || cand[2] || cand[3]) {
-                        const float target = __fmul_rn(unit24(rr.z), wsum);
-                        float cum = 0.0f;
-                        int pick = -1, lastc = 0;
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            if (!cand[k]) continue;
-                            lastc = k;
-                            cum = __fadd_rn(cum, cw[k]);
-                            if (pick < 0 && cum > target) pick = k;
-                        }
-                        if (pick < 0) pick = lastc;
-                        prod = corner_id(g, pick);
-                        val = produce<FMT>(a.tex, mlpw, corner_x(g, pick), corner_y(g, pick));
-                        selbits |= ((uint32_t)pick << 2) | (1u << 4);
-                    }
-                }
-                __syncwarp();
-                evals = __popc(__ballot_sync(FULL, active && prod != INVALID_ID));
-                color = fallback_gather<FMT>(f, active, prod, val, false, s);
             }
-        }
 
-        // ---- outputs
-        if (inframe) st_stream_f4(a.out + pix, color);
-        if (debug && inframe) {
-            if (a.dbg_pid) a.dbg_pid[pix] = (MODE == MODE_4TAP) ? INVALID_ID : prod;
-            if (a.dbg_sel) a.dbg_sel[pix] = selbits;
+            // ---- outputs
+            if (inframe) st_stream_f4(a.out + pix, color);
+            if (debug && inframe) {
+                if (a.dbg_pid) a.dbg_pid[pix] = (MODE == MODE_4TAP) ? INVALID_ID : prod;
+                if (a.dbg_sel) a.dbg_sel[pix] = selbits;
+            }
+            // ---- a8: per-wave record
+            if (lane == 0)
+                a.rec[w] = (uint32_t)(evals & 0xFF) | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)na << 16) |
+                           ((uint32_t)path << 22) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26);
         }
-        // ---- a8: per-wave record
-        if (lane == 0)
-            a.rec[w] = (uint32_t)(evals & 0xFF) | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)na << 16) |
-                       ((uint32_t)path << 22) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26);
         __syncwarp();
+
+        // advance by S waves without dividing
+        wx += a.S_wx;
+        wy += a.S_wy;
+        fr += a.S_fr;
+        base += a.S_base;
+        if (wx >= a.nwx) { wx -= a.nwx; ++wy; base += 4u * (unsigned)a.Wf - 8u * (unsigned)a.nwx; }
+        if (wy >= a.nwy) { wy -= a.nwy; ++fr; base += a.fpx - 4u * (unsigned)a.Wf * (unsigned)a.nwy; }
     }
 }
 
 template <int FMT, int MODE>
-static cudaError_t launch_one(const KArgs &k, cudaStream_t stream) {
+static cudaError_t launch_one(KArgs k, cudaStream_t stream) {
     auto kern = ctf_filter_kernel<FMT, MODE>;
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -558,10 +761,16 @@ static cudaError_t launch_one(const KArgs &k, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0);
     if (e != cudaSuccess) return e;
-    const long long need = (k.total_waves + kWarps - 1) / kWarps;
+    const long long need = ((long long)k.total_waves + kWarps - 1) / kWarps;
     long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
+    k.S = (unsigned)(grid * kWarps);
+    k.S_fr = (int)(k.S / (unsigned)k.wpf);
+    const int rem = (int)(k.S - (unsigned)k.S_fr * (unsigned)k.wpf);
+    k.S_wy = rem / k.nwx;
+    k.S_wx = rem - k.S_wy * k.nwx;
+    k.S_base = (unsigned)k.S_fr * k.fpx + 4u * (unsigned)k.S_wy * (unsigned)k.Wf + 8u * (unsigned)k.S_wx;
     kern<<<(unsigned)grid, kWarps * 32, 0, stream>>>(k);
     return cudaGetLastError();
 }
@@ -600,8 +809,10 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.Wf = a.Wf;
     k.Hf = a.Hf;
     k.nwx = (a.Wf + 7) / 8;
-    k.wpf = k.nwx * ((a.Hf + 3) / 4);
-    k.total_waves = (long long)k.wpf * a.frames;
+    k.nwy = (a.Hf + 3) / 4;
+    k.wpf = k.nwx * k.nwy;
+    k.fpx = (unsigned)a.Wf * (unsigned)a.Hf;
+    k.total_waves = (unsigned)((long long)k.wpf * a.frames);
     k.Wflt = (float)a.W;
     k.Hflt = (float)a.H;
     k.fallback = a.fallback;

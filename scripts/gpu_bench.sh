@@ -1,16 +1,18 @@
-# bench + ncu evidence on one B200 (run under gpurun from the repo root)
+# tests + bench + ncu evidence on one B200 (run under gpurun from the repo root)
 set -x
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 TAG=${TAG:-r01}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
+if [ "${TESTS:-1}" = "1" ]; then
+  timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
+fi
 timeout 900 python bench.py --steps ${STEPS:-20} --warmup 3 --cpu-seconds ${CPUS:-12} > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 tail -5 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
 # launch list of the same command (cold-cache, serialised: compare shares)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_$TAG.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:ctf_ -c 40 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch_bench_$TAG.json 2>&1
 tail -3 gpurun_out/launches_$TAG.csv
 # one full capture of the dominant kernel (16-frame batch)
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ctf_filter_kernel -s 3 -c 1 \
     -o gpurun_out/prof_$TAG python bench.py --frames 16 --warmup 3 --profile-launches 1 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -3 gpurun_out/ncu_full_$TAG.log
-ls -la gpurun_out
