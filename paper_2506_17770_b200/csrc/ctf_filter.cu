@@ -35,12 +35,10 @@ struct KArgs {
     float4 *out;
     uint32_t *rec;
     uint32_t *dbg_pid, *dbg_sel, *dbg_unread;
-    unsigned fpx;                   // pixels per frame
-    unsigned total_waves;           // < 2^31 (validated on the host; all pixel indices < 2^32)
+    unsigned fpx;                   // pixels per frame (all pixel indices < 2^32, validated on the host)
     int Wf, Hf, nwx, nwy, wpf;
-    unsigned S;                     // grid stride in waves
-    int S_fr, S_wy, S_wx;           // S = S_fr*wpf + S_wy*nwx + S_wx
-    unsigned S_base;                // pixel-index increment for S (mod 2^32)
+    int cpr, cpf;                   // work items (runs of kChunk waves) per wave-row / per frame
+    unsigned nchunks;
     float Wflt, Hflt;
     int fallback;
     uint32_t flags, frame_index, seed_lo, seed_hi;
@@ -153,31 +151,35 @@ __device__ __forceinline__ int stf_corner(const Foot &f, uint4 r) {
 }
 
 // ------------------------------------------------------------------ AABB bitmask
-// Wave AABB and a bit position t = (y - miny) * 2^lgP + (x - minx) per texel.
+// Wave bounding-box origin (min corner, 2 redux.sync) and a bitmask window of width
+// 2^lgP anchored there: bit t = (y - miny) * 2^lgP + (x - minx).  The window shape is
+// the first of 8x4, 4x8 (32 bits), 8x8 (64), 16x8, 8x16, 32x4 (128) that holds every
+// active footprint (one vote each); K = words, 0 = does not fit (sort path).
 struct Box {
-    int minx, miny, lgP, area;
-    bool fits;      // area <= 128 with width <= 32: usable as a register bitmask
+    int minx, miny, lgP, K;
+    bool fits;
 };
 
 __device__ __forceinline__ Box wave_box(const Foot &f, bool active) {
     Box b;
     b.minx = __reduce_min_sync(FULL, active ? f.xa : INT_MAX);
-    const int maxx = __reduce_max_sync(FULL, active ? f.xb : INT_MIN);
     b.miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
-    const int maxy = __reduce_max_sync(FULL, active ? f.yb : INT_MIN);
-    const int bw = maxx - b.minx + 1, bh = maxy - b.miny + 1;
-    b.lgP = bw <= 1 ? 0 : 32 - __clz(bw - 1);
-    const bool small = bw <= 32 && bh <= 128;
-    b.area = small ? (bh << b.lgP) : INT_MAX;
-    b.fits = small && b.area <= 128;
+    const unsigned dx = (unsigned)(f.xb - b.minx), dy = (unsigned)(f.yb - b.miny);
+    if (__all_sync(FULL, !active || (dx < 8u && dy < 4u))) { b.lgP = 3; b.K = 1; }
+    else if (__all_sync(FULL, !active || (dx < 4u && dy < 8u))) { b.lgP = 2; b.K = 1; }
+    else if (__all_sync(FULL, !active || (dx < 8u && dy < 8u))) { b.lgP = 3; b.K = 2; }
+    else if (__all_sync(FULL, !active || (dx < 16u && dy < 8u))) { b.lgP = 4; b.K = 4; }
+    else if (__all_sync(FULL, !active || (dx < 8u && dy < 16u))) { b.lgP = 3; b.K = 4; }
+    else if (__all_sync(FULL, !active || (dx < 32u && dy < 4u))) { b.lgP = 5; b.K = 4; }
+    else { b.lgP = 0; b.K = 0; }
+    b.fits = b.K != 0;
     return b;
 }
 __device__ __forceinline__ uint32_t box_t(const Box &b, int x, int y) {
     return ((uint32_t)(y - b.miny) << b.lgP) + (uint32_t)(x - b.minx);
 }
-__device__ __forceinline__ uint32_t box_xy(const Box &b, uint32_t t) {  // t -> packed (y << 16 | x)
-    return ((uint32_t)(b.miny + (int)(t >> b.lgP)) << 16) | (uint32_t)(b.minx + (int)(t & ((1u << b.lgP) - 1u)));
-}
+__device__ __forceinline__ int box_x(const Box &b, uint32_t t) { return b.minx + (int)(t & ((1u << b.lgP) - 1u)); }
+__device__ __forceinline__ int box_y(const Box &b, uint32_t t) { return b.miny + (int)(t >> b.lgP); }
 
 // K-word (K*32-bit) wave mask, OR-reduced across the warp.
 template <int K>
@@ -223,13 +225,13 @@ struct WMask {
         return prefix(t >> 5) + __popc(word(t >> 5) & ((1u << (t & 31u)) - 1u));
     }
     __device__ __forceinline__ bool test(uint32_t t) const { return (word(t >> 5) >> (t & 31u)) & 1u; }
-    // lane j owns bit j of every word: write rank -> packed (y,x) for ranks < 32
-    __device__ __forceinline__ void push(uint32_t *tbl, const Box &b, unsigned lane, unsigned lt) const {
+    // lane j owns bit j of every word: write rank -> bit position t for ranks < 32
+    __device__ __forceinline__ void push(uint32_t *tbl, unsigned lane, unsigned lt) const {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             if ((w[k] >> lane) & 1u) {
                 const int r = pre[k] + __popc(w[k] & lt);
-                if (r < 32) tbl[r] = box_xy(b, ((uint32_t)k << 5) | lane);
+                if (r < 32) tbl[r] = ((uint32_t)k << 5) | lane;
             }
         }
     }
@@ -448,7 +450,7 @@ __device__ __noinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bo
         // (1) planned STF texels as a bitmask (one bit per lane)
         P.reduce_bit(box_t(b, sx, sy), active);
         np = P.n;
-        P.push(s.tbl, b, lane, lt);
+        P.push(s.tbl, lane, lt);
     } else {
         const uint32_t pid = (uint32_t)(sy * W + sx);
         const uint32_t sk = warp_sort32(active ? ((pid << 5) | lane) : INVALID_ID);
@@ -467,7 +469,7 @@ __device__ __noinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bo
     if (active) {
         if (ar < np) {
             const uint32_t e = s.tbl[ar];
-            if (b.fits) { qx = (int)(e & 0xffffu); qy = (int)(e >> 16); }
+            if (b.fits) { qx = box_x(b, e); qy = box_y(b, e); }
             else { qy = (int)(e / (uint32_t)W); qx = (int)(e - (uint32_t)qy * (uint32_t)W); }
             produced = true;
         } else {
@@ -529,7 +531,7 @@ __device__ __forceinline__ int collect_mask(const Foot &f, const Box &b, bool ac
     rho[1] = rho[0] + (int)dxs;
     rho[2] = B.rank(t2);
     rho[3] = rho[2] + (int)dxs;
-    if (B.n <= 32) B.push(s.tbl, b, lane, lanemask_lt());
+    if (B.n <= 32) B.push(s.tbl, lane, lanemask_lt());
     return B.n;
 }
 
@@ -579,7 +581,9 @@ static __device__ __noinline__ Collected collect_sort(const Foot f, bool active,
 }
 
 // ----------------------------------------------------------------------- kernel
-template <int FMT, int MODE>
+constexpr int kChunk = 16;  // waves per work item: a run of consecutive waves in one wave-row
+
+template <int FMT, int MODE, bool DBG>
 __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_filter_kernel(const KArgs a) {
     __shared__ WarpSmem smem[kWarps];
     __shared__ __align__(16) float mlpw[FMT == FMT_MLP ? kMlpParams : 4];
@@ -589,43 +593,56 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
     }
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     WarpSmem &s = smem[warp];
-    const bool debug = (a.flags & FLAG_DEBUG) != 0;
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
-    const unsigned laneoff = (unsigned)(ly * a.Wf + lx);
     const unsigned lt = lanemask_lt();
+    const unsigned nwarps = gridDim.x * kWarps;
 
-    unsigned w = blockIdx.x * kWarps + warp;
-    if (w >= a.total_waves) return;
-    int fr = (int)(w / (unsigned)a.wpf);
-    const int rw = (int)(w - (unsigned)fr * (unsigned)a.wpf);
-    int wy = rw / a.nwx, wx = rw - wy * a.nwx;
-    unsigned base = (unsigned)fr * a.fpx + (unsigned)(wy * 4) * (unsigned)a.Wf + (unsigned)(wx * 8);
-
-    for (; w < a.total_waves; w += a.S) {
-        const int px = wx * 8 + lx, py = wy * 4 + ly;
-        const bool inframe = px < a.Wf && py < a.Hf;
-        const unsigned pix = base + laneoff;
+    // work item c = (frame, wave-row, run of kChunk waves); warps stride over items
+    for (unsigned c = blockIdx.x * kWarps + warp; c < a.nchunks; c += nwarps) {
+        const int fr = (int)(c / (unsigned)a.cpf);
+        const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
+        const int wy = rr / a.cpr;
+        const int wx0 = (rr - wy * a.cpr) * kChunk;
+        const int wx1 = min(wx0 + kChunk, a.nwx);
+        const int py = wy * 4 + ly;
+        const bool rowok = py < a.Hf;
         const uint32_t frame = a.frame_index + (uint32_t)fr;
+        unsigned w = (unsigned)fr * (unsigned)a.wpf + (unsigned)(wy * a.nwx + wx0);    // record index
+        unsigned pix = (unsigned)fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)(wx0 * 8 + lx);
+        int px = wx0 * 8 + lx;
 
-        // ---- a1: load + classify
-        float2 uv = make_float2(__int_as_float(0x7fc00000), 0.f);
-        uint2 gr = make_uint2(0u, 0u);
-        if (inframe) {
-            uv = ld_stream_f2(a.uv + pix);
-            if (a.grad) gr = ld_stream_u2(a.grad + pix);
+        // software pipeline: wave wx+1's uv/grad loads are issued before wave wx is
+        // processed, so their HBM latency hides behind this wave's work
+        float2 uv_n = make_float2(__int_as_float(0x7fc00000), 0.f);
+        uint2 gr_n = make_uint2(0u, 0u);
+        if (rowok && px < a.Wf) {
+            uv_n = ld_stream_f2(a.uv + pix);
+            if (a.grad) gr_n = ld_stream_u2(a.grad + pix);
         }
-        const bool active = inframe && !isnan(uv.x);
-        const unsigned A = __ballot_sync(FULL, active);
-        const int na = __popc(A);
-
-        if (na == 0) {
-            if (inframe) st_stream_f4(a.out + pix, make_float4(0.f, 0.f, 0.f, 0.f));
-            if (debug && inframe) {
-                if (a.dbg_pid) a.dbg_pid[pix] = INVALID_ID;
-                if (a.dbg_sel) a.dbg_sel[pix] = 0u;
+        for (int wx = wx0; wx < wx1; ++wx, ++w, pix += 8u, px += 8) {
+            const bool inframe = rowok && px < a.Wf;
+            const float2 uv = uv_n;
+            const uint2 gr = gr_n;
+            uv_n = make_float2(__int_as_float(0x7fc00000), 0.f);
+            gr_n = make_uint2(0u, 0u);
+            if (wx + 1 < wx1 && rowok && px + 8 < a.Wf) {
+                uv_n = ld_stream_f2(a.uv + (pix + 8u));
+                if (a.grad) gr_n = ld_stream_u2(a.grad + (pix + 8u));
             }
-            if (lane == 0) a.rec[w] = ((MODE == MODE_COLLAB ? 0u : 0xFFu) << 8) | (1u << 26);
-        } else {
+
+            // ---- a1: classify
+            const bool active = inframe && !isnan(uv.x);
+            const unsigned A = __ballot_sync(FULL, active);
+            const int na = __popc(A);
+            if (na == 0) {
+                if (inframe) st_stream_f4(a.out + pix, make_float4(0.f, 0.f, 0.f, 0.f));
+                if (DBG && inframe) {
+                    if (a.dbg_pid) a.dbg_pid[pix] = INVALID_ID;
+                    if (a.dbg_sel) a.dbg_sel[pix] = 0u;
+                }
+                if (lane == 0) a.rec[w] = ((MODE == MODE_COLLAB ? 0u : 0xFFu) << 8) | (1u << 26);
+                continue;
+            }
             bool mag_lane = true;
             if (a.grad) {
                 // R-20: squares of fp16 values are exact in fp32, so fma(g0, g0, g1*g1)
@@ -637,17 +654,16 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
                 mag_lane = rx <= 1.0f && ry <= 1.0f;  // max(rx, ry) <= 1
             }
             const bool wave_mag = a.grad != nullptr && __all_sync(FULL, !active || mag_lane);
+            const uint32_t rec_base = ((uint32_t)na << 16) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26);
 
             // ---- a2: footprint
             const Foot f = footprint(uv, a);
 
-            uint32_t prod = INVALID_ID, selbits = 0u;
+            uint32_t prod = INVALID_ID, selbits = 0u, rec;
             float4 color = make_float4(0.f, 0.f, 0.f, 0.f);
-            int n = 0xFF, evals = 0, path = 0;
 
             if constexpr (MODE == MODE_4TAP) {
-                path = PATH_4TAP;
-                evals = 4 * na;
+                rec = rec_base | (0xFFu << 8) | ((uint32_t)PATH_4TAP << 22) | (uint32_t)((4 * na) & 0xFF);
                 if (active) {
                     Texel<FMT> p[4];
                     p[0] = produce<FMT>(a.tex, mlpw, f.xa, f.ya);
@@ -657,34 +673,34 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
                     color = blend4<FMT>(p, f.w);
                 }
             } else if constexpr (MODE == MODE_STF || MODE == MODE_WC) {
-                path = MODE == MODE_STF ? PATH_STF : PATH_WC;
                 Box b;
                 b.fits = false;
+                b.K = 0;
                 if constexpr (MODE == MODE_WC) b = wave_box(f, active);
                 const FbOut o = run_fallback<FMT>(MODE == MODE_STF ? FB_STF : FB_WC, f, b, active, A, na, px, py,
                                                   frame, a, mlpw, s);
                 color = o.color;
                 prod = o.prod;
                 selbits = o.selbits;
-                evals = o.evals;
+                rec = rec_base | (0xFFu << 8) | ((uint32_t)(MODE == MODE_STF ? PATH_STF : PATH_WC) << 22) |
+                      (uint32_t)(o.evals & 0xFF);
             } else {
                 // ---- a3: collect the exact unique set U and canonical ranks
                 const Box b = wave_box(f, active);
-                int rho[4];
-                if (b.area <= 32) n = collect_mask<1>(f, b, active, rho, s, lane);
-                else if (b.area <= 64) n = collect_mask<2>(f, b, active, rho, s, lane);
-                else if (b.area <= 128) n = collect_mask<4>(f, b, active, rho, s, lane);
+                int rho[4], n;
+                if (b.K == 1) n = collect_mask<1>(f, b, active, rho, s, lane);
+                else if (b.K == 2) n = collect_mask<2>(f, b, active, rho, s, lane);
+                else if (b.K == 4) n = collect_mask<4>(f, b, active, rho, s, lane);
                 else {
-                    const Collected c = collect_sort(f, active, s, lane, a.tex.W);
-                    n = c.n;
+                    const Collected cc = collect_sort(f, active, s, lane, a.tex.W);
+                    n = cc.n;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) rho[k] = c.rho[k];
+                    for (int k = 0; k < 4; ++k) rho[k] = cc.rho[k];
                 }
                 __syncwarp();
                 // ---- a4: decide
                 if (n <= na && !(a.flags & FLAG_FORCE_FALLBACK)) {
-                    path = PATH_EXACT;
-                    evals = n;
+                    rec = rec_base | ((uint32_t)n * 0x101u);  // evals = n, path 0
                     const bool full = A == FULL;
                     const int ar = __popc(A & lt);
                     if (!full) {
@@ -695,9 +711,12 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
                     const bool producer = active && ar < n;
                     Texel<FMT> val = Texel<FMT>::zero();
                     if (producer) {
-                        const uint32_t xy = s.tbl[ar];
-                        val = produce<FMT>(a.tex, mlpw, xy & 0xffffu, xy >> 16);
-                        if (debug) prod = (xy >> 16) * (uint32_t)a.tex.W + (xy & 0xffffu);
+                        const uint32_t e = s.tbl[ar];
+                        int qx, qy;
+                        if (b.fits) { qx = box_x(b, e); qy = box_y(b, e); }
+                        else { qx = (int)(e & 0xffffu); qy = (int)(e >> 16); }
+                        val = produce<FMT>(a.tex, mlpw, qx, qy);
+                        if (DBG) prod = (uint32_t)(qy * a.tex.W + qx);
                     }
                     // ---- a6: gather from lanes h(rho_k, A) and blend
                     int src[4];
@@ -712,48 +731,38 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
 #pragma unroll
                     for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
                     if (active) color = blend4<FMT>(p, f.w);
-                    if (debug && a.dbg_unread) {
+                    if (DBG && a.dbg_unread) {
                         int bad = 0;
 #pragma unroll
                         for (int k = 0; k < 4; ++k) bad += (active && !__shfl_sync(FULL, producer, src[k])) ? 1 : 0;
                         if (bad) atomicAdd(a.dbg_unread, (unsigned)bad);
                     }
                 } else {
-                    path = PATH_FB_STF + a.fallback;
                     const FbOut o = run_fallback<FMT>(a.fallback, f, b, active, A, na, px, py, frame, a, mlpw, s);
                     color = o.color;
                     prod = o.prod;
                     selbits = o.selbits;
-                    evals = o.evals;
+                    rec = rec_base | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)(PATH_FB_STF + a.fallback) << 22) |
+                          (uint32_t)(o.evals & 0xFF);
                 }
             }
 
             // ---- outputs
             if (inframe) st_stream_f4(a.out + pix, color);
-            if (debug && inframe) {
+            if (DBG && inframe) {
                 if (a.dbg_pid) a.dbg_pid[pix] = (MODE == MODE_4TAP) ? INVALID_ID : prod;
                 if (a.dbg_sel) a.dbg_sel[pix] = selbits;
             }
             // ---- a8: per-wave record
-            if (lane == 0)
-                a.rec[w] = (uint32_t)(evals & 0xFF) | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)na << 16) |
-                           ((uint32_t)path << 22) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26);
+            if (lane == 0) a.rec[w] = rec;
+            __syncwarp();
         }
-        __syncwarp();
-
-        // advance by S waves without dividing
-        wx += a.S_wx;
-        wy += a.S_wy;
-        fr += a.S_fr;
-        base += a.S_base;
-        if (wx >= a.nwx) { wx -= a.nwx; ++wy; base += 4u * (unsigned)a.Wf - 8u * (unsigned)a.nwx; }
-        if (wy >= a.nwy) { wy -= a.nwy; ++fr; base += a.fpx - 4u * (unsigned)a.Wf * (unsigned)a.nwy; }
     }
 }
 
-template <int FMT, int MODE>
+template <int FMT, int MODE, bool DBG>
 static cudaError_t launch_one(KArgs k, cudaStream_t stream) {
-    auto kern = ctf_filter_kernel<FMT, MODE>;
+    auto kern = ctf_filter_kernel<FMT, MODE, DBG>;
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -761,27 +770,26 @@ static cudaError_t launch_one(KArgs k, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0);
     if (e != cudaSuccess) return e;
-    const long long need = ((long long)k.total_waves + kWarps - 1) / kWarps;
+    const long long need = ((long long)k.nchunks + kWarps - 1) / kWarps;
     long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    k.S = (unsigned)(grid * kWarps);
-    k.S_fr = (int)(k.S / (unsigned)k.wpf);
-    const int rem = (int)(k.S - (unsigned)k.S_fr * (unsigned)k.wpf);
-    k.S_wy = rem / k.nwx;
-    k.S_wx = rem - k.S_wy * k.nwx;
-    k.S_base = (unsigned)k.S_fr * k.fpx + 4u * (unsigned)k.S_wy * (unsigned)k.Wf + 8u * (unsigned)k.S_wx;
     kern<<<(unsigned)grid, kWarps * 32, 0, stream>>>(k);
     return cudaGetLastError();
+}
+
+template <int FMT, int MODE>
+static cudaError_t launch_dbg(const KArgs &k, cudaStream_t stream) {
+    return (k.flags & FLAG_DEBUG) ? launch_one<FMT, MODE, true>(k, stream) : launch_one<FMT, MODE, false>(k, stream);
 }
 
 template <int FMT>
 static cudaError_t launch_fmt(const KArgs &k, int mode, cudaStream_t stream) {
     switch (mode) {
-    case MODE_4TAP: return launch_one<FMT, MODE_4TAP>(k, stream);
-    case MODE_STF: return launch_one<FMT, MODE_STF>(k, stream);
-    case MODE_WC: return launch_one<FMT, MODE_WC>(k, stream);
-    default: return launch_one<FMT, MODE_COLLAB>(k, stream);
+    case MODE_4TAP: return launch_dbg<FMT, MODE_4TAP>(k, stream);
+    case MODE_STF: return launch_dbg<FMT, MODE_STF>(k, stream);
+    case MODE_WC: return launch_dbg<FMT, MODE_WC>(k, stream);
+    default: return launch_dbg<FMT, MODE_COLLAB>(k, stream);
     }
 }
 
@@ -812,7 +820,9 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.nwy = (a.Hf + 3) / 4;
     k.wpf = k.nwx * k.nwy;
     k.fpx = (unsigned)a.Wf * (unsigned)a.Hf;
-    k.total_waves = (unsigned)((long long)k.wpf * a.frames);
+    k.cpr = (k.nwx + kChunk - 1) / kChunk;
+    k.cpf = k.cpr * k.nwy;
+    k.nchunks = (unsigned)((long long)k.cpf * a.frames);
     k.Wflt = (float)a.W;
     k.Hflt = (float)a.H;
     k.fallback = a.fallback;
