@@ -630,6 +630,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
                 if (a.grad) gr_n = ld_stream_u2(a.grad + (pix + 8u));
             }
 
+            __syncwarp();  // order this wave's shared-memory tables after the previous wave's reads
             // ---- a1: classify
             const bool active = inframe && !isnan(uv.x);
             const unsigned A = __ballot_sync(FULL, active);
@@ -732,10 +733,11 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
                     for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
                     if (active) color = blend4<FMT>(p, f.w);
                     if (DBG && a.dbg_unread) {
-                        int bad = 0;
+                        unsigned bad = 0;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) bad += (active && !__shfl_sync(FULL, producer, src[k])) ? 1 : 0;
-                        if (bad) atomicAdd(a.dbg_unread, (unsigned)bad);
+                        for (int k = 0; k < 4; ++k) bad += (active && !__shfl_sync(FULL, producer, src[k])) ? 1u : 0u;
+                        bad = __reduce_add_sync(FULL, bad);       // warp-uniform: no divergent atomic
+                        if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
                     }
                 } else {
                     const FbOut o = run_fallback<FMT>(a.fallback, f, b, active, A, na, px, py, frame, a, mlpw, s);

@@ -244,3 +244,16 @@ def test_abi_errors(ctf):
     with pytest.raises(ctf.CtfError) as e:
         ctf.filter_frame(bad, uv, None, 3)
     assert e.value.code == ctf.CTF_EINVAL
+
+
+@pytest.mark.parametrize("mode,fb,fl", [(3, 3, 0), (3, 2, 0), (3, 0, 2), (0, 0, 0), (2, 0, 0)])
+def test_release_kernel_matches_oracle(ctf, mode, fb, fl):
+    """The non-debug kernel instantiation (what bench.py runs) against the oracle."""
+    import oracle
+    tex = bc1_tex(512, 512, 13, "image")
+    uv, g = synthetic.perspective_plane(203, 117, 512, 512, synthetic.PLANE_C4)
+    o = oracle.filter_frame(tex, uv, g, mode, fb, fl, seed=21, frame_index=2)
+    dt = to_dev_tex(ctf, tex)
+    out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, fl, 21, 2)
+    np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+    assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
