@@ -735,7 +735,10 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
                     if (DBG && a.dbg_unread) {
                         unsigned bad = 0;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) bad += (active && !__shfl_sync(FULL, producer, src[k])) ? 1u : 0u;
+                        for (int k = 0; k < 4; ++k) {
+                            const int pk = __shfl_sync(FULL, (int)producer, src[k]);  // every lane shuffles
+                            bad += (active && !pk) ? 1u : 0u;
+                        }
                         bad = __reduce_add_sync(FULL, bad);       // warp-uniform: no divergent atomic
                         if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
                     }

@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 TAG=${TAG:-r01}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 if [ "${TESTS:-1}" = "1" ]; then
-  timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
+  timeout 600 python -m pytest tests -m gpu -x -q --timeout=120 2>&1 | tail -15
 fi
 timeout 900 python bench.py --steps ${STEPS:-20} --warmup 3 --cpu-seconds ${CPUS:-12} > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 tail -5 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
