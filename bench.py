@@ -1,16 +1,20 @@
 #!/usr/bin/env python
 """bench.py — throughput of the collaborative texture filtering hot path on B200.
 
-Workload (BASELINE.json configs[4], "config 5"): a batch of 64 4K (3840x2160)
-frames of the animated camera path over the perspective ground plane
-(synthetic.camera_path_frame: magnification ~0.5-9.4), BC1-style 4096^2
-texture, CTF_MODE_COLLAB with the C+ fallback, per-pixel uv + fp16 Jacobian
-in, RGBA fp32 + per-wave records out.  One step = one ctf_filter_batch call
-(one persistent-kernel launch) over the rank's 64 frames.  Inputs are resident
-in HBM before timing; the batch (17 GB of I/O) is far larger than L2, so no
-L2 flush is needed between steps.  Multi-GPU: weak scaling — every rank
-filters its own 64 frames (distinct RNG frame indices); NCCL is used only to
-gather statistics and the max-over-ranks time.
+Headline workload (BASELINE.json configs[4], "config 5"): a batch of 64 4K
+(3840x2160) frames of the animated camera path over the perspective ground
+plane (synthetic.camera_path_frame: magnification ~0.5-9.4), BC1-style 4096^2
+texture, CTF_MODE_COLLAB with the C+ fallback, per-pixel uv + fp16 Jacobian in,
+RGBA fp32 + per-wave records out.  One step = one ctf_filter_batch call (one
+persistent-kernel launch) over the rank's 64 frames.  Inputs are resident in
+HBM before timing; the batch (17 GB of I/O) is far larger than L2, so no L2
+flush is needed between steps.  Multi-GPU: weak scaling — every rank filters
+its own 64 frames (distinct RNG frame indices); NCCL carries only the
+max-over-ranks time and one all_gather of statistics (paper_2506_17770_b200.dist).
+
+At N = 1 the line also carries "configs": the other §8 configurations
+(1: 64x64 launch latency, 2: 1080p, 3: 4K latent-MLP COLLAB vs 4-tap,
+4: 4K mixed minification with every fallback), each timed on the device.
 
   python bench.py [--gpus N --steps K --warmup W]          # our CUDA path
   python bench.py --impl reference ...                      # CPU oracle arm
@@ -37,6 +41,7 @@ METRIC = "4K filtered Gpix/s per B200 (1/2/4/8 GPUs); texel evals/pixel; error v
 UNIT = "Gpix/s"
 MODES = {"collab": 3, "4tap": 0, "stf": 1, "wc": 2}
 FALLBACKS = {"stf": 0, "wc": 1, "c": 2, "cplus": 3}
+MLP_FMA_PER_EVAL = 32 * 12 + 32 * 32 + 4 * 32   # 1536 FMA per latent-MLP texel (R-10)
 
 
 def parse_args():
@@ -56,7 +61,8 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-configs", action="store_true", help="skip the other §8 configurations")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--profile-launches", type=int, default=0,
                     help="(for ncu) run this many launches after warmup, no timing/json")
@@ -131,12 +137,12 @@ def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback (B200_PROFILING.md)"
+        return float(d.get("hbm_gbs", 6650.0)), float(d.get("sm_max_mhz", 1965.0)), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1965.0, "fallback (B200_PROFILING.md)"
 
 
 def ncu_traffic(frames: int, wf: int, hf: int):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    """dram bytes per launch of the dominant kernel, scaled from the committed ncu --set full capture."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
@@ -148,11 +154,6 @@ def ncu_traffic(frames: int, wf: int, hf: int):
         return None
 
 
-def make_texture(args):
-    import synthetic
-    return synthetic.bc1_texture(args.tex, args.tex, args.seed, "image")
-
-
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -160,20 +161,19 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def oracle_sample(blocks, tex_size, frames_np, mode, fb, seed, frame_base, budget_s):
-    """Time the oracle on whole frames until the budget is spent; returns (pixels, seconds, nframes)."""
-    import oracle
-    tex = {"format": 1, "width": tex_size, "height": tex_size, "bc1": blocks}
-    px, t_total, n = 0, 0.0, 0
-    for i, (f, uv, g) in enumerate(frames_np):
-        t0 = time.perf_counter()
-        oracle.filter_frame(tex, uv, g, mode, fb, 0, seed, frame_base + f, debug=False)
-        t_total += time.perf_counter() - t0
-        px += uv.shape[0] * uv.shape[1]
-        n += 1
-        if t_total >= budget_s:
-            break
-    return px, t_total, n
+def time_launches(fn, reps: int, stream) -> float:
+    """Mean device time (ms) of `reps` back-to-back calls, CUDA events on the launching stream."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -185,13 +185,12 @@ def run_reference(args):
     import synthetic
     os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
     oracle.build_oracle()
-    blocks = make_texture(args)
+    blocks = synthetic.bc1_texture(args.tex, args.tex, args.seed, "image")
     mode, fb = MODES[args.mode], FALLBACKS[args.fallback]
     tex = {"format": 1, "width": args.tex, "height": args.tex, "bc1": blocks}
     # each step: one full 4K frame of the camera path (a bounded sample of the 64-frame batch)
     times = []
-    nsteps = args.warmup + args.steps
-    for s in range(nsteps):
+    for s in range(args.warmup + args.steps):
         f = (s * 7) % 64
         uv, g = synthetic.camera_path_frame(f, args.width, args.height, args.tex, args.tex)
         if args.no_grad:
@@ -217,6 +216,75 @@ def run_reference(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- other §8 configs
+def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: float) -> dict:
+    """Configs 1-4 of BASELINE.json, each timed on the device (rank 0, N = 1)."""
+    import synthetic
+    res = {}
+    fp32_peak_tflops = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FFMA issue peak at max SM clock
+
+    def run(tex, uv, g, mode, fb, reps):
+        out = torch.empty(uv.shape[:-1] + (4,), dtype=torch.float32, device=dev)
+        rec = torch.empty(((uv.shape[0] + 3) // 4, (uv.shape[1] + 7) // 8), dtype=torch.int32, device=dev)
+        ms = time_launches(lambda: ctf.filter_frame(tex, uv, g, mode, fb, 0, seed, 0, out=out, rec=rec,
+                                                    stream=stream), reps, stream)
+        st = ctf.stats(rec, uv.shape[1], uv.shape[0], 1, stream=stream)
+        return ms, st, out
+
+    def entry(wf, hf, ms, st, nbytes=None):
+        e = {"ms": ms, "gpix_s": wf * hf / (ms / 1e3) / 1e9,
+             "texel_evals_per_px": st["texel_evals"] / max(1, st["pixels_active"]),
+             "exact_wave_frac": st["waves_exact"] / max(1, st["waves_live"])}
+        if nbytes is not None:
+            e["hbm_frac"] = nbytes / (ms / 1e3) / 1e9 / peak_gbs
+        return e
+
+    # config 1: 64x64 frame, 32^2 BC1, uniform 4x — launch-latency bound
+    t1 = ctf.Texture.bc1(synthetic.bc1_texture(32, 32, seed, "image"), 32, 32, device=dev)
+    uv, g = synthetic.rotated_quad(64, 64, 32, 32, 4.0, 30.0)
+    uv, g = torch.from_numpy(uv).to(dev), torch.from_numpy(g).to(dev)
+    ms, st, _ = run(t1, uv, g, 3, 3, 200)
+    res["1_64x64_bc1_m4"] = dict(entry(64, 64, ms, st), us_per_launch=ms * 1e3)
+
+    # config 2: 1080p, 2048^2 BC1, perspective plane (m ~0.9-9.4, mean 4.3)
+    t2 = ctf.Texture.bc1(synthetic.bc1_texture(2048, 2048, seed, "image"), 2048, 2048, device=dev)
+    uv, g = synthetic.perspective_plane_torch(1920, 1080, 2048, 2048, synthetic.PLANE_C2, device=dev)
+    ms, st, _ = run(t2, uv, g, 3, 3, 50)
+    res["2_1080p_bc1_collab_cplus"] = entry(1920, 1080, ms, st, 1920 * 1080 * 32)
+
+    # config 3: 4K, 4096^2 latent-MLP texture, COLLAB vs 4-tap (FP32-pipe bound)
+    t3 = ctf.Texture.latent_mlp(synthetic.latent_texture(4096, 4096, seed), synthetic.mlp_weights(seed + 1),
+                                4096, 4096, device=dev)
+    uv, g = synthetic.perspective_plane_torch(3840, 2160, 4096, 4096, synthetic.PLANE_C2, device=dev)
+    for name, mode in (("collab_cplus", 3), ("4tap", 0)):
+        ms, st, out = run(t3, uv, g, mode, 3, 3)
+        e = entry(3840, 2160, ms, st)
+        fl = st["texel_evals"] * MLP_FMA_PER_EVAL * 2
+        e["mlp_tflops"] = fl / (ms / 1e3) / 1e12
+        e["fp32_frac"] = e["mlp_tflops"] / fp32_peak_tflops
+        res[f"3_4k_latent_mlp_{name}"] = e
+        if mode == 3:
+            collab_out = out
+        else:
+            d = (collab_out.double() - out.double())
+            res["3_4k_latent_mlp_collab_cplus"]["max_abs_err_vs_4tap"] = float(d.abs().max())
+    # config 4: 4K, 4096^2 BC1, grazing plane (horizon, minified waves), every fallback
+    t4 = ctf.Texture.bc1(synthetic.bc1_texture(4096, 4096, seed, "image"), 4096, 4096, device=dev)
+    uv, g = synthetic.perspective_plane_torch(3840, 2160, 4096, 4096, synthetic.PLANE_C4, device=dev)
+    _, _, ref = run(t4, uv, g, 0, 0, 1)
+    ref = ref.clone()
+    for name, fb in FALLBACKS.items():
+        ms, st, out = run(t4, uv, g, 3, fb, 10)
+        e = entry(3840, 2160, ms, st, 3840 * 2160 * 32)
+        e["fallback_wave_frac"] = st["waves_fallback"] / max(1, st["waves_live"])
+        cov = ~torch.isnan(uv[..., 0])
+        err = (out - ref)[cov].double()
+        mse = float((err * err).mean())
+        e["psnr_vs_bilinear_db"] = 10 * float(np.log10(1.0 / mse)) if mse > 0 else float("inf")
+        res[f"4_4k_mixed_bc1_collab_{name}"] = e
+    return res
+
+
 # ----------------------------------------------------------------------------- our arm
 def main():
     args = parse_args()
@@ -224,15 +292,16 @@ def main():
         return run_reference(args)
 
     import torch
-    import torch.distributed as dist
+    import torch.distributed as tdist
 
     import synthetic
     from paper_2506_17770_b200 import build as pbuild
+    from paper_2506_17770_b200 import dist as cdist
     import paper_2506_17770_b200.ctf as ctf
 
     ws, rank, local = dist_env()
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     pbuild.build()
@@ -240,16 +309,16 @@ def main():
 
     F, Wf, Hf, T = args.frames, args.width, args.height, args.tex
     mode, fb = MODES[args.mode], FALLBACKS[args.fallback]
-    blocks = make_texture(args)
+    blocks = synthetic.bc1_texture(T, T, args.seed, "image")
     tex = ctf.Texture.bc1(blocks, T, T, device=dev)
-    frame_base = rank * F
+    path_frames, frame_base = cdist.weak_frames(F, rank)
     uv = torch.empty((F, Hf, Wf, 2), dtype=torch.float32, device=dev)
     grad = None if args.no_grad else torch.empty((F, Hf, Wf, 4), dtype=torch.float16, device=dev)
-    for f in range(F):
-        u, g = synthetic.camera_path_frame_torch((frame_base + f) % 64, Wf, Hf, T, T, device=dev)
-        uv[f].copy_(u)
+    for i, f in enumerate(path_frames):
+        u, g = synthetic.camera_path_frame_torch(f, Wf, Hf, T, T, device=dev)
+        uv[i].copy_(u)
         if grad is not None:
-            grad[f].copy_(g)
+            grad[i].copy_(g)
         del u, g
     out = torch.empty((F, Hf, Wf, 4), dtype=torch.float32, device=dev)
     nwy, nwx = (Hf + 3) // 4, (Wf + 7) // 8
@@ -274,7 +343,7 @@ def main():
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if ws > 1:
-        dist.barrier()
+        tdist.barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -286,57 +355,37 @@ def main():
     t1.record(stream)
     torch.cuda.synchronize()
     if ws > 1:
-        dist.barrier()
+        tdist.barrier()
     clk = clocks.stop()
-    elapsed_ms = t0.elapsed_time(t1)
+    elapsed_ms = cdist.max_over_ranks(t0.elapsed_time(t1), device=dev)
     kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    if ws > 1:
-        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / args.steps
-    pixels_per_step = ws * F * Wf * Hf
-    value = pixels_per_step / (ms_per_step / 1e3) / 1e9
+    value = ws * F * Wf * Hf / (ms_per_step / 1e3) / 1e9
 
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / mean launch time
     nwaves = nwy * nwx
     bytes_per_launch = F * (Wf * Hf * (8 + (0 if grad is None else 8) + 16) + nwaves * 4)
     k_ms = statistics.mean(kernel_ms)
     achieved = bytes_per_launch / (k_ms / 1e3) / 1e9
-    peak, peak_src = measured_peaks()
+    peak, sm_mhz, peak_src = measured_peaks()
     traffic = ncu_traffic(F, Wf, Hf)
 
-    # quality + statistics (off the timed path): 4-tap reference, ctf_stats, NCCL gather
+    # quality + statistics (off the timed path): 4-tap reference, ctf_stats, NCCL all_gather
     ref = torch.empty_like(out)
-    out2 = torch.empty_like(out)
-    ctf.filter_batch(tex, uv, grad, mode, fb, 0, args.seed, frame_base, out=out2, rec=rec, stream=stream)
-    ctf.filter_batch(tex, uv, grad, 0, 0, 0, args.seed, frame_base, out=ref, rec=torch.empty_like(rec),
-                     stream=stream)
-    st = ctf.stats(rec, Wf, Hf, F, out2, ref, stream=stream)
-    del ref, out2
-    keys = ["waves_live", "waves_exact", "waves_fallback", "waves_magnified", "pixels_active",
-            "pixels_in_magnified_waves", "texel_evals", "texel_evals_in_magnified_waves", "err_pixels"]
-    vec = torch.tensor([st[k] for k in keys], dtype=torch.float64, device=dev)
-    fvec = torch.tensor([st["sum_sq_err"], st["max_abs_err"]], dtype=torch.float64, device=dev)
-    if ws > 1:
-        gv = [torch.zeros_like(vec) for _ in range(ws)]
-        gf = [torch.zeros_like(fvec) for _ in range(ws)]
-        dist.all_gather(gv, vec)
-        dist.all_gather(gf, fvec)
-        vec = torch.stack(gv).sum(0)     # rank order: deterministic
-        ssum = sum(float(x[0]) for x in gf)
-        smax = max(float(x[1]) for x in gf)
-    else:
-        ssum, smax = float(fvec[0]), float(fvec[1])
-    tot = dict(zip(keys, [int(x) for x in vec.tolist()]))
-    mse = ssum / max(1, 4 * tot["pixels_active"])
+    ctf.filter_batch(tex, uv, grad, 0, 0, 0, args.seed, frame_base, out=ref, rec=torch.empty_like(rec), stream=stream)
+    st = ctf.stats(rec, Wf, Hf, F, out, ref, stream=stream)
+    del ref
+    tot = cdist.reduce_stats(st, device=dev)
+    mse = tot["sum_sq_err"] / max(1, 4 * tot["pixels_active"])
     quality = {
         "texel_evals_per_px": tot["texel_evals"] / max(1, tot["pixels_active"]),
         "texel_evals_per_px_magnified_waves": tot["texel_evals_in_magnified_waves"] / max(1, tot["pixels_in_magnified_waves"]),
         "exact_wave_frac": tot["waves_exact"] / max(1, tot["waves_live"]),
         "magnified_wave_frac": tot["waves_magnified"] / max(1, tot["waves_live"]),
+        "max_unique_per_wave": tot["max_unique_per_wave"],
+        "max_evals_per_lane": tot["max_evals_per_lane"],
         "psnr_vs_bilinear_db": (10.0 * np.log10(1.0 / mse)) if mse > 0 else float("inf"),
-        "max_abs_err_vs_bilinear": smax,
+        "max_abs_err_vs_bilinear": tot["max_abs_err"],
     }
 
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
@@ -350,7 +399,7 @@ def main():
         pipe = ctf.HostPipeline(Wf, Hf, max(1, E // 4), grad is not None, device=dev)
         pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream)  # warm
         if ws > 1:
-            dist.barrier()
+            tdist.barrier()
         torch.cuda.synchronize()
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
@@ -359,16 +408,16 @@ def main():
             pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream)
         a1.record(stream)
         torch.cuda.synchronize()
-        e_ms = a0.elapsed_time(a1) / args.e2e_steps
-        if ws > 1:
-            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+        e_ms = cdist.max_over_ranks(a0.elapsed_time(a1) / args.e2e_steps, device=dev)
         e2e = {"value": ws * E * Wf * Hf / (e_ms / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": E * Wf * Hf * (8 + (0 if grad is None else 8)),
                "d2h_bytes_per_step": E * (Wf * Hf * 16 + nwaves * 4), "frames_per_step": E,
                "ms_per_step": e_ms, "api": "ctf_filter_frames_host (pinned host buffers)"}
         del uv_h, g_h, out_h, rec_h, pipe
+
+    configs = None
+    if rank == 0 and ws == 1 and not args.no_configs:
+        configs = other_configs(ctf, torch, dev, stream, args.seed, peak, sm_mhz)
 
     # CPU oracle baseline on a bounded sample (rank 0, N = 1 only)
     cpu = None
@@ -376,12 +425,20 @@ def main():
         os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
         import oracle
         oracle.build_oracle()
-        sample = []
-        for f in (0, 16, 32, 48, 8, 24, 40, 56):
-            sample.append((f, uv[f].cpu().numpy(), None if grad is None else grad[f].cpu().numpy()))
-        px, secs, nfr = oracle_sample(blocks, T, sample, mode, fb, args.seed, frame_base, args.cpu_seconds)
+        otex = {"format": 1, "width": T, "height": T, "bc1": blocks}
+        px, secs, nfr = 0, 0.0, 0
+        order = list(range(0, F, 8)) + [f for f in range(F) if f % 8]
+        while secs < args.cpu_seconds and nfr < 4 * F:
+            i = order[nfr % F]
+            u_np = uv[i].cpu().numpy()
+            g_np = None if grad is None else grad[i].cpu().numpy()
+            c0 = time.perf_counter()
+            oracle.filter_frame(otex, u_np, g_np, mode, fb, 0, args.seed, frame_base + i, debug=False)
+            secs += time.perf_counter() - c0
+            px += Wf * Hf
+            nfr += 1
         cpu = {"value": px / secs / 1e9, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
-               "sample": f"{nfr} full 4K frames of the batch (frames 0,16,32,...), {secs:.1f} s"}
+               "sample": f"{nfr} full 4K frames of the batch (every 8th first), {secs:.1f} s of oracle time"}
 
     if rank == 0:
         line = {
@@ -402,10 +459,11 @@ def main():
             "e2e": e2e,
             "gpu_launches": args.steps,
             "clocks": clk,
+            "configs": configs,
         }
         print(json.dumps(line))
     if ws > 1:
-        dist.destroy_process_group()
+        tdist.destroy_process_group()
     return 0
 
 

@@ -67,6 +67,10 @@ typedef struct {
                                 LATENT_MLP: fp16 latents [(H/4)][(W/4)][8].                 */
     const float *mlp_dev;    /* LATENT_MLP: 1604 fp32 = W1[32][12] b1[32] W2[32][32] b2[32]
                                 W3[4][32] b3[4]; NULL for BC1.                               */
+    const float *mlp_host;   /* LATENT_MLP, optional: HOST copy of the same 1604 weights.  The
+                                kernel receives the weights by value in its parameter block
+                                (constant bank); without this copy every launch first copies
+                                them from mlp_dev synchronously.  NULL for BC1.              */
 } ctf_texture;
 
 /* Filter modes (P:606-609 naming: method + fallback in parentheses). */

@@ -44,6 +44,7 @@ ctf::LaunchArgs make_args(const ctf_texture *tex, const float *uv, const uint16_
     a.H = tex->height;
     a.tex_data = tex->data_dev;
     a.mlp = tex->mlp_dev;
+    a.mlp_host = tex->mlp_host;
     a.uv = uv;
     a.grad = grad;
     a.Wf = Wf;

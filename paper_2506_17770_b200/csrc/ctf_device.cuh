@@ -92,8 +92,18 @@ struct TexArgs {
     int W, H;
     const uint2 *bc1;       // BC1 blocks
     const uint4 *latent;    // 8 x fp16 per latent texel
-    const float *mlp;       // packed weights (global)
 };
+
+constexpr int kMlpWeights = 32 * 12 + 32 + 32 * 32 + 32 + 4 * 32 + 4;  // 1604 (R-10)
+// Latent-MLP weights travel BY VALUE in the kernel parameter block (constant bank 0):
+// every lane reads the same weight at the same time, so FFMA takes it straight from
+// the constant cache with no load instruction.  BC1 kernels get an empty struct.
+struct MlpWeights {
+    float v[kMlpWeights];
+};
+struct NoWeights {};
+template <int FMT> struct WeightsOf { using type = NoWeights; };
+template <> struct WeightsOf<2> { using type = MlpWeights; };
 
 // Synthetic BC1-style decode of texel (x, y) (R-9).  Integer only and branch-free.
 // Both endpoints are expanded at once in 16-bit lanes (e0 low, e1 high); the palette
@@ -148,8 +158,9 @@ __device__ __forceinline__ void rgba8_to_float(uint32_t v, float (&c)[4]) {
 }
 
 // Latent + MLP decode (R-10; NTC-style inference-on-sample).  fp32 FFMA.
-// `w` points at the packed weights staged in shared memory.
-__device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const float *__restrict__ w, int x, int y) {
+// Weights are read from the kernel parameter block with compile-time offsets.
+__device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const MlpWeights &wt, int x, int y) {
+    const float *w = wt.v;
     const int lw = t.W >> 2, lh = t.H >> 2;
     // sample point ((x-1.5)/4, (y-1.5)/4): integer part and phase in eighths (exact weights)
     const int gx8 = 2 * x - 3, gy8 = 2 * y - 3;                 // 8 * position
@@ -213,11 +224,10 @@ __device__ __forceinline__ void Texel<FMT_BC1>::expand_biased(float (&c)[4]) con
     c[3] = f16_add_f32((unsigned short)(ba >> 16), 0.0f);
 }
 
-template <int FMT> __device__ __forceinline__ Texel<FMT> produce(const TexArgs &t, const float *w, uint32_t x, uint32_t y);
-template <> __device__ __forceinline__ Texel<FMT_BC1> produce<FMT_BC1>(const TexArgs &t, const float *, uint32_t x, uint32_t y) {
+__device__ __forceinline__ Texel<FMT_BC1> produce(const TexArgs &t, const NoWeights &, uint32_t x, uint32_t y) {
     return {bc1_decode(t, (int)x, (int)y)};
 }
-template <> __device__ __forceinline__ Texel<FMT_MLP> produce<FMT_MLP>(const TexArgs &t, const float *w, uint32_t x, uint32_t y) {
+__device__ __forceinline__ Texel<FMT_MLP> produce(const TexArgs &t, const MlpWeights &w, uint32_t x, uint32_t y) {
     return {mlp_decode(t, w, (int)x, (int)y)};
 }
 

@@ -20,6 +20,7 @@
 //   a8 per-wave record
 #include <climits>
 #include <cmath>
+#include <cstring>
 
 #include "ctf_device.cuh"
 #include "ctf_internal.h"
@@ -405,9 +406,9 @@ __device__ __forceinline__ int cplus_pick(const Foot &g, float u2, Planned plann
 }
 
 template <int FMT>
-__device__ __noinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bool active, unsigned A, int na,
-                                           int px, int py, uint32_t frame, const KArgs &a, const float *mlpw,
-                                           WarpSmem &s) {
+__device__ __forceinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bool active, unsigned A, int na,
+                                              int px, int py, uint32_t frame, const KArgs &a,
+                                              const typename WeightsOf<FMT>::type &mw, WarpSmem &s) {
     const unsigned lane = lane_id();
     const unsigned lt = lanemask_lt();
     const int W = a.tex.W;
@@ -422,7 +423,7 @@ __device__ __noinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bo
         o.evals = na;
         if (active) {
             o.prod = corner_id(f, ksel, W);
-            val = produce<FMT>(a.tex, mlpw, corner_x(f, ksel), corner_y(f, ksel));
+            val = produce(a.tex, mw, corner_x(f, ksel), corner_y(f, ksel));
             o.color = scaled<FMT>(val);
         }
         return o;
@@ -431,7 +432,7 @@ __device__ __noinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bo
         o.evals = na;
         if (active) {
             o.prod = corner_id(f, ksel, W);
-            val = produce<FMT>(a.tex, mlpw, corner_x(f, ksel), corner_y(f, ksel));
+            val = produce(a.tex, mw, corner_x(f, ksel), corner_y(f, ksel));
         }
         if (b.fits)
             o.color = gather_mask<FMT>(f, b, active, true, box_t(b, corner_x(f, ksel), corner_y(f, ksel)), val,
@@ -505,7 +506,7 @@ __device__ __noinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bo
         }
     }
     if (produced) {
-        val = produce<FMT>(a.tex, mlpw, qx, qy);
+        val = produce(a.tex, mw, qx, qy);
         o.prod = (uint32_t)(qy * W + qx);
     }
     __syncwarp();
@@ -516,6 +517,22 @@ __device__ __noinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bo
     else
         o.color = gather_sorted<FMT>(f, active, o.prod, val, false, s, W);
     return o;
+}
+
+// BC1: keep the rarely taken fallback out of line (smaller hot loop); the latent-MLP
+// variant stays inline so its weights remain kernel-parameter (constant-bank) operands.
+static __device__ __noinline__ FbOut run_fallback_bc1(int fb, const Foot f, const Box b, bool active, unsigned A,
+                                                      int na, int px, int py, uint32_t frame, const KArgs &a,
+                                                      WarpSmem &s) {
+    return run_fallback<FMT_BC1>(fb, f, b, active, A, na, px, py, frame, a, NoWeights{}, s);
+}
+
+template <int FMT>
+__device__ __forceinline__ FbOut fallback(int fb, const Foot &f, const Box &b, bool active, unsigned A, int na, int px,
+                                          int py, uint32_t frame, const KArgs &a,
+                                          const typename WeightsOf<FMT>::type &mw, WarpSmem &s) {
+    if constexpr (FMT == FMT_BC1) return run_fallback_bc1(fb, f, b, active, A, na, px, py, frame, a, s);
+    else return run_fallback<FMT>(fb, f, b, active, A, na, px, py, frame, a, mw, s);
 }
 
 // --------------------------------------------------------------- exact collect
@@ -584,13 +601,9 @@ static __device__ __noinline__ Collected collect_sort(const Foot f, bool active,
 constexpr int kChunk = 16;  // waves per work item: a run of consecutive waves in one wave-row
 
 template <int FMT, int MODE, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_filter_kernel(const KArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1))
+    ctf_filter_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ WarpSmem smem[kWarps];
-    __shared__ __align__(16) float mlpw[FMT == FMT_MLP ? kMlpParams : 4];
-    if constexpr (FMT == FMT_MLP) {
-        for (int i = threadIdx.x; i < kMlpParams; i += blockDim.x) mlpw[i] = __ldg(a.tex.mlp + i);
-        __syncthreads();
-    }
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     WarpSmem &s = smem[warp];
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
@@ -666,20 +679,37 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
             if constexpr (MODE == MODE_4TAP) {
                 rec = rec_base | (0xFFu << 8) | ((uint32_t)PATH_4TAP << 22) | (uint32_t)((4 * na) & 0xFF);
                 if (active) {
-                    Texel<FMT> p[4];
-                    p[0] = produce<FMT>(a.tex, mlpw, f.xa, f.ya);
-                    p[1] = produce<FMT>(a.tex, mlpw, f.xb, f.ya);
-                    p[2] = produce<FMT>(a.tex, mlpw, f.xa, f.yb);
-                    p[3] = produce<FMT>(a.tex, mlpw, f.xb, f.yb);
-                    color = blend4<FMT>(p, f.w);
+                    if constexpr (FMT == FMT_BC1) {
+                        Texel<FMT> p[4];
+                        p[0] = produce(a.tex, mw, f.xa, f.ya);
+                        p[1] = produce(a.tex, mw, f.xb, f.ya);
+                        p[2] = produce(a.tex, mw, f.xa, f.yb);
+                        p[3] = produce(a.tex, mw, f.xb, f.yb);
+                        color = blend4<FMT>(p, f.w);
+                    } else {
+                        // one decode at a time (no interleaving of four MLPs); same op order as blend4
+                        float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+                        for (int k = 0; k < 4; ++k) {
+                            const float4 v = produce(a.tex, mw, corner_x(f, k), corner_y(f, k)).v;
+                            const float wk = (k == 0 ? f.w[0] : k == 1 ? f.w[1] : k == 2 ? f.w[2] : f.w[3]);
+                            if (k == 0) {
+                                c[0] = wk * v.x; c[1] = wk * v.y; c[2] = wk * v.z; c[3] = wk * v.w;
+                            } else {
+                                c[0] = fmaf(wk, v.x, c[0]); c[1] = fmaf(wk, v.y, c[1]);
+                                c[2] = fmaf(wk, v.z, c[2]); c[3] = fmaf(wk, v.w, c[3]);
+                            }
+                        }
+                        color = make_float4(c[0], c[1], c[2], c[3]);
+                    }
                 }
             } else if constexpr (MODE == MODE_STF || MODE == MODE_WC) {
                 Box b;
                 b.fits = false;
                 b.K = 0;
                 if constexpr (MODE == MODE_WC) b = wave_box(f, active);
-                const FbOut o = run_fallback<FMT>(MODE == MODE_STF ? FB_STF : FB_WC, f, b, active, A, na, px, py,
-                                                  frame, a, mlpw, s);
+                const FbOut o = fallback<FMT>(MODE == MODE_STF ? FB_STF : FB_WC, f, b, active, A, na, px, py,
+                                              frame, a, mw, s);
                 color = o.color;
                 prod = o.prod;
                 selbits = o.selbits;
@@ -716,7 +746,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
                         int qx, qy;
                         if (b.fits) { qx = box_x(b, e); qy = box_y(b, e); }
                         else { qx = (int)(e & 0xffffu); qy = (int)(e >> 16); }
-                        val = produce<FMT>(a.tex, mlpw, qx, qy);
+                        val = produce(a.tex, mw, qx, qy);
                         if (DBG) prod = (uint32_t)(qy * a.tex.W + qx);
                     }
                     // ---- a6: gather from lanes h(rho_k, A) and blend
@@ -743,7 +773,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
                         if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
                     }
                 } else {
-                    const FbOut o = run_fallback<FMT>(a.fallback, f, b, active, A, na, px, py, frame, a, mlpw, s);
+                    const FbOut o = fallback<FMT>(a.fallback, f, b, active, A, na, px, py, frame, a, mw, s);
                     color = o.color;
                     prod = o.prod;
                     selbits = o.selbits;
@@ -766,7 +796,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1)) ctf_fil
 }
 
 template <int FMT, int MODE, bool DBG>
-static cudaError_t launch_one(KArgs k, cudaStream_t stream) {
+static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
     auto kern = ctf_filter_kernel<FMT, MODE, DBG>;
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -779,22 +809,23 @@ static cudaError_t launch_one(KArgs k, cudaStream_t stream) {
     long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kWarps * 32, 0, stream>>>(k);
+    kern<<<(unsigned)grid, kWarps * 32, 0, stream>>>(k, mw);
     return cudaGetLastError();
 }
 
 template <int FMT, int MODE>
-static cudaError_t launch_dbg(const KArgs &k, cudaStream_t stream) {
-    return (k.flags & FLAG_DEBUG) ? launch_one<FMT, MODE, true>(k, stream) : launch_one<FMT, MODE, false>(k, stream);
+static cudaError_t launch_dbg(const KArgs &k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
+    return (k.flags & FLAG_DEBUG) ? launch_one<FMT, MODE, true>(k, mw, stream)
+                                  : launch_one<FMT, MODE, false>(k, mw, stream);
 }
 
 template <int FMT>
-static cudaError_t launch_fmt(const KArgs &k, int mode, cudaStream_t stream) {
+static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::type &mw, int mode, cudaStream_t stream) {
     switch (mode) {
-    case MODE_4TAP: return launch_dbg<FMT, MODE_4TAP>(k, stream);
-    case MODE_STF: return launch_dbg<FMT, MODE_STF>(k, stream);
-    case MODE_WC: return launch_dbg<FMT, MODE_WC>(k, stream);
-    default: return launch_dbg<FMT, MODE_COLLAB>(k, stream);
+    case MODE_4TAP: return launch_dbg<FMT, MODE_4TAP>(k, mw, stream);
+    case MODE_STF: return launch_dbg<FMT, MODE_STF>(k, mw, stream);
+    case MODE_WC: return launch_dbg<FMT, MODE_WC>(k, mw, stream);
+    default: return launch_dbg<FMT, MODE_COLLAB>(k, mw, stream);
     }
 }
 
@@ -811,7 +842,6 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.tex.H = a.H;
     k.tex.bc1 = reinterpret_cast<const uint2 *>(a.tex_data);
     k.tex.latent = reinterpret_cast<const uint4 *>(a.tex_data);
-    k.tex.mlp = a.mlp;
     k.uv = reinterpret_cast<const float2 *>(a.uv);
     k.grad = reinterpret_cast<const uint2 *>(a.grad);
     k.out = reinterpret_cast<float4 *>(a.out);
@@ -836,9 +866,19 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.seed_lo = (uint32_t)a.seed;
     k.seed_hi = (uint32_t)(a.seed >> 32);
 #if CTF_TU_FMT == 1
-    return launch_fmt<FMT_BC1>(k, a.mode, stream);
+    return launch_fmt<FMT_BC1>(k, NoWeights{}, a.mode, stream);
 #else
-    return launch_fmt<FMT_MLP>(k, a.mode, stream);
+    // weights by value: from the caller's host copy, else one synchronous copy from the device
+    static_assert(sizeof(MlpWeights) == sizeof(float) * kMlpParams, "weight layout");
+    MlpWeights mw;
+    if (a.mlp_host) {
+        memcpy(mw.v, a.mlp_host, sizeof(mw.v));
+    } else {
+        cudaError_t e = cudaMemcpyAsync(mw.v, a.mlp, sizeof(mw.v), cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) return e;
+    }
+    return launch_fmt<FMT_MLP>(k, mw, a.mode, stream);
 #endif
 }
 

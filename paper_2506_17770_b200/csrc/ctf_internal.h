@@ -13,7 +13,8 @@ struct LaunchArgs {
     // texture
     int fmt, W, H;
     const void *tex_data;   // BC1 blocks or fp16 latents
-    const float *mlp;
+    const float *mlp;       // device copy of the MLP weights
+    const float *mlp_host;  // optional host copy (passed by value to the kernel)
     // frames
     const float *uv;        // [frames][Hf][Wf][2]
     const uint16_t *grad;   // [frames][Hf][Wf][4] fp16 bits or nullptr

@@ -31,7 +31,8 @@ class CtfError(RuntimeError):
 
 class ctf_texture(ctypes.Structure):
     _fields_ = [("format", ctypes.c_int32), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
-                ("addr", ctypes.c_int32), ("data_dev", ctypes.c_void_p), ("mlp_dev", ctypes.c_void_p)]
+                ("addr", ctypes.c_int32), ("data_dev", ctypes.c_void_p), ("mlp_dev", ctypes.c_void_p),
+                ("mlp_host", ctypes.c_void_p)]
 
 
 class ctf_params(ctypes.Structure):
@@ -118,7 +119,10 @@ class Texture:
     def __init__(self, fmt: int, width: int, height: int, data: torch.Tensor, mlp: torch.Tensor | None = None):
         self.fmt, self.width, self.height = fmt, width, height
         self.data, self.mlp = data, mlp
-        self.desc = ctf_texture(fmt, width, height, 0, data.data_ptr(), mlp.data_ptr() if mlp is not None else None)
+        # host copy of the MLP weights: passed by value into the kernel parameter block
+        self.mlp_host = mlp.detach().cpu().contiguous() if mlp is not None else None
+        self.desc = ctf_texture(fmt, width, height, 0, data.data_ptr(), mlp.data_ptr() if mlp is not None else None,
+                                self.mlp_host.data_ptr() if self.mlp_host is not None else None)
 
     @staticmethod
     def bc1(blocks, width: int, height: int, device="cuda") -> "Texture":

@@ -58,7 +58,7 @@ def test_validation_errors_without_gpu():
     """Host-side validation runs before any CUDA call, so it is testable on CPU."""
     import paper_2506_17770_b200.ctf as c
     lib = c.load_library()
-    tex = c.ctf_texture(1, 32, 32, 0, 0x1000, None)
+    tex = c.ctf_texture(1, 32, 32, 0, 0x1000, None, None)
     p = c.ctf_params(3, 3, 0, 0, 0)
     V = ctypes.c_void_p
     # null uv
