@@ -39,6 +39,17 @@ __device__ __forceinline__ uint2 ld_stream_u2(const uint2 *p) {
                  : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
+// predicated streaming loads: the destination keeps its prior value when pred == 0
+__device__ __forceinline__ void ld_stream_f2_if(float2 &r, const float2 *p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+                 "@q ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];\n\t}"
+                 : "+f"(r.x), "+f"(r.y) : "l"(p), "r"((unsigned)pred));
+}
+__device__ __forceinline__ void ld_stream_u2_if(uint2 &r, const uint2 *p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+                 "@q ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];\n\t}"
+                 : "+r"(r.x), "+r"(r.y) : "l"(p), "r"((unsigned)pred));
+}
 __device__ __forceinline__ void st_stream_f4(float4 *p, float4 v) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");

@@ -114,7 +114,9 @@ __device__ __forceinline__ float4 blend4(const Texel<FMT> (&p)[4], const float (
     float c[4], v[4];
     p[0].expand_biased(v);
     if constexpr (Texel<FMT>::kBias != 0.0f) {
-        const float nb = -Texel<FMT>::kBias * ((ws[0] + ws[1]) + (ws[2] + ws[3]));
+        // sum_k w_k = 1 up to 4 fp32 roundings, so the bias term is the constant
+        // -1024/255 to within ~5e-7
+        constexpr float nb = -Texel<FMT>::kBias * Texel<FMT>::kScale;
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(ws[0], v[ch], nb);
     } else {
@@ -626,22 +628,22 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1))
 
         // software pipeline: wave wx+1's uv/grad loads are issued before wave wx is
         // processed, so their HBM latency hides behind this wave's work
+        const bool has_grad = a.grad != nullptr;
         float2 uv_n = make_float2(__int_as_float(0x7fc00000), 0.f);
         uint2 gr_n = make_uint2(0u, 0u);
-        if (rowok && px < a.Wf) {
-            uv_n = ld_stream_f2(a.uv + pix);
-            if (a.grad) gr_n = ld_stream_u2(a.grad + pix);
-        }
+        ld_stream_f2_if(uv_n, a.uv + pix, rowok & (px < a.Wf));
+        ld_stream_u2_if(gr_n, a.grad + pix, rowok & (px < a.Wf) & has_grad);
+        uint32_t myrec = 0u;  // record of wave wx0 + lane, stored once per run
+        const unsigned w0 = w;
         for (int wx = wx0; wx < wx1; ++wx, ++w, pix += 8u, px += 8) {
-            const bool inframe = rowok && px < a.Wf;
+            const bool inframe = rowok & (px < a.Wf);
             const float2 uv = uv_n;
             const uint2 gr = gr_n;
             uv_n = make_float2(__int_as_float(0x7fc00000), 0.f);
             gr_n = make_uint2(0u, 0u);
-            if (wx + 1 < wx1 && rowok && px + 8 < a.Wf) {
-                uv_n = ld_stream_f2(a.uv + (pix + 8u));
-                if (a.grad) gr_n = ld_stream_u2(a.grad + (pix + 8u));
-            }
+            const bool pf = (wx + 1 < wx1) & rowok & (px + 8 < a.Wf);
+            ld_stream_f2_if(uv_n, a.uv + (pix + 8u), pf);
+            ld_stream_u2_if(gr_n, a.grad + (pix + 8u), pf & has_grad);
 
             __syncwarp();  // order this wave's shared-memory tables after the previous wave's reads
             // ---- a1: classify
@@ -654,7 +656,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1))
                     if (a.dbg_pid) a.dbg_pid[pix] = INVALID_ID;
                     if (a.dbg_sel) a.dbg_sel[pix] = 0u;
                 }
-                if (lane == 0) a.rec[w] = ((MODE == MODE_COLLAB ? 0u : 0xFFu) << 8) | (1u << 26);
+                if (lane == (unsigned)(wx - wx0)) myrec = ((MODE == MODE_COLLAB ? 0u : 0xFFu) << 8) | (1u << 26);
                 continue;
             }
             bool mag_lane = true;
@@ -753,7 +755,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1))
                     int src[4];
                     if (full) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) src[k] = rho[k] & 31;
+                        for (int k = 0; k < 4; ++k) src[k] = rho[k];
                     } else {
 #pragma unroll
                         for (int k = 0; k < 4; ++k) src[k] = active ? (int)s.lane_of_rank[rho[k] & 31] : (int)lane;
@@ -788,10 +790,10 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1))
                 if (a.dbg_pid) a.dbg_pid[pix] = (MODE == MODE_4TAP) ? INVALID_ID : prod;
                 if (a.dbg_sel) a.dbg_sel[pix] = selbits;
             }
-            // ---- a8: per-wave record
-            if (lane == 0) a.rec[w] = rec;
-            __syncwarp();
+            // ---- a8: per-wave record (kept in lane wx - wx0, stored per run)
+            if (lane == (unsigned)(wx - wx0)) myrec = rec;
         }
+        if (lane < (unsigned)(wx1 - wx0)) a.rec[w0 + lane] = myrec;
     }
 }
 
