@@ -198,30 +198,31 @@ __device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const MlpWeights 
     in[10] = ((x >> 2) & 1) ? 0.5f : -0.5f;
     in[11] = ((y >> 2) & 1) ? 0.5f : -0.5f;
     const float *W1 = w, *b1 = W1 + 32 * 12, *W2 = b1 + 32, *b2 = W2 + 32 * 32, *W3 = b2 + 32, *b3 = W3 + 4 * 32;
-    float h1[32];
+    // Outer-product order keeps ~50 values live instead of ~100: each hidden unit k of
+    // layer 1 is formed and immediately scattered into the 32 layer-2 accumulators;
+    // then each layer-2 unit feeds the 4 outputs.  Same 1536 FMAs, weights read from
+    // the constant bank (kernel parameters).
+    float acc2[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc2[j] = b2[j];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        float h = b1[k];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) h = fmaf(W1[k * 12 + i], in[i], h);
+        h = fmaxf(h, 0.f);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc2[j] = fmaf(W2[j * 32 + k], h, acc2[j]);
+    }
+    float o[4] = {b3[0], b3[1], b3[2], b3[3]};
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-        float acc = b1[j];
+        const float h = fmaxf(acc2[j], 0.f);
 #pragma unroll
-        for (int k = 0; k < 12; ++k) acc = fmaf(W1[j * 12 + k], in[k], acc);
-        h1[j] = fmaxf(acc, 0.f);
+        for (int c = 0; c < 4; ++c) o[c] = fmaf(W3[c * 32 + j], h, o[c]);
     }
-    float h2[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        float acc = b2[j];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) acc = fmaf(W2[j * 32 + k], h1[k], acc);
-        h2[j] = fmaxf(acc, 0.f);
-    }
-    float o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        float acc = b3[j];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) acc = fmaf(W3[j * 32 + k], h2[k], acc);
-        o[j] = fminf(fmaxf(acc, 0.f), 1.f);
-    }
+    for (int c = 0; c < 4; ++c) o[c] = fminf(fmaxf(o[c], 0.f), 1.f);
     return make_float4(o[0], o[1], o[2], o[3]);
 }
 

@@ -371,11 +371,16 @@ __device__ __forceinline__ float4 gather_mask(const Foot &f, const Box &b, bool 
 }
 
 // ------------------------------------------------------------------ fallbacks
-struct FbOut {
-    float4 color;
-    uint32_t prod;     // texel id produced by this lane (or INVALID)
+// A fallback runs in two phases around the kernel's single texel-production site:
+//   fb_plan   decides which texel (if any) this lane produces (STF choice, C+ plan
+//             and Eq. 2 spare-lane picks), and
+//   fb_finish gathers the produced values of the wave and combines them (Eq. 1 / WC),
+// so no fallback code needs the texture decoder (or the MLP weights).
+struct Plan {
+    bool produced;
+    int qx, qy;          // texel this lane produces
+    int ksel;            // STF corner of this lane's own pixel
     uint32_t selbits;
-    int evals;
 };
 
 // C+ spare lane: candidate pick from served lane l's footprint g (R-18 v): distinct
@@ -407,55 +412,32 @@ __device__ __forceinline__ int cplus_pick(const Foot &g, float u2, Planned plann
     return pick < 0 ? lastc : pick;
 }
 
-template <int FMT>
-__device__ __forceinline__ FbOut run_fallback(int fb, const Foot f, const Box b, bool active, unsigned A, int na,
-                                              int px, int py, uint32_t frame, const KArgs &a,
-                                              const typename WeightsOf<FMT>::type &mw, WarpSmem &s) {
+static __device__ __noinline__ Plan fb_plan(int fb, const Foot f, const Box b, bool active, unsigned A, int na, int px,
+                                            int py, uint32_t frame, uint32_t seed_lo, uint32_t seed_hi, int W,
+                                            WarpSmem &s) {
     const unsigned lane = lane_id();
     const unsigned lt = lanemask_lt();
-    const int W = a.tex.W;
-    FbOut o;
-    o.prod = INVALID_ID;
-    o.color = make_float4(0.f, 0.f, 0.f, 0.f);
-    const uint4 rr = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo, a.seed_hi);
-    const int ksel = stf_corner(f, rr);
-    o.selbits = active ? (uint32_t)ksel : 0u;
-    Texel<FMT> val = Texel<FMT>::zero();
-    if (fb == FB_STF) {  // one-tap STF
-        o.evals = na;
-        if (active) {
-            o.prod = corner_id(f, ksel, W);
-            val = produce(a.tex, mw, corner_x(f, ksel), corner_y(f, ksel));
-            o.color = scaled<FMT>(val);
-        }
-        return o;
-    }
-    if (fb == FB_WC || fb == FB_C) {  // every lane produces its STF texel
-        o.evals = na;
-        if (active) {
-            o.prod = corner_id(f, ksel, W);
-            val = produce(a.tex, mw, corner_x(f, ksel), corner_y(f, ksel));
-        }
-        if (b.fits)
-            o.color = gather_mask<FMT>(f, b, active, true, box_t(b, corner_x(f, ksel), corner_y(f, ksel)), val,
-                                       fb == FB_WC, s);
-        else
-            o.color = gather_sorted<FMT>(f, active, o.prod, val, fb == FB_WC, s, W);
-        return o;
-    }
-    // ---- C+ 
+    Plan pl;
+    const uint4 rr = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), seed_lo, seed_hi);
+    pl.ksel = stf_corner(f, rr);
+    pl.selbits = active ? (uint32_t)pl.ksel : 0u;
+    pl.qx = corner_x(f, pl.ksel);
+    pl.qy = corner_y(f, pl.ksel);
+    pl.produced = active;
+    if (fb != FB_CPLUS) return pl;  // STF, WC, C: every lane produces its STF texel
+
+    // ---- C+ (P:485-518): (1) planned STF texels, deduplicated and ranked ascending
+    pl.produced = false;
     const int ar = __popc(A & lt);
     if (active) s.lane_of_rank[ar] = (uint8_t)lane;
-    const int sx = corner_x(f, ksel), sy = corner_y(f, ksel);
     int np;
     WMask<4> P;
     if (b.fits) {
-        // (1) planned STF texels as a bitmask (one bit per lane)
-        P.reduce_bit(box_t(b, sx, sy), active);
+        P.reduce_bit(box_t(b, pl.qx, pl.qy), active);   // one bit per lane
         np = P.n;
         P.push(s.tbl, lane, lt);
     } else {
-        const uint32_t pid = (uint32_t)(sy * W + sx);
+        const uint32_t pid = (uint32_t)(pl.qy * W + pl.qx);
         const uint32_t sk = warp_sort32(active ? ((pid << 5) | lane) : INVALID_ID);
         const uint32_t skp = __shfl_up_sync(FULL, sk, 1);
         const bool firstp = sk != INVALID_ID && (lane == 0 || (sk >> 5) != (skp >> 5));
@@ -466,19 +448,18 @@ __device__ __forceinline__ FbOut run_fallback(int fb, const Foot f, const Box b,
     }
     __syncwarp();
     // (2) active ranks < n_p produce the planned texels; (3) the rest are spare lanes (Eq. 2)
-    bool spare = false, produced = false;
+    bool spare = false;
     int l = (int)lane;
-    int qx = 0, qy = 0;
     if (active) {
         if (ar < np) {
             const uint32_t e = s.tbl[ar];
-            if (b.fits) { qx = box_x(b, e); qy = box_y(b, e); }
-            else { qy = (int)(e / (uint32_t)W); qx = (int)(e - (uint32_t)qy * (uint32_t)W); }
-            produced = true;
+            if (b.fits) { pl.qx = box_x(b, e); pl.qy = box_y(b, e); }
+            else { pl.qy = (int)(e / (uint32_t)W); pl.qx = (int)(e - (uint32_t)pl.qy * (uint32_t)W); }
+            pl.produced = true;
         } else {
             spare = true;
             l = (int)s.lane_of_rank[eq2_lane_rank(ar, np, na)];
-            o.selbits |= (1u << 5) | ((uint32_t)l << 8);
+            pl.selbits |= (1u << 5) | ((uint32_t)l << 8);
         }
     }
     Foot g;
@@ -501,40 +482,40 @@ __device__ __forceinline__ FbOut run_fallback(int fb, const Foot f, const Box b,
             });
         }
         if (pick >= 0) {
-            qx = corner_x(g, pick);
-            qy = corner_y(g, pick);
-            produced = true;
-            o.selbits |= ((uint32_t)pick << 2) | (1u << 4);
+            pl.qx = corner_x(g, pick);
+            pl.qy = corner_y(g, pick);
+            pl.produced = true;
+            pl.selbits |= ((uint32_t)pick << 2) | (1u << 4);
         }
     }
-    if (produced) {
-        val = produce(a.tex, mw, qx, qy);
-        o.prod = (uint32_t)(qy * W + qx);
-    }
     __syncwarp();
-    o.evals = __popc(__ballot_sync(FULL, active && produced));
-    // (4) every lane filters with Eq. 1 over the produced set
-    if (b.fits)
-        o.color = gather_mask<FMT>(f, b, active, produced, box_t(b, qx, qy), val, false, s);
-    else
-        o.color = gather_sorted<FMT>(f, active, o.prod, val, false, s, W);
-    return o;
+    return pl;
 }
 
-// BC1: keep the rarely taken fallback out of line (smaller hot loop); the latent-MLP
-// variant stays inline so its weights remain kernel-parameter (constant-bank) operands.
-static __device__ __noinline__ FbOut run_fallback_bc1(int fb, const Foot f, const Box b, bool active, unsigned A,
-                                                      int na, int px, int py, uint32_t frame, const KArgs &a,
-                                                      WarpSmem &s) {
-    return run_fallback<FMT_BC1>(fb, f, b, active, A, na, px, py, frame, a, NoWeights{}, s);
-}
+struct Finished {
+    float4 color;
+    int evals;
+};
 
+// (4) every lane filters with the produced texels of the wave: one-tap (STF), the WC
+// stand-in, or Eq. 1 (C, C+)
 template <int FMT>
-__device__ __forceinline__ FbOut fallback(int fb, const Foot &f, const Box &b, bool active, unsigned A, int na, int px,
-                                          int py, uint32_t frame, const KArgs &a,
-                                          const typename WeightsOf<FMT>::type &mw, WarpSmem &s) {
-    if constexpr (FMT == FMT_BC1) return run_fallback_bc1(fb, f, b, active, A, na, px, py, frame, a, s);
-    else return run_fallback<FMT>(fb, f, b, active, A, na, px, py, frame, a, mw, s);
+static __device__ __noinline__ Finished fb_finish(int fb, const Foot f, const Box b, bool active, int na, const Plan pl,
+                                                  const Texel<FMT> val, int W, WarpSmem &s) {
+    Finished o;
+    if (fb == FB_STF) {
+        o.evals = na;
+        o.color = active ? scaled<FMT>(val) : make_float4(0.f, 0.f, 0.f, 0.f);
+        return o;
+    }
+    o.evals = (fb == FB_CPLUS) ? __popc(__ballot_sync(FULL, active && pl.produced)) : na;
+    const bool wc = fb == FB_WC;
+    if (b.fits)
+        o.color = gather_mask<FMT>(f, b, active, pl.produced, box_t(b, pl.qx, pl.qy), val, wc, s);
+    else
+        o.color = gather_sorted<FMT>(f, active, pl.produced ? (uint32_t)(pl.qy * W + pl.qx) : INVALID_ID, val, wc,
+                                     s, W);
+    return o;
 }
 
 // --------------------------------------------------------------- exact collect
@@ -603,7 +584,7 @@ static __device__ __noinline__ Collected collect_sort(const Foot f, bool active,
 constexpr int kChunk = 16;  // waves per work item: a run of consecutive waves in one wave-row
 
 template <int FMT, int MODE, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1))
+__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 2))
     ctf_filter_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ WarpSmem smem[kWarps];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -705,52 +686,63 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1))
                         color = make_float4(c[0], c[1], c[2], c[3]);
                     }
                 }
-            } else if constexpr (MODE == MODE_STF || MODE == MODE_WC) {
+            } else {
+                // ---- a3/a4 (COLLAB) or the pure STF / WC modes: decide who produces what
                 Box b;
                 b.fits = false;
                 b.K = 0;
-                if constexpr (MODE == MODE_WC) b = wave_box(f, active);
-                const FbOut o = fallback<FMT>(MODE == MODE_STF ? FB_STF : FB_WC, f, b, active, A, na, px, py,
-                                              frame, a, mw, s);
-                color = o.color;
-                prod = o.prod;
-                selbits = o.selbits;
-                rec = rec_base | (0xFFu << 8) | ((uint32_t)(MODE == MODE_STF ? PATH_STF : PATH_WC) << 22) |
-                      (uint32_t)(o.evals & 0xFF);
-            } else {
-                // ---- a3: collect the exact unique set U and canonical ranks
-                const Box b = wave_box(f, active);
-                int rho[4], n;
-                if (b.K == 1) n = collect_mask<1>(f, b, active, rho, s, lane);
-                else if (b.K == 2) n = collect_mask<2>(f, b, active, rho, s, lane);
-                else if (b.K == 4) n = collect_mask<4>(f, b, active, rho, s, lane);
-                else {
-                    const Collected cc = collect_sort(f, active, s, lane, a.tex.W);
-                    n = cc.n;
+                b.lgP = 0;
+                b.minx = b.miny = 0;
+                int rho[4] = {0, 0, 0, 0}, n = 0xFF, fb;
+                bool exact = false;
+                if constexpr (MODE == MODE_COLLAB) {
+                    // collect the exact unique set U and canonical ranks
+                    b = wave_box(f, active);
+                    if (b.K == 1) n = collect_mask<1>(f, b, active, rho, s, lane);
+                    else if (b.K == 2) n = collect_mask<2>(f, b, active, rho, s, lane);
+                    else if (b.K == 4) n = collect_mask<4>(f, b, active, rho, s, lane);
+                    else {
+                        const Collected cc = collect_sort(f, active, s, lane, a.tex.W);
+                        n = cc.n;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) rho[k] = cc.rho[k];
+                        for (int k = 0; k < 4; ++k) rho[k] = cc.rho[k];
+                    }
+                    __syncwarp();
+                    exact = n <= na && !(a.flags & FLAG_FORCE_FALLBACK);   // a4
+                    fb = a.fallback;
+                } else {
+                    fb = MODE == MODE_STF ? FB_STF : FB_WC;
+                    if constexpr (MODE == MODE_WC) b = wave_box(f, active);
                 }
-                __syncwarp();
-                // ---- a4: decide
-                if (n <= na && !(a.flags & FLAG_FORCE_FALLBACK)) {
-                    rec = rec_base | ((uint32_t)n * 0x101u);  // evals = n, path 0
-                    const bool full = A == FULL;
+                const bool full = A == FULL;
+                Plan pl;
+                if (exact) {
+                    // ---- a5: active rank r < n produces U[r] on lane h(r, A) (P:1378-1380)
                     const int ar = __popc(A & lt);
                     if (!full) {
                         if (active) s.lane_of_rank[ar] = (uint8_t)lane;
                         __syncwarp();
                     }
-                    // ---- a5: active rank r < n produces U[r] on lane h(r, A)
-                    const bool producer = active && ar < n;
-                    Texel<FMT> val = Texel<FMT>::zero();
-                    if (producer) {
+                    pl.produced = active && ar < n;
+                    pl.qx = pl.qy = 0;
+                    if (pl.produced) {
                         const uint32_t e = s.tbl[ar];
-                        int qx, qy;
-                        if (b.fits) { qx = box_x(b, e); qy = box_y(b, e); }
-                        else { qx = (int)(e & 0xffffu); qy = (int)(e >> 16); }
-                        val = produce(a.tex, mw, qx, qy);
-                        if (DBG) prod = (uint32_t)(qy * a.tex.W + qx);
+                        if (b.fits) { pl.qx = box_x(b, e); pl.qy = box_y(b, e); }
+                        else { pl.qx = (int)(e & 0xffffu); pl.qy = (int)(e >> 16); }
                     }
+                    pl.selbits = 0u;
+                } else {
+                    pl = fb_plan(fb, f, b, active, A, na, px, py, frame, a.seed_lo, a.seed_hi, a.tex.W, s);
+                }
+                selbits = pl.selbits;
+                // ---- the single texel-production site (<= 1 evaluation per lane)
+                Texel<FMT> val = Texel<FMT>::zero();
+                if (pl.produced) {
+                    val = produce(a.tex, mw, pl.qx, pl.qy);
+                    prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
+                }
+                if (exact) {
+                    rec = rec_base | ((uint32_t)n * 0x101u);  // evals = n, path 0
                     // ---- a6: gather from lanes h(rho_k, A) and blend
                     int src[4];
                     if (full) {
@@ -768,19 +760,19 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 1))
                         unsigned bad = 0;
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            const int pk = __shfl_sync(FULL, (int)producer, src[k]);  // every lane shuffles
+                            const int pk = __shfl_sync(FULL, (int)pl.produced, src[k]);  // every lane shuffles
                             bad += (active && !pk) ? 1u : 0u;
                         }
                         bad = __reduce_add_sync(FULL, bad);       // warp-uniform: no divergent atomic
                         if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
                     }
                 } else {
-                    const FbOut o = fallback<FMT>(a.fallback, f, b, active, A, na, px, py, frame, a, mw, s);
+                    // ---- a7: fallback combine
+                    const Finished o = fb_finish<FMT>(fb, f, b, active, na, pl, val, a.tex.W, s);
                     color = o.color;
-                    prod = o.prod;
-                    selbits = o.selbits;
-                    rec = rec_base | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)(PATH_FB_STF + a.fallback) << 22) |
-                          (uint32_t)(o.evals & 0xFF);
+                    const uint32_t path = MODE == MODE_COLLAB ? (uint32_t)(PATH_FB_STF + fb)
+                                                              : (uint32_t)(MODE == MODE_STF ? PATH_STF : PATH_WC);
+                    rec = rec_base | ((uint32_t)(n & 0xFF) << 8) | (path << 22) | (uint32_t)(o.evals & 0xFF);
                 }
             }
 
