@@ -66,6 +66,8 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--profile-launches", type=int, default=0,
                     help="(for ncu) run this many launches after warmup, no timing/json")
+    ap.add_argument("--profile-config3", type=int, default=0,
+                    help="(for ncu) run this many config-3 latent-MLP COLLAB launches and exit")
     return ap.parse_args()
 
 
@@ -306,6 +308,14 @@ def main():
     dev = torch.device(f"cuda:{local}")
     pbuild.build()
     ctf.load_library()
+    if args.profile_config3:
+        t3 = ctf.Texture.latent_mlp(synthetic.latent_texture(4096, 4096, args.seed),
+                                    synthetic.mlp_weights(args.seed + 1), 4096, 4096, device=dev)
+        u3, g3 = synthetic.perspective_plane_torch(3840, 2160, 4096, 4096, synthetic.PLANE_C2, device=dev)
+        for _ in range(args.profile_config3):
+            ctf.filter_frame(t3, u3, g3, 3, 3, 0, args.seed, 0)
+        torch.cuda.synchronize()
+        return 0
 
     F, Wf, Hf, T = args.frames, args.width, args.height, args.tex
     mode, fb = MODES[args.mode], FALLBACKS[args.fallback]

@@ -412,9 +412,9 @@ __device__ __forceinline__ int cplus_pick(const Foot &g, float u2, Planned plann
     return pick < 0 ? lastc : pick;
 }
 
-static __device__ __noinline__ Plan fb_plan(int fb, const Foot f, const Box b, bool active, unsigned A, int na, int px,
-                                            int py, uint32_t frame, uint32_t seed_lo, uint32_t seed_hi, int W,
-                                            WarpSmem &s) {
+__device__ __forceinline__ Plan fb_plan_impl(int fb, const Foot &f, const Box &b, bool active, unsigned A, int na,
+                                              int px, int py, uint32_t frame, uint32_t seed_lo, uint32_t seed_hi,
+                                              int W, WarpSmem &s) {
     const unsigned lane = lane_id();
     const unsigned lt = lanemask_lt();
     Plan pl;
@@ -500,8 +500,8 @@ struct Finished {
 // (4) every lane filters with the produced texels of the wave: one-tap (STF), the WC
 // stand-in, or Eq. 1 (C, C+)
 template <int FMT>
-static __device__ __noinline__ Finished fb_finish(int fb, const Foot f, const Box b, bool active, int na, const Plan pl,
-                                                  const Texel<FMT> val, int W, WarpSmem &s) {
+__device__ __forceinline__ Finished fb_finish_impl(int fb, const Foot &f, const Box &b, bool active, int na,
+                                                   const Plan &pl, const Texel<FMT> &val, int W, WarpSmem &s) {
     Finished o;
     if (fb == FB_STF) {
         o.evals = na;
@@ -516,6 +516,40 @@ static __device__ __noinline__ Finished fb_finish(int fb, const Foot f, const Bo
         o.color = gather_sorted<FMT>(f, active, pl.produced ? (uint32_t)(pl.qy * W + pl.qx) : INVALID_ID, val, wc,
                                      s, W);
     return o;
+}
+
+// Out-of-line entry points.  Latent-MLP: plan and finish are separate calls so the
+// kernel keeps ONE inline copy of the 1.5k-FMA decoder (its weights are kernel
+// parameters).  BC1: plan + decode + finish in one out-of-line call (cheap decoder,
+// smaller hot loop).
+static __device__ __noinline__ Plan fb_plan(int fb, const Foot f, const Box b, bool active, unsigned A, int na, int px,
+                                            int py, uint32_t frame, uint32_t seed_lo, uint32_t seed_hi, int W,
+                                            WarpSmem &s) {
+    return fb_plan_impl(fb, f, b, active, A, na, px, py, frame, seed_lo, seed_hi, W, s);
+}
+template <int FMT>
+static __device__ __noinline__ Finished fb_finish(int fb, const Foot f, const Box b, bool active, int na, const Plan pl,
+                                                  const Texel<FMT> val, int W, WarpSmem &s) {
+    return fb_finish_impl<FMT>(fb, f, b, active, na, pl, val, W, s);
+}
+struct FbAll {
+    Finished fin;
+    uint32_t prod, selbits;
+};
+static __device__ __noinline__ FbAll fb_all_bc1(int fb, const Foot f, const Box b, bool active, unsigned A, int na,
+                                                int px, int py, uint32_t frame, const KArgs &a, WarpSmem &s) {
+    const int W = a.tex.W;
+    const Plan pl = fb_plan_impl(fb, f, b, active, A, na, px, py, frame, a.seed_lo, a.seed_hi, W, s);
+    Texel<FMT_BC1> val = Texel<FMT_BC1>::zero();
+    FbAll r;
+    r.prod = INVALID_ID;
+    r.selbits = pl.selbits;
+    if (pl.produced) {
+        val = produce(a.tex, NoWeights{}, pl.qx, pl.qy);
+        r.prod = (uint32_t)(pl.qy * W + pl.qx);
+    }
+    r.fin = fb_finish_impl<FMT_BC1>(fb, f, b, active, na, pl, val, W, s);
+    return r;
 }
 
 // --------------------------------------------------------------- exact collect
@@ -731,15 +765,25 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 2))
                         else { pl.qx = (int)(e & 0xffffu); pl.qy = (int)(e >> 16); }
                     }
                     pl.selbits = 0u;
+                } else if constexpr (FMT == FMT_BC1) {
+                    pl.produced = false;
+                    pl.qx = pl.qy = 0;
                 } else {
                     pl = fb_plan(fb, f, b, active, A, na, px, py, frame, a.seed_lo, a.seed_hi, a.tex.W, s);
                 }
-                selbits = pl.selbits;
+                FbAll fball;
+                if constexpr (FMT == FMT_BC1) {
+                    if (!exact) fball = fb_all_bc1(fb, f, b, active, A, na, px, py, frame, a, s);
+                }
+                selbits = (FMT == FMT_BC1 && !exact) ? fball.selbits : pl.selbits;
                 // ---- the single texel-production site (<= 1 evaluation per lane)
                 Texel<FMT> val = Texel<FMT>::zero();
                 if (pl.produced) {
                     val = produce(a.tex, mw, pl.qx, pl.qy);
                     prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
+                }
+                if constexpr (FMT == FMT_BC1) {
+                    if (!exact) prod = fball.prod;
                 }
                 if (exact) {
                     rec = rec_base | ((uint32_t)n * 0x101u);  // evals = n, path 0
@@ -768,7 +812,9 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 2))
                     }
                 } else {
                     // ---- a7: fallback combine
-                    const Finished o = fb_finish<FMT>(fb, f, b, active, na, pl, val, a.tex.W, s);
+                    Finished o;
+                    if constexpr (FMT == FMT_BC1) o = fball.fin;
+                    else o = fb_finish<FMT>(fb, f, b, active, na, pl, val, a.tex.W, s);
                     color = o.color;
                     const uint32_t path = MODE == MODE_COLLAB ? (uint32_t)(PATH_FB_STF + fb)
                                                               : (uint32_t)(MODE == MODE_STF ? PATH_STF : PATH_WC);

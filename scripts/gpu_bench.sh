@@ -16,3 +16,8 @@ tail -3 gpurun_out/launches_$TAG.csv
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ctf_filter_kernel -s 3 -c 1 \
     -o gpurun_out/prof_$TAG python bench.py --frames 16 --warmup 3 --profile-launches 1 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -3 gpurun_out/ncu_full_$TAG.log
+if [ "${MLPPROF:-0}" = "1" ]; then
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctf_filter_kernel -s 1 -c 1 \
+    -o gpurun_out/prof_mlp_$TAG python bench.py --profile-config3 2 > gpurun_out/ncu_mlp_$TAG.log 2>&1
+tail -2 gpurun_out/ncu_mlp_$TAG.log
+fi
