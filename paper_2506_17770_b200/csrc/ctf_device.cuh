@@ -197,11 +197,13 @@ __device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const MlpWeights 
     in[9] = (float)((y & 3) * 2 - 3) * 0.25f;
     in[10] = ((x >> 2) & 1) ? 0.5f : -0.5f;
     in[11] = ((y >> 2) & 1) ? 0.5f : -0.5f;
-    const float *W1 = w, *b1 = W1 + 32 * 12, *W2 = b1 + 32, *b2 = W2 + 32 * 32, *W3 = b2 + 32, *b3 = W3 + 4 * 32;
+    // Kernel weight layout (repacked by the launcher so every access is contiguous and
+    // the compiler can fetch 4 weights per LDCU.128): W1[k][12], b1[32], W2T[k][j] =
+    // W2[j][k], b2[32], W3T[j][4] = W3[c][j], b3[4].
+    const float *W1 = w, *b1 = W1 + 32 * 12, *W2T = b1 + 32, *b2 = W2T + 32 * 32, *W3T = b2 + 32, *b3 = W3T + 4 * 32;
     // Outer-product order keeps ~50 values live instead of ~100: each hidden unit k of
     // layer 1 is formed and immediately scattered into the 32 layer-2 accumulators;
-    // then each layer-2 unit feeds the 4 outputs.  Same 1536 FMAs, weights read from
-    // the constant bank (kernel parameters).
+    // then each layer-2 unit feeds the 4 outputs.  Same 1536 FMAs.
     float acc2[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) acc2[j] = b2[j];
@@ -212,14 +214,14 @@ __device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const MlpWeights 
         for (int i = 0; i < 12; ++i) h = fmaf(W1[k * 12 + i], in[i], h);
         h = fmaxf(h, 0.f);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc2[j] = fmaf(W2[j * 32 + k], h, acc2[j]);
+        for (int j = 0; j < 32; ++j) acc2[j] = fmaf(W2T[k * 32 + j], h, acc2[j]);
     }
     float o[4] = {b3[0], b3[1], b3[2], b3[3]};
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const float h = fmaxf(acc2[j], 0.f);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) o[c] = fmaf(W3[c * 32 + j], h, o[c]);
+        for (int c = 0; c < 4; ++c) o[c] = fmaf(W3T[j * 4 + c], h, o[c]);
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) o[c] = fminf(fmaxf(o[c], 0.f), 1.f);
