@@ -134,7 +134,7 @@ typedef struct {
  * Filter one frame.
  *   tex        texture descriptor (host struct; its pointers are device pointers)
  *   uv_dev     float[Hf][Wf][2] normalised (u, v); u = NaN marks an uncovered pixel.
- *              Coordinates are clamped to [-16, 16] before use (R-2 iii).  8-B aligned.
+ *              Coordinates are clamped to [0, 1] before use (clamp-to-edge, R-2).  8-B aligned.
  *   grad_dev   fp16 bits [Hf][Wf][4] = (du/dx, dv/dx, du/dy, dv/dy) in texel units, or
  *              NULL (then the magnified bit is 0).  8-B aligned.
  *   Wf, Hf     frame size in pixels, any value >= 1 (partial waves at the right/bottom).
