@@ -103,6 +103,7 @@ struct TexArgs {
     int W, H;
     const uint2 *bc1;       // BC1 blocks
     const uint4 *latent;    // 8 x fp16 per latent texel
+    const float *mlp_dev;   // MLP weights in the ABI layout (per-lane rows of the batched decoder)
 };
 
 constexpr int kMlpWeights = 32 * 12 + 32 + 32 * 32 + 32 + 4 * 32 + 4;  // 1604 (R-10)
@@ -170,8 +171,8 @@ __device__ __forceinline__ void rgba8_to_float(uint32_t v, float (&c)[4]) {
 
 // Latent + MLP decode (R-10; NTC-style inference-on-sample).  fp32 FFMA.
 // Weights are read from the kernel parameter block with compile-time offsets.
-__device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const MlpWeights &wt, int x, int y) {
-    const float *w = wt.v;
+// The 12 MLP inputs of texel (x, y): bilinear latent sample + 4 positional features.
+__device__ __forceinline__ void mlp_features(const TexArgs &t, int x, int y, float (&in)[12]) {
     const int lw = t.W >> 2, lh = t.H >> 2;
     // sample point ((x-1.5)/4, (y-1.5)/4): integer part and phase in eighths (exact weights)
     const int gx8 = 2 * x - 3, gy8 = 2 * y - 3;                 // 8 * position
@@ -182,7 +183,6 @@ __device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const MlpWeights 
     const uint4 q00 = __ldg(t.latent + (size_t)y0 * lw + x0), q01 = __ldg(t.latent + (size_t)y0 * lw + x1);
     const uint4 q10 = __ldg(t.latent + (size_t)y1 * lw + x0), q11 = __ldg(t.latent + (size_t)y1 * lw + x1);
     const float w00 = (1.f - fx) * (1.f - fy), w01 = fx * (1.f - fy), w10 = (1.f - fx) * fy, w11 = fx * fy;
-    float in[12];
     const uint32_t *a0 = &q00.x, *a1 = &q01.x, *a2 = &q10.x, *a3 = &q11.x;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -197,6 +197,16 @@ __device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const MlpWeights 
     in[9] = (float)((y & 3) * 2 - 3) * 0.25f;
     in[10] = ((x >> 2) & 1) ? 0.5f : -0.5f;
     in[11] = ((y >> 2) & 1) ? 0.5f : -0.5f;
+}
+
+// Latent + MLP decode of one texel by one lane (R-10; NTC-style inference-on-sample,
+// P:729-752).  fp32 FFMA; weights read from the kernel parameter block with
+// compile-time offsets.  The wave-batched decoder in ctf_filter.cu performs the same
+// operations in the same order per output, so both give bit-identical texels.
+__device__ __forceinline__ float4 mlp_decode(const TexArgs &t, const MlpWeights &wt, int x, int y) {
+    const float *w = wt.v;
+    float in[12];
+    mlp_features(t, x, y, in);
     // Kernel weight layout (repacked by the launcher so every access is contiguous and
     // the compiler can fetch 4 weights per LDCU.128): W1[k][12], b1[32], W2T[k][j] =
     // W2[j][k], b2[32], W3T[j][4] = W3[c][j], b3[4].

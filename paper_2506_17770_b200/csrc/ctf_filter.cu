@@ -614,15 +614,109 @@ static __device__ __noinline__ Collected collect_sort(const Foot f, bool active,
     return c;
 }
 
+// ------------------------------------------------ wave-batched latent-MLP decode
+// The n unique texels of an exact wave are decoded TOGETHER: lane j owns hidden unit j
+// (its rows of W1 and W2 live in registers for the whole kernel) and loops over the n
+// texels; the producer of texel r only computes its 12 inputs and the 4 outputs.  Per
+// wave: ~62 instructions per texel + ~190 fixed, instead of the full 1.5k-FMA decoder on
+// every lane (SIMT).  Each output is the same sequence of fp32 operations as mlp_decode,
+// so the texels are bit-identical (P:855-869 split decode across lanes).
+struct MlpBatchSmem {
+    float4 in[32][3];    // texel r's 12 inputs (rows >= n are never consumed)
+    float h1[4][32];     // layer-1 activations of the 4 texels in flight
+    float h2[32][36];    // layer-2 activations per texel (row stride 36: conflict-free LDS.128)
+};
+
+struct MlpLaneWeights {
+    float w1[12], w2[32], b1, b2;   // row `lane` of W1 / W2 and its biases (ABI layout)
+};
+
+__device__ __forceinline__ void load_lane_weights(const float *__restrict__ m, unsigned lane, MlpLaneWeights &lw) {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) lw.w1[i] = __ldg(m + lane * 12 + i);
+    lw.b1 = __ldg(m + 384 + lane);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) lw.w2[k] = __ldg(m + 416 + lane * 32 + k);
+    lw.b2 = __ldg(m + 1440 + lane);
+}
+
+// Texels are processed 4 at a time so every lane runs 4 independent FMA chains.
+__device__ __forceinline__ float4 mlp_decode_batched(const TexArgs &t, const MlpWeights &mw, MlpBatchSmem &ms,
+                                                     const MlpLaneWeights &lw, bool producer, int r, int qx, int qy,
+                                                     int n, unsigned lane) {
+    if (producer) {
+        float in[12];
+        mlp_features(t, qx, qy, in);
+        ms.in[r][0] = make_float4(in[0], in[1], in[2], in[3]);
+        ms.in[r][1] = make_float4(in[4], in[5], in[6], in[7]);
+        ms.in[r][2] = make_float4(in[8], in[9], in[10], in[11]);
+    }
+    __syncwarp();
+    for (int t0 = 0; t0 < n; t0 += 4) {
+        // layer 1: lane = hidden unit, 4 texels
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int tq = min(t0 + q, 31);
+            const float4 i0 = ms.in[tq][0], i1 = ms.in[tq][1], i2 = ms.in[tq][2];
+            float h = lw.b1;
+            h = fmaf(lw.w1[0], i0.x, h); h = fmaf(lw.w1[1], i0.y, h); h = fmaf(lw.w1[2], i0.z, h);
+            h = fmaf(lw.w1[3], i0.w, h); h = fmaf(lw.w1[4], i1.x, h); h = fmaf(lw.w1[5], i1.y, h);
+            h = fmaf(lw.w1[6], i1.z, h); h = fmaf(lw.w1[7], i1.w, h); h = fmaf(lw.w1[8], i2.x, h);
+            h = fmaf(lw.w1[9], i2.y, h); h = fmaf(lw.w1[10], i2.z, h); h = fmaf(lw.w1[11], i2.w, h);
+            ms.h1[q][lane] = fmaxf(h, 0.f);
+        }
+        __syncwarp();
+        // layer 2: lane = hidden unit, 4 texels, k ascending (same order as mlp_decode)
+        float acc[4] = {lw.b2, lw.b2, lw.b2, lw.b2};
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 hv = reinterpret_cast<const float4 *>(ms.h1[q])[k4];
+                acc[q] = fmaf(lw.w2[4 * k4 + 0], hv.x, acc[q]);
+                acc[q] = fmaf(lw.w2[4 * k4 + 1], hv.y, acc[q]);
+                acc[q] = fmaf(lw.w2[4 * k4 + 2], hv.z, acc[q]);
+                acc[q] = fmaf(lw.w2[4 * k4 + 3], hv.w, acc[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (t0 + q < 32) ms.h2[t0 + q][lane] = fmaxf(acc[q], 0.f);
+        __syncwarp();
+    }
+    // layer 3: the producer of texel r forms its 4 outputs (weights warp-uniform)
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (producer) {
+        const float *W3T = mw.v + 1472, *b3 = mw.v + 1600;   // kernel layout: W3T[j][c], b3[c]
+        float oc[4] = {b3[0], b3[1], b3[2], b3[3]};
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 hv = *reinterpret_cast<const float4 *>(&ms.h2[r][4 * j4]);
+            const float hj[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) oc[c] = fmaf(W3T[(4 * j4 + jj) * 4 + c], hj[jj], oc[c]);
+        }
+        o = make_float4(fminf(fmaxf(oc[0], 0.f), 1.f), fminf(fmaxf(oc[1], 0.f), 1.f), fminf(fmaxf(oc[2], 0.f), 1.f),
+                        fminf(fmaxf(oc[3], 0.f), 1.f));
+    }
+    return o;
+}
+
 // ----------------------------------------------------------------------- kernel
 constexpr int kChunk = 16;  // waves per work item: a run of consecutive waves in one wave-row
 
 template <int FMT, int MODE, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 2))
+__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MODE_COLLAB ? 1 : 2)))
     ctf_filter_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ WarpSmem smem[kWarps];
+    extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent-MLP COLLAB: batch buffers
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     WarpSmem &s = smem[warp];
+    constexpr bool kBatchMlp = FMT == FMT_MLP && MODE == MODE_COLLAB;
+    MlpLaneWeights lw;
+    if constexpr (kBatchMlp) load_lane_weights(a.tex.mlp_dev, lane, lw);
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned lt = lanemask_lt();
     const unsigned nwarps = gridDim.x * kWarps;
@@ -654,8 +748,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 2))
             const bool inframe = rowok & (px < a.Wf);
             const float2 uv = uv_n;
             const uint2 gr = gr_n;
-            uv_n = make_float2(__int_as_float(0x7fc00000), 0.f);
-            gr_n = make_uint2(0u, 0u);
+            // (no reset needed: lanes whose next pixel is outside the frame are inactive there)
             const bool pf = (wx + 1 < wx1) & rowok & (px + 8 < a.Wf);
             ld_stream_f2_if(uv_n, a.uv + (pix + 8u), pf);
             ld_stream_u2_if(gr_n, a.grad + (pix + 8u), pf & has_grad);
@@ -778,7 +871,17 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : 2))
                 selbits = (FMT == FMT_BC1 && !exact) ? fball.selbits : pl.selbits;
                 // ---- the single texel-production site (<= 1 evaluation per lane)
                 Texel<FMT> val = Texel<FMT>::zero();
-                if (pl.produced) {
+                if constexpr (kBatchMlp) {
+                    if (exact) {
+                        MlpBatchSmem &ms = reinterpret_cast<MlpBatchSmem *>(dyn_smem)[warp];
+                        val.v = mlp_decode_batched(a.tex, mw, ms, lw, pl.produced, __popc(A & lt), pl.qx, pl.qy, n,
+                                                   lane);
+                        if (pl.produced) prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
+                    } else if (pl.produced) {
+                        val = produce(a.tex, mw, pl.qx, pl.qy);
+                        prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
+                    }
+                } else if (pl.produced) {
                     val = produce(a.tex, mw, pl.qx, pl.qy);
                     prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
                 }
@@ -839,17 +942,22 @@ template <int FMT, int MODE, bool DBG>
 static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
     auto kern = ctf_filter_kernel<FMT, MODE, DBG>;
     int dev = 0, sms = 0, per_sm = 0;
+    const size_t dyn = (FMT == FMT_MLP && MODE == MODE_COLLAB) ? kWarps * sizeof(MlpBatchSmem) : 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0);
+    if (dyn > 0) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return e;
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, dyn);
     if (e != cudaSuccess) return e;
     const long long need = ((long long)k.nchunks + kWarps - 1) / kWarps;
     long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kWarps * 32, 0, stream>>>(k, mw);
+    kern<<<(unsigned)grid, kWarps * 32, dyn, stream>>>(k, mw);
     return cudaGetLastError();
 }
 
@@ -882,6 +990,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.tex.H = a.H;
     k.tex.bc1 = reinterpret_cast<const uint2 *>(a.tex_data);
     k.tex.latent = reinterpret_cast<const uint4 *>(a.tex_data);
+    k.tex.mlp_dev = a.mlp;
     k.uv = reinterpret_cast<const float2 *>(a.uv);
     k.grad = reinterpret_cast<const uint2 *>(a.grad);
     k.out = reinterpret_cast<float4 *>(a.out);
