@@ -28,6 +28,9 @@
 namespace ctf {
 
 constexpr int kWarps = 8;  // warps per CTA
+#ifndef CTF_MLP_COLLAB_MINB
+#define CTF_MLP_COLLAB_MINB 2  // latent-MLP COLLAB: resident CTAs per SM (register budget)
+#endif
 
 struct KArgs {
     TexArgs tex;
@@ -708,7 +711,7 @@ __device__ __forceinline__ float4 mlp_decode_batched(const TexArgs &t, const Mlp
 constexpr int kChunk = 16;  // waves per work item: a run of consecutive waves in one wave-row
 
 template <int FMT, int MODE, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MODE_COLLAB ? 1 : 2)))
+__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MODE_COLLAB ? CTF_MLP_COLLAB_MINB : 2)))
     ctf_filter_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ WarpSmem smem[kWarps];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent-MLP COLLAB: batch buffers
@@ -864,7 +867,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                 } else {
                     pl = fb_plan(fb, f, b, active, A, na, px, py, frame, a.seed_lo, a.seed_hi, a.tex.W, s);
                 }
-                FbAll fball;
+                FbAll fball{};
                 if constexpr (FMT == FMT_BC1) {
                     if (!exact) fball = fb_all_bc1(fb, f, b, active, A, na, px, py, frame, a, s);
                 }
