@@ -1,0 +1,11 @@
+# compute-sanitizer passes over small GPU parity cases (run under gpurun)
+set -x
+mkdir -p gpurun_out
+TAG=${TAG:-r01}
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 3 --print-limit 20 \
+    python -m pytest tests/test_gpu_parity.py -q -x -k "config1_uniform_4x and 1-30 or tiny_frames or clustered or latent_mlp_texture" \
+    > gpurun_out/sanitize_${tool}_$TAG.log 2>&1
+  echo "$tool exit=$?"
+  tail -4 gpurun_out/sanitize_${tool}_$TAG.log
+done

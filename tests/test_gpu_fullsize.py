@@ -1,0 +1,118 @@
+"""Full-size parity at BASELINE.json's configurations, in the launch configuration bench.py
+times (release kernel, batched launch), against the oracle on SAMPLED waves (-m gpu).
+
+Every wave of the frame is produced by the GPU; the oracle recomputes a seeded random
+sample of waves plus every fallback wave it is handed (up to a cap), and the records and
+colours of those waves must match (records bit-exact, colours <= 1e-5).
+"""
+import numpy as np
+import pytest
+
+import synthetic
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ATOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ctf():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2506_17770_b200.ctf as c
+    c.load_library()
+    return c
+
+
+def sample_waves(rec_gpu: np.ndarray, nsample: int, seed: int, extra_fallback: int = 400):
+    rng = np.random.default_rng(seed)
+    nw = rec_gpu.size
+    pick = set(rng.choice(nw, size=min(nsample, nw), replace=False).tolist())
+    path = (rec_gpu.reshape(-1) >> 22) & 7
+    fb = np.flatnonzero((path >= 1) & (path <= 4))
+    if fb.size:
+        pick.update(rng.choice(fb, size=min(extra_fallback, fb.size), replace=False).tolist())
+    return np.array(sorted(pick), dtype=np.int32)
+
+
+def check_sampled(tex_np, uv_np, g_np, out_gpu, rec_gpu, waves, mode, fb, seed, frame_index):
+    import oracle
+    o = oracle.filter_waves(tex_np, uv_np, g_np, waves, mode, fb, 0, seed, frame_index)
+    hf, wf = uv_np.shape[:2]
+    nwx = (wf + 7) // 8
+    rg = rec_gpu.reshape(-1)[waves]
+    ro = o["rec"].reshape(-1)[waves]
+    np.testing.assert_array_equal(rg, ro)
+    worst = 0.0
+    for w in waves.tolist():
+        wy, wx = divmod(w, nwx)
+        ys, xs = slice(wy * 4, min(wy * 4 + 4, hf)), slice(wx * 8, min(wx * 8 + 8, wf))
+        worst = max(worst, float(np.abs(out_gpu[ys, xs].astype(np.float64) - o["out"][ys, xs]).max()))
+    assert worst <= ATOL, worst
+    return worst
+
+
+def test_config2_1080p_bc1(ctf):
+    W = 2048
+    blocks = synthetic.bc1_texture(W, W, 7, "image")
+    uv, g = synthetic.perspective_plane(1920, 1080, W, W, synthetic.PLANE_C2)
+    tex = ctf.Texture.bc1(blocks, W, W)
+    out, rec = ctf.filter_frame(tex, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), 3, 3, 0, 7, 0)
+    rec = rec.cpu().numpy().view(np.uint32)
+    waves = sample_waves(rec, 3000, 1)
+    check_sampled({"format": 1, "width": W, "height": W, "bc1": blocks}, uv, g, out.cpu().numpy(), rec, waves,
+                  3, 3, 7, 0)
+
+
+@pytest.mark.parametrize("fb", [0, 1, 2, 3])
+def test_config4_4k_mixed_every_fallback(ctf, fb):
+    W = 4096
+    blocks = synthetic.bc1_texture(W, W, 7, "image")
+    uv, g = synthetic.perspective_plane(3840, 2160, W, W, synthetic.PLANE_C4)
+    tex = ctf.Texture.bc1(blocks, W, W)
+    out, rec = ctf.filter_frame(tex, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), 3, fb, 0, 11, 3)
+    rec = rec.cpu().numpy().view(np.uint32)
+    path = (rec >> 22) & 7
+    assert ((path >= 1) & (path <= 4)).mean() > 0.05      # the scene exercises the fallback
+    waves = sample_waves(rec, 2000, 2 + fb, extra_fallback=800)
+    check_sampled({"format": 1, "width": W, "height": W, "bc1": blocks}, uv, g, out.cpu().numpy(), rec, waves,
+                  3, fb, 11, 3)
+
+
+def test_config3_4k_latent_mlp(ctf):
+    W = 4096
+    lat, mlp = synthetic.latent_texture(W, W, 7), synthetic.mlp_weights(8)
+    uv, g = synthetic.perspective_plane(3840, 2160, W, W, synthetic.PLANE_C2)
+    tex = ctf.Texture.latent_mlp(lat, mlp, W, W)
+    uvd, gd = torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda()
+    out, rec = ctf.filter_frame(tex, uvd, gd, 3, 3, 0, 7, 0)
+    ref, _ = ctf.filter_frame(tex, uvd, gd, 0, 0, 0, 7, 0)
+    rec = rec.cpu().numpy().view(np.uint32)
+    waves = sample_waves(rec, 1500, 3)
+    check_sampled({"format": 2, "width": W, "height": W, "latent": lat, "mlp": mlp}, uv, g, out.cpu().numpy(), rec,
+                  waves, 3, 3, 7, 0)
+    # the wave-batched decoder performs the single-lane decoder's operations in the same order
+    ex = ((rec >> 22) & 7) == 0
+    px = np.repeat(np.repeat(ex, 4, 0), 8, 1)[:2160, :3840]
+    assert torch.equal(out[torch.from_numpy(px).cuda()], ref[torch.from_numpy(px).cuda()])
+
+
+def test_config5_batch_as_benchmarked(ctf):
+    """The bench's 64-frame 4K camera-path batch (one launch); frames sampled, waves sampled."""
+    W, F = 4096, 64
+    blocks = synthetic.bc1_texture(W, W, 7, "image")
+    tex = ctf.Texture.bc1(blocks, W, W)
+    uv = torch.empty((F, 2160, 3840, 2), dtype=torch.float32, device="cuda")
+    g = torch.empty((F, 2160, 3840, 4), dtype=torch.float16, device="cuda")
+    for f in range(F):
+        u, gg = synthetic.camera_path_frame_torch(f, 3840, 2160, W, W)
+        uv[f].copy_(u)
+        g[f].copy_(gg)
+    out, rec = ctf.filter_batch(tex, uv, g, 3, 3, 0, 7, 0)
+    torch.cuda.synchronize()
+    for f in (0, 21, 47, 63):
+        r = rec[f].cpu().numpy().view(np.uint32)
+        waves = sample_waves(r, 800, 10 + f, extra_fallback=200)
+        check_sampled({"format": 1, "width": W, "height": W, "bc1": blocks}, uv[f].cpu().numpy(), g[f].cpu().numpy(),
+                      out[f].cpu().numpy(), r, waves, 3, 3, 7, f)
