@@ -350,7 +350,10 @@ __device__ __forceinline__ float4 gather_mask(const Foot &f, const Box &b, bool 
     const unsigned lane = lane_id();
     WMask<4> D;
     D.reduce_bit(prod_t, active && produced);
-    if (active && produced) s.lane_of_t[prod_t] = (uint8_t)lane;  // any producer of t will do
+    // several lanes may produce the same texel (STF, C+ extras): __match_any_sync groups
+    // them and only the lowest lane of each group publishes itself as the source of t
+    const unsigned peers = __match_any_sync(FULL, (active && produced) ? prod_t : 0xFFFFFFFFu);
+    if (active && produced && (unsigned)(__ffs(peers) - 1) == lane) s.lane_of_t[prod_t] = (uint8_t)lane;
     __syncwarp();
     bool first[4], known[4];
     float dw[4];
