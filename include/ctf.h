@@ -78,7 +78,13 @@ typedef enum {
     CTF_MODE_BILINEAR_4TAP = 0, /* classic bilinear, 4 evaluations per pixel      */
     CTF_MODE_STF = 1,           /* one-tap stochastic texture filtering (Pharr 2024) */
     CTF_MODE_WAVECOMM = 2,      /* wave-communication STF stand-in (R-16)        */
-    CTF_MODE_COLLAB = 3         /* collaborative filtering + fallback (§3)       */
+    CTF_MODE_COLLAB = 3,        /* collaborative filtering, List semantics: exact iff the
+                                   wave's unique texels n <= active lanes (§3.1)  */
+    CTF_MODE_BOX = 4,           /* Box Sampling: exact iff AABB area <= active lanes; lanes
+                                   produce the whole AABB (§3.2)    */
+    CTF_MODE_MASK16 = 5,        /* Mask Sampling 16x16: exact iff AABB <= 16x16 and n <= a
+                                   (§3.3)                            */
+    CTF_MODE_MASK11 = 6         /* Mask Sampling 11x11                           */
 } ctf_mode;
 
 typedef enum {
@@ -95,7 +101,7 @@ enum {
 
 typedef struct {
     int32_t mode;          /* ctf_mode                                                     */
-    int32_t fallback;      /* ctf_fallback; ignored unless mode == CTF_MODE_COLLAB          */
+    int32_t fallback;      /* ctf_fallback; used by the collaborative modes (COLLAB..MASK11)*/
     uint32_t flags;        /* CTF_FLAG_*                                                   */
     uint32_t frame_index;  /* RNG counter word; batch frame f uses frame_index + f          */
     uint64_t seed;         /* RNG key (R-11: Philox4x32-10, ctr = (x, y, frame, 0))         */
@@ -114,9 +120,10 @@ typedef struct {
 
 /*
  * Per-wave record (u32), one per wave, [frames][ceil(Hf/4)][ceil(Wf/8)]:
- *   bits 0-7   texel evaluations in the wave (exact: n; 4TAP: 4a; STF/WC/C: a;
- *              C+: n_p + spare lanes that produced)
- *   bits 8-15  n = number of unique texels the wave needs (COLLAB; 0xFF otherwise)
+ *   bits 0-7   texel evaluations in the wave (exact: n, Box: AABB area; 4TAP: 4a;
+ *              STF/WC/C: a; C+: n_p + spare lanes that produced)
+ *   bits 8-15  n = number of unique texels the wave needs (collaborative modes; 0xFF
+ *              for 4TAP / STF / WC)
  *   bits 16-21 a = active lanes
  *   bits 22-24 path: 0 exact, 1 fb-STF, 2 fb-WC, 3 fb-C, 4 fb-C+, 5 4TAP, 6 STF, 7 WC
  *   bit  25    magnified: grad given and every active lane has

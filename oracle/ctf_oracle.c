@@ -37,7 +37,7 @@
 #define INVALID_ID 0xFFFFFFFFu
 
 /* modes / fallbacks / flags as numbered in DESIGN.md (the boundary's values) */
-enum { M_4TAP = 0, M_STF = 1, M_WC = 2, M_COLLAB = 3 };
+enum { M_4TAP = 0, M_STF = 1, M_WC = 2, M_COLLAB = 3, M_BOX = 4, M_MASK16 = 5, M_MASK11 = 6 };
 enum { FB_STF = 0, FB_WC = 1, FB_C = 2, FB_CPLUS = 3 };
 enum { FL_DEBUG = 1u, FL_FORCE_FALLBACK = 2u };
 enum { PATH_EXACT = 0, PATH_FB_STF = 1, PATH_FB_WC = 2, PATH_FB_C = 3, PATH_FB_CPLUS = 4,
@@ -432,13 +432,41 @@ static void wave(const frame_t *F, int wx, int wy)
         for (int lane = 0; lane < 32; ++lane)
             if (L[lane].active) for (int k = 0; k < 4; ++k) U[m++] = L[lane].id[k];
         n = sort_unique(U, m);
-        if (n <= a && !(F->flags & FL_FORCE_FALLBACK)) {            /* R-6 */
+        /* wave AABB of the clamped footprints */
+        int minx = 1 << 30, maxx = -1, miny = 1 << 30, maxy = -1;
+        for (int lane = 0; lane < 32; ++lane) {
+            if (!L[lane].active) continue;
+            int xa = (int)(L[lane].id[0] % (uint32_t)tex->W), ya = (int)(L[lane].id[0] / (uint32_t)tex->W);
+            int xb = (int)(L[lane].id[3] % (uint32_t)tex->W), yb = (int)(L[lane].id[3] / (uint32_t)tex->W);
+            if (xa < minx) minx = xa;
+            if (ya < miny) miny = ya;
+            if (xb > maxx) maxx = xb;
+            if (yb > maxy) maxy = yb;
+        }
+        int bw = 0, bh = 0, ok = 0;
+        if (a > 0) {
+            bw = maxx - minx + 1;
+            bh = maxy - miny + 1;
+            if (F->mode == M_BOX) ok = bw * bh <= a;                              /* P:345-346 + remap */
+            else if (F->mode == M_MASK16) ok = bw <= 16 && bh <= 16 && n <= a;
+            else if (F->mode == M_MASK11) ok = bw <= 11 && bh <= 11 && n <= a;
+            else ok = n <= a;                                                     /* List, R-6 */
+        }
+        if (a > 0 && ok && !(F->flags & FL_FORCE_FALLBACK)) {
             path = PATH_EXACT;
-            /* step 2: rank r is produced by lane h(r, A) (R-7) */
-            for (int r = 0; r < n; ++r) prod[act[r]] = U[r];
+            if (F->mode == M_BOX) {
+                /* Box: active rank i < bw*bh produces AABB texel (i mod bw, i div bw)
+                 * (LaneIdxToCoord P:1069-1076, with edge remapping P:1381) */
+                for (int i = 0; i < bw * bh; ++i)
+                    prod[act[i]] = (uint32_t)(miny + i / bw) * (uint32_t)tex->W + (uint32_t)(minx + i % bw);
+                evals = bw * bh;
+            } else {
+                /* step 2: rank r is produced by lane h(r, A) (R-7) */
+                for (int r = 0; r < n; ++r) prod[act[r]] = U[r];
+                evals = n;
+            }
             /* step 3: each lane gathers its 4 texels; result = plain bilinear (R-8) */
             for (int lane = 0; lane < 32; ++lane) if (L[lane].active) blend_exact(tex, &L[lane], col[lane]);
-            evals = n;
         } else {
             run_fallback = F->fallback;
             path = PATH_FB_STF + F->fallback;
@@ -524,7 +552,7 @@ static void wave(const frame_t *F, int wx, int wy)
         evals = nprod;
     }
 
-    if (a == 0) { evals = 0; path = 0; if (F->mode == M_COLLAB) n = 0; }
+    if (a == 0) { evals = 0; path = 0; if (F->mode >= M_COLLAB) n = 0; }
     *rec = (uint32_t)(evals & 0xFF) | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)a << 16) |
            ((uint32_t)path << 22) | ((uint32_t)magnified << 25) | ((uint32_t)(a < 32) << 26);
 
@@ -551,7 +579,7 @@ int oracle_filter_frame(int format, int W, int H, const uint8_t *bc1, const uint
     if (format == FMT_BC1 && (!bc1 || W % 4 || H % 4)) return -1;
     if (format == FMT_LATENT_MLP && (!latent || !mlp || W % 4 || H % 4)) return -1;
     if (format != FMT_BC1 && format != FMT_LATENT_MLP) return -1;
-    if (mode < 0 || mode > 3 || fallback < 0 || fallback > 3) return -1;
+    if (mode < 0 || mode > 6 || fallback < 0 || fallback > 3) return -1;
     tex_t tex = { format, W, H, bc1, latent, mlp };
     frame_t F = { &tex, uv, grad, Wf, Hf, mode, fallback, flags, seed, frame_index,
                   out, rec, produced_id, selection };

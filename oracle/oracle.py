@@ -16,7 +16,7 @@ ORACLE_SRC = HERE / "ctf_oracle.c"
 ORACLE_SO = HERE / "libctf_oracle.so"
 
 FMT_BC1, FMT_LATENT_MLP = 1, 2
-M_4TAP, M_STF, M_WC, M_COLLAB = 0, 1, 2, 3
+M_4TAP, M_STF, M_WC, M_COLLAB, M_BOX, M_MASK16, M_MASK11 = 0, 1, 2, 3, 4, 5, 6
 FB_STF, FB_WC, FB_C, FB_CPLUS = 0, 1, 2, 3
 FL_DEBUG, FL_FORCE_FALLBACK = 1, 2
 

@@ -20,7 +20,7 @@ int validate(const ctf_texture *tex, const float *uv, const uint16_t *grad, int3
     if (tex->addr != CTF_ADDR_CLAMP) return CTF_EINVAL;
     if (!tex->data_dev) return CTF_EINVAL;
     if (tex->format == CTF_FMT_LATENT_MLP && !tex->mlp_dev) return CTF_EINVAL;
-    if (p->mode < CTF_MODE_BILINEAR_4TAP || p->mode > CTF_MODE_COLLAB) return CTF_EINVAL;
+    if (p->mode < CTF_MODE_BILINEAR_4TAP || p->mode > CTF_MODE_MASK11) return CTF_EINVAL;
     if (p->fallback < CTF_FB_STF || p->fallback > CTF_FB_CPLUS) return CTF_EINVAL;
     // texel ids y*W+x must fit 24 bits (sort keys) and coordinates 16 bits
     if ((int64_t)tex->width * tex->height > (1LL << 24) || tex->width > 65535 || tex->height > 65535)

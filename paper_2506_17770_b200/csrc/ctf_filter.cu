@@ -45,8 +45,10 @@ struct KArgs {
     unsigned nchunks;
     float Wflt, Hflt;
     int fallback;
+    int variant;                    // COLLAB kernel: VAR_LIST / VAR_BOX / VAR_MASK16 / VAR_MASK11
     uint32_t flags, frame_index, seed_lo, seed_hi;
 };
+enum { VAR_LIST = 0, VAR_BOX = 1, VAR_MASK16 = 2, VAR_MASK11 = 3 };
 
 struct WarpSmem {
     uint32_t tbl[32];       // rank -> packed (y << 16 | x) of U[rank] (exact) / planned P (C+, sort path)
@@ -827,6 +829,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                 b.lgP = 0;
                 b.minx = b.miny = 0;
                 int rho[4] = {0, 0, 0, 0}, n = 0xFF, fb;
+                int box_w = 0, box_n = 0;   // Box variant: AABB width and area
                 bool exact = false;
                 if constexpr (MODE == MODE_COLLAB) {
                     // collect the exact unique set U and canonical ranks
@@ -841,7 +844,23 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                         for (int k = 0; k < 4; ++k) rho[k] = cc.rho[k];
                     }
                     __syncwarp();
-                    exact = n <= na && !(a.flags & FLAG_FORCE_FALLBACK);   // a4
+                    // a4: List semantics exact iff n <= a (R-6).  The paper's Box and
+                    // Mask variants add AABB conditions.
+                    if (a.variant == VAR_LIST) {
+                        exact = n <= na;
+                    } else {
+                        const int bw = __reduce_max_sync(FULL, active ? f.xb : INT_MIN) - b.minx + 1;
+                        const int bh = __reduce_max_sync(FULL, active ? f.yb : INT_MIN) - b.miny + 1;
+                        if (a.variant == VAR_BOX) {
+                            box_w = bw;
+                            box_n = bw * bh;
+                            exact = box_n <= na;
+                        } else {
+                            const int lim = a.variant == VAR_MASK16 ? 16 : 11;
+                            exact = bw <= lim && bh <= lim && n <= na;
+                        }
+                    }
+                    exact = exact && !(a.flags & FLAG_FORCE_FALLBACK);
                     fb = a.fallback;
                 } else {
                     fb = MODE == MODE_STF ? FB_STF : FB_WC;
@@ -856,14 +875,30 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                         if (active) s.lane_of_rank[ar] = (uint8_t)lane;
                         __syncwarp();
                     }
-                    pl.produced = active && ar < n;
                     pl.qx = pl.qy = 0;
-                    if (pl.produced) {
-                        const uint32_t e = s.tbl[ar];
-                        if (b.fits) { pl.qx = box_x(b, e); pl.qy = box_y(b, e); }
-                        else { pl.qx = (int)(e & 0xffffu); pl.qy = (int)(e >> 16); }
-                    }
                     pl.selbits = 0u;
+                    if (a.variant != VAR_BOX) {
+                        pl.produced = active && ar < n;
+                        if (pl.produced) {
+                            const uint32_t e = s.tbl[ar];
+                            if (b.fits) { pl.qx = box_x(b, e); pl.qy = box_y(b, e); }
+                            else { pl.qx = (int)(e & 0xffffu); pl.qy = (int)(e >> 16); }
+                        }
+                    } else {
+                        // Box: active rank i < w*h produces AABB texel (i mod w, i div w)
+                        // (LaneIdxToCoord); corners gather by their local index
+                        // (CoordToLaneIdx) through h(., A)
+                        pl.produced = active && ar < box_n;
+                        const int yq = ar / box_w;
+                        pl.qx = b.minx + (ar - yq * box_w);
+                        pl.qy = b.miny + yq;
+                        const int t0 = (f.ya - b.miny) * box_w + (f.xa - b.minx);
+                        const int t2 = (f.yb - b.miny) * box_w + (f.xa - b.minx);
+                        rho[0] = t0;
+                        rho[1] = t0 + (f.xb - f.xa);
+                        rho[2] = t2;
+                        rho[3] = t2 + (f.xb - f.xa);
+                    }
                 } else if constexpr (FMT == FMT_BC1) {
                     pl.produced = false;
                     pl.qx = pl.qy = 0;
@@ -880,8 +915,8 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                 if constexpr (kBatchMlp) {
                     if (exact) {
                         MlpBatchSmem &ms = reinterpret_cast<MlpBatchSmem *>(dyn_smem)[warp];
-                        val.v = mlp_decode_batched(a.tex, mw, ms, lw, pl.produced, __popc(A & lt), pl.qx, pl.qy, n,
-                                                   lane);
+                        val.v = mlp_decode_batched(a.tex, mw, ms, lw, pl.produced, __popc(A & lt), pl.qx, pl.qy,
+                                                   a.variant == VAR_BOX ? box_n : n, lane);
                         if (pl.produced) prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
                     } else if (pl.produced) {
                         val = produce(a.tex, mw, pl.qx, pl.qy);
@@ -895,7 +930,8 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                     if (!exact) prod = fball.prod;
                 }
                 if (exact) {
-                    rec = rec_base | ((uint32_t)n * 0x101u);  // evals = n, path 0
+                    // evals = n (Box: the AABB area), path 0
+                    rec = rec_base | ((uint32_t)n << 8) | (uint32_t)(a.variant == VAR_BOX ? box_n : n);
                     // ---- a6: gather from lanes h(rho_k, A) and blend
                     int src[4];
                     if (full) {
@@ -1016,6 +1052,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.Wflt = (float)a.W;
     k.Hflt = (float)a.H;
     k.fallback = a.fallback;
+    k.variant = a.mode >= 4 ? a.mode - 3 : VAR_LIST;   // BOX / MASK16 / MASK11 run in the COLLAB kernel
     k.flags = a.flags;
     k.frame_index = a.frame_index;
     k.seed_lo = (uint32_t)a.seed;

@@ -17,7 +17,7 @@ LIB_PATH = PKG / "libctf.so"
 
 CTF_OK, CTF_EINVAL, CTF_EUNSUPPORTED, CTF_EALIGN, CTF_ECUDA = 0, -1, -2, -3, -4
 FMT_BC1, FMT_LATENT_MLP = 1, 2
-MODE_4TAP, MODE_STF, MODE_WAVECOMM, MODE_COLLAB = 0, 1, 2, 3
+MODE_4TAP, MODE_STF, MODE_WAVECOMM, MODE_COLLAB, MODE_BOX, MODE_MASK16, MODE_MASK11 = 0, 1, 2, 3, 4, 5, 6
 FB_STF, FB_WAVECOMM, FB_C, FB_CPLUS = 0, 1, 2, 3
 FLAG_DEBUG, FLAG_FORCE_FALLBACK = 1, 2
 _STATUS = {0: "CTF_OK", -1: "CTF_EINVAL", -2: "CTF_EUNSUPPORTED", -3: "CTF_EALIGN", -4: "CTF_ECUDA"}

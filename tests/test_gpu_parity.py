@@ -65,7 +65,8 @@ def assert_parity(g, o, what=""):
 
 
 MODES = [(0, 0, 0), (1, 0, 0), (2, 0, 0), (3, 0, 0), (3, 1, 0), (3, 2, 0), (3, 3, 0),
-         (3, 0, 2), (3, 1, 2), (3, 2, 2), (3, 3, 2)]
+         (3, 0, 2), (3, 1, 2), (3, 2, 2), (3, 3, 2),
+         (4, 3, 0), (4, 0, 0), (5, 2, 0), (5, 3, 0), (6, 3, 0), (6, 1, 0)]   # Box, Mask16, Mask11
 
 
 @pytest.mark.parametrize("theta", [0.0, 30.0, 45.0])
@@ -150,7 +151,7 @@ def test_perspective_mixed_minification(ctf):
         assert_parity(gg, o, f"mode={mode} fb={fb} flags={fl}")
 
 
-@pytest.mark.parametrize("mode,fb,fl", [(0, 0, 0), (3, 3, 0), (3, 2, 2), (3, 3, 2), (1, 0, 0)])
+@pytest.mark.parametrize("mode,fb,fl", [(0, 0, 0), (3, 3, 0), (3, 2, 2), (3, 3, 2), (1, 0, 0), (4, 3, 0), (5, 3, 0)])
 def test_latent_mlp_texture(ctf, mode, fb, fl):
     """Config-3 format at small size: latent grid + MLP decode."""
     tex = mlp_tex(64, 64, 3)

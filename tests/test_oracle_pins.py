@@ -393,3 +393,62 @@ def test_mlp_decode_matches_independent_fp64():
         h2 = np.maximum(W2 @ h1 + b2, 0)
         o = np.clip(W3 @ h2 + b3, 0, 1)
         np.testing.assert_allclose(oracle.mlp_texel(t["latent"], t["mlp"], W, H, x, y), o, atol=1e-12)
+
+
+# ------------------------------------------- Box / Mask sampling (Fig. 4) --
+@pytest.mark.slow
+def test_box_threshold_45_degrees():
+    """Box needs m > 2.35 at 45°; at m = 2.36 it is perfect for every rotation."""
+    rows = {r[0]: r[1:] for r in golden_rows("thresholds.txt")}
+    tex = bc1_tex(1024, 1024, 1, "constant")
+    m_bad, th_bad = float(rows["box_fails_at"][0]), float(rows["box_fails_at"][1])
+    fails = 0
+    for j in range(6):
+        uv, _ = synthetic.rotated_quad(800, 800, 1024, 1024, m_bad, th_bad, jitter_seed=j)
+        fails += int((decode_record(filter_frame(tex, uv, None, 4, FB_STF, debug=False)["rec"])["path"] != 0).sum())
+    assert fails > 0
+    m_ok = float(rows["box_perfect_above"][0])
+    for th in np.arange(0.0, 90.01, 5.0):
+        uv, _ = synthetic.rotated_quad(640, 640, 1024, 1024, m_ok, float(th), jitter_seed=1)
+        assert np.all(decode_record(filter_frame(tex, uv, None, 4, FB_STF, debug=False)["rec"])["path"] == 0), th
+
+
+def test_mask_equals_list_and_11_equals_16_on_the_quad():
+    """List and Mask 'cover identical areas' and the 11x11 mask gives results
+    identical to 16x16 for bilinear: on rotated quads the records and images agree."""
+    tex = bc1_tex(256, 256, 5, "image")
+    for m, th in [(1.6, 37.5), (1.2, 20.0), (2.2, 45.0), (0.9, 10.0)]:
+        uv, g = synthetic.rotated_quad(96, 48, 256, 256, m, th, jitter_seed=2)
+        r = {mode: filter_frame(tex, uv, g, mode, FB_CPLUS, seed=3) for mode in (3, 5, 6)}
+        for mode in (5, 6):
+            np.testing.assert_array_equal(r[mode]["rec"], r[3]["rec"])
+            np.testing.assert_array_equal(r[mode]["out"], r[3]["out"])
+
+
+def test_box_produces_whole_aabb_and_is_exact():
+    """Box: lane h(i,A) produces AABB texel (i mod w, i div w) (LaneIdxToCoord, P:1069-1076);
+    evals = AABB area >= n; the image equals bilinear wherever it succeeds."""
+    W = 64
+    tex = bc1_tex(W, W, 9, "image")
+    uv, g = synthetic.rotated_quad(40, 20, W, W, 3.0, 30.0, coverage="circle", radius=9.0)
+    rb = filter_frame(tex, uv, g, 4, FB_C)
+    r4 = filter_frame(tex, uv, g, 0, 0)
+    d = decode_record(rb["rec"])
+    ex = (d["path"] == 0) & (d["a"] > 0)
+    assert ex.any() and np.all(d["evals"][ex] >= d["n"][ex])
+    px = np.repeat(np.repeat(ex, 4, 0), 8, 1)[:20, :40]
+    np.testing.assert_array_equal(rb["out"][px], r4["out"][px])
+    # one wave in detail: produced ids are the AABB in row-major order on the active lanes
+    wy, wx = np.argwhere(ex)[0]
+    pid = rb["produced_id"][wy * 4:wy * 4 + 4, wx * 8:wx * 8 + 8].reshape(-1)
+    lanes_uv = uv[wy * 4:wy * 4 + 4, wx * 8:wx * 8 + 8].reshape(-1, 2)
+    act = [l for l in range(32) if not np.isnan(lanes_uv[l, 0])]
+    xs, ys = [], []
+    for l in act:
+        ids, _ = oracle.footprint(float(lanes_uv[l, 0]), float(lanes_uv[l, 1]), W, W)
+        xs += [int(i) % W for i in ids]
+        ys += [int(i) // W for i in ids]
+    bw = max(xs) - min(xs) + 1
+    area = bw * (max(ys) - min(ys) + 1)
+    expect = [(min(ys) + i // bw) * W + min(xs) + i % bw for i in range(area)]
+    assert [int(pid[l]) for l in act[:area]] == expect
