@@ -284,6 +284,15 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
         mse = float((err * err).mean())
         e["psnr_vs_bilinear_db"] = 10 * float(np.log10(1.0 / mse)) if mse > 0 else float("inf")
         res[f"4_4k_mixed_bc1_collab_{name}"] = e
+    # the paper's three exact methods on the same grazing scene, C+ fallback (Fig. 4 / Fig. 7 shape)
+    for name, mode in (("list", 3), ("box", 4), ("mask16", 5), ("mask11", 6)):
+        ms, st, out = run(t4, uv, g, mode, 3, 10)
+        e = entry(3840, 2160, ms, st, 3840 * 2160 * 32)
+        cov = ~torch.isnan(uv[..., 0])
+        err = (out - ref)[cov].double()
+        mse = float((err * err).mean())
+        e["psnr_vs_bilinear_db"] = 10 * float(np.log10(1.0 / mse)) if mse > 0 else float("inf")
+        res[f"4_4k_mixed_bc1_method_{name}_cplus"] = e
     return res
 
 
