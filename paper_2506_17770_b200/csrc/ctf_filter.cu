@@ -775,21 +775,35 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                 if (lane == (unsigned)(wx - wx0)) myrec = ((MODE == MODE_COLLAB ? 0u : 0xFFu) << 8) | (1u << 26);
                 continue;
             }
+            // Partial wave: inactive lanes borrow the first active lane's inputs, so the
+            // wave-wide reductions below need no per-lane predicates (a duplicate footprint
+            // changes no min, max, OR or unique set).  Their outputs are discarded.
+            float2 uvm = uv;
+            uint2 grm = gr;
+            if (A != FULL) {
+                const int leader = __ffs(A) - 1;
+                const float lu = __shfl_sync(FULL, uv.x, leader), lv = __shfl_sync(FULL, uv.y, leader);
+                const unsigned g0 = __shfl_sync(FULL, gr.x, leader), g1 = __shfl_sync(FULL, gr.y, leader);
+                if (!active) {
+                    uvm = make_float2(lu, lv);
+                    grm = make_uint2(g0, g1);
+                }
+            }
             bool mag_lane = true;
             if (a.grad) {
                 // R-20: squares of fp16 values are exact in fp32, so fma(g0, g0, g1*g1)
                 // rounds once exactly like the fp32 sum of the two products
-                const float rx = fma_f32_f16((unsigned short)(gr.x & 0xffffu), (unsigned short)(gr.x & 0xffffu),
-                                             fma_f32_f16((unsigned short)(gr.x >> 16), (unsigned short)(gr.x >> 16), 0.0f));
-                const float ry = fma_f32_f16((unsigned short)(gr.y & 0xffffu), (unsigned short)(gr.y & 0xffffu),
-                                             fma_f32_f16((unsigned short)(gr.y >> 16), (unsigned short)(gr.y >> 16), 0.0f));
+                const float rx = fma_f32_f16((unsigned short)(grm.x & 0xffffu), (unsigned short)(grm.x & 0xffffu),
+                                             fma_f32_f16((unsigned short)(grm.x >> 16), (unsigned short)(grm.x >> 16), 0.0f));
+                const float ry = fma_f32_f16((unsigned short)(grm.y & 0xffffu), (unsigned short)(grm.y & 0xffffu),
+                                             fma_f32_f16((unsigned short)(grm.y >> 16), (unsigned short)(grm.y >> 16), 0.0f));
                 mag_lane = rx <= 1.0f && ry <= 1.0f;  // max(rx, ry) <= 1
             }
-            const bool wave_mag = a.grad != nullptr && __all_sync(FULL, !active || mag_lane);
+            const bool wave_mag = a.grad != nullptr && __all_sync(FULL, mag_lane);
             const uint32_t rec_base = ((uint32_t)na << 16) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26);
 
             // ---- a2: footprint
-            const Foot f = footprint(uv, a);
+            const Foot f = footprint(uvm, a);
 
             uint32_t prod = INVALID_ID, selbits = 0u, rec;
             float4 color = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -833,12 +847,12 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                 bool exact = false;
                 if constexpr (MODE == MODE_COLLAB) {
                     // collect the exact unique set U and canonical ranks
-                    b = wave_box(f, active);
-                    if (b.K == 1) n = collect_mask<1>(f, b, active, rho, s, lane);
-                    else if (b.K == 2) n = collect_mask<2>(f, b, active, rho, s, lane);
-                    else if (b.K == 4) n = collect_mask<4>(f, b, active, rho, s, lane);
+                    b = wave_box(f, true);   // inactive lanes carry a duplicate footprint
+                    if (b.K == 1) n = collect_mask<1>(f, b, true, rho, s, lane);
+                    else if (b.K == 2) n = collect_mask<2>(f, b, true, rho, s, lane);
+                    else if (b.K == 4) n = collect_mask<4>(f, b, true, rho, s, lane);
                     else {
-                        const Collected cc = collect_sort(f, active, s, lane, a.tex.W);
+                        const Collected cc = collect_sort(f, true, s, lane, a.tex.W);
                         n = cc.n;
 #pragma unroll
                         for (int k = 0; k < 4; ++k) rho[k] = cc.rho[k];
@@ -849,8 +863,8 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
                     if (a.variant == VAR_LIST) {
                         exact = n <= na;
                     } else {
-                        const int bw = __reduce_max_sync(FULL, active ? f.xb : INT_MIN) - b.minx + 1;
-                        const int bh = __reduce_max_sync(FULL, active ? f.yb : INT_MIN) - b.miny + 1;
+                        const int bw = __reduce_max_sync(FULL, f.xb) - b.minx + 1;
+                        const int bh = __reduce_max_sync(FULL, f.yb) - b.miny + 1;
                         if (a.variant == VAR_BOX) {
                             box_w = bw;
                             box_n = bw * bh;
