@@ -415,7 +415,8 @@ def main():
         g_h = None if grad is None else grad[:E].cpu().pin_memory()
         out_h = torch.empty((E, Hf, Wf, 4), dtype=torch.float32).pin_memory()
         rec_h = torch.empty((E, nwy, nwx), dtype=torch.int32).pin_memory()
-        pipe = ctf.HostPipeline(Wf, Hf, max(1, E // 4), grad is not None, device=dev)
+        chunk = 1  # one frame per chunk: the copy engines overlap H2D(c+1), kernel(c), D2H(c-1)
+        pipe = ctf.HostPipeline(Wf, Hf, chunk, grad is not None, device=dev)
         pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream)  # warm
         if ws > 1:
             tdist.barrier()
@@ -428,10 +429,29 @@ def main():
         a1.record(stream)
         torch.cuda.synchronize()
         e_ms = cdist.max_over_ranks(a0.elapsed_time(a1) / args.e2e_steps, device=dev)
+        h2d_b = E * Wf * Hf * (8 + (0 if grad is None else 8))
+        d2h_b = E * (Wf * Hf * 16 + nwaves * 4)
+        # the link bound: each direction's pinned-copy bandwidth, measured alone
+        bw = {}
+        for name, (src, dst) in {"h2d": (out_h, out), "d2h": (out, out_h)}.items():
+            n = min(src[0].numel(), dst[0].numel()) * 4
+            s_, d_ = src[0].view(-1), dst[0].view(-1)
+            d_.copy_(s_, non_blocking=True)
+            torch.cuda.synchronize()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            for _ in range(5):
+                d_.copy_(s_, non_blocking=True)
+            b1.record(stream)
+            torch.cuda.synchronize()
+            bw[name] = 5 * n / (b0.elapsed_time(b1) / 1e3) / 1e9
+        link_ms = max(h2d_b / bw["h2d"], d2h_b / bw["d2h"]) / 1e6
         e2e = {"value": ws * E * Wf * Hf / (e_ms / 1e3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": E * Wf * Hf * (8 + (0 if grad is None else 8)),
-               "d2h_bytes_per_step": E * (Wf * Hf * 16 + nwaves * 4), "frames_per_step": E,
-               "ms_per_step": e_ms, "api": "ctf_filter_frames_host (pinned host buffers)"}
+               "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "frames_per_step": E,
+               "chunk_frames": chunk, "ms_per_step": e_ms,
+               "pcie_gbs": {"h2d": bw["h2d"], "d2h": bw["d2h"]},
+               "link_bound_ms_per_step": link_ms, "link_frac": link_ms / e_ms,
+               "api": "ctf_filter_frames_host (pinned host buffers)"}
         del uv_h, g_h, out_h, rec_h, pipe
 
     configs = None

@@ -28,6 +28,15 @@
 namespace ctf {
 
 constexpr int kWarps = 8;  // warps per CTA
+#ifndef CTF_BC1_MINB
+#define CTF_BC1_MINB 4  // BC1: resident CTAs per SM (64 registers)
+#endif
+#ifndef CTF_BC1_ROUNDS
+#define CTF_BC1_ROUNDS 8  // BC1: target CTAs per resident CTA slot
+#endif
+#ifndef CTF_BC1_MAX_IPW
+#define CTF_BC1_MAX_IPW 4  // BC1: at most this many work items per warp
+#endif
 #ifndef CTF_MLP_COLLAB_MINB
 #define CTF_MLP_COLLAB_MINB 2  // latent-MLP COLLAB: resident CTAs per SM (register budget)
 #endif
@@ -43,6 +52,7 @@ struct KArgs {
     int Wf, Hf, nwx, nwy, wpf;
     int cpr, cpf;                   // work items (runs of kChunk waves) per wave-row / per frame
     unsigned nchunks;
+    unsigned ipc;                   // work items per CTA (claimed dynamically by its warps)
     float Wflt, Hflt;
     int fallback;
     int variant;                    // COLLAB kernel: VAR_LIST / VAR_BOX / VAR_MASK16 / VAR_MASK11
@@ -269,45 +279,62 @@ template <int FMT>
 __device__ __forceinline__ float4 combine_eq1(const Foot &f, const bool (&first)[4], const float (&dw)[4],
                                               const bool (&known)[4], const int (&dup)[4], const Texel<FMT> (&p)[4],
                                               bool wc) {
+    // Branch-free over the lane's cases (R-23).  The oracle's special cases hold bitwise:
+    // every nonzero-weight texel known -> blend4 over the corners, i.e. exact bilinear
+    // (c8); N = 1 -> that texel (Sp = p exactly).  Otherwise C / C+ evaluate
+    // Eq. 1 as blend4 over the known corners (= sum w_i p_i) plus (1 - Sw) / N * Sp,
+    // which agrees with the oracle's fmaf chain to fp32 rounding.
     bool all_known = true;
-    int N = 0, last = 0;
-    float Sw = 0.f, Swp[4] = {0.f, 0.f, 0.f, 0.f}, Sp[4] = {0.f, 0.f, 0.f, 0.f};
+    int N = 0;
+    float Sw = 0.f, Sp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if (!first[k] || dw[k] == 0.0f) continue;
         if (!known[k]) { all_known = false; continue; }
         ++N;
-        last = k;
         Sw += dw[k];
         float v[4];
         p[k].expand(v);
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-            Swp[ch] = fmaf(dw[k], v[ch], Swp[ch]);
-            Sp[ch] += v[ch];
-        }
+        for (int ch = 0; ch < 4; ++ch) Sp[ch] += v[ch];
     }
-    if (all_known) {  // every nonzero-weight texel known -> exact bilinear
-        Texel<FMT> q[4];
+    Texel<FMT> q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int d = dup[k];
+        const Texel<FMT> src = d == 0 ? p[0] : d == 1 ? p[1] : d == 2 ? p[2] : p[3];
+        const bool kd = d == 0 ? known[0] : d == 1 ? known[1] : d == 2 ? known[2] : known[3];
+        q[k] = kd ? src : Texel<FMT>::zero();
+    }
+    const float4 bl = blend4<FMT>(q, f.w);  // sum over the known corners of w_k p_k (scaled)
+    const float sc = Texel<FMT>::kScale;
+    const bool one = N == 1 && !all_known;
+    float c[4];
+    if (wc) {  // WC stand-in (R-16): weights renormalised over the known texels
+        float Swp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int d = dup[k];
-            const Texel<FMT> src = d == 0 ? p[0] : d == 1 ? p[1] : d == 2 ? p[2] : p[3];
-            const bool kd = d == 0 ? known[0] : d == 1 ? known[1] : d == 2 ? known[2] : known[3];
-            q[k] = kd ? src : Texel<FMT>::zero();
+            if (!first[k] || dw[k] == 0.0f || !known[k]) continue;
+            float v[4];
+            p[k].expand(v);
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) Swp[ch] = fmaf(dw[k], v[ch], Swp[ch]);
         }
-        return blend4<FMT>(q, f.w);
+        const float r = sc / Sw;
+        c[0] = all_known ? bl.x : Swp[0] * r;
+        c[1] = all_known ? bl.y : Swp[1] * r;
+        c[2] = all_known ? bl.z : Swp[2] * r;
+        c[3] = all_known ? bl.w : Swp[3] * r;
+    } else {  // Eq. 1
+        const float rest = (all_known || N == 0) ? 0.0f : __fdividef(1.0f - Sw, (float)N) * sc;
+        c[0] = fmaf(rest, Sp[0], bl.x);
+        c[1] = fmaf(rest, Sp[1], bl.y);
+        c[2] = fmaf(rest, Sp[2], bl.z);
+        c[3] = fmaf(rest, Sp[3], bl.w);
     }
-    if (N == 1) return scaled<FMT>(last == 0 ? p[0] : last == 1 ? p[1] : last == 2 ? p[2] : p[3]);
-    const float sc = Texel<FMT>::kScale;
-    float c[4];
-    if (wc) {
+    if (one) {
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) c[ch] = Swp[ch] / Sw * sc;
-    } else {
-        const float rest = (1.0f - Sw) / (float)N;
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(rest, Sp[ch], Swp[ch]) * sc;
+        for (int ch = 0; ch < 4; ++ch) c[ch] = Sp[ch] * sc;
     }
     return make_float4(c[0], c[1], c[2], c[3]);
 }
@@ -716,7 +743,7 @@ __device__ __forceinline__ float4 mlp_decode_batched(const TexArgs &t, const Mlp
 constexpr int kChunk = 16;  // waves per work item: a run of consecutive waves in one wave-row
 
 template <int FMT, int MODE, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MODE_COLLAB ? CTF_MLP_COLLAB_MINB : 2)))
+__global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : (MODE == MODE_COLLAB ? CTF_MLP_COLLAB_MINB : 2)))
     ctf_filter_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ WarpSmem smem[kWarps];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent-MLP COLLAB: batch buffers
@@ -727,10 +754,31 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? 4 : (MODE == MO
     if constexpr (kBatchMlp) load_lane_weights(a.tex.mlp_dev, lane, lw);
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned lt = lanemask_lt();
-    const unsigned nwarps = gridDim.x * kWarps;
 
-    // work item c = (frame, wave-row, run of kChunk waves); warps stride over items
-    for (unsigned c = blockIdx.x * kWarps + warp; c < a.nchunks; c += nwarps) {
+    // work item c = (frame, wave-row, run of kChunk waves); items are interleaved over
+    // the whole batch so every warp gets the same mix of sky / exact / fallback regions.
+    //   BC1: warp (b, w) takes items b*kWarps + w + j*gridDim.x*kWarps, j < ipc/kWarps
+    //        (short static lists; the grid is many CTAs and the block scheduler balances);
+    //   MLP: one CTA per slot, CTA b owns items b + k*gridDim.x and its warps claim k
+    //        from a shared counter (long items, per-warp weight preload).
+    __shared__ unsigned s_next;
+    if constexpr (FMT != FMT_BC1) {
+        if (threadIdx.x == 0) s_next = kWarps;
+        __syncthreads();
+    }
+    const unsigned per_warp = a.ipc / kWarps;
+    for (unsigned k = warp;;) {
+        const unsigned c = (FMT == FMT_BC1)
+                               ? (blockIdx.x * kWarps + (k % kWarps)) + (k / kWarps) * gridDim.x * kWarps
+                               : blockIdx.x + k * gridDim.x;
+        if ((FMT == FMT_BC1 ? k / kWarps >= per_warp : k >= a.ipc) || c >= a.nchunks) break;
+        if constexpr (FMT == FMT_BC1) {
+            k += kWarps;
+        } else {
+            unsigned nx = 0u;
+            if (lane == 0) nx = atomicAdd(&s_next, 1u);
+            k = __shfl_sync(FULL, nx, 0);
+        }
         const int fr = (int)(c / (unsigned)a.cpf);
         const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
         const int wy = rr / a.cpr;
@@ -1006,12 +1054,37 @@ static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, 
     if (dyn > 0) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         if (e != cudaSuccess) return e;
+        // ask for a shared-memory carveout that holds the register-limited number of CTAs
+        // (the default config can be too small for two 58 KB CTAs, halving occupancy)
+        int max_smem = 0, regs_ctas = 0;
+        e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        if (e != cudaSuccess) return e;
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, kern);
+        if (e != cudaSuccess) return e;
+        regs_ctas = 65536 / (fa.numRegs * kWarps * 32);
+        const size_t per_cta = dyn + fa.sharedSizeBytes + 1024;  // + the driver's reserved 1 KB
+        const int pct = (int)((100 * per_cta * (size_t)(regs_ctas > 0 ? regs_ctas : 1) + max_smem - 1) / max_smem);
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+        if (e != cudaSuccess) return e;
     }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, dyn);
     if (e != cudaSuccess) return e;
-    const long long need = ((long long)k.nchunks + kWarps - 1) / kWarps;
-    long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
-    if (grid > need) grid = need;
+    // items per CTA.  BC1: ipc / kWarps items per warp, 1..4, about CTF_BC1_ROUNDS CTAs
+    // per resident slot (small batches keep the tail short; 4 per warp bounds the number
+    // of CTAs of a 64-frame batch).  Latent-MLP: one CTA per slot.
+    const long long slots = (long long)sms * (per_sm > 0 ? per_sm : 1);
+    long long ipc;
+    if (FMT == FMT_BC1) {
+        long long ipw = ((long long)k.nchunks + slots * kWarps * CTF_BC1_ROUNDS / 2) / (slots * kWarps * CTF_BC1_ROUNDS);
+        ipw = ipw < 1 ? 1 : ipw > CTF_BC1_MAX_IPW ? CTF_BC1_MAX_IPW : ipw;
+        ipc = ipw * kWarps;
+    } else {
+        ipc = ((long long)k.nchunks + slots - 1) / slots;
+        if (ipc < 1) ipc = 1;
+    }
+    k.ipc = (unsigned)ipc;
+    long long grid = ((long long)k.nchunks + ipc - 1) / ipc;
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, kWarps * 32, dyn, stream>>>(k, mw);
     return cudaGetLastError();
