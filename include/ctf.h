@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define CTF_ABI_VERSION 1
+#define CTF_ABI_VERSION 2
 
 typedef enum {
     CTF_OK = 0,
@@ -99,12 +99,29 @@ enum {
     CTF_FLAG_FORCE_FALLBACK = 1u << 1  /* COLLAB: every wave runs the fallback */
 };
 
+/* Texture filters (§5.4 "Bicubic Filtering").  The bicubic filters use a 4x4
+ * footprint (taps x0-1..x0+2, y0-1..y0+2, clamp-to-edge) with the weights of DESIGN.md
+ * R-25; every mode above applies except WAVECOMM (mode and fallback -> EUNSUPPORTED), and
+ * with a bicubic filter:
+ *   - BILINEAR_4TAP means the full filter (16 evaluations per pixel);
+ *   - STF is the positivized two-lobe estimator, 1-2 evaluations per pixel;
+ *   - the fallbacks draw their one-tap samples with probability |w| / sum |w|;
+ *   - max_evals = 2 lets the exact path use up to 2 evaluations per lane (n <= 2a,
+ *     P:917-931 and Fig. 13b); the fallbacks keep <= 1. */
+typedef enum {
+    CTF_FILTER_BILINEAR = 0,
+    CTF_FILTER_BSPLINE = 1,      /* uniform cubic B-spline (approximating, weights >= 0)      */
+    CTF_FILTER_CATMULL_ROM = 2   /* Catmull-Rom (interpolating, negative lobes)               */
+} ctf_filter;
+
 typedef struct {
     int32_t mode;          /* ctf_mode                                                     */
     int32_t fallback;      /* ctf_fallback; used by the collaborative modes (COLLAB..MASK11)*/
     uint32_t flags;        /* CTF_FLAG_*                                                   */
     uint32_t frame_index;  /* RNG counter word; batch frame f uses frame_index + f          */
     uint64_t seed;         /* RNG key (R-11: Philox4x32-10, ctr = (x, y, frame, 0))         */
+    int32_t filter;        /* ctf_filter (ABI 2); 0 = bilinear                             */
+    int32_t max_evals;     /* exact-path evaluations per lane: 0 or 1, or 2 (bicubic only)  */
 } ctf_params;
 
 /* Optional per-pixel debug outputs (only with CTF_FLAG_DEBUG; any may be NULL). */
@@ -120,17 +137,19 @@ typedef struct {
 
 /*
  * Per-wave record (u32), one per wave, [frames][ceil(Hf/4)][ceil(Wf/8)]:
- *   bits 0-7   texel evaluations in the wave (exact: n, Box: AABB area; 4TAP: 4a;
- *              STF/WC/C: a; C+: n_p + spare lanes that produced)
+ *   bits 0-7   texel evaluations in the wave, low 8 bits (exact: n, Box: AABB area;
+ *              4TAP: 4a (16a bicubic); STF/WC/C: a (positivized STF: 1-2 per lane); C+:
+ *              n_p + spare lanes that produced); bits 27-29 hold bits 8-10
  *   bits 8-15  n = number of unique texels the wave needs (collaborative modes; 0xFF
- *              for 4TAP / STF / WC)
+ *              for 4TAP / STF / WC).  Bicubic: saturated at max_evals * a + 1 (R-28)
  *   bits 16-21 a = active lanes
  *   bits 22-24 path: 0 exact, 1 fb-STF, 2 fb-WC, 3 fb-C, 4 fb-C+, 5 4TAP, 6 STF, 7 WC
  *   bit  25    magnified: grad given and every active lane has
  *              max(|J_x|^2, |J_y|^2) <= 1 in texel units (R-20)
  *   bit  26    partial: a < 32
+ *   bits 27-29 evals bits 8-10
  */
-#define CTF_REC_EVALS(r) ((r) & 0xFFu)
+#define CTF_REC_EVALS(r) (((r) & 0xFFu) | ((((r) >> 27) & 0x7u) << 8))
 #define CTF_REC_N(r) (((r) >> 8) & 0xFFu)
 #define CTF_REC_A(r) (((r) >> 16) & 0x3Fu)
 #define CTF_REC_PATH(r) (((r) >> 22) & 0x7u)

@@ -28,6 +28,12 @@
  *     evaluation, never by the paper ("parity unpinned" by the paper);
  *   - the WC stand-in rule (R-16) and the C+ selection law (R-18 v):
  *     pinned only by their special cases ("parity unpinned" beyond those).
+ * Bicubic filters (wave_bicubic, R-24..R-28) are pinned in
+ * tests/test_oracle_bicubic.py by the kernels' closed-form moments, texel-centre
+ * interpolation / smoothing, linear reproduction on a ramp, brute-force unique
+ * sets and the expectations of the stochastic estimators; the C+ selection law
+ * for bicubic (R-18 v with |w|) is, as for bilinear, pinned only by its special
+ * cases.
  */
 #include <math.h>
 #include <stdint.h>
@@ -565,46 +571,412 @@ static void wave(const frame_t *F, int wx, int wy)
     }
 }
 
+/* ========================================================================= */
+/* Bicubic filters: cubic B-spline and Catmull-Rom (§5.4; the      */
+/* 4x4 footprint and "<= 2 evaluations per lane", Fig. 13          */
+/* P:1731-1753).  Readings R-24 .. R-28 in DESIGN.md.                         */
+/* ========================================================================= */
+enum { FILTER_BILINEAR = 0, FILTER_BSPLINE = 1, FILTER_CATMULL_ROM = 2 };
+
+/* R-25: weights of the taps x0-1, x0, x0+1, x0+2 at fraction s in [0,1); the
+ * uniform cubic B-spline and Catmull-Rom kernels (the paper names the filters,
+ * P:704-708, not their formulas).  fp32, one rounding per operation, in the
+ * order written (they decide integers: STF / C+ picks). */
+void oracle_cubic_weights(int filter, float s, float w[4])
+{
+    float r = 1.0f - s;
+    float s2 = s * s, s3 = s2 * s, r2 = r * r;
+    if (filter == FILTER_BSPLINE) {
+        float r3 = r2 * r;
+        w[0] = r3 / 6.0f;
+        w[1] = ((3.0f * s3 - 6.0f * s2) + 4.0f) / 6.0f;
+        w[2] = (((3.0f * s2 - 3.0f * s3) + 3.0f * s) + 1.0f) / 6.0f;
+        w[3] = s3 / 6.0f;
+    } else {
+        w[0] = -0.5f * (s * r2);
+        w[1] = ((3.0f * s3 - 5.0f * s2) + 2.0f) * 0.5f;
+        w[2] = ((4.0f * s2 - 3.0f * s3) + s) * 0.5f;
+        w[3] = -0.5f * (s2 * r);
+    }
+}
+
+typedef struct {
+    int active, magnified;
+    int x[4], y[4];        /* clamped tap columns x0-1+i and rows y0-1+j (R-24)          */
+    float wx[4], wy[4];    /* tap weights (R-25)                                           */
+    int xa, nc, ya, nr;    /* distinct columns xa..xa+nc-1, rows ya..ya+nr-1              */
+    float mx[4], my[4];    /* per distinct column / row: sum of its taps' weights, fp32,
+                              taps in ascending order (clamp duplicates merge, R-25)        */
+} lane16_t;
+
+static void make_lane16(lane16_t *L, int filter, const float *uv, const uint16_t *grad, int W, int H)
+{
+    /* R-24: the same coordinate rule as the bilinear footprint (R-2) */
+    float uc = fminf(fmaxf(uv[0], 0.0f), 1.0f);
+    float vc = fminf(fmaxf(uv[1], 0.0f), 1.0f);
+    float fx = fmaf(uc, (float)W, -0.5f), fy = fmaf(vc, (float)H, -0.5f);
+    float flx = floorf(fx), fly = floorf(fy);
+    int x0 = (int)flx, y0 = (int)fly;
+    oracle_cubic_weights(filter, fx - flx, L->wx);
+    oracle_cubic_weights(filter, fy - fly, L->wy);
+    for (int i = 0; i < 4; ++i) {
+        L->x[i] = clampi(x0 - 1 + i, 0, W - 1);
+        L->y[i] = clampi(y0 - 1 + i, 0, H - 1);
+    }
+    L->xa = L->x[0]; L->nc = L->x[3] - L->x[0] + 1;
+    L->ya = L->y[0]; L->nr = L->y[3] - L->y[0] + 1;
+    for (int i = 0; i < 4; ++i) { L->mx[i] = 0.0f; L->my[i] = 0.0f; }
+    for (int i = 0; i < 4; ++i) {
+        L->mx[L->x[i] - L->xa] = L->mx[L->x[i] - L->xa] + L->wx[i];
+        L->my[L->y[i] - L->ya] = L->my[L->y[i] - L->ya] + L->wy[i];
+    }
+    L->magnified = 0;
+    if (grad) {   /* R-20, unchanged */
+        float g0 = half_to_float(grad[0]), g1 = half_to_float(grad[1]);
+        float g2 = half_to_float(grad[2]), g3 = half_to_float(grad[3]);
+        volatile float a0 = g0 * g0, a1 = g1 * g1, a2 = g2 * g2, a3 = g3 * g3;
+        float rx = a0 + a1, ry = a2 + a3;
+        L->magnified = ((rx > ry ? rx : ry) <= 1.0f);
+    }
+}
+
+static uint32_t cell_id(const lane16_t *L, int c, int r, int W)
+{
+    return (uint32_t)(L->ya + r) * (uint32_t)W + (uint32_t)(L->xa + c);
+}
+
+/* the plain definition: sum over the 16 taps of wx_i * wy_j * p(x_i, y_j), fp64 */
+static void blend16_exact(const tex_t *tex, const lane16_t *L, double c[4])
+{
+    for (int ch = 0; ch < 4; ++ch) c[ch] = 0.0;
+    for (int j = 0; j < 4; ++j)
+        for (int i = 0; i < 4; ++i) {
+            double p[4];
+            produce(tex, (uint32_t)L->y[j] * (uint32_t)tex->W + (uint32_t)L->x[i], p);
+            double w = (double)L->wx[i] * (double)L->wy[j];
+            for (int ch = 0; ch < 4; ++ch) c[ch] += w * p[ch];
+        }
+}
+
+/* R-26 one-tap STF for a separable filter: column ~ |wx|, row ~ |wy| (so P(tap) =
+ * |w_ij| / sum |w|, "absolute values of filter weights"), each by the
+ * inverse CDF in fp32 (first cumulative sum > u * S, else the last nonzero tap). */
+static int cubic_pick(const float w[4], float u, float *S_out)
+{
+    float S = 0.0f;
+    int last = 0;
+    for (int i = 0; i < 4; ++i) { S = S + fabsf(w[i]); if (w[i] != 0.0f) last = i; }
+    volatile float target = u * S;
+    float cum = 0.0f;
+    *S_out = S;
+    for (int i = 0; i < 4; ++i) {
+        cum = cum + fabsf(w[i]);
+        if (cum > target) return i;
+    }
+    return last;
+}
+
+/* the one-tap estimate sign(w) * (Sx * Sy) * p of lane L's STF tap; returns its id */
+static uint32_t stf16(const tex_t *tex, const lane16_t *L, const double u[4], double c[4])
+{
+    float Sx, Sy;
+    int i = cubic_pick(L->wx, (float)u[0], &Sx);
+    int j = cubic_pick(L->wy, (float)u[1], &Sy);
+    uint32_t id = (uint32_t)L->y[j] * (uint32_t)tex->W + (uint32_t)L->x[i];
+    if (c) {
+        double p[4];
+        produce(tex, id, p);
+        double sgn = ((L->wx[i] < 0.0f) != (L->wy[j] < 0.0f)) ? -1.0 : 1.0;
+        for (int ch = 0; ch < 4; ++ch) c[ch] = sgn * (double)Sx * (double)Sy * p[ch];
+    }
+    return id;
+}
+
+/* R-27 positivized STF (the paper's 2-evaluation baseline for filters with negative
+ * lobes): taps k = 4j + i in row-major order with w_k = wx_i * wy_j (fp32);
+ * W+ = sum of positive w_k, W- = sum of -w_k over negative ones (fp32, k ascending);
+ * p+ ~ w_k over the positive taps (u0), p- ~ -w_k over the negative taps (u1), by the
+ * inverse CDF as in R-26; c = W+ p+ - W- p-.  Returns the number of evaluations. */
+static int stf16_positivized(const tex_t *tex, const lane16_t *L, const double u[4], double c[4])
+{
+    float wk[16], Wp = 0.0f, Wn = 0.0f;
+    int lastp = -1, lastn = -1;
+    for (int k = 0; k < 16; ++k) {
+        wk[k] = L->wx[k & 3] * L->wy[k >> 2];
+        if (wk[k] > 0.0f) { Wp = Wp + wk[k]; lastp = k; }
+        else if (wk[k] < 0.0f) { Wn = Wn + (-wk[k]); lastn = k; }
+    }
+    for (int ch = 0; ch < 4; ++ch) c[ch] = 0.0;
+    int evals = 0;
+    for (int lobe = 0; lobe < 2; ++lobe) {
+        float Wl = lobe ? Wn : Wp;
+        if (!(Wl > 0.0f)) continue;
+        volatile float target = (float)u[lobe] * Wl;
+        float cum = 0.0f;
+        int pick = lobe ? lastn : lastp;
+        for (int k = 0; k < 16; ++k) {
+            if (lobe ? !(wk[k] < 0.0f) : !(wk[k] > 0.0f)) continue;
+            cum = cum + (lobe ? -wk[k] : wk[k]);
+            if (cum > target) { pick = k; break; }
+        }
+        double p[4];
+        produce(tex, (uint32_t)L->y[pick >> 2] * (uint32_t)tex->W + (uint32_t)L->x[pick & 3], p);
+        for (int ch = 0; ch < 4; ++ch) c[ch] += (lobe ? -(double)Wl : (double)Wl) * p[ch];
+        ++evals;
+    }
+    return evals;
+}
+
+/* Eq. 1 over the known cells of L's footprint: distinct texels in
+ * row-major order with merged weight mw = mx[c] * my[r] (fp32) != 0 (R-14, R-28). */
+static void blend16_fallback(const tex_t *tex, const lane16_t *L, const uint32_t *produced, int nprod,
+                             double c[4])
+{
+    int all_known = 1, N = 0;
+    double Swp[4] = { 0, 0, 0, 0 }, Sp[4] = { 0, 0, 0, 0 }, Sw = 0.0, plast[4] = { 0, 0, 0, 0 };
+    for (int r = 0; r < L->nr; ++r)
+        for (int q = 0; q < L->nc; ++q) {
+            float mw = L->mx[q] * L->my[r];
+            if (mw == 0.0f) continue;
+            uint32_t id = cell_id(L, q, r, tex->W);
+            if (!in_list(produced, nprod, id)) { all_known = 0; continue; }
+            double p[4];
+            produce(tex, id, p);
+            for (int ch = 0; ch < 4; ++ch) { Swp[ch] += (double)mw * p[ch]; Sp[ch] += p[ch]; plast[ch] = p[ch]; }
+            Sw += (double)mw;
+            ++N;
+        }
+    if (all_known) { blend16_exact(tex, L, c); return; }
+    if (N == 1) { for (int ch = 0; ch < 4; ++ch) c[ch] = plast[ch]; return; }
+    for (int ch = 0; ch < 4; ++ch) c[ch] = Swp[ch] + (1.0 - Sw) * Sp[ch] / N;   /* Eq. 1 */
+}
+
+static void wave_bicubic(const frame_t *F, int filter, int E, int wx, int wy)
+{
+    const tex_t *tex = F->tex;
+    const int W = tex->W;
+    lane16_t L[32];
+    int px[32], py[32], inframe[32];
+    uint32_t A = 0;
+    for (int lane = 0; lane < 32; ++lane) {
+        px[lane] = wx * 8 + (lane & 7);
+        py[lane] = wy * 4 + (lane >> 3);
+        inframe[lane] = px[lane] < F->Wf && py[lane] < F->Hf;
+        memset(&L[lane], 0, sizeof(lane16_t));
+        if (!inframe[lane]) continue;
+        size_t pix = (size_t)py[lane] * F->Wf + px[lane];
+        const float *uvp = F->uv + 2 * pix;
+        if (isnan(uvp[0])) continue;
+        L[lane].active = 1;
+        A |= 1u << lane;
+        make_lane16(&L[lane], filter, uvp, F->grad ? F->grad + 4 * pix : NULL, W, tex->H);
+    }
+    int a = __builtin_popcount(A);
+    int nwx = (F->Wf + 7) / 8;
+    uint32_t *rec = &F->rec[(size_t)wy * nwx + wx];
+    double col[32][4];
+    for (int lane = 0; lane < 32; ++lane) for (int ch = 0; ch < 4; ++ch) col[lane][ch] = 0.0;
+    int magnified = 0;
+    if (F->grad && a > 0) {
+        magnified = 1;
+        for (int lane = 0; lane < 32; ++lane) if (L[lane].active && !L[lane].magnified) magnified = 0;
+    }
+    int act[32];
+    for (int r = 0; r < a; ++r) act[r] = oracle_h((uint32_t)r, A);
+    double u[32][4];
+    for (int lane = 0; lane < 32; ++lane)
+        if (L[lane].active) pixel_uniforms(px[lane], py[lane], F->frame, F->seed, u[lane]);
+
+    int n = 0xFF, evals = 0, path = 0, run_fallback = -1;
+    if (F->mode == M_4TAP) {
+        /* the full filter: 16 evaluations per pixel */
+        path = PATH_4TAP;
+        for (int lane = 0; lane < 32; ++lane) if (L[lane].active) blend16_exact(tex, &L[lane], col[lane]);
+        evals = 16 * a;
+    } else if (F->mode == M_STF) {
+        path = PATH_STF;
+        for (int lane = 0; lane < 32; ++lane)
+            if (L[lane].active) evals += stf16_positivized(tex, &L[lane], u[lane], col[lane]);
+    } else {
+        /* collect: the exact set of distinct texels over all active 4x4 footprints (R-4) */
+        uint32_t *U = (uint32_t *)malloc(sizeof(uint32_t) * 512);
+        int m = 0, minx = 1 << 30, maxx = -1, miny = 1 << 30, maxy = -1;
+        for (int lane = 0; lane < 32; ++lane) {
+            if (!L[lane].active) continue;
+            for (int r = 0; r < L[lane].nr; ++r)
+                for (int q = 0; q < L[lane].nc; ++q) U[m++] = cell_id(&L[lane], q, r, W);
+            if (L[lane].xa < minx) minx = L[lane].xa;
+            if (L[lane].ya < miny) miny = L[lane].ya;
+            if (L[lane].xa + L[lane].nc - 1 > maxx) maxx = L[lane].xa + L[lane].nc - 1;
+            if (L[lane].ya + L[lane].nr - 1 > maxy) maxy = L[lane].ya + L[lane].nr - 1;
+        }
+        int nu = sort_unique(U, m);
+        free(U);
+        const int cap = E * a;                      /* <= E evaluations per lane */
+        n = nu < cap + 1 ? nu : cap + 1;            /* record: n saturated at E*a + 1 (R-28) */
+        int ok = 0, bw = 0, bh = 0;
+        if (a > 0) {
+            bw = maxx - minx + 1;
+            bh = maxy - miny + 1;
+            if (F->mode == M_BOX) ok = bw * bh <= cap;
+            else if (F->mode == M_MASK16) ok = bw <= 16 && bh <= 16 && nu <= cap;
+            else if (F->mode == M_MASK11) ok = bw <= 11 && bh <= 11 && nu <= cap;
+            else ok = nu <= cap;
+        }
+        if (a > 0 && ok && !(F->flags & FL_FORCE_FALLBACK)) {
+            /* rank r (or Box index r) is produced by lane h(r mod a, A) as its
+             * (r div a)-th evaluation; the result is the plain 16-tap filter */
+            path = PATH_EXACT;
+            evals = (F->mode == M_BOX) ? bw * bh : nu;
+            for (int lane = 0; lane < 32; ++lane) if (L[lane].active) blend16_exact(tex, &L[lane], col[lane]);
+        } else {
+            run_fallback = F->fallback;
+            path = PATH_FB_STF + F->fallback;
+        }
+    }
+
+    if (run_fallback == FB_STF) {
+        for (int lane = 0; lane < 32; ++lane) if (L[lane].active) stf16(tex, &L[lane], u[lane], col[lane]);
+        evals = a;
+    } else if (run_fallback == FB_C || run_fallback == FB_CPLUS) {
+        /* planned texels: every lane's one-tap STF choice (R-26) */
+        uint32_t P[32], produced[32];
+        int np = 0, nprod = 0;
+        for (int lane = 0; lane < 32; ++lane)
+            if (L[lane].active) P[np++] = stf16(tex, &L[lane], u[lane], NULL);
+        if (run_fallback == FB_C) {
+            for (int i = 0; i < np; ++i) produced[nprod++] = P[i];      /* every lane produces */
+            evals = a;
+        } else {
+            np = sort_unique(P, np);                                     /* C+ plan (R-17) */
+            for (int i = 0; i < np; ++i) produced[nprod++] = P[i];
+            for (int j = np; j < a; ++j) {                               /* Eq. 2 spare lanes */
+                int cl = act[j];
+                const lane16_t *Ll = &L[act[oracle_eq2(j, np, a)]];
+                uint32_t fid[16]; float fw[16]; int nf = 0;
+                for (int r = 0; r < Ll->nr; ++r)
+                    for (int q = 0; q < Ll->nc; ++q) {
+                        float mw = Ll->mx[q] * Ll->my[r];
+                        uint32_t id = cell_id(Ll, q, r, W);
+                        if (mw == 0.0f || in_list(P, np, id)) continue;
+                        fid[nf] = id; fw[nf] = fabsf(mw); ++nf;
+                    }
+                if (nf == 0) continue;
+                float wsum = 0.0f;
+                for (int q = 0; q < nf; ++q) wsum = wsum + fw[q];
+                volatile float target = (float)u[cl][2] * wsum;
+                int pick = nf - 1;
+                float cum = 0.0f;
+                for (int q = 0; q < nf; ++q) {
+                    cum = cum + fw[q];
+                    if (cum > target) { pick = q; break; }
+                }
+                produced[nprod++] = fid[pick];
+            }
+            evals = nprod;
+        }
+        for (int lane = 0; lane < 32; ++lane)
+            if (L[lane].active) blend16_fallback(tex, &L[lane], produced, nprod, col[lane]);
+    }
+
+    if (a == 0) { evals = 0; path = 0; if (F->mode >= M_COLLAB) n = 0; }
+    *rec = (uint32_t)(evals & 0xFF) | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)a << 16) |
+           ((uint32_t)path << 22) | ((uint32_t)magnified << 25) | ((uint32_t)(a < 32) << 26) |
+           ((uint32_t)((evals >> 8) & 7) << 27);
+    for (int lane = 0; lane < 32; ++lane) {
+        if (!inframe[lane]) continue;
+        size_t pix = (size_t)py[lane] * F->Wf + px[lane];
+        for (int ch = 0; ch < 4; ++ch) F->out[4 * pix + ch] = col[lane][ch];
+        if (F->produced_id) F->produced_id[pix] = INVALID_ID;
+        if (F->selection) F->selection[pix] = 0;
+    }
+}
+
 /* ------------------------------------------------------------------------- */
 /* Frame entry.  Returns 0, or -1 on invalid arguments.                       */
 /*   out: fp64 [Hf][Wf][4]; rec: u32 [ceil(Hf/4)][ceil(Wf/8)];                */
 /*   produced_id / selection: u32 [Hf][Wf] or NULL.                           */
 /* ------------------------------------------------------------------------- */
-int oracle_filter_frame(int format, int W, int H, const uint8_t *bc1, const uint16_t *latent,
-                        const float *mlp, const float *uv, const uint16_t *grad, int Wf, int Hf,
-                        int mode, int fallback, unsigned flags, uint64_t seed, uint32_t frame_index,
-                        double *out, uint32_t *rec, uint32_t *produced_id, uint32_t *selection)
+static int check_args(int format, int W, int H, const uint8_t *bc1, const uint16_t *latent, const float *mlp,
+                      const float *uv, int Wf, int Hf, int mode, int fallback, int filter, int max_evals,
+                      const double *out, const uint32_t *rec)
 {
     if (W <= 0 || H <= 0 || Wf <= 0 || Hf <= 0 || !uv || !out || !rec) return -1;
     if (format == FMT_BC1 && (!bc1 || W % 4 || H % 4)) return -1;
     if (format == FMT_LATENT_MLP && (!latent || !mlp || W % 4 || H % 4)) return -1;
     if (format != FMT_BC1 && format != FMT_LATENT_MLP) return -1;
     if (mode < 0 || mode > 6 || fallback < 0 || fallback > 3) return -1;
-    tex_t tex = { format, W, H, bc1, latent, mlp };
-    frame_t F = { &tex, uv, grad, Wf, Hf, mode, fallback, flags, seed, frame_index,
-                  out, rec, produced_id, selection };
-    int nwx = (Wf + 7) / 8, nwy = (Hf + 3) / 4;
-    long nw = (long)nwx * nwy;
-#pragma omp parallel for schedule(dynamic, 64)
-    for (long w = 0; w < nw; ++w) wave(&F, (int)(w % nwx), (int)(w / nwx));
+    if (filter < FILTER_BILINEAR || filter > FILTER_CATMULL_ROM || max_evals < 0 || max_evals > 2) return -1;
+    if (filter == FILTER_BILINEAR && max_evals > 1) return -1;
+    if (filter != FILTER_BILINEAR && (mode == M_WC || fallback == FB_WC)) return -1;   /* R-28 */
     return 0;
 }
 
+static void run_wave(const frame_t *F, int filter, int E, int wx, int wy)
+{
+    if (filter == FILTER_BILINEAR) wave(F, wx, wy);
+    else wave_bicubic(F, filter, E, wx, wy);
+}
+
+/* filter: 0 bilinear, 1 cubic B-spline, 2 Catmull-Rom (R-25); max_evals: texel
+ * evaluations per lane on the exact path, 0/1 or 2 (bicubic only). */
+int oracle_filter_frame2(int format, int W, int H, const uint8_t *bc1, const uint16_t *latent,
+                         const float *mlp, const float *uv, const uint16_t *grad, int Wf, int Hf,
+                         int mode, int fallback, unsigned flags, uint64_t seed, uint32_t frame_index,
+                         int filter, int max_evals,
+                         double *out, uint32_t *rec, uint32_t *produced_id, uint32_t *selection)
+{
+    if (check_args(format, W, H, bc1, latent, mlp, uv, Wf, Hf, mode, fallback, filter, max_evals, out, rec))
+        return -1;
+    tex_t tex = { format, W, H, bc1, latent, mlp };
+    frame_t F = { &tex, uv, grad, Wf, Hf, mode, fallback, flags, seed, frame_index,
+                  out, rec, produced_id, selection };
+    int E = max_evals < 1 ? 1 : max_evals;
+    int nwx = (Wf + 7) / 8, nwy = (Hf + 3) / 4;
+    long nw = (long)nwx * nwy;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (long w = 0; w < nw; ++w) run_wave(&F, filter, E, (int)(w % nwx), (int)(w / nwx));
+    return 0;
+}
+
+int oracle_filter_frame(int format, int W, int H, const uint8_t *bc1, const uint16_t *latent,
+                        const float *mlp, const float *uv, const uint16_t *grad, int Wf, int Hf,
+                        int mode, int fallback, unsigned flags, uint64_t seed, uint32_t frame_index,
+                        double *out, uint32_t *rec, uint32_t *produced_id, uint32_t *selection)
+{
+    return oracle_filter_frame2(format, W, H, bc1, latent, mlp, uv, grad, Wf, Hf, mode, fallback, flags, seed,
+                                frame_index, FILTER_BILINEAR, 1, out, rec, produced_id, selection);
+}
+
 /* Same, restricted to a list of waves (sampled parity at full size). */
+int oracle_filter_waves2(int format, int W, int H, const uint8_t *bc1, const uint16_t *latent,
+                         const float *mlp, const float *uv, const uint16_t *grad, int Wf, int Hf,
+                         int mode, int fallback, unsigned flags, uint64_t seed, uint32_t frame_index,
+                         int filter, int max_evals, const int32_t *wave_list, int nlist,
+                         double *out, uint32_t *rec, uint32_t *produced_id, uint32_t *selection)
+{
+    if (!wave_list ||
+        check_args(format, W, H, bc1, latent, mlp, uv, Wf, Hf, mode, fallback, filter, max_evals, out, rec))
+        return -1;
+    tex_t tex = { format, W, H, bc1, latent, mlp };
+    frame_t F = { &tex, uv, grad, Wf, Hf, mode, fallback, flags, seed, frame_index,
+                  out, rec, produced_id, selection };
+    int E = max_evals < 1 ? 1 : max_evals;
+    int nwx = (Wf + 7) / 8;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int i = 0; i < nlist; ++i) run_wave(&F, filter, E, wave_list[i] % nwx, wave_list[i] / nwx);
+    return 0;
+}
+
 int oracle_filter_waves(int format, int W, int H, const uint8_t *bc1, const uint16_t *latent,
                         const float *mlp, const float *uv, const uint16_t *grad, int Wf, int Hf,
                         int mode, int fallback, unsigned flags, uint64_t seed, uint32_t frame_index,
                         const int32_t *wave_list, int nlist,
                         double *out, uint32_t *rec, uint32_t *produced_id, uint32_t *selection)
 {
-    if (W <= 0 || H <= 0 || Wf <= 0 || Hf <= 0 || !uv || !out || !rec || !wave_list) return -1;
-    tex_t tex = { format, W, H, bc1, latent, mlp };
-    frame_t F = { &tex, uv, grad, Wf, Hf, mode, fallback, flags, seed, frame_index,
-                  out, rec, produced_id, selection };
-    int nwx = (Wf + 7) / 8;
-#pragma omp parallel for schedule(dynamic, 16)
-    for (int i = 0; i < nlist; ++i) wave(&F, wave_list[i] % nwx, wave_list[i] / nwx);
-    return 0;
+    return oracle_filter_waves2(format, W, H, bc1, latent, mlp, uv, grad, Wf, Hf, mode, fallback, flags, seed,
+                                frame_index, FILTER_BILINEAR, 1, wave_list, nlist, out, rec, produced_id,
+                                selection);
 }
 
 /* Number of distinct texels in an arbitrary list (brute force, for pins). */

@@ -19,6 +19,7 @@ FMT_BC1, FMT_LATENT_MLP = 1, 2
 M_4TAP, M_STF, M_WC, M_COLLAB, M_BOX, M_MASK16, M_MASK11 = 0, 1, 2, 3, 4, 5, 6
 FB_STF, FB_WC, FB_C, FB_CPLUS = 0, 1, 2, 3
 FL_DEBUG, FL_FORCE_FALLBACK = 1, 2
+FILTER_BILINEAR, FILTER_BSPLINE, FILTER_CATMULL_ROM = 0, 1, 2
 
 _lib = None
 
@@ -44,6 +45,13 @@ def load_oracle():
         lib.oracle_filter_waves.argtypes = [i32, i32, i32, P, P, P, P, P, i32, i32,
                                             i32, i32, u32, u64, u32, P, i32, P, P, P, P]
         lib.oracle_filter_waves.restype = i32
+        lib.oracle_filter_frame2.argtypes = [i32, i32, i32, P, P, P, P, P, i32, i32,
+                                             i32, i32, u32, u64, u32, i32, i32, P, P, P, P]
+        lib.oracle_filter_frame2.restype = i32
+        lib.oracle_filter_waves2.argtypes = [i32, i32, i32, P, P, P, P, P, i32, i32,
+                                             i32, i32, u32, u64, u32, i32, i32, P, i32, P, P, P, P]
+        lib.oracle_filter_waves2.restype = i32
+        lib.oracle_cubic_weights.argtypes = [i32, ctypes.c_float, P]
         lib.oracle_philox4x32_10.argtypes = [P, P, P]
         lib.oracle_bc1_texel.argtypes = [P, i32, i32, i32, P]
         lib.oracle_mlp_texel.argtypes = [P, P, i32, i32, i32, i32, P]
@@ -73,7 +81,8 @@ def _tex_args(tex):
 
 
 def filter_frame(tex: dict, uv: np.ndarray, grad: np.ndarray | None, mode: int, fallback: int = FB_CPLUS,
-                 flags: int = 0, seed: int = 0, frame_index: int = 0, debug: bool = True):
+                 flags: int = 0, seed: int = 0, frame_index: int = 0, debug: bool = True,
+                 filter: int = FILTER_BILINEAR, max_evals: int = 1):
     """Run the oracle on one frame.  Returns dict(out fp64 [Hf][Wf][4], rec, produced_id, selection)."""
     lib = load_oracle()
     hf, wf = uv.shape[:2]
@@ -84,16 +93,17 @@ def filter_frame(tex: dict, uv: np.ndarray, grad: np.ndarray | None, mode: int, 
     rec = np.zeros(((hf + 3) // 4, (wf + 7) // 8), np.uint32)
     pid = np.zeros((hf, wf), np.uint32) if debug else None
     sel = np.zeros((hf, wf), np.uint32) if debug else None
-    rc = lib.oracle_filter_frame(fmt, W, H, _ptr(bc1), _ptr(lat), _ptr(mlp), _ptr(uv), _ptr(g), wf, hf,
-                                 mode, fallback, flags, seed, frame_index,
-                                 _ptr(out), _ptr(rec), _ptr(pid), _ptr(sel))
+    rc = lib.oracle_filter_frame2(fmt, W, H, _ptr(bc1), _ptr(lat), _ptr(mlp), _ptr(uv), _ptr(g), wf, hf,
+                                  mode, fallback, flags, seed, frame_index, filter, max_evals,
+                                  _ptr(out), _ptr(rec), _ptr(pid), _ptr(sel))
     if rc != 0:
         raise ValueError("oracle_filter_frame: invalid arguments")
     return {"out": out, "rec": rec, "produced_id": pid, "selection": sel}
 
 
 def filter_waves(tex: dict, uv: np.ndarray, grad: np.ndarray | None, waves: np.ndarray, mode: int,
-                 fallback: int = FB_CPLUS, flags: int = 0, seed: int = 0, frame_index: int = 0):
+                 fallback: int = FB_CPLUS, flags: int = 0, seed: int = 0, frame_index: int = 0,
+                 filter: int = FILTER_BILINEAR, max_evals: int = 1):
     """Oracle restricted to the listed wave indices (wy * nwx + wx); other outputs stay 0."""
     lib = load_oracle()
     hf, wf = uv.shape[:2]
@@ -105,19 +115,27 @@ def filter_waves(tex: dict, uv: np.ndarray, grad: np.ndarray | None, waves: np.n
     rec = np.zeros(((hf + 3) // 4, (wf + 7) // 8), np.uint32)
     pid = np.zeros((hf, wf), np.uint32)
     sel = np.zeros((hf, wf), np.uint32)
-    rc = lib.oracle_filter_waves(fmt, W, H, _ptr(bc1), _ptr(lat), _ptr(mlp), _ptr(uv), _ptr(g), wf, hf,
-                                 mode, fallback, flags, seed, frame_index, _ptr(waves), len(waves),
-                                 _ptr(out), _ptr(rec), _ptr(pid), _ptr(sel))
+    rc = lib.oracle_filter_waves2(fmt, W, H, _ptr(bc1), _ptr(lat), _ptr(mlp), _ptr(uv), _ptr(g), wf, hf,
+                                  mode, fallback, flags, seed, frame_index, filter, max_evals,
+                                  _ptr(waves), len(waves), _ptr(out), _ptr(rec), _ptr(pid), _ptr(sel))
     if rc != 0:
         raise ValueError("oracle_filter_waves: invalid arguments")
     return {"out": out, "rec": rec, "produced_id": pid, "selection": sel}
+
+
+def cubic_weights(filter: int, s: float) -> np.ndarray:
+    """fp32 tap weights of the B-spline (1) / Catmull-Rom (2) kernel at fraction s (R-25)."""
+    lib = load_oracle()
+    w = np.zeros(4, np.float32)
+    lib.oracle_cubic_weights(filter, ctypes.c_float(s), _ptr(w))
+    return w
 
 
 def decode_record(rec: np.ndarray) -> dict:
     """Per-wave record fields (DESIGN.md / include/ctf.h layout)."""
     r = rec.astype(np.uint64)
     return {
-        "evals": (r & 0xFF).astype(np.int64),
+        "evals": ((r & 0xFF) | (((r >> 27) & 0x7) << 8)).astype(np.int64),
         "n": ((r >> 8) & 0xFF).astype(np.int64),
         "a": ((r >> 16) & 0x3F).astype(np.int64),
         "path": ((r >> 22) & 0x7).astype(np.int64),
@@ -151,8 +169,9 @@ def frame_stats(rec: np.ndarray, out: np.ndarray | None = None, ref: np.ndarray 
         "max_unique_per_wave": int(d["n"][nvalid].max()) if nvalid.any() else 0,
         "unique_hist": hist,
     }
-    # evals per lane: exact path <= 1, fallbacks <= 1, 4TAP = 4
-    per_lane = np.where(d["path"] == 5, 4, np.where(d["evals"] > 0, 1, 0))
+    # evals per lane = ceil(evals / a): exact path and fallbacks 1 (2 with max_evals = 2 or
+    # positivized STF), 4TAP 4 (16 for bicubic)
+    per_lane = (d["evals"] + np.maximum(d["a"], 1) - 1) // np.maximum(d["a"], 1)
     st["max_evals_per_lane"] = int(per_lane[live].max()) if live.any() else 0
     if out is not None and ref is not None:
         o = out.astype(np.float64).reshape(-1, 4)

@@ -22,6 +22,8 @@ UNITS = [
     ("ctf_filter.cu", ["-DCTF_TU_FMT=1"], "ctf_filter_bc1.o"),
     ("ctf_filter.cu", ["-DCTF_TU_FMT=2"], "ctf_filter_mlp.o"),
     ("ctf_stats.cu", [], "ctf_stats.o"),
+    ("ctf_bicubic.cu", ["-DCTF_TU_FMT=1"], "ctf_bicubic_bc1.o"),
+    ("ctf_bicubic.cu", ["-DCTF_TU_FMT=2"], "ctf_bicubic_mlp.o"),
 ]
 HEADERS = ["ctf_device.cuh", "ctf_internal.h"]
 

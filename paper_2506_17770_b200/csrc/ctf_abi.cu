@@ -22,6 +22,15 @@ int validate(const ctf_texture *tex, const float *uv, const uint16_t *grad, int3
     if (tex->format == CTF_FMT_LATENT_MLP && !tex->mlp_dev) return CTF_EINVAL;
     if (p->mode < CTF_MODE_BILINEAR_4TAP || p->mode > CTF_MODE_MASK11) return CTF_EINVAL;
     if (p->fallback < CTF_FB_STF || p->fallback > CTF_FB_CPLUS) return CTF_EINVAL;
+    if (p->filter < CTF_FILTER_BILINEAR || p->filter > CTF_FILTER_CATMULL_ROM) return CTF_EINVAL;
+    if (p->max_evals < 0 || p->max_evals > 2) return CTF_EINVAL;
+    if (p->filter == CTF_FILTER_BILINEAR && p->max_evals > 1) return CTF_EUNSUPPORTED;
+    if (p->filter != CTF_FILTER_BILINEAR) {
+        // R-28: no WC estimator for signed weights; per-pixel debug outputs are bilinear-only
+        if (p->mode == CTF_MODE_WAVECOMM || p->fallback == CTF_FB_WAVECOMM) return CTF_EUNSUPPORTED;
+        if (p->flags & CTF_FLAG_DEBUG) return CTF_EUNSUPPORTED;
+        if (!ctf::bicubic_built()) return CTF_EUNSUPPORTED;
+    }
     // texel ids y*W+x must fit 24 bits (sort keys) and coordinates 16 bits
     if ((int64_t)tex->width * tex->height > (1LL << 24) || tex->width > 65535 || tex->height > 65535)
         return CTF_EUNSUPPORTED;
@@ -57,6 +66,8 @@ ctf::LaunchArgs make_args(const ctf_texture *tex, const float *uv, const uint16_
     a.flags = p->flags;
     a.frame_index = p->frame_index;
     a.seed = p->seed;
+    a.filter = p->filter;
+    a.max_evals = p->max_evals < 1 ? 1 : p->max_evals;
     if (dbg && (p->flags & CTF_FLAG_DEBUG)) {
         a.dbg_pid = dbg->produced_id_dev;
         a.dbg_sel = dbg->selection_dev;

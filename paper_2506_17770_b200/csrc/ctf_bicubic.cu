@@ -1,0 +1,589 @@
+// ctf_bicubic.cu — collaborative filtering with the bicubic filters of §5.4
+// ("Bicubic Filtering"): cubic B-spline and Catmull-Rom, 4x4 footprints,
+// <= 1 or <= 2 texel evaluations per lane on the exact path (Fig. 13).
+//
+// Same wave model as the bilinear kernel (one 8x4 wave per warp), with:
+//   a2  footprint: taps x0-1..x0+2 / y0-1..y0+2 clamped (R-24), weights R-25, clamp
+//       duplicates merged per axis -> an nc x nr grid of distinct cells per lane;
+//   a3  collect: the wave's distinct texels in ascending id by "peeling" — each step one
+//       redux.sync.min over the lanes' next unconsumed cell; a lane learns the rank of each
+//       of its row starts as it is consumed (its cells in a row have consecutive ranks);
+//       stops after E*a + 1 texels (the decision needs no more; R-28);
+//   a4  exact iff n <= E*a (List), AABB area <= E*a (Box), AABB <= MxM and n <= E*a (Mask);
+//   a5  rank r is produced by lane h(r mod a, A) as its (r div a)-th evaluation;
+//   a6  16 shuffles (32 when n > a) + the 16-cell fma chain;
+//   a7  fallbacks STF / C / C+ with |w|-proportional one-tap samples (R-26);
+//   STF mode: the positivized two-lobe estimator (R-27).
+// Independent of oracle/.  P:n = PAPER.md line; R-n = DESIGN.md reading.
+#include <climits>
+#include <cstdint>
+
+#include "ctf_device.cuh"
+#include "ctf_internal.h"
+
+#ifndef CTF_TU_FMT
+#define CTF_TU_FMT 1
+#endif
+
+namespace ctf {
+namespace {
+
+constexpr int kBWarps = 8;
+constexpr int kBChunk = 16;  // waves per work item (a run in one wave-row)
+enum { FILT_BSPLINE = 1, FILT_CATMULL_ROM = 2 };
+enum { BVAR_LIST = 0, BVAR_BOX = 1, BVAR_MASK16 = 2, BVAR_MASK11 = 3 };
+
+struct BArgs {
+    TexArgs tex;
+    const float2 *uv;
+    const uint2 *grad;
+    float4 *out;
+    uint32_t *rec;
+    unsigned fpx;
+    int Wf, Hf, nwx, nwy, wpf, cpr, cpf;
+    unsigned nchunks, ipw;
+    float Wflt, Hflt;
+    int filter, E, fallback, variant;
+    uint32_t flags, frame_index, seed_lo, seed_hi;
+};
+
+struct BSmem {
+    uint32_t tbl[72];         // exact: rank -> texel id (<= 2*32 + 1); C+: sorted planned ids
+    uint32_t sorted[32];      // fallback gather: sorted (id << 5 | lane) of produced texels
+    uint8_t lane_of_rank[32]; // h(r, A)
+};
+
+// ------------------------------------------------------------------ weights (R-25)
+// fp32, one rounding per operation in the written order (no contraction): they decide
+// integers (STF / C+ picks), so the oracle computes the identical values.
+__device__ __forceinline__ void cubic_weights(int filter, float s, float (&w)[4]) {
+    const float r = __fsub_rn(1.0f, s);
+    const float s2 = __fmul_rn(s, s), s3 = __fmul_rn(s2, s), r2 = __fmul_rn(r, r);
+    if (filter == FILT_BSPLINE) {
+        w[0] = __fdiv_rn(__fmul_rn(r2, r), 6.0f);
+        w[1] = __fdiv_rn(__fadd_rn(__fsub_rn(__fmul_rn(3.0f, s3), __fmul_rn(6.0f, s2)), 4.0f), 6.0f);
+        w[2] = __fdiv_rn(__fadd_rn(__fadd_rn(__fsub_rn(__fmul_rn(3.0f, s2), __fmul_rn(3.0f, s3)), __fmul_rn(3.0f, s)),
+                                   1.0f),
+                         6.0f);
+        w[3] = __fdiv_rn(s3, 6.0f);
+    } else {
+        w[0] = __fmul_rn(-0.5f, __fmul_rn(s, r2));
+        w[1] = __fmul_rn(__fadd_rn(__fsub_rn(__fmul_rn(3.0f, s3), __fmul_rn(5.0f, s2)), 2.0f), 0.5f);
+        w[2] = __fmul_rn(__fadd_rn(__fsub_rn(__fmul_rn(4.0f, s2), __fmul_rn(3.0f, s3)), s), 0.5f);
+        w[3] = __fmul_rn(-0.5f, __fmul_rn(s2, r));
+    }
+}
+
+// One lane's 4x4 footprint (R-24): distinct columns xa..xa+nc-1, rows ya..ya+nr-1,
+// merged weights per distinct column / row (taps in ascending order).
+struct Foot16 {
+    int xa, nc, ya, nr;
+    float wx[4], wy[4];   // tap weights
+    float mx[4], my[4];   // merged (0 beyond nc / nr)
+    int cx[4], ry[4];     // tap -> distinct column / row index
+};
+
+__device__ __forceinline__ void merge_axis(const float (&w)[4], const int (&idx)[4], float (&m)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (idx[i] == c) acc = __fadd_rn(acc, w[i]);
+        m[c] = acc;
+    }
+}
+
+// fx = fma(clamp(u), W, -0.5) -> (x0, s); shared with the C+ spare-lane recomputation
+__device__ __forceinline__ Foot16 footprint16(int filter, int x0, int y0, float s, float t, int W, int H) {
+    Foot16 f;
+    cubic_weights(filter, s, f.wx);
+    cubic_weights(filter, t, f.wy);
+    f.xa = min(max(x0 - 1, 0), W - 1);
+    f.ya = min(max(y0 - 1, 0), H - 1);
+    const int xb = min(max(x0 + 2, 0), W - 1), yb = min(max(y0 + 2, 0), H - 1);
+    f.nc = xb - f.xa + 1;
+    f.nr = yb - f.ya + 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f.cx[i] = min(max(x0 - 1 + i, 0), W - 1) - f.xa;
+        f.ry[i] = min(max(y0 - 1 + i, 0), H - 1) - f.ya;
+    }
+    merge_axis(f.wx, f.cx, f.mx);
+    merge_axis(f.wy, f.ry, f.my);
+    return f;
+}
+
+__device__ __forceinline__ float sel4(const float (&v)[4], int i) {
+    return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
+}
+__device__ __forceinline__ int sel4i(const int (&v)[4], int i) { return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3]; }
+
+// the 16-cell blend: acc over cells (r outer, c inner) of (mx[c] * my[r]) * v, then scale.
+// The exact path, the full filter and Eq. 1's "all known" case use this one chain.
+template <int FMT>
+struct Acc {
+    float c[4];
+    __device__ __forceinline__ Acc() { c[0] = c[1] = c[2] = c[3] = 0.0f; }
+    __device__ __forceinline__ void add(float w, const Texel<FMT> &t) {
+        float v[4];
+        t.expand(v);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(w, v[ch], c[ch]);
+    }
+};
+
+// R-26: index of the tap drawn with probability |w_i| / S (fp32 inverse CDF)
+__device__ __forceinline__ int cubic_pick(const float (&w)[4], float u, float &S) {
+    S = 0.0f;
+    int last = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        S = __fadd_rn(S, fabsf(w[i]));
+        if (w[i] != 0.0f) last = i;
+    }
+    const float target = __fmul_rn(u, S);
+    float cum = 0.0f;
+    int pick = -1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        cum = __fadd_rn(cum, fabsf(w[i]));
+        if (pick < 0 && cum > target) pick = i;
+    }
+    return pick < 0 ? last : pick;
+}
+
+__device__ __forceinline__ int eq2_rank(int j, int np, int na) {  // Eq. 2, R-18
+    if (np >= na - 1) return 0;
+    return (2 * (na - 1) * (j - np) + (na - 1 - np)) / (2 * (na - 1 - np));
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
+    ctf_bicubic_kernel(const BArgs a, const typename WeightsOf<FMT>::type mw, const int MODE) {
+    __shared__ BSmem smem[kBWarps];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    BSmem &s = smem[warp];
+    const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
+    const unsigned lt = lanemask_lt();
+    const int W = a.tex.W, H = a.tex.H;
+    const float sc = Texel<FMT>::kScale;
+
+    for (unsigned j = 0; j < a.ipw; ++j) {
+        const unsigned c = (blockIdx.x * kBWarps + warp) + j * gridDim.x * kBWarps;
+        if (c >= a.nchunks) break;
+        const int fr = (int)(c / (unsigned)a.cpf);
+        const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
+        const int wy = rr / a.cpr;
+        const int wx0 = (rr - wy * a.cpr) * kBChunk;
+        const int wx1 = min(wx0 + kBChunk, a.nwx);
+        const int py = wy * 4 + ly;
+        const uint32_t frame = a.frame_index + (uint32_t)fr;
+        for (int wx = wx0; wx < wx1; ++wx) {
+            const int px = wx * 8 + lx;
+            const bool inframe = py < a.Hf && px < a.Wf;
+            const unsigned pix = (unsigned)fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)px;
+            const unsigned widx = (unsigned)fr * (unsigned)a.wpf + (unsigned)(wy * a.nwx + wx);
+            float2 uv = make_float2(__int_as_float(0x7fc00000), 0.0f);
+            uint2 gr = make_uint2(0u, 0u);
+            if (inframe) {
+                uv = ld_stream_f2(a.uv + pix);
+                if (a.grad) gr = ld_stream_u2(a.grad + pix);
+            }
+            __syncwarp();
+            // ---- a1: classify
+            const bool active = inframe && !isnan(uv.x);
+            const unsigned A = __ballot_sync(FULL, active);
+            const int na = __popc(A);
+            if (na == 0) {
+                if (inframe) st_stream_f4(a.out + pix, make_float4(0.f, 0.f, 0.f, 0.f));
+                if (lane == 0) a.rec[widx] = ((MODE == MODE_COLLAB ? 0u : 0xFFu) << 8) | (1u << 26);
+                continue;
+            }
+            bool mag_lane = true;
+            if (a.grad && active) {
+                const float rx = fma_f32_f16((unsigned short)(gr.x & 0xffffu), (unsigned short)(gr.x & 0xffffu),
+                                             fma_f32_f16((unsigned short)(gr.x >> 16), (unsigned short)(gr.x >> 16), 0.0f));
+                const float ry = fma_f32_f16((unsigned short)(gr.y & 0xffffu), (unsigned short)(gr.y & 0xffffu),
+                                             fma_f32_f16((unsigned short)(gr.y >> 16), (unsigned short)(gr.y >> 16), 0.0f));
+                mag_lane = rx <= 1.0f && ry <= 1.0f;
+            }
+            const bool wave_mag = a.grad != nullptr && __all_sync(FULL, mag_lane);
+            const int ar = __popc(A & lt);
+            if (active) s.lane_of_rank[ar] = (uint8_t)lane;
+            // ---- a2: footprint (R-24, R-25)
+            const float fx = fmaf(__saturatef(uv.x), a.Wflt, -0.5f), fy = fmaf(__saturatef(uv.y), a.Hflt, -0.5f);
+            const float flx = floorf(fx), fly = floorf(fy);
+            const int x0 = (int)flx, y0 = (int)fly;
+            const float fs = __fsub_rn(fx, flx), ft = __fsub_rn(fy, fly);
+            const Foot16 f = footprint16(a.filter, x0, y0, fs, ft, W, H);
+            __syncwarp();
+
+            float4 color = make_float4(0.f, 0.f, 0.f, 0.f);
+            int evals = 0, n = 0xFF, path = 0;
+            int run_fb = -1;
+            if (MODE == MODE_4TAP) {
+                // the full filter: every lane evaluates its 16 taps (cells; clamp duplicates
+                // are evaluated once per tap in the count, once per cell here)
+                Acc<FMT> acc;
+#pragma unroll 1
+                for (int q = 0; q < 16; ++q) {
+                    const int r = q >> 2, cc = q & 3;
+                    const bool valid = active && r < f.nr && cc < f.nc;
+                    Texel<FMT> v = Texel<FMT>::zero();
+                    if (valid) v = produce(a.tex, mw, (uint32_t)(f.xa + cc), (uint32_t)(f.ya + r));
+                    acc.add(__fmul_rn(sel4(f.mx, cc), sel4(f.my, r)), v);
+                }
+                color = make_float4(acc.c[0] * sc, acc.c[1] * sc, acc.c[2] * sc, acc.c[3] * sc);
+                evals = 16 * na;
+                path = PATH_4TAP;
+            } else if (MODE == MODE_STF) {
+                // R-27 positivized STF: one draw per lobe, c = W+ p+ - W- p-
+                const uint4 rnd = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo, a.seed_hi);
+                float Wp = 0.0f, Wn = 0.0f;
+                int lastp = 0, lastn = 0;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const float w = __fmul_rn(f.wx[k & 3], f.wy[k >> 2]);
+                    if (w > 0.0f) { Wp = __fadd_rn(Wp, w); lastp = k; }
+                    else if (w < 0.0f) { Wn = __fadd_rn(Wn, -w); lastn = k; }
+                }
+                int pk[2];
+#pragma unroll
+                for (int lobe = 0; lobe < 2; ++lobe) {
+                    const float Wl = lobe ? Wn : Wp;
+                    const float target = __fmul_rn(unit24(lobe ? rnd.y : rnd.x), Wl);
+                    float cum = 0.0f;
+                    int pick = -1;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float w = __fmul_rn(f.wx[k & 3], f.wy[k >> 2]);
+                        const bool in = lobe ? (w < 0.0f) : (w > 0.0f);
+                        if (in) {
+                            cum = __fadd_rn(cum, lobe ? -w : w);
+                            if (pick < 0 && cum > target) pick = k;
+                        }
+                    }
+                    pk[lobe] = pick < 0 ? (lobe ? lastn : lastp) : pick;
+                }
+                float cc4[4] = {0.f, 0.f, 0.f, 0.f};
+                const bool two = Wn > 0.0f;
+#pragma unroll 1
+                for (int lobe = 0; lobe < 2; ++lobe) {
+                    if (!__any_sync(FULL, active && (lobe == 0 || two))) break;
+                    const bool need = active && (lobe == 0 || two);
+                    const int k = pk[lobe];
+                    Texel<FMT> v = Texel<FMT>::zero();
+                    if (need)
+                        v = produce(a.tex, mw, (uint32_t)(f.xa + sel4i(f.cx, k & 3)), (uint32_t)(f.ya + sel4i(f.ry, k >> 2)));
+                    float e[4];
+                    v.expand(e);
+                    const float Wl = lobe ? -Wn : Wp;
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) cc4[ch] = need ? fmaf(Wl, e[ch], cc4[ch]) : cc4[ch];
+                }
+                color = make_float4(cc4[0] * sc, cc4[1] * sc, cc4[2] * sc, cc4[3] * sc);
+                evals = __reduce_add_sync(FULL, active ? (two ? 2 : 1) : 0);
+                path = PATH_STF;
+            } else {
+                // ---- a3: collect by peeling (ascending id; ranks of the lane's row starts)
+                const int E = a.E;
+                const int limit = E * na + 1;
+                int r = 0, cc = 0;
+                uint32_t cur = active ? (uint32_t)f.ya * (uint32_t)W + (uint32_t)f.xa : INVALID_ID;
+                int rr[4] = {0, 0, 0, 0};
+                int count = 0;
+                while (count < limit) {
+                    const uint32_t m = __reduce_min_sync(FULL, cur);
+                    if (m == INVALID_ID) break;
+                    if (lane == 0) s.tbl[count] = m;
+                    if (cur == m) {
+                        if (cc == 0) {
+                            rr[0] = r == 0 ? count : rr[0];
+                            rr[1] = r == 1 ? count : rr[1];
+                            rr[2] = r == 2 ? count : rr[2];
+                            rr[3] = r == 3 ? count : rr[3];
+                        }
+                        if (++cc == f.nc) { cc = 0; ++r; }
+                        cur = (r < f.nr) ? (uint32_t)(f.ya + r) * (uint32_t)W + (uint32_t)(f.xa + cc) : INVALID_ID;
+                    }
+                    ++count;
+                }
+                n = count;  // exact when <= E*a, else saturated at E*a + 1 (R-28)
+                // ---- a4: decide
+                const int minx = __reduce_min_sync(FULL, active ? f.xa : INT_MAX);
+                const int miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
+                const int maxx = __reduce_max_sync(FULL, active ? f.xa + f.nc - 1 : INT_MIN);
+                const int maxy = __reduce_max_sync(FULL, active ? f.ya + f.nr - 1 : INT_MIN);
+                const int bw = maxx - minx + 1, bh = maxy - miny + 1;
+                bool ok;
+                if (a.variant == BVAR_BOX) ok = bw * bh <= E * na;
+                else if (a.variant == BVAR_MASK16) ok = bw <= 16 && bh <= 16 && n <= E * na;
+                else if (a.variant == BVAR_MASK11) ok = bw <= 11 && bh <= 11 && n <= E * na;
+                else ok = n <= E * na;
+                if (a.flags & FLAG_FORCE_FALLBACK) ok = false;
+                __syncwarp();
+                if (ok) {
+                    // ---- a5: produce (<= E per lane)
+                    const bool box = a.variant == BVAR_BOX;
+                    const int total = box ? bw * bh : n;
+                    Texel<FMT> val[2] = {Texel<FMT>::zero(), Texel<FMT>::zero()};
+#pragma unroll 1
+                    for (int slot = 0; slot < 2; ++slot) {
+                        if (slot * na >= total) break;
+                        const int i = ar + slot * na;
+                        Texel<FMT> v = Texel<FMT>::zero();
+                        if (active && i < total) {
+                            uint32_t tx, ty;
+                            if (box) {
+                                ty = (uint32_t)(miny + i / bw);
+                                tx = (uint32_t)(minx + i % bw);
+                            } else {
+                                const uint32_t id = s.tbl[i];
+                                ty = id / (uint32_t)W;
+                                tx = id - ty * (uint32_t)W;
+                            }
+                            v = produce(a.tex, mw, tx, ty);
+                        }
+                        if (slot == 0) val[0] = v; else val[1] = v;
+                    }
+                    // ---- a6: gather (16 shuffles, 32 when n > a) + blend
+                    const bool two = total > na;
+                    const bool full = A == FULL;
+                    Acc<FMT> acc;
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const int rq = q >> 2, cq = q & 3;
+                        const bool valid = active && rq < f.nr && cq < f.nc;
+                        int rank;
+                        if (box) rank = (f.ya + rq - miny) * bw + (f.xa + cq - minx);
+                        else rank = (rq == 0 ? rr[0] : rq == 1 ? rr[1] : rq == 2 ? rr[2] : rr[3]) + cq;
+                        int slot = 0;
+                        if (rank >= na) { rank -= na; slot = 1; }
+                        int src = (int)lane;
+                        if (valid) src = full ? rank : (int)s.lane_of_rank[rank];
+                        Texel<FMT> v = Texel<FMT>::shfl(val[0], src);
+                        if (two) {
+                            const Texel<FMT> v1 = Texel<FMT>::shfl(val[1], src);
+                            if (slot) v = v1;
+                        }
+                        acc.add(__fmul_rn(sel4(f.mx, cq), sel4(f.my, rq)), v);
+                    }
+                    color = make_float4(acc.c[0] * sc, acc.c[1] * sc, acc.c[2] * sc, acc.c[3] * sc);
+                    evals = total;
+                    path = PATH_EXACT;
+                } else {
+                    run_fb = a.fallback;
+                    path = PATH_FB_STF + a.fallback;
+                }
+            }
+
+            if (run_fb >= 0) {
+                // ---- a7: fallbacks; one-tap plan (R-26)
+                const uint4 rnd = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo, a.seed_hi);
+                float Sx, Sy;
+                const int pi = cubic_pick(f.wx, unit24(rnd.x), Sx);
+                const int pj = cubic_pick(f.wy, unit24(rnd.y), Sy);
+                const int qx = f.xa + sel4i(f.cx, pi), qy = f.ya + sel4i(f.ry, pj);
+                if (run_fb == FB_STF) {
+                    Texel<FMT> v = Texel<FMT>::zero();
+                    if (active) v = produce(a.tex, mw, (uint32_t)qx, (uint32_t)qy);
+                    float e[4];
+                    v.expand(e);
+                    const bool neg = (sel4(f.wx, pi) < 0.0f) != (sel4(f.wy, pj) < 0.0f);
+                    const float g = __fmul_rn(__fmul_rn(Sx, Sy), neg ? -sc : sc);
+                    color = make_float4(e[0] * g, e[1] * g, e[2] * g, e[3] * g);
+                    evals = na;
+                } else {
+                    uint32_t prod = active ? (uint32_t)qy * (uint32_t)W + (uint32_t)qx : INVALID_ID;
+                    if (run_fb == FB_CPLUS) {
+                        // C+ (P:485-518): planned ids deduplicated ascending on lanes h(i, A) ...
+                        const uint32_t sk = warp_sort32(prod);
+                        const uint32_t skp = __shfl_up_sync(FULL, sk, 1);
+                        const bool firstp = sk != INVALID_ID && (lane == 0 || sk != skp);
+                        const unsigned F = __ballot_sync(FULL, firstp);
+                        const int np = __popc(F);
+                        if (firstp) s.tbl[__popc(F & lt)] = sk;
+                        if ((int)lane >= np) s.tbl[lane] = INVALID_ID;
+                        __syncwarp();
+                        prod = INVALID_ID;
+                        int l = (int)lane;
+                        bool spare = false;
+                        if (active) {
+                            if (ar < np) prod = s.tbl[ar];
+                            else { spare = true; l = (int)s.lane_of_rank[eq2_rank(ar, np, na)]; }
+                        }
+                        // ... spare lanes pick from served lane l's footprint (R-18 with |w|)
+                        const int gx0 = __shfl_sync(FULL, x0, l), gy0 = __shfl_sync(FULL, y0, l);
+                        const float gs = __shfl_sync(FULL, fs, l), gt = __shfl_sync(FULL, ft, l);
+                        if (spare) {
+                            const Foot16 g = footprint16(a.filter, gx0, gy0, gs, gt, W, H);
+                            float wsum = 0.0f;
+                            float cw[16];
+                            uint32_t cid[16];
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) {
+                                const int rq = q >> 2, cq = q & 3;
+                                const float mwq = __fmul_rn(sel4(g.mx, cq), sel4(g.my, rq));
+                                const uint32_t id = (uint32_t)(g.ya + rq) * (uint32_t)W + (uint32_t)(g.xa + cq);
+                                bool cand = rq < g.nr && cq < g.nc && mwq != 0.0f;
+                                if (cand) {
+                                    const int pos = lower_bound32(s.tbl, id);
+                                    cand = !(pos < 32 && s.tbl[pos] == id);
+                                }
+                                cw[q] = cand ? fabsf(mwq) : 0.0f;
+                                cid[q] = cand ? id : INVALID_ID;
+                                if (cand) wsum = __fadd_rn(wsum, cw[q]);
+                            }
+                            if (wsum > 0.0f) {  // no candidate -> produce nothing
+                                const float target = __fmul_rn(unit24(rnd.z), wsum);
+                                float cum = 0.0f;
+                                uint32_t pick = INVALID_ID, lastc = INVALID_ID;
+#pragma unroll
+                                for (int q = 0; q < 16; ++q) {
+                                    if (cid[q] == INVALID_ID) continue;
+                                    lastc = cid[q];
+                                    cum = __fadd_rn(cum, cw[q]);
+                                    if (pick == INVALID_ID && cum > target) pick = cid[q];
+                                }
+                                prod = pick != INVALID_ID ? pick : lastc;
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    // produce (one site), then every lane gathers the wave's produced set
+                    Texel<FMT> val = Texel<FMT>::zero();
+                    if (prod != INVALID_ID) {
+                        const uint32_t ty = prod / (uint32_t)W;
+                        val = produce(a.tex, mw, prod - ty * (uint32_t)W, ty);
+                    }
+                    evals = (run_fb == FB_CPLUS) ? __popc(__ballot_sync(FULL, prod != INVALID_ID)) : na;
+                    s.sorted[lane] = warp_sort32(prod != INVALID_ID ? ((prod << 5) | lane) : INVALID_ID);
+                    __syncwarp();
+                    // Eq. 1 over the known cells (R-23 evaluation order, R-28)
+                    bool all_known = true;
+                    int N = 0;
+                    float Sw = 0.0f, Sp[4] = {0.f, 0.f, 0.f, 0.f};
+                    Acc<FMT> acc;
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const int rq = q >> 2, cq = q & 3;
+                        const float mwq = __fmul_rn(sel4(f.mx, cq), sel4(f.my, rq));
+                        const bool need = active && rq < f.nr && cq < f.nc && mwq != 0.0f;
+                        bool known = false;
+                        int src = (int)lane;
+                        if (need) {
+                            const uint32_t id = (uint32_t)(f.ya + rq) * (uint32_t)W + (uint32_t)(f.xa + cq);
+                            const int pos = lower_bound32(s.sorted, id << 5);
+                            if (pos < 32) {
+                                const uint32_t hit = s.sorted[pos];
+                                if ((hit >> 5) == id) { known = true; src = (int)(hit & 31u); }
+                            }
+                        }
+                        Texel<FMT> v = Texel<FMT>::shfl(val, src);
+                        if (!known) v = Texel<FMT>::zero();
+                        if (need && !known) all_known = false;
+                        if (known) {
+                            ++N;
+                            Sw = __fadd_rn(Sw, mwq);
+                            float e[4];
+                            v.expand(e);
+#pragma unroll
+                            for (int ch = 0; ch < 4; ++ch) Sp[ch] = __fadd_rn(Sp[ch], e[ch]);
+                        }
+                        acc.add(mwq, v);
+                    }
+                    __syncwarp();
+                    float cc4[4];
+                    const float rest = (all_known || N == 0) ? 0.0f : __fdividef(__fsub_rn(1.0f, Sw), (float)N);
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) cc4[ch] = fmaf(rest, Sp[ch], acc.c[ch]) * sc;
+                    if (N == 1 && !all_known) {
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) cc4[ch] = Sp[ch] * sc;
+                    }
+                    color = make_float4(cc4[0], cc4[1], cc4[2], cc4[3]);
+                }
+            }
+            if (!active) color = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (inframe) st_stream_f4(a.out + pix, color);
+            // ---- a8: record
+            if (lane == 0) {
+                const uint32_t ev = (uint32_t)evals;
+                a.rec[widx] = (ev & 0xFFu) | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)na << 16) |
+                              ((uint32_t)path << 22) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26) |
+                              (((ev >> 8) & 7u) << 27);
+            }
+        }
+    }
+}
+
+template <int FMT>
+cudaError_t launch_bicubic(BArgs k, const typename WeightsOf<FMT>::type &mw, int mode, cudaStream_t stream) {
+    auto kern = ctf_bicubic_kernel<FMT>;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBWarps * 32, 0);
+    if (e != cudaSuccess) return e;
+    const long long slots = (long long)sms * (per_sm > 0 ? per_sm : 1);
+    long long ipw = ((long long)k.nchunks + slots * kBWarps * 4 - 1) / (slots * kBWarps * 4);
+    ipw = ipw < 1 ? 1 : ipw > 4 ? 4 : ipw;
+    k.ipw = (unsigned)ipw;
+    long long grid = ((long long)k.nchunks + ipw * kBWarps - 1) / (ipw * kBWarps);
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, kBWarps * 32, 0, stream>>>(k, mw, mode <= MODE_STF ? mode : MODE_COLLAB);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+#if CTF_TU_FMT == 1
+bool bicubic_built() { return true; }
+cudaError_t launch_bicubic_bc1(const LaunchArgs &a, cudaStream_t stream) {
+#else
+cudaError_t launch_bicubic_mlp(const LaunchArgs &a, cudaStream_t stream) {
+#endif
+    BArgs k;
+    k.tex.W = a.W;
+    k.tex.H = a.H;
+    k.tex.bc1 = reinterpret_cast<const uint2 *>(a.tex_data);
+    k.tex.latent = reinterpret_cast<const uint4 *>(a.tex_data);
+    k.tex.mlp_dev = a.mlp;
+    k.uv = reinterpret_cast<const float2 *>(a.uv);
+    k.grad = reinterpret_cast<const uint2 *>(a.grad);
+    k.out = reinterpret_cast<float4 *>(a.out);
+    k.rec = a.rec;
+    k.Wf = a.Wf;
+    k.Hf = a.Hf;
+    k.nwx = (a.Wf + 7) / 8;
+    k.nwy = (a.Hf + 3) / 4;
+    k.wpf = k.nwx * k.nwy;
+    k.fpx = (unsigned)a.Wf * (unsigned)a.Hf;
+    k.cpr = (k.nwx + kBChunk - 1) / kBChunk;
+    k.cpf = k.cpr * k.nwy;
+    k.nchunks = (unsigned)((long long)k.cpf * a.frames);
+    k.ipw = 1;
+    k.Wflt = (float)a.W;
+    k.Hflt = (float)a.H;
+    k.filter = a.filter;
+    k.E = a.max_evals < 1 ? 1 : a.max_evals;
+    k.fallback = a.fallback;
+    k.variant = a.mode >= 4 ? a.mode - 3 : BVAR_LIST;
+    k.flags = a.flags;
+    k.frame_index = a.frame_index;
+    k.seed_lo = (uint32_t)a.seed;
+    k.seed_hi = (uint32_t)(a.seed >> 32);
+#if CTF_TU_FMT == 1
+    return launch_bicubic<FMT_BC1>(k, NoWeights{}, a.mode, stream);
+#else
+    MlpWeights mw;
+    const cudaError_t e = mlp_weights_by_value(a, stream, mw.v);
+    if (e != cudaSuccess) return e;
+    return launch_bicubic<FMT_MLP>(k, mw, a.mode, stream);
+#endif
+}
+
+}  // namespace ctf

@@ -1147,28 +1147,10 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
 #if CTF_TU_FMT == 1
     return launch_fmt<FMT_BC1>(k, NoWeights{}, a.mode, stream);
 #else
-    // weights by value: from the caller's host copy, else one synchronous copy from the device
     static_assert(sizeof(MlpWeights) == sizeof(float) * kMlpParams, "weight layout");
-    MlpWeights src, mw;
-    if (a.mlp_host) {
-        memcpy(src.v, a.mlp_host, sizeof(src.v));
-    } else {
-        cudaError_t e = cudaMemcpyAsync(src.v, a.mlp, sizeof(src.v), cudaMemcpyDeviceToHost, stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) return e;
-    }
-    // repack from the ABI layout (W1[32][12] b1 W2[32][32] b2 W3[4][32] b3) into the
-    // kernel's access order (W1, b1, W2 transposed, b2, W3 transposed, b3)
-    const float *W1 = src.v, *b1 = W1 + 384, *W2 = b1 + 32, *b2 = W2 + 1024, *W3 = b2 + 32, *b3 = W3 + 128;
-    float *o = mw.v;
-    memcpy(o, W1, sizeof(float) * 384);
-    memcpy(o + 384, b1, sizeof(float) * 32);
-    for (int k = 0; k < 32; ++k)
-        for (int j = 0; j < 32; ++j) o[416 + k * 32 + j] = W2[j * 32 + k];
-    memcpy(o + 1440, b2, sizeof(float) * 32);
-    for (int j = 0; j < 32; ++j)
-        for (int c = 0; c < 4; ++c) o[1472 + j * 4 + c] = W3[c * 32 + j];
-    memcpy(o + 1600, b3, sizeof(float) * 4);
+    MlpWeights mw;
+    const cudaError_t e = mlp_weights_by_value(a, stream, mw.v);
+    if (e != cudaSuccess) return e;
     return launch_fmt<FMT_MLP>(k, mw, a.mode, stream);
 #endif
 }

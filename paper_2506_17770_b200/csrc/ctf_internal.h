@@ -3,6 +3,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 namespace ctf {
@@ -25,14 +26,45 @@ struct LaunchArgs {
     int mode, fallback;
     uint32_t flags, frame_index;
     uint64_t seed;
+    int filter;             // ctf_filter: 0 bilinear, 1 B-spline, 2 Catmull-Rom
+    int max_evals;          // exact-path evaluations per lane (1 or 2)
     // debug
     uint32_t *dbg_pid, *dbg_sel, *dbg_unread;
 };
 
 cudaError_t launch_filter_bc1(const LaunchArgs &a, cudaStream_t stream);  // ctf_filter.cu, CTF_TU_FMT=1
 cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream);  // ctf_filter.cu, CTF_TU_FMT=2
+cudaError_t launch_bicubic_bc1(const LaunchArgs &a, cudaStream_t stream);  // ctf_bicubic.cu, CTF_TU_FMT=1
+cudaError_t launch_bicubic_mlp(const LaunchArgs &a, cudaStream_t stream);  // ctf_bicubic.cu, CTF_TU_FMT=2
+bool bicubic_built();
 inline cudaError_t launch_filter(const LaunchArgs &a, cudaStream_t stream) {
+    if (a.filter != 0) return a.fmt == 1 ? launch_bicubic_bc1(a, stream) : launch_bicubic_mlp(a, stream);
     return a.fmt == 1 ? launch_filter_bc1(a, stream) : launch_filter_mlp(a, stream);
+}
+
+// Latent-MLP weights for the kernel parameter block, repacked from the ABI layout
+// (W1[32][12] b1 W2[32][32] b2 W3[4][32] b3) into the kernels' access order (W1, b1,
+// W2 transposed, b2, W3 transposed, b3).  Source: the caller's host copy, else one
+// synchronous copy from the device.
+inline cudaError_t mlp_weights_by_value(const LaunchArgs &a, cudaStream_t stream, float (&o)[kMlpParams]) {
+    float src[kMlpParams];
+    if (a.mlp_host) {
+        memcpy(src, a.mlp_host, sizeof(src));
+    } else {
+        cudaError_t e = cudaMemcpyAsync(src, a.mlp, sizeof(src), cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) return e;
+    }
+    const float *W1 = src, *b1 = W1 + 384, *W2 = b1 + 32, *b2 = W2 + 1024, *W3 = b2 + 32, *b3 = W3 + 128;
+    memcpy(o, W1, sizeof(float) * 384);
+    memcpy(o + 384, b1, sizeof(float) * 32);
+    for (int k = 0; k < 32; ++k)
+        for (int j = 0; j < 32; ++j) o[416 + k * 32 + j] = W2[j * 32 + k];
+    memcpy(o + 1440, b2, sizeof(float) * 32);
+    for (int j = 0; j < 32; ++j)
+        for (int c = 0; c < 4; ++c) o[1472 + j * 4 + c] = W3[c * 32 + j];
+    memcpy(o + 1600, b3, sizeof(float) * 4);
+    return cudaSuccess;
 }
 
 struct StatsDev {  // device-side accumulation, converted to ctf_frame_stats on the host

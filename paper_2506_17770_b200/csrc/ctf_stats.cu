@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(kStatThreads) stats_records_kernel(const uint3
     unsigned int maxl = 0, maxn = 0;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nrec; i += (long long)gridDim.x * blockDim.x) {
         const uint32_t r = rec[i];
-        const uint32_t e = r & 0xFFu, n = (r >> 8) & 0xFFu, a = (r >> 16) & 0x3Fu, path = (r >> 22) & 7u;
+        const uint32_t e = (r & 0xFFu) | (((r >> 27) & 7u) << 8), n = (r >> 8) & 0xFFu, a = (r >> 16) & 0x3Fu, path = (r >> 22) & 7u;
         const uint32_t m = (r >> 25) & 1u, p = (r >> 26) & 1u;
         if (a == 0) continue;
         ++live;
@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(kStatThreads) stats_records_kernel(const uint3
         pix += a;
         ev += e;
         if (m) { ++mag; pixmag += a; evmag += e; }
-        const unsigned int per_lane = (path == 5) ? 4u : (e > 0 ? 1u : 0u);
+        const unsigned int per_lane = (e + a - 1u) / a;  // ceil(evals / a): 4TAP 4 (16 bicubic), else 1-2
         maxl = max(maxl, per_lane);
         if (n <= 128) {
             maxn = max(maxn, n);

@@ -20,6 +20,7 @@ FMT_BC1, FMT_LATENT_MLP = 1, 2
 MODE_4TAP, MODE_STF, MODE_WAVECOMM, MODE_COLLAB, MODE_BOX, MODE_MASK16, MODE_MASK11 = 0, 1, 2, 3, 4, 5, 6
 FB_STF, FB_WAVECOMM, FB_C, FB_CPLUS = 0, 1, 2, 3
 FLAG_DEBUG, FLAG_FORCE_FALLBACK = 1, 2
+FILTER_BILINEAR, FILTER_BSPLINE, FILTER_CATMULL_ROM = 0, 1, 2
 _STATUS = {0: "CTF_OK", -1: "CTF_EINVAL", -2: "CTF_EUNSUPPORTED", -3: "CTF_EALIGN", -4: "CTF_ECUDA"}
 
 
@@ -37,7 +38,8 @@ class ctf_texture(ctypes.Structure):
 
 class ctf_params(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("fallback", ctypes.c_int32), ("flags", ctypes.c_uint32),
-                ("frame_index", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
+                ("frame_index", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("filter", ctypes.c_int32),
+                ("max_evals", ctypes.c_int32)]
 
 
 class ctf_debug(ctypes.Structure):
@@ -145,7 +147,7 @@ def num_waves(wf: int, hf: int) -> int:
 def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS,
                  flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
                  rec: torch.Tensor | None = None, debug: dict | None = None,
-                 stream: torch.cuda.Stream | None = None):
+                 stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR, max_evals: int = 1):
     """uv: float32 [F][Hf][Wf][2] (or [Hf][Wf][2]); grad: float16 [..][4] or None.
     Returns (out float32 [..][4], rec int32 [F][nwy][nwx]).  `debug` may hold tensors
     'produced_id', 'selection' (int32, pixel-shaped) and 'unread' (int32 [1])."""
@@ -161,7 +163,7 @@ def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
         out = torch.empty((frames, hf, wf, 4), device=uv.device, dtype=torch.float32)
     if rec is None:
         rec = torch.empty((frames, (hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
-    p = ctf_params(mode, fallback, flags, frame_index, seed)
+    p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
     dbg = None
     if debug is not None:
         dbg = ctf_debug(_ptr(debug.get("produced_id")), _ptr(debug.get("selection")), _ptr(debug.get("unread")))
@@ -178,7 +180,7 @@ def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
 def filter_frame(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS,
                  flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
                  rec: torch.Tensor | None = None, debug: dict | None = None,
-                 stream: torch.cuda.Stream | None = None):
+                 stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR, max_evals: int = 1):
     """One frame through ctf_filter_frame.  uv float32 [Hf][Wf][2]."""
     lib = load_library()
     hf, wf = uv.shape[0], uv.shape[1]
@@ -186,7 +188,7 @@ def filter_frame(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
         out = torch.empty((hf, wf, 4), device=uv.device, dtype=torch.float32)
     if rec is None:
         rec = torch.empty(((hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
-    p = ctf_params(mode, fallback, flags, frame_index, seed)
+    p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
     dbg = None
     if debug is not None:
         dbg = ctf_debug(_ptr(debug.get("produced_id")), _ptr(debug.get("selection")), _ptr(debug.get("unread")))
@@ -220,13 +222,14 @@ class HostPipeline:
 
     def run(self, tex: Texture, uv_host: torch.Tensor, grad_host: torch.Tensor | None, out_host: torch.Tensor,
             rec_host: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS, flags: int = 0, seed: int = 0,
-            frame_index: int = 0, stream: torch.cuda.Stream | None = None):
+            frame_index: int = 0, stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR,
+            max_evals: int = 1):
         lib = load_library()
         for t in (uv_host, grad_host, out_host, rec_host):
             if t is not None and (t.is_cuda or not t.is_contiguous()):
                 raise ValueError("host pipeline expects contiguous CPU (ideally pinned) tensors")
         frames = uv_host.shape[0]
-        p = ctf_params(mode, fallback, flags, frame_index, seed)
+        p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
         hp = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
         rc = lib.ctf_filter_frames_host(ctypes.byref(tex.desc), hp(uv_host), hp(grad_host), self.wf, self.hf,
                                         frames, self.chunk, ctypes.byref(p), hp(out_host), hp(rec_host),
