@@ -293,6 +293,27 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
         mse = float((err * err).mean())
         e["psnr_vs_bilinear_db"] = 10 * float(np.log10(1.0 / mse)) if mse > 0 else float("inf")
         res[f"4_4k_mixed_bc1_method_{name}_cplus"] = e
+    # bicubic filters (§5.4, Fig. 13): 4K perspective plane of config 3 with the BC1 texture
+    uv, g = synthetic.perspective_plane_torch(3840, 2160, 4096, 4096, synthetic.PLANE_C2, device=dev)
+    cov = ~torch.isnan(uv[..., 0])
+    for fname, filt in (("bspline", 1), ("catmull_rom", 2)):
+        def runb(mode, fb, E, reps):
+            out = torch.empty(uv.shape[:-1] + (4,), dtype=torch.float32, device=dev)
+            rec = torch.empty(((uv.shape[0] + 3) // 4, (uv.shape[1] + 7) // 8), dtype=torch.int32, device=dev)
+            ms = time_launches(lambda: ctf.filter_frame(t4, uv, g, mode, fb, 0, seed, 0, out=out, rec=rec,
+                                                        stream=stream, filter=filt, max_evals=E), reps, stream)
+            return ms, ctf.stats(rec, uv.shape[1], uv.shape[0], 1, stream=stream), out
+        _, _, full = runb(0, 0, 1, 1)
+        full = full.clone()
+        for name, mode, fb, E in (("full16", 0, 0, 1), ("stf_positivized", 1, 0, 1), ("list_cplus_e1", 3, 3, 1),
+                                  ("list_cplus_e2", 3, 3, 2), ("box_cplus_e2", 4, 3, 2)):
+            ms, st, out = runb(mode, fb, E, 3 if mode == 0 else 10)
+            e = entry(3840, 2160, ms, st, 3840 * 2160 * 32)
+            err = (out - full)[cov].double()
+            mse = float((err * err).mean())
+            e["psnr_vs_full_filter_db"] = 10 * float(np.log10(1.0 / mse)) if mse > 0 else float("inf")
+            e["max_evals_per_lane"] = st["max_evals_per_lane"]
+            res[f"6_4k_bicubic_{fname}_{name}"] = e
     return res
 
 
