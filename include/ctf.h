@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define CTF_ABI_VERSION 2
+#define CTF_ABI_VERSION 3
 
 typedef enum {
     CTF_OK = 0,
@@ -218,8 +218,15 @@ int ctf_filter_frames_host(const ctf_texture *tex, const float *uv_host, const u
                            const ctf_params *p, float *out_host, uint32_t *rec_host,
                            void *workspace_dev, size_t workspace_bytes, void *stream);
 
-/* Kernel launches issued by the calls above (for launch accounting); and ABI version. */
-int ctf_launches_per_call(int32_t frames, int batched);
+/*
+ * Kernel launches one call above issues (for launch accounting): format / mode / filter
+ * as in ctf_texture / ctf_params, `frames` frames, `batched` != 0 for ctf_filter_batch
+ * (one pass over all frames) else ctf_filter_frame once per frame.  The BC1 COLLAB
+ * bilinear path is two kernels per pass (the lean kernel, then the general path over
+ * the waves it left: partial coverage, windows wider than 8x8); every other path is
+ * one.  Returns -1 for an invalid format / mode / filter.
+ */
+int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int batched);
 int ctf_abi_version(void);
 
 #ifdef __cplusplus

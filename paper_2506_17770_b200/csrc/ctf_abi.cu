@@ -84,7 +84,13 @@ extern "C" {
 
 int ctf_abi_version(void) { return CTF_ABI_VERSION; }
 
-int ctf_launches_per_call(int32_t frames, int batched) { return batched ? 1 : (frames > 0 ? frames : 0); }
+int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int batched) {
+    if ((format != CTF_FMT_BC1 && format != CTF_FMT_LATENT_MLP) || mode < 0 || mode > CTF_MODE_MASK11 || filter < 0 ||
+        filter > 2)
+        return -1;
+    const int per_pass = ctf::launches_per_pass(format, mode, filter);
+    return per_pass * (batched ? 1 : (frames > 0 ? frames : 0));
+}
 
 int ctf_filter_batch(const ctf_texture *tex, const float *uv_dev, const uint16_t *grad_dev, int32_t Wf, int32_t Hf,
                      int32_t frames, const ctf_params *p, float *out_dev, uint32_t *rec_dev, const ctf_debug *dbg,

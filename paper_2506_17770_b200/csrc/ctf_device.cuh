@@ -55,6 +55,16 @@ __device__ __forceinline__ void st_stream_f4(float4 *p, float4 v) {
                  : "memory");
 }
 
+// predicated shared store without a branch (keeps the warp provably converged)
+__device__ __forceinline__ void st_shared_u32_if(uint32_t *p, uint32_t v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
+                 ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v), "r"((unsigned)pred) : "memory");
+}
+__device__ __forceinline__ void st_shared_u8_if(uint8_t *p, uint32_t v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u8 [%0], %1;\n\t}"
+                 ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v), "r"((unsigned)pred) : "memory");
+}
+
 // ---------------------------------------------------------- Philox4x32-10 (R-11)
 // Salmon et al. SC'11; counter (x, y, frame, 0), key (seed_lo, seed_hi).
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
@@ -70,6 +80,70 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 // uniform in [0,1) on the 2^-24 grid: exact in fp32 (R-11)
 __device__ __forceinline__ float unit24(uint32_t r) { return __uint2float_rn(r >> 8) * 5.9604644775390625e-08f; }
 
+// ------------------------------------------------------- packed fp32 (sm_100 FFMA2)
+// Two fp32 lanes in one 64-bit register pair; each lane is an ordinary IEEE fp32
+// operation with one rounding, so results equal the scalar instructions bit for bit.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t r) {
+    float2 v;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+
+// RGBA8 -> (v / 255.0f) per channel, correctly rounded like the IEEE division of R-9:
+// a byte permute places v under the exponent of 2^23 (exact 2^23 + v), FADD2 removes
+// the 2^23, then q = v * (1/255) is corrected once, q += (v - 255 q) * (1/255) (FFMA2;
+// exact for every v in [0, 255]).  12 instructions per texel, no I2F.
+__device__ __forceinline__ float4 rgba8_unorm(uint32_t v) {
+    uint64_t rg = f2pack(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540)),
+                         __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541)));
+    uint64_t ba = f2pack(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7542)),
+                         __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7543)));
+    const uint64_t mag = f2pack(-8388608.0f, -8388608.0f), r = f2pack(1.0f / 255.0f, 1.0f / 255.0f),
+                   n255 = f2pack(-255.0f, -255.0f);
+    rg = fadd2(rg, mag);
+    ba = fadd2(ba, mag);
+    uint64_t q0 = fmul2(rg, r), q1 = fmul2(ba, r);
+    q0 = ffma2(ffma2(q0, n255, rg), r, q0);
+    q1 = ffma2(ffma2(q1, n255, ba), r, q1);
+    const float2 a = f2unpack(q0), b = f2unpack(q1);
+    return make_float4(a.x, a.y, b.x, b.y);
+}
+
+// Exact bilinear blend (c8 / R-8): per channel c = fma(w3,p3, fma(w2,p2, fma(w1,p1, w0*p0))),
+// two channels per FFMA2.  Every exact path (COLLAB fast / generic, 4TAP, Eq. 1's
+// all-known case) calls this, so they agree bit for bit.
+__device__ __forceinline__ float4 blend4f(const float4 (&p)[4], const float (&w)[4]) {
+    uint64_t rg = fmul2(f2pack(p[0].x, p[0].y), f2pack(w[0], w[0]));
+    uint64_t ba = fmul2(f2pack(p[0].z, p[0].w), f2pack(w[0], w[0]));
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+        rg = ffma2(f2pack(p[k].x, p[k].y), f2pack(w[k], w[k]), rg);
+        ba = ffma2(f2pack(p[k].z, p[k].w), f2pack(w[k], w[k]), ba);
+    }
+    const float2 a = f2unpack(rg), b = f2unpack(ba);
+    return make_float4(a.x, a.y, b.x, b.y);
+}
+
 // ------------------------------------------------------------------ texels
 // A produced texel and how lanes exchange it (step 3 "gather"; WaveReadLaneAt).
 template <int FMT> struct Texel;
@@ -80,6 +154,7 @@ template <> struct Texel<FMT_BC1> {
     __device__ __forceinline__ float ch(int c) const { return (float)((v >> (8 * c)) & 255u); }
     __device__ __forceinline__ void expand(float (&c)[4]) const;         // exact v in [0, 255]
     __device__ __forceinline__ void expand_biased(float (&c)[4]) const;  // 1024 + v (no constant operand)
+    __device__ __forceinline__ float4 to_f4() const { return rgba8_unorm(v); }  // v / 255 (R-9)
     __device__ __forceinline__ static Texel zero() { return {0u}; }
     static constexpr float kScale = 1.0f / 255.0f;  // bytes -> [0,1] (R-9)
     static constexpr float kBias = 1024.0f;
@@ -94,6 +169,7 @@ template <> struct Texel<FMT_MLP> {
     __device__ __forceinline__ float ch(int c) const { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
     __device__ __forceinline__ void expand(float (&c)[4]) const { c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w; }
     __device__ __forceinline__ void expand_biased(float (&c)[4]) const { expand(c); }
+    __device__ __forceinline__ float4 to_f4() const { return v; }
     __device__ __forceinline__ static Texel zero() { return {make_float4(0.f, 0.f, 0.f, 0.f)}; }
     static constexpr float kScale = 1.0f;
     static constexpr float kBias = 0.0f;

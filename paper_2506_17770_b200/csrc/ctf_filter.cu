@@ -120,43 +120,16 @@ __device__ __forceinline__ uint32_t corner_id(const Foot &f, int k, int W) {
 
 // Exact bilinear of 4 gathered texels (c8).  The same code runs in 4TAP and in
 // COLLAB-exact, so the two are bit-identical on exact waves.
+// Texel values as fp32 in [0, 1] (BC1: v / 255 correctly rounded, R-9), then the
+// FFMA2 chain of blend4f.
 template <int FMT>
 __device__ __forceinline__ float4 blend4(const Texel<FMT> (&p)[4], const float (&w)[4]) {
-    // c = sum_k (w_k * scale) * v_k.  BC1 texels expand to (1024 + v) without a
-    // constant operand (FHADD with RZ); the bias is removed by starting the fma
-    // chain at -1024 * sum_k w_k * scale (|error| <= ~2e-6).
-    const float sc = Texel<FMT>::kScale;
-    float ws[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) ws[k] = w[k] * sc;
-    float c[4], v[4];
-    p[0].expand_biased(v);
-    if constexpr (Texel<FMT>::kBias != 0.0f) {
-        // sum_k w_k = 1 up to 4 fp32 roundings, so the bias term is the constant
-        // -1024/255 to within ~5e-7
-        constexpr float nb = -Texel<FMT>::kBias * Texel<FMT>::kScale;
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(ws[0], v[ch], nb);
-    } else {
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) c[ch] = ws[0] * v[ch];
-    }
-#pragma unroll
-    for (int k = 1; k < 4; ++k) {
-        p[k].expand_biased(v);
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(ws[k], v[ch], c[ch]);
-    }
-    return make_float4(c[0], c[1], c[2], c[3]);
+    const float4 v[4] = {p[0].to_f4(), p[1].to_f4(), p[2].to_f4(), p[3].to_f4()};
+    return blend4f(v, w);
 }
 
 template <int FMT>
-__device__ __forceinline__ float4 scaled(const Texel<FMT> &p) {
-    const float sc = Texel<FMT>::kScale;
-    float v[4];
-    p.expand(v);
-    return make_float4(v[0] * sc, v[1] * sc, v[2] * sc, v[3] * sc);
-}
+__device__ __forceinline__ float4 scaled(const Texel<FMT> &p) { return p.to_f4(); }
 
 // Eq. 2 generalised to a active lanes (R-18 iv), round half up.
 __device__ __forceinline__ int eq2_lane_rank(int j, int np, int na) {
@@ -278,10 +251,9 @@ __device__ __forceinline__ void distinct_corners(const Foot &f, bool (&first)[4]
 }
 
 // Eq. 1 / WC combine from the gathered values of the lane's distinct corners (c14-c16).
-template <int FMT>
-__device__ __forceinline__ float4 combine_eq1(const Foot &f, const bool (&first)[4], const float (&dw)[4],
-                                              const bool (&known)[4], const int (&dup)[4], const Texel<FMT> (&p)[4],
-                                              bool wc) {
+__device__ __forceinline__ float4 combine_eq1f(const Foot &f, const bool (&first)[4], const float (&dw)[4],
+                                               const bool (&known)[4], const int (&dup)[4], const float4 (&pv)[4],
+                                               bool wc) {
     // Branch-free over the lane's cases (R-23).  The oracle's special cases hold bitwise:
     // every nonzero-weight texel known -> blend4 over the corners, i.e. exact bilinear
     // (c8); N = 1 -> that texel (Sp = p exactly).  Otherwise C / C+ evaluate
@@ -296,21 +268,17 @@ __device__ __forceinline__ float4 combine_eq1(const Foot &f, const bool (&first)
         if (!known[k]) { all_known = false; continue; }
         ++N;
         Sw += dw[k];
-        float v[4];
-        p[k].expand(v);
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) Sp[ch] += v[ch];
+        Sp[0] += pv[k].x; Sp[1] += pv[k].y; Sp[2] += pv[k].z; Sp[3] += pv[k].w;
     }
-    Texel<FMT> q[4];
+    float4 q[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int d = dup[k];
-        const Texel<FMT> src = d == 0 ? p[0] : d == 1 ? p[1] : d == 2 ? p[2] : p[3];
+        const float4 src = d == 0 ? pv[0] : d == 1 ? pv[1] : d == 2 ? pv[2] : pv[3];
         const bool kd = d == 0 ? known[0] : d == 1 ? known[1] : d == 2 ? known[2] : known[3];
-        q[k] = kd ? src : Texel<FMT>::zero();
+        q[k] = kd ? src : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const float4 bl = blend4<FMT>(q, f.w);  // sum over the known corners of w_k p_k (scaled)
-    const float sc = Texel<FMT>::kScale;
+    const float4 bl = blend4f(q, f.w);  // sum over the known corners of w_k p_k
     const bool one = N == 1 && !all_known;
     float c[4];
     if (wc) {  // WC stand-in (R-16): weights renormalised over the known texels
@@ -318,18 +286,18 @@ __device__ __forceinline__ float4 combine_eq1(const Foot &f, const bool (&first)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (!first[k] || dw[k] == 0.0f || !known[k]) continue;
-            float v[4];
-            p[k].expand(v);
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) Swp[ch] = fmaf(dw[k], v[ch], Swp[ch]);
+            Swp[0] = fmaf(dw[k], pv[k].x, Swp[0]);
+            Swp[1] = fmaf(dw[k], pv[k].y, Swp[1]);
+            Swp[2] = fmaf(dw[k], pv[k].z, Swp[2]);
+            Swp[3] = fmaf(dw[k], pv[k].w, Swp[3]);
         }
-        const float r = sc / Sw;
+        const float r = 1.0f / Sw;
         c[0] = all_known ? bl.x : Swp[0] * r;
         c[1] = all_known ? bl.y : Swp[1] * r;
         c[2] = all_known ? bl.z : Swp[2] * r;
         c[3] = all_known ? bl.w : Swp[3] * r;
     } else {  // Eq. 1
-        const float rest = (all_known || N == 0) ? 0.0f : __fdividef(1.0f - Sw, (float)N) * sc;
+        const float rest = (all_known || N == 0) ? 0.0f : __fdividef(1.0f - Sw, (float)N);
         c[0] = fmaf(rest, Sp[0], bl.x);
         c[1] = fmaf(rest, Sp[1], bl.y);
         c[2] = fmaf(rest, Sp[2], bl.z);
@@ -337,9 +305,16 @@ __device__ __forceinline__ float4 combine_eq1(const Foot &f, const bool (&first)
     }
     if (one) {
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) c[ch] = Sp[ch] * sc;
+        for (int ch = 0; ch < 4; ++ch) c[ch] = Sp[ch];
     }
     return make_float4(c[0], c[1], c[2], c[3]);
+}
+template <int FMT>
+__device__ __forceinline__ float4 combine_eq1(const Foot &f, const bool (&first)[4], const float (&dw)[4],
+                                              const bool (&known)[4], const int (&dup)[4], const Texel<FMT> (&p)[4],
+                                              bool wc) {
+    const float4 pv[4] = {p[0].to_f4(), p[1].to_f4(), p[2].to_f4(), p[3].to_f4()};   // texel values in [0, 1]
+    return combine_eq1f(f, first, dw, known, dup, pv, wc);
 }
 
 // Gather via sorted (id << 5 | lane) keys + binary search (any AABB size).
@@ -894,6 +869,247 @@ __device__ __forceinline__ float4 mlp_decode_tc(const TexArgs &t, const TcWeight
 // ----------------------------------------------------------------------- kernel
 constexpr int kChunk = 16;  // waves per work item: a run of consecutive waves in one wave-row
 
+struct MlpCtx {  // latent-MLP COLLAB decoder state (unused by BC1)
+    TcWeights *tw;
+    TcScratch *tsc;
+    MlpLaneWeights *lw;
+    unsigned char *dyn;
+    unsigned warp;
+};
+
+struct WaveOut {
+    float4 color;
+    uint32_t rec, prod, selbits;
+};
+
+// One live wave (A != 0) through the general path: every mode, Box / Mask variant,
+// window size, partial wave and fallback.  The BC1 COLLAB List kernel below sends only
+// its rare waves here (out of line).
+template <int FMT, int MODE, bool DBG>
+__device__ __forceinline__ WaveOut wave_general(const KArgs &a, const typename WeightsOf<FMT>::type &mw, WarpSmem &s,
+                                                const MlpCtx &mc, float2 uv, uint2 gr, bool active, unsigned A,
+                                                int na, int px, int py, uint32_t frame) {
+    const unsigned lane = lane_id();
+    const unsigned lt = lanemask_lt();
+    constexpr bool kBatchMlp = FMT == FMT_MLP && MODE == MODE_COLLAB;
+    (void)mc;
+    (void)kBatchMlp;
+    // Partial wave: inactive lanes borrow the first active lane's inputs, so the
+    // wave-wide reductions below need no per-lane predicates (a duplicate footprint
+    // changes no min, max, OR or unique set).  Their outputs are discarded.
+    float2 uvm = uv;
+    uint2 grm = gr;
+    if (A != FULL) {
+        const int leader = __ffs(A) - 1;
+        const float lu = __shfl_sync(FULL, uv.x, leader), lv = __shfl_sync(FULL, uv.y, leader);
+        const unsigned g0 = __shfl_sync(FULL, gr.x, leader), g1 = __shfl_sync(FULL, gr.y, leader);
+        if (!active) {
+            uvm = make_float2(lu, lv);
+            grm = make_uint2(g0, g1);
+        }
+    }
+    bool mag_lane = true;
+    if (a.grad) {
+        // R-20: squares of fp16 values are exact in fp32, so fma(g0, g0, g1*g1)
+        // rounds once exactly like the fp32 sum of the two products
+        const float rx = fma_f32_f16((unsigned short)(grm.x & 0xffffu), (unsigned short)(grm.x & 0xffffu),
+                                     fma_f32_f16((unsigned short)(grm.x >> 16), (unsigned short)(grm.x >> 16), 0.0f));
+        const float ry = fma_f32_f16((unsigned short)(grm.y & 0xffffu), (unsigned short)(grm.y & 0xffffu),
+                                     fma_f32_f16((unsigned short)(grm.y >> 16), (unsigned short)(grm.y >> 16), 0.0f));
+        mag_lane = rx <= 1.0f && ry <= 1.0f;  // max(rx, ry) <= 1
+    }
+    const bool wave_mag = a.grad != nullptr && __all_sync(FULL, mag_lane);
+    const uint32_t rec_base = ((uint32_t)na << 16) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26);
+
+    // ---- a2: footprint
+    const Foot f = footprint(uvm, a);
+
+    uint32_t prod = INVALID_ID, selbits = 0u, rec;
+    float4 color = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    if constexpr (MODE == MODE_4TAP) {
+        rec = rec_base | (0xFFu << 8) | ((uint32_t)PATH_4TAP << 22) | (uint32_t)((4 * na) & 0xFF);
+        if (active) {
+            if constexpr (FMT == FMT_BC1) {
+                Texel<FMT> p[4];
+                p[0] = produce(a.tex, mw, f.xa, f.ya);
+                p[1] = produce(a.tex, mw, f.xb, f.ya);
+                p[2] = produce(a.tex, mw, f.xa, f.yb);
+                p[3] = produce(a.tex, mw, f.xb, f.yb);
+                color = blend4<FMT>(p, f.w);
+            } else {
+                // one decode at a time (no interleaving of four MLPs); same op order as blend4
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+                for (int k = 0; k < 4; ++k) {
+                    const float4 v = produce(a.tex, mw, corner_x(f, k), corner_y(f, k)).v;
+                    const float wk = (k == 0 ? f.w[0] : k == 1 ? f.w[1] : k == 2 ? f.w[2] : f.w[3]);
+                    if (k == 0) {
+                        c[0] = wk * v.x; c[1] = wk * v.y; c[2] = wk * v.z; c[3] = wk * v.w;
+                    } else {
+                        c[0] = fmaf(wk, v.x, c[0]); c[1] = fmaf(wk, v.y, c[1]);
+                        c[2] = fmaf(wk, v.z, c[2]); c[3] = fmaf(wk, v.w, c[3]);
+                    }
+                }
+                color = make_float4(c[0], c[1], c[2], c[3]);
+            }
+        }
+    } else {
+        // ---- a3/a4 (COLLAB) or the pure STF / WC modes: decide who produces what
+        Box b;
+        b.fits = false;
+        b.K = 0;
+        b.lgP = 0;
+        b.minx = b.miny = 0;
+        int rho[4] = {0, 0, 0, 0}, n = 0xFF, fb;
+        int box_w = 0, box_n = 0;   // Box variant: AABB width and area
+        bool exact = false;
+        if constexpr (MODE == MODE_COLLAB) {
+            // collect the exact unique set U and canonical ranks
+            b = wave_box(f, true);   // inactive lanes carry a duplicate footprint
+            if (b.K == 1) n = collect_mask<1>(f, b, true, rho, s, lane);
+            else if (b.K == 2) n = collect_mask<2>(f, b, true, rho, s, lane);
+            else if (b.K == 4) n = collect_mask<4>(f, b, true, rho, s, lane);
+            else {
+                const Collected cc = collect_sort(f, true, s, lane, a.tex.W);
+                n = cc.n;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) rho[k] = cc.rho[k];
+            }
+            __syncwarp();
+            // a4: List semantics exact iff n <= a (R-6).  The paper's Box and
+            // Mask variants add AABB conditions.
+            if (a.variant == VAR_LIST) {
+                exact = n <= na;
+            } else {
+                const int bw = __reduce_max_sync(FULL, f.xb) - b.minx + 1;
+                const int bh = __reduce_max_sync(FULL, f.yb) - b.miny + 1;
+                if (a.variant == VAR_BOX) {
+                    box_w = bw;
+                    box_n = bw * bh;
+                    exact = box_n <= na;
+                } else {
+                    const int lim = a.variant == VAR_MASK16 ? 16 : 11;
+                    exact = bw <= lim && bh <= lim && n <= na;
+                }
+            }
+            exact = exact && !(a.flags & FLAG_FORCE_FALLBACK);
+            fb = a.fallback;
+        } else {
+            fb = MODE == MODE_STF ? FB_STF : FB_WC;
+            if constexpr (MODE == MODE_WC) b = wave_box(f, active);
+        }
+        const bool full = A == FULL;
+        Plan pl;
+        if (exact) {
+            // ---- a5: active rank r < n produces U[r] on lane h(r, A)
+            const int ar = __popc(A & lt);
+            if (!full) {
+                if (active) s.lane_of_rank[ar] = (uint8_t)lane;
+                __syncwarp();
+            }
+            pl.qx = pl.qy = 0;
+            pl.selbits = 0u;
+            if (a.variant != VAR_BOX) {
+                pl.produced = active && ar < n;
+                if (pl.produced) {
+                    const uint32_t e = s.tbl[ar];
+                    if (b.fits) { pl.qx = box_x(b, e); pl.qy = box_y(b, e); }
+                    else { pl.qx = (int)(e & 0xffffu); pl.qy = (int)(e >> 16); }
+                }
+            } else {
+                // Box: active rank i < w*h produces AABB texel (i mod w, i div w)
+                // (LaneIdxToCoord); corners gather by their local index
+                // (CoordToLaneIdx) through h(., A)
+                pl.produced = active && ar < box_n;
+                const int yq = ar / box_w;
+                pl.qx = b.minx + (ar - yq * box_w);
+                pl.qy = b.miny + yq;
+                const int t0 = (f.ya - b.miny) * box_w + (f.xa - b.minx);
+                const int t2 = (f.yb - b.miny) * box_w + (f.xa - b.minx);
+                rho[0] = t0;
+                rho[1] = t0 + (f.xb - f.xa);
+                rho[2] = t2;
+                rho[3] = t2 + (f.xb - f.xa);
+            }
+        } else if constexpr (FMT == FMT_BC1) {
+            pl.produced = false;
+            pl.qx = pl.qy = 0;
+        } else {
+            pl = fb_plan(fb, f, b, active, A, na, px, py, frame, a.seed_lo, a.seed_hi, a.tex.W, s);
+        }
+        FbAll fball{};
+        if constexpr (FMT == FMT_BC1) {
+            if (!exact) fball = fb_all_bc1(fb, f, b, active, A, na, px, py, frame, a, s);
+        }
+        selbits = (FMT == FMT_BC1 && !exact) ? fball.selbits : pl.selbits;
+        // ---- the single texel-production site (<= 1 evaluation per lane)
+        Texel<FMT> val = Texel<FMT>::zero();
+        if constexpr (kBatchMlp) {
+#if CTF_MLP_TC
+            // exact and fallback waves alike: the wave's produced texels (row = lane)
+            // go through the tensor-core decoder together
+            val.v = mlp_decode_tc(a.tex, *mc.tw, *mc.tsc, pl.produced, pl.qx, pl.qy, lane);
+            if (pl.produced) prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
+#else
+            if (exact) {
+                MlpBatchSmem &ms = reinterpret_cast<MlpBatchSmem *>(mc.dyn)[mc.warp];
+                val.v = mlp_decode_batched(a.tex, mw, ms, *mc.lw, pl.produced, __popc(A & lt), pl.qx, pl.qy,
+                                           a.variant == VAR_BOX ? box_n : n, lane);
+                if (pl.produced) prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
+            } else if (pl.produced) {
+                val = produce(a.tex, mw, pl.qx, pl.qy);
+                prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
+            }
+#endif
+        } else if (pl.produced) {
+            val = produce(a.tex, mw, pl.qx, pl.qy);
+            prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
+        }
+        if constexpr (FMT == FMT_BC1) {
+            if (!exact) prod = fball.prod;
+        }
+        if (exact) {
+            // evals = n (Box: the AABB area), path 0
+            rec = rec_base | ((uint32_t)n << 8) | (uint32_t)(a.variant == VAR_BOX ? box_n : n);
+            // ---- a6: gather from lanes h(rho_k, A) and blend
+            int src[4];
+            if (full) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) src[k] = rho[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) src[k] = active ? (int)s.lane_of_rank[rho[k] & 31] : (int)lane;
+            }
+            Texel<FMT> p[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
+            if (active) color = blend4<FMT>(p, f.w);
+            if (DBG && a.dbg_unread) {
+                unsigned bad = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int pk = __shfl_sync(FULL, (int)pl.produced, src[k]);  // every lane shuffles
+                    bad += (active && !pk) ? 1u : 0u;
+                }
+                bad = __reduce_add_sync(FULL, bad);       // warp-uniform: no divergent atomic
+                if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
+            }
+        } else {
+            // ---- a7: fallback combine
+            Finished o;
+            if constexpr (FMT == FMT_BC1) o = fball.fin;
+            else o = fb_finish<FMT>(fb, f, b, active, na, pl, val, a.tex.W, s);
+            color = o.color;
+            const uint32_t path = MODE == MODE_COLLAB ? (uint32_t)(PATH_FB_STF + fb)
+                                                      : (uint32_t)(MODE == MODE_STF ? PATH_STF : PATH_WC);
+            rec = rec_base | ((uint32_t)(n & 0xFF) << 8) | (path << 22) | (uint32_t)(o.evals & 0xFF);
+        }
+    }
+
+    return {color, rec, prod, selbits};
+}
+
 template <int FMT, int MODE, bool DBG>
 __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : (MODE == MODE_COLLAB ? CTF_MLP_COLLAB_MINB : 2)))
     ctf_filter_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
@@ -902,17 +1118,20 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : 
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     WarpSmem &s = smem[warp];
     constexpr bool kBatchMlp = FMT == FMT_MLP && MODE == MODE_COLLAB;
+    MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
 #if CTF_MLP_TC
     // tensor-core decoder: weights (hi / lo fp16) shared by the CTA, scratch per warp
     TcWeights &tw = *reinterpret_cast<TcWeights *>(dyn_smem);
     TcScratch &tsc = reinterpret_cast<TcScratch *>(dyn_smem + sizeof(TcWeights))[warp];
     if constexpr (kBatchMlp) fill_tc_weights(mw, tw);
+    mc.tw = &tw;
+    mc.tsc = &tsc;
 #else
     MlpLaneWeights lw;
     if constexpr (kBatchMlp) load_lane_weights(a.tex.mlp_dev, lane, lw);
+    mc.lw = &lw;
 #endif
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
-    const unsigned lt = lanemask_lt();
 
     // work item c = (frame, wave-row, run of kChunk waves); items are interleaved over
     // the whole batch so every warp gets the same mix of sky / exact / fallback regions.
@@ -982,231 +1201,445 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : 
                 if (lane == (unsigned)(wx - wx0)) myrec = ((MODE == MODE_COLLAB ? 0u : 0xFFu) << 8) | (1u << 26);
                 continue;
             }
-            // Partial wave: inactive lanes borrow the first active lane's inputs, so the
-            // wave-wide reductions below need no per-lane predicates (a duplicate footprint
-            // changes no min, max, OR or unique set).  Their outputs are discarded.
-            float2 uvm = uv;
-            uint2 grm = gr;
-            if (A != FULL) {
-                const int leader = __ffs(A) - 1;
-                const float lu = __shfl_sync(FULL, uv.x, leader), lv = __shfl_sync(FULL, uv.y, leader);
-                const unsigned g0 = __shfl_sync(FULL, gr.x, leader), g1 = __shfl_sync(FULL, gr.y, leader);
-                if (!active) {
-                    uvm = make_float2(lu, lv);
-                    grm = make_uint2(g0, g1);
-                }
-            }
-            bool mag_lane = true;
-            if (a.grad) {
-                // R-20: squares of fp16 values are exact in fp32, so fma(g0, g0, g1*g1)
-                // rounds once exactly like the fp32 sum of the two products
-                const float rx = fma_f32_f16((unsigned short)(grm.x & 0xffffu), (unsigned short)(grm.x & 0xffffu),
-                                             fma_f32_f16((unsigned short)(grm.x >> 16), (unsigned short)(grm.x >> 16), 0.0f));
-                const float ry = fma_f32_f16((unsigned short)(grm.y & 0xffffu), (unsigned short)(grm.y & 0xffffu),
-                                             fma_f32_f16((unsigned short)(grm.y >> 16), (unsigned short)(grm.y >> 16), 0.0f));
-                mag_lane = rx <= 1.0f && ry <= 1.0f;  // max(rx, ry) <= 1
-            }
-            const bool wave_mag = a.grad != nullptr && __all_sync(FULL, mag_lane);
-            const uint32_t rec_base = ((uint32_t)na << 16) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26);
-
-            // ---- a2: footprint
-            const Foot f = footprint(uvm, a);
-
-            uint32_t prod = INVALID_ID, selbits = 0u, rec;
-            float4 color = make_float4(0.f, 0.f, 0.f, 0.f);
-
-            if constexpr (MODE == MODE_4TAP) {
-                rec = rec_base | (0xFFu << 8) | ((uint32_t)PATH_4TAP << 22) | (uint32_t)((4 * na) & 0xFF);
-                if (active) {
-                    if constexpr (FMT == FMT_BC1) {
-                        Texel<FMT> p[4];
-                        p[0] = produce(a.tex, mw, f.xa, f.ya);
-                        p[1] = produce(a.tex, mw, f.xb, f.ya);
-                        p[2] = produce(a.tex, mw, f.xa, f.yb);
-                        p[3] = produce(a.tex, mw, f.xb, f.yb);
-                        color = blend4<FMT>(p, f.w);
-                    } else {
-                        // one decode at a time (no interleaving of four MLPs); same op order as blend4
-                        float c[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-                        for (int k = 0; k < 4; ++k) {
-                            const float4 v = produce(a.tex, mw, corner_x(f, k), corner_y(f, k)).v;
-                            const float wk = (k == 0 ? f.w[0] : k == 1 ? f.w[1] : k == 2 ? f.w[2] : f.w[3]);
-                            if (k == 0) {
-                                c[0] = wk * v.x; c[1] = wk * v.y; c[2] = wk * v.z; c[3] = wk * v.w;
-                            } else {
-                                c[0] = fmaf(wk, v.x, c[0]); c[1] = fmaf(wk, v.y, c[1]);
-                                c[2] = fmaf(wk, v.z, c[2]); c[3] = fmaf(wk, v.w, c[3]);
-                            }
-                        }
-                        color = make_float4(c[0], c[1], c[2], c[3]);
-                    }
-                }
-            } else {
-                // ---- a3/a4 (COLLAB) or the pure STF / WC modes: decide who produces what
-                Box b;
-                b.fits = false;
-                b.K = 0;
-                b.lgP = 0;
-                b.minx = b.miny = 0;
-                int rho[4] = {0, 0, 0, 0}, n = 0xFF, fb;
-                int box_w = 0, box_n = 0;   // Box variant: AABB width and area
-                bool exact = false;
-                if constexpr (MODE == MODE_COLLAB) {
-                    // collect the exact unique set U and canonical ranks
-                    b = wave_box(f, true);   // inactive lanes carry a duplicate footprint
-                    if (b.K == 1) n = collect_mask<1>(f, b, true, rho, s, lane);
-                    else if (b.K == 2) n = collect_mask<2>(f, b, true, rho, s, lane);
-                    else if (b.K == 4) n = collect_mask<4>(f, b, true, rho, s, lane);
-                    else {
-                        const Collected cc = collect_sort(f, true, s, lane, a.tex.W);
-                        n = cc.n;
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) rho[k] = cc.rho[k];
-                    }
-                    __syncwarp();
-                    // a4: List semantics exact iff n <= a (R-6).  The paper's Box and
-                    // Mask variants add AABB conditions.
-                    if (a.variant == VAR_LIST) {
-                        exact = n <= na;
-                    } else {
-                        const int bw = __reduce_max_sync(FULL, f.xb) - b.minx + 1;
-                        const int bh = __reduce_max_sync(FULL, f.yb) - b.miny + 1;
-                        if (a.variant == VAR_BOX) {
-                            box_w = bw;
-                            box_n = bw * bh;
-                            exact = box_n <= na;
-                        } else {
-                            const int lim = a.variant == VAR_MASK16 ? 16 : 11;
-                            exact = bw <= lim && bh <= lim && n <= na;
-                        }
-                    }
-                    exact = exact && !(a.flags & FLAG_FORCE_FALLBACK);
-                    fb = a.fallback;
-                } else {
-                    fb = MODE == MODE_STF ? FB_STF : FB_WC;
-                    if constexpr (MODE == MODE_WC) b = wave_box(f, active);
-                }
-                const bool full = A == FULL;
-                Plan pl;
-                if (exact) {
-                    // ---- a5: active rank r < n produces U[r] on lane h(r, A)
-                    const int ar = __popc(A & lt);
-                    if (!full) {
-                        if (active) s.lane_of_rank[ar] = (uint8_t)lane;
-                        __syncwarp();
-                    }
-                    pl.qx = pl.qy = 0;
-                    pl.selbits = 0u;
-                    if (a.variant != VAR_BOX) {
-                        pl.produced = active && ar < n;
-                        if (pl.produced) {
-                            const uint32_t e = s.tbl[ar];
-                            if (b.fits) { pl.qx = box_x(b, e); pl.qy = box_y(b, e); }
-                            else { pl.qx = (int)(e & 0xffffu); pl.qy = (int)(e >> 16); }
-                        }
-                    } else {
-                        // Box: active rank i < w*h produces AABB texel (i mod w, i div w)
-                        // (LaneIdxToCoord); corners gather by their local index
-                        // (CoordToLaneIdx) through h(., A)
-                        pl.produced = active && ar < box_n;
-                        const int yq = ar / box_w;
-                        pl.qx = b.minx + (ar - yq * box_w);
-                        pl.qy = b.miny + yq;
-                        const int t0 = (f.ya - b.miny) * box_w + (f.xa - b.minx);
-                        const int t2 = (f.yb - b.miny) * box_w + (f.xa - b.minx);
-                        rho[0] = t0;
-                        rho[1] = t0 + (f.xb - f.xa);
-                        rho[2] = t2;
-                        rho[3] = t2 + (f.xb - f.xa);
-                    }
-                } else if constexpr (FMT == FMT_BC1) {
-                    pl.produced = false;
-                    pl.qx = pl.qy = 0;
-                } else {
-                    pl = fb_plan(fb, f, b, active, A, na, px, py, frame, a.seed_lo, a.seed_hi, a.tex.W, s);
-                }
-                FbAll fball{};
-                if constexpr (FMT == FMT_BC1) {
-                    if (!exact) fball = fb_all_bc1(fb, f, b, active, A, na, px, py, frame, a, s);
-                }
-                selbits = (FMT == FMT_BC1 && !exact) ? fball.selbits : pl.selbits;
-                // ---- the single texel-production site (<= 1 evaluation per lane)
-                Texel<FMT> val = Texel<FMT>::zero();
-                if constexpr (kBatchMlp) {
-#if CTF_MLP_TC
-                    // exact and fallback waves alike: the wave's produced texels (row = lane)
-                    // go through the tensor-core decoder together
-                    val.v = mlp_decode_tc(a.tex, tw, tsc, pl.produced, pl.qx, pl.qy, lane);
-                    if (pl.produced) prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
-#else
-                    if (exact) {
-                        MlpBatchSmem &ms = reinterpret_cast<MlpBatchSmem *>(dyn_smem)[warp];
-                        val.v = mlp_decode_batched(a.tex, mw, ms, lw, pl.produced, __popc(A & lt), pl.qx, pl.qy,
-                                                   a.variant == VAR_BOX ? box_n : n, lane);
-                        if (pl.produced) prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
-                    } else if (pl.produced) {
-                        val = produce(a.tex, mw, pl.qx, pl.qy);
-                        prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
-                    }
-#endif
-                } else if (pl.produced) {
-                    val = produce(a.tex, mw, pl.qx, pl.qy);
-                    prod = (uint32_t)(pl.qy * a.tex.W + pl.qx);
-                }
-                if constexpr (FMT == FMT_BC1) {
-                    if (!exact) prod = fball.prod;
-                }
-                if (exact) {
-                    // evals = n (Box: the AABB area), path 0
-                    rec = rec_base | ((uint32_t)n << 8) | (uint32_t)(a.variant == VAR_BOX ? box_n : n);
-                    // ---- a6: gather from lanes h(rho_k, A) and blend
-                    int src[4];
-                    if (full) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) src[k] = rho[k];
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) src[k] = active ? (int)s.lane_of_rank[rho[k] & 31] : (int)lane;
-                    }
-                    Texel<FMT> p[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
-                    if (active) color = blend4<FMT>(p, f.w);
-                    if (DBG && a.dbg_unread) {
-                        unsigned bad = 0;
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const int pk = __shfl_sync(FULL, (int)pl.produced, src[k]);  // every lane shuffles
-                            bad += (active && !pk) ? 1u : 0u;
-                        }
-                        bad = __reduce_add_sync(FULL, bad);       // warp-uniform: no divergent atomic
-                        if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
-                    }
-                } else {
-                    // ---- a7: fallback combine
-                    Finished o;
-                    if constexpr (FMT == FMT_BC1) o = fball.fin;
-                    else o = fb_finish<FMT>(fb, f, b, active, na, pl, val, a.tex.W, s);
-                    color = o.color;
-                    const uint32_t path = MODE == MODE_COLLAB ? (uint32_t)(PATH_FB_STF + fb)
-                                                              : (uint32_t)(MODE == MODE_STF ? PATH_STF : PATH_WC);
-                    rec = rec_base | ((uint32_t)(n & 0xFF) << 8) | (path << 22) | (uint32_t)(o.evals & 0xFF);
-                }
-            }
-
+            const WaveOut o = wave_general<FMT, MODE, DBG>(a, mw, s, mc, uv, gr, active, A, na, px, py, frame);
             // ---- outputs
-            if (inframe) st_stream_f4(a.out + pix, color);
+            if (inframe) st_stream_f4(a.out + pix, o.color);
             if (DBG && inframe) {
-                if (a.dbg_pid) a.dbg_pid[pix] = (MODE == MODE_4TAP) ? INVALID_ID : prod;
-                if (a.dbg_sel) a.dbg_sel[pix] = selbits;
+                if (a.dbg_pid) a.dbg_pid[pix] = (MODE == MODE_4TAP) ? INVALID_ID : o.prod;
+                if (a.dbg_sel) a.dbg_sel[pix] = o.selbits;
             }
             // ---- a8: per-wave record (kept in lane wx - wx0, stored per run)
+            if (lane == (unsigned)(wx - wx0)) myrec = o.rec;
+        }
+        if (lane < (unsigned)(wx1 - wx0)) a.rec[w0 + lane] = myrec;
+    }
+}
+
+#if CTF_TU_FMT == 1
+// ------------------------------------------- BC1 COLLAB (List) kernel: the lean path
+// On a magnified frame nearly every wave is FULL (32 active lanes) with a footprint
+// bounding box that fits an 8x4 / 4x8 window (one 32-bit mask) or an 8x8 window (two
+// words).  Those waves run the straight-line code below, exact or fallback:
+//   collect  : 2 redux.min (AABB origin) + 1-3 votes (window) + 1-2
+//              redux.or (WaveActiveBitOr) + popc ranks (h^-1);
+//   decide   : exact iff n <= 32 (the wave is full);
+//   produce  : exact: lane r < n decodes U[r] (h(r, A) = r); fallback: the
+//              STF / C+ plan below; one decode site, converted to fp32 once (v / 255);
+//   gather   : the produced values go through shared memory (one STS.128 per producer,
+//              LDS.128 per corner) — WaveReadLaneAt with the conversion
+//              done once per texel instead of once per read;
+//   filter   : exact: blend4f (FFMA2), bit-identical to every other exact path;
+//              fallback: one-tap / WC / Eq. 1 (combine_eq1f, as the general path).
+// The remaining waves (partial coverage; windows wider than 8x8, e.g. minified waves)
+// are marked in their record with kSlowMark and finished by ctf_collab_bc1_rest_kernel
+// through the general path (wave_general): the record buffer is the work list, so no
+// workspace is needed, and the lean kernel contains no call (a call makes ptxas guard
+// every warp collective with a divergence check).
+constexpr uint32_t kSlowMark = 0xFFFFFFFFu;   // never a COLLAB record (path <= 4, n <= 128)
+
+struct FastSmem {
+    float4 xch[64];           // exact: rank -> produced value; fallback: window position -> produced value
+    uint8_t bit_of_rank[32];  // rank -> window bit (0..63)
+};
+
+#ifndef CTF_FAST_MINB
+#define CTF_FAST_MINB 6  // resident CTAs per SM (40 registers, no spills)
+#endif
+
+// 64-bit window masks held as two words (hi = 0 for a 32-bit window)
+__device__ __forceinline__ uint32_t bit_lo(uint32_t t) { return t < 32u ? 1u << t : 0u; }
+__device__ __forceinline__ uint32_t bit_hi(uint32_t t) { return t >= 32u ? 1u << (t - 32u) : 0u; }
+__device__ __forceinline__ bool test64(uint32_t lo, uint32_t hi, uint32_t t) {
+    return ((t < 32u ? lo : hi) >> (t & 31u)) & 1u;
+}
+__device__ __forceinline__ int rank64(uint32_t lo, uint32_t hi, uint32_t t) {   // set bits below t
+    return t < 32u ? __popc(lo & ((1u << t) - 1u)) : __popc(lo) + __popc(hi & ((1u << (t - 32u)) - 1u));
+}
+
+// Distinct texels of a footprint and their merged fp32 weights (R-14) from the clamp
+// flags alone: corner k is the first occurrence of its texel iff (k & 1 -> xb != xa) and
+// (k & 2 -> yb != ya), and the duplicates are added in corner order — the same values,
+// bit for bit, as distinct_corners() (adding +0 is exact).
+struct Merged {
+    float dw[4];
+    bool first[4];
+};
+__device__ __forceinline__ Merged merge_corners(const Foot &f) {
+    const bool ddx = f.xb != f.xa, ddy = f.yb != f.ya;
+    Merged m;
+    m.dw[0] = __fadd_rn(__fadd_rn(__fadd_rn(f.w[0], ddx ? 0.0f : f.w[1]), ddy ? 0.0f : f.w[2]),
+                        (ddx || ddy) ? 0.0f : f.w[3]);
+    m.dw[1] = __fadd_rn(f.w[1], ddy ? 0.0f : f.w[3]);
+    m.dw[2] = __fadd_rn(f.w[2], ddx ? 0.0f : f.w[3]);
+    m.dw[3] = f.w[3];
+    m.first[0] = true;
+    m.first[1] = ddx;
+    m.first[2] = ddy;
+    m.first[3] = ddx && ddy;
+    return m;
+}
+
+// C+ spare-lane pick (R-18 v) over served lane g's footprint, straight-line: the distinct
+// nonzero-weight texels not planned, chosen ~ merged weight with u2 (first cumulative
+// sum > u2 * sum, else the last candidate); -1 when there is none.  = cplus_pick().
+template <typename Planned>
+__device__ __forceinline__ int cplus_pick_lean(const Foot &g, float u2, Planned planned) {
+    const Merged m = merge_corners(g);
+    bool cand[4];
+    float wsum = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cand[k] = m.first[k] && m.dw[k] != 0.0f && !planned(corner_x(g, k), corner_y(g, k));
+        wsum = __fadd_rn(wsum, cand[k] ? m.dw[k] : 0.0f);
+    }
+    const float target = __fmul_rn(u2, wsum);
+    float cum = 0.0f;
+    int pick = -1, lastc = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cum = __fadd_rn(cum, cand[k] ? m.dw[k] : 0.0f);
+        pick = (pick < 0 && cand[k] && cum > target) ? k : pick;
+        lastc = cand[k] ? k : lastc;
+    }
+    return pick < 0 ? lastc : pick;
+}
+
+// One-tap / WC stand-in / Eq. 1 from per-corner values pv[k] (0 where the texel was not
+// produced; in[k] = produced), straight-line.  Same operations in the same order as
+// combine_eq1f over distinct_corners (adding / fma-ing exact zeros changes nothing), so
+// the special cases hold bit for bit and the rest matches it exactly.
+__device__ __forceinline__ float4 combine_eq1_lean(const Foot &f, const bool (&in)[4], const float4 (&pv)[4], bool wc) {
+    const Merged m = merge_corners(f);
+    bool all_known = true;
+    int N = 0;
+    float Sw = 0.0f;
+    uint64_t sp01 = f2pack(0.f, 0.f), sp23 = f2pack(0.f, 0.f), sq01 = f2pack(0.f, 0.f), sq23 = f2pack(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool contrib = m.first[k] && m.dw[k] != 0.0f;
+        const bool kn = contrib && in[k];
+        all_known = all_known && (!contrib || in[k]);
+        N += kn ? 1 : 0;
+        Sw = __fadd_rn(Sw, kn ? m.dw[k] : 0.0f);
+        const float one = kn ? 1.0f : 0.0f, wk = kn ? m.dw[k] : 0.0f;
+        sp01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(one, one), sp01);   // Sp += p (exact product)
+        sp23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(one, one), sp23);
+        sq01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(wk, wk), sq01);     // WC: sum dw * p
+        sq23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(wk, wk), sq23);
+    }
+    const float4 bl = blend4f(pv, f.w);   // sum over the known corners of w_k p_k
+    const float2 a01 = f2unpack(sp01), a23 = f2unpack(sp23);
+    float4 c;
+    if (wc) {
+        const float2 q01 = f2unpack(sq01), q23 = f2unpack(sq23);
+        const float r = 1.0f / Sw;
+        c = all_known ? bl : make_float4(q01.x * r, q01.y * r, q23.x * r, q23.y * r);
+    } else {
+        const float rest = (all_known || N == 0) ? 0.0f : __fdividef(1.0f - Sw, (float)N);
+        c = make_float4(fmaf(rest, a01.x, bl.x), fmaf(rest, a01.y, bl.y), fmaf(rest, a23.x, bl.z),
+                        fmaf(rest, a23.y, bl.w));
+    }
+    if (N == 1 && !all_known) c = make_float4(a01.x, a01.y, a23.x, a23.y);
+    return c;
+}
+
+// One FULL wave (32 active lanes) through the lean path.  Returns done = false when the
+// window does not fit 8x8, or (FALLBACK = false) when the wave needs a fallback.
+struct LeanOut {
+    float4 color;
+    uint32_t rec, prod, selbits;
+    bool done;
+};
+
+template <bool DBG, bool FALLBACK>
+__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float2 uv, uint2 gr, int px, int py,
+                                             uint32_t frame) {
+    const unsigned lane = lane_id(), lt = lanemask_lt(), lanebit = 1u << lane;
+    const bool has_grad = a.grad != nullptr;
+    LeanOut o;
+    o.color = make_float4(0.f, 0.f, 0.f, 0.f);
+    o.rec = 0u;
+    o.prod = INVALID_ID;
+    o.selbits = 0u;
+    o.done = false;
+    // ---- a1: magnified class (R-20), as in the general path
+    bool mag_lane = true;
+    if (has_grad) {
+        const float rx = fma_f32_f16((unsigned short)(gr.x & 0xffffu), (unsigned short)(gr.x & 0xffffu),
+                                     fma_f32_f16((unsigned short)(gr.x >> 16), (unsigned short)(gr.x >> 16), 0.0f));
+        const float ry = fma_f32_f16((unsigned short)(gr.y & 0xffffu), (unsigned short)(gr.y & 0xffffu),
+                                     fma_f32_f16((unsigned short)(gr.y >> 16), (unsigned short)(gr.y >> 16), 0.0f));
+        mag_lane = rx <= 1.0f && ry <= 1.0f;
+    }
+    const bool wave_mag = has_grad && __all_sync(FULL, mag_lane);
+    // ---- a2: footprint
+    const Foot f = footprint(uv, a);
+    // ---- a3: AABB origin and window
+    const int minx = __reduce_min_sync(FULL, f.xa), miny = __reduce_min_sync(FULL, f.ya);
+    const unsigned dx = (unsigned)(f.xb - minx), dy = (unsigned)(f.yb - miny);
+    int K = 0;
+    unsigned lgP = 3u;
+    if (__all_sync(FULL, (dx | (dy << 1)) < 8u)) K = 1;                      // 8x4
+    else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; lgP = 2u; }   // 4x8
+    else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                        // 8x8
+    if (K != 0) {
+        o.done = true;
+        const uint32_t pmask = (1u << lgP) - 1u;
+        const uint32_t t0 = ((uint32_t)(f.ya - miny) << lgP) + (uint32_t)(f.xa - minx);
+        const uint32_t t2 = t0 + ((uint32_t)(f.yb - f.ya) << lgP);
+        const uint32_t dxs = (uint32_t)(f.xb - f.xa);
+        const uint32_t pat = 1u + dxs + dxs;   // bits t and t + dxs (same window row)
+        int n, r0, r2;
+        if (K == 1) {
+            const uint32_t wm = __reduce_or_sync(FULL, (pat << t0) | (pat << t2));
+            n = __popc(wm);
+            r0 = __popc(wm & ((1u << t0) - 1u));
+            r2 = __popc(wm & ((1u << t2) - 1u));
+            if (wm & lanebit) fs.bit_of_rank[__popc(wm & lt)] = (uint8_t)lane;
+        } else {
+            const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
+            const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
+            const uint32_t wh = __reduce_or_sync(FULL, (uint32_t)(m >> 32));
+            const int nl = __popc(wl);
+            n = nl + __popc(wh);
+            r0 = rank64(wl, wh, t0);
+            r2 = rank64(wl, wh, t2);
+            if (wl & lanebit) fs.bit_of_rank[__popc(wl & lt)] = (uint8_t)lane;
+            const int rh = nl + __popc(wh & lt);
+            if ((wh & lanebit) && rh < 32) fs.bit_of_rank[rh] = (uint8_t)(32u + lane);
+        }
+        // ---- a4: exact iff n <= a = 32 (always for a 32-bit window)
+        const bool exact = n <= 32 && !(a.flags & FLAG_FORCE_FALLBACK);
+        if (!FALLBACK && !exact) {
+            o.done = false;   // left to the second kernel
+            return o;
+        }
+        __syncwarp();
+        bool produced;
+        int qx = 0, qy = 0;
+        const int fb = a.fallback;
+        if (exact) {
+            // ---- a5: lane r < n produces U[r]
+            produced = (int)lane < n;
+            const uint32_t e = fs.bit_of_rank[lane];
+            qx = minx + (int)(e & pmask);
+            qy = miny + (int)(e >> lgP);
+        } else {
+            // ---- a7 plan: every lane's STF texel; C+ dedupes it
+            // and spreads the spare lanes over the wave with Eq. 2
+            const uint4 rn = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo,
+                                           a.seed_hi);
+            const int ksel = stf_corner(f, rn);
+            qx = corner_x(f, ksel);
+            qy = corner_y(f, ksel);
+            o.selbits = (uint32_t)ksel;
+            produced = true;
+            if (fb == FB_CPLUS) {
+                const uint32_t tp = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
+                const uint32_t pl = __reduce_or_sync(FULL, bit_lo(tp));   // planned set P
+                const uint32_t ph = __reduce_or_sync(FULL, bit_hi(tp));
+                const int npl = __popc(pl), np = npl + __popc(ph);
+                if (pl & lanebit) fs.bit_of_rank[__popc(pl & lt)] = (uint8_t)lane;
+                if (ph & lanebit) fs.bit_of_rank[npl + __popc(ph & lt)] = (uint8_t)(32u + lane);
+                __syncwarp();
+                const bool spare = (int)lane >= np;
+                const int l = spare ? eq2_lane_rank((int)lane, np, 32) : (int)lane;   // h(., A) = id
+                Foot g;
+                g.xa = __shfl_sync(FULL, f.xa, l);
+                g.xb = __shfl_sync(FULL, f.xb, l);
+                g.ya = __shfl_sync(FULL, f.ya, l);
+                g.yb = __shfl_sync(FULL, f.yb, l);
+                g.s = __shfl_sync(FULL, f.s, l);
+                g.t = __shfl_sync(FULL, f.t, l);
+                make_weights(g);
+                const int pick = cplus_pick_lean(g, unit24(rn.z), [&](int x, int y) {
+                    return test64(pl, ph, ((uint32_t)(y - miny) << lgP) + (uint32_t)(x - minx));
+                });
+                const uint32_t e = fs.bit_of_rank[lane & 31u];
+                if (!spare) {   // planned rank `lane` < n_p
+                    qx = minx + (int)(e & pmask);
+                    qy = miny + (int)(e >> lgP);
+                } else {
+                    o.selbits |= (1u << 5) | ((uint32_t)l << 8);
+                    produced = pick >= 0;
+                    qx = produced ? corner_x(g, pick) : qx;
+                    qy = produced ? corner_y(g, pick) : qy;
+                    o.selbits |= produced ? (((uint32_t)pick << 2) | (1u << 4)) : 0u;
+                }
+            }
+        }
+        // ---- the single texel-production site (<= 1 evaluation per lane)
+        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (produced) {
+            val = rgba8_unorm(bc1_decode(a.tex, qx, qy));
+            if (DBG) o.prod = (uint32_t)(qy * a.tex.W + qx);
+        }
+        if (exact) {
+            if (produced) fs.xch[lane] = val;
+            __syncwarp();
+            // ---- a6: gather (ranks rho_k; the wave is full so h(r, A) = r) + blend
+            const float4 p[4] = {fs.xch[r0], fs.xch[r0 + (int)dxs], fs.xch[r2], fs.xch[r2 + (int)dxs]};
+            o.color = blend4f(p, f.w);
+            o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
+            if (DBG && a.dbg_unread) {
+                const unsigned bad = __reduce_add_sync(
+                    FULL, (unsigned)(r0 >= n) + (unsigned)(r0 + (int)dxs >= n) + (unsigned)(r2 >= n) +
+                              (unsigned)(r2 + (int)dxs >= n));
+                if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
+            }
+        } else {
+            // ---- a7 finish: one-tap (STF), WC stand-in or Eq. 1 (C, C+) over the
+            // produced set D of the wave
+            const int evals = fb == FB_CPLUS ? __popc(__ballot_sync(FULL, produced)) : 32;
+            if (fb == FB_STF) {
+                o.color = val;
+            } else {
+                const uint32_t tq = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
+                const uint32_t dl = __reduce_or_sync(FULL, produced ? bit_lo(tq) : 0u);
+                const uint32_t dh = __reduce_or_sync(FULL, produced ? bit_hi(tq) : 0u);
+                // one publisher per produced texel (the decode is deterministic); the
+                // values are indexed by window position
+                const unsigned peers = __match_any_sync(FULL, produced ? tq : 0xFFFFFFFFu);
+                if (produced && (unsigned)(__ffs(peers) - 1) == lane) fs.xch[tq] = val;
+                __syncwarp();
+                bool in[4];
+                float4 pv[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t t = ((uint32_t)(corner_y(f, k) - miny) << lgP) +
+                                       (uint32_t)(corner_x(f, k) - minx);
+                    in[k] = test64(dl, dh, t);
+                    pv[k] = in[k] ? fs.xch[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                o.color = combine_eq1_lean(f, in, pv, fb == FB_WC);
+            }
+            o.rec = (uint32_t)evals | ((uint32_t)n << 8) | (32u << 16) |
+                  ((uint32_t)(PATH_FB_STF + fb) << 22) | ((uint32_t)wave_mag << 25);
+        }
+    }
+    return o;
+}
+
+template <bool DBG>
+__global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_kernel(const KArgs a) {
+    __shared__ FastSmem fsm[kWarps];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    FastSmem &fs = fsm[warp];
+    const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
+    const unsigned per_warp = a.ipc / kWarps;
+    for (unsigned k = warp;; k += kWarps) {
+        const unsigned c = (blockIdx.x * kWarps + (k % kWarps)) + (k / kWarps) * gridDim.x * kWarps;
+        if (k / kWarps >= per_warp || c >= a.nchunks) break;
+        const int fr = (int)(c / (unsigned)a.cpf);
+        const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
+        const int wy = rr / a.cpr;
+        const int wx0 = (rr - wy * a.cpr) * kChunk;
+        const int wx1 = min(wx0 + kChunk, a.nwx);
+        const int py = wy * 4 + ly;
+        const bool rowok = py < a.Hf;
+        const uint32_t frame = a.frame_index + (uint32_t)fr;
+        const unsigned w0 = (unsigned)fr * (unsigned)a.wpf + (unsigned)(wy * a.nwx + wx0);
+        unsigned pix = (unsigned)fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)(wx0 * 8 + lx);
+        int px = wx0 * 8 + lx;
+        const bool has_grad = a.grad != nullptr;
+        float2 uv_n = make_float2(__int_as_float(0x7fc00000), 0.f);
+        uint2 gr_n = make_uint2(0u, 0u);
+        ld_stream_f2_if(uv_n, a.uv + pix, rowok & (px < a.Wf));
+        ld_stream_u2_if(gr_n, a.grad + pix, rowok & (px < a.Wf) & has_grad);
+        uint32_t myrec = 0u;
+        for (int wx = wx0; wx < wx1; ++wx, pix += 8u, px += 8) {
+            const bool inframe = rowok & (px < a.Wf);
+            const float2 uv = uv_n;
+            const uint2 gr = gr_n;
+            const bool pf = (wx + 1 < wx1) & rowok & (px + 8 < a.Wf);
+            ld_stream_f2_if(uv_n, a.uv + (pix + 8u), pf);
+            ld_stream_u2_if(gr_n, a.grad + (pix + 8u), pf & has_grad);
+            __syncwarp();  // the previous wave's shared-memory reads are done
+
+            const bool active = inframe && !isnan(uv.x);
+            const unsigned A = __ballot_sync(FULL, active);
+            uint32_t rec;
+            if (A == FULL) {
+                const LeanOut o = lean_wave<DBG, false>(a, fs, uv, gr, px, py, frame);
+                rec = o.done ? o.rec : kSlowMark;
+                if (o.done) {
+                    st_stream_f4(a.out + pix, o.color);
+                    if (DBG) {
+                        if (a.dbg_pid) a.dbg_pid[pix] = o.prod;
+                        if (a.dbg_sel) a.dbg_sel[pix] = 0u;
+                    }
+                }
+            } else if (A == 0u) {   // empty wave: partial, n = 0, zero colour
+                rec = 1u << 26;
+                if (inframe) st_stream_f4(a.out + pix, make_float4(0.f, 0.f, 0.f, 0.f));
+                if (DBG && inframe) {
+                    if (a.dbg_pid) a.dbg_pid[pix] = INVALID_ID;
+                    if (a.dbg_sel) a.dbg_sel[pix] = 0u;
+                }
+            } else {
+                rec = kSlowMark;   // partial wave: second kernel
+            }
             if (lane == (unsigned)(wx - wx0)) myrec = rec;
         }
         if (lane < (unsigned)(wx1 - wx0)) a.rec[w0 + lane] = myrec;
     }
 }
+
+// Second pass over the waves the lean kernel marked with kSlowMark: full waves whose
+// window fits 8x8 (they need a fallback) take the lean fallback; partial waves and wider
+// windows take the general path.  Warps stride over groups of 32 records (one
+// coalesced 128-B load + ballot each).
+template <bool DBG>
+__global__ void __launch_bounds__(kWarps * 32, CTF_BC1_MINB) ctf_collab_bc1_rest_kernel(const KArgs a, unsigned nrec) {
+    __shared__ WarpSmem smem[kWarps];
+    __shared__ FastSmem fsm[kWarps];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    WarpSmem &s = smem[warp];
+    FastSmem &fs = fsm[warp];
+    const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
+    const MlpCtx mc{nullptr, nullptr, nullptr, nullptr, 0u};
+    const unsigned ngroups = (nrec + 31u) / 32u, gwarps = gridDim.x * kWarps;
+    for (unsigned g = blockIdx.x * kWarps + warp; g < ngroups; g += gwarps) {
+        const unsigned wi0 = g * 32u;
+        const uint32_t r = (wi0 + lane < nrec) ? a.rec[wi0 + lane] : 0u;
+        unsigned todo = __ballot_sync(FULL, r == kSlowMark);
+        while (todo) {
+            const unsigned wi = wi0 + (unsigned)(__ffs(todo) - 1);
+            todo &= todo - 1u;
+            const unsigned fr = wi / (unsigned)a.wpf, rem = wi - fr * (unsigned)a.wpf;
+            const int wy = (int)(rem / (unsigned)a.nwx), wx = (int)rem - wy * a.nwx;
+            const int px = wx * 8 + lx, py = wy * 4 + ly;
+            const bool inframe = px < a.Wf && py < a.Hf;
+            const unsigned pix = fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)px;
+            float2 uv = make_float2(__int_as_float(0x7fc00000), 0.f);
+            uint2 gr = make_uint2(0u, 0u);
+            ld_stream_f2_if(uv, a.uv + pix, inframe);
+            ld_stream_u2_if(gr, a.grad + pix, inframe & (a.grad != nullptr));
+            __syncwarp();
+            const bool active = inframe && !isnan(uv.x);
+            const unsigned A = __ballot_sync(FULL, active);
+            const uint32_t frame = a.frame_index + fr;
+            LeanOut o;
+            o.done = false;
+            if (A == FULL) o = lean_wave<DBG, true>(a, fs, uv, gr, px, py, frame);
+            if (!o.done) {
+                const WaveOut go = wave_general<FMT_BC1, MODE_COLLAB, DBG>(a, NoWeights{}, s, mc, uv, gr, active, A,
+                                                                           __popc(A), px, py, frame);
+                o.color = go.color;
+                o.rec = go.rec;
+                o.prod = go.prod;
+                o.selbits = go.selbits;
+            }
+            if (inframe) st_stream_f4(a.out + pix, o.color);
+            if (DBG && inframe) {
+                if (a.dbg_pid) a.dbg_pid[pix] = o.prod;
+                if (a.dbg_sel) a.dbg_sel[pix] = o.selbits;
+            }
+            if (lane == 0) a.rec[wi] = o.rec;
+        }
+    }
+}
+#endif
 
 template <int FMT, int MODE, bool DBG>
 static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
@@ -1260,8 +1693,49 @@ static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, 
     return cudaGetLastError();
 }
 
+#if CTF_TU_FMT == 1
+#ifndef CTF_FAST
+#define CTF_FAST 1  // BC1 COLLAB List runs the lean kernel (0: the general kernel, for A/B timing)
+#endif
+// same work split as the general BC1 kernel
+template <bool DBG>
+static cudaError_t launch_fast(KArgs k, cudaStream_t stream) {
+    auto kern = ctf_collab_bc1_kernel<DBG>;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0);
+    if (e != cudaSuccess) return e;
+    const long long slots = (long long)sms * (per_sm > 0 ? per_sm : 1);
+    long long ipw = ((long long)k.nchunks + slots * kWarps * CTF_BC1_ROUNDS / 2) / (slots * kWarps * CTF_BC1_ROUNDS);
+    ipw = ipw < 1 ? 1 : ipw > CTF_BC1_MAX_IPW ? CTF_BC1_MAX_IPW : ipw;
+    k.ipc = (unsigned)(ipw * kWarps);
+    long long grid = ((long long)k.nchunks + k.ipc - 1) / k.ipc;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, kWarps * 32, 0, stream>>>(k);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // second pass over the marked waves: at most one resident wave of CTAs
+    auto rest = ctf_collab_bc1_rest_kernel<DBG>;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rest, kWarps * 32, 0);
+    if (e != cudaSuccess) return e;
+    const unsigned nrec = (unsigned)((long long)k.wpf * (k.nchunks / (unsigned)k.cpf));
+    const long long groups = ((long long)nrec + 31) / 32;
+    long long g2 = (long long)sms * (per_sm > 0 ? per_sm : 1);
+    if (g2 * kWarps > groups) g2 = (groups + kWarps - 1) / kWarps;
+    rest<<<(unsigned)(g2 < 1 ? 1 : g2), kWarps * 32, 0, stream>>>(k, nrec);
+    return cudaGetLastError();
+}
+#endif
+
 template <int FMT, int MODE>
 static cudaError_t launch_dbg(const KArgs &k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
+#if CTF_TU_FMT == 1
+    if (CTF_FAST && FMT == FMT_BC1 && MODE == MODE_COLLAB && k.variant == VAR_LIST)
+        return (k.flags & FLAG_DEBUG) ? launch_fast<true>(k, stream) : launch_fast<false>(k, stream);
+#endif
     return (k.flags & FLAG_DEBUG) ? launch_one<FMT, MODE, true>(k, mw, stream)
                                   : launch_one<FMT, MODE, false>(k, mw, stream);
 }
@@ -1280,6 +1754,10 @@ static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::typ
 #error "compile ctf_filter.cu with -DCTF_TU_FMT=1 (BC1) or =2 (latent MLP)"
 #endif
 #if CTF_TU_FMT == 1
+int launches_per_pass(int fmt, int mode, int filter) {
+    return (CTF_FAST && fmt == FMT_BC1 && mode == MODE_COLLAB && filter == 0) ? 2 : 1;
+}
+
 cudaError_t launch_filter_bc1(const LaunchArgs &a, cudaStream_t stream) {
 #else
 cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {

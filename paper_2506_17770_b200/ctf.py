@@ -86,7 +86,7 @@ def load_library(path: Path | str | None = None):
     lib.ctf_host_workspace_bytes.argtypes = [I32, I32, I32, ctypes.c_int]
     lib.ctf_host_workspace_bytes.restype = ctypes.c_size_t
     lib.ctf_filter_frames_host.argtypes = [PT, V, V, I32, I32, I32, I32, PP, V, V, V, ctypes.c_size_t, V]
-    lib.ctf_launches_per_call.argtypes = [I32, ctypes.c_int]
+    lib.ctf_launches_per_call.argtypes = [I32, I32, I32, I32, ctypes.c_int]
     for fn in ("ctf_filter_frame", "ctf_filter_batch", "ctf_stats", "ctf_filter_frames_host",
                "ctf_launches_per_call", "ctf_abi_version"):
         getattr(lib, fn).restype = ctypes.c_int
@@ -138,6 +138,14 @@ class Texture:
             raise ValueError("latent grid must be float16")
         w = torch.as_tensor(mlp).to(device=device, dtype=torch.float32).contiguous()
         return Texture(FMT_LATENT_MLP, width, height, lat, w)
+
+
+def launches_per_call(fmt: int, mode: int, filt: int = 0, frames: int = 1, batched: bool = True) -> int:
+    """Kernel launches one filter call issues (ctf_launches_per_call)."""
+    n = load_library().ctf_launches_per_call(fmt, mode, filt, frames, int(batched))
+    if n < 0:
+        raise CtfError("ctf_launches_per_call", CTF_EINVAL)
+    return n
 
 
 def num_waves(wf: int, hf: int) -> int:

@@ -8,5 +8,6 @@ python -c "from paper_2506_17770_b200 import build; build.build()"
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
   -I include -DCTF_TU_FMT=1 "$@" -c ${SRC:-$P/csrc/ctf_filter.cu} -o /tmp/variant_bc1_$$.o
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart=static -o "$out" \
-  $P/build/ctf_abi.o /tmp/variant_bc1_$$.o $P/build/ctf_filter_mlp.o $P/build/ctf_stats.o
+  $P/build/ctf_abi.o /tmp/variant_bc1_$$.o $P/build/ctf_filter_mlp.o $P/build/ctf_stats.o \
+  $P/build/ctf_bicubic_bc1.o $P/build/ctf_bicubic_mlp.o
 rm -f /tmp/variant_bc1_$$.o

@@ -10,7 +10,9 @@ from collections import defaultdict
 
 rep, waves = sys.argv[1], float(sys.argv[2])
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 60
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+import os
+kf = ["-k", os.environ["NCU_KERNEL"]] if os.environ.get("NCU_KERNEL") else []
+out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 cur_file = None

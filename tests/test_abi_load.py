@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     lib.ctf_abi_version.restype = ctypes.c_int
-    assert lib.ctf_abi_version() == 2
+    assert lib.ctf_abi_version() == 3
 
 
 def test_binding_declares_all_exports():
@@ -73,4 +73,8 @@ def test_validation_errors_without_gpu():
     assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EINVAL
     tex.width, tex.height = 8192, 8192
     assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EUNSUPPORTED
-    assert lib.ctf_launches_per_call(64, 1) == 1 and lib.ctf_launches_per_call(64, 0) == 64
+    lib.ctf_launches_per_call.argtypes = [ctypes.c_int32] * 4 + [ctypes.c_int]
+    # BC1 COLLAB bilinear: lean kernel + rest kernel per pass; everything else one kernel
+    assert lib.ctf_launches_per_call(1, 3, 0, 64, 1) == 2 and lib.ctf_launches_per_call(1, 3, 0, 64, 0) == 128
+    assert lib.ctf_launches_per_call(1, 0, 0, 64, 1) == 1 and lib.ctf_launches_per_call(2, 3, 0, 8, 0) == 8
+    assert lib.ctf_launches_per_call(3, 3, 0, 1, 1) == -1
