@@ -132,11 +132,14 @@ template <int FMT>
 __device__ __forceinline__ float4 scaled(const Texel<FMT> &p) { return p.to_f4(); }
 
 // Eq. 2 generalised to a active lanes (R-18 iv), round half up.
+// floor(num / den) for 0 <= num < 2^11, 0 < den <= 62 as floor((num + 1/2) * rcp(den)):
+// the fractional part of (num + 1/2) / den lies in [1/(2 den), 1 - 1/(2 den)], a margin
+// of >= 1/124 against an fp32 error < 2^-12, so the result is the exact integer quotient.
 __device__ __forceinline__ int eq2_lane_rank(int j, int np, int na) {
     if (np >= na - 1) return 0;
     const int num = 2 * (na - 1) * (j - np) + (na - 1 - np);
     const int den = 2 * (na - 1 - np);
-    return num / den;
+    return __float2int_rz(((float)num + 0.5f) * __frcp_rn((float)den));
 }
 
 // STF corner (R-12): dx = (u0 < s), dy = (u1 < t).
@@ -1308,7 +1311,8 @@ __device__ __forceinline__ int cplus_pick_lean(const Foot &g, float u2, Planned 
 // produced; in[k] = produced), straight-line.  Same operations in the same order as
 // combine_eq1f over distinct_corners (adding / fma-ing exact zeros changes nothing), so
 // the special cases hold bit for bit and the rest matches it exactly.
-__device__ __forceinline__ float4 combine_eq1_lean(const Foot &f, const bool (&in)[4], const float4 (&pv)[4], bool wc) {
+template <bool WC>
+__device__ __forceinline__ float4 combine_eq1_lean(const Foot &f, const bool (&in)[4], const float4 (&pv)[4]) {
     const Merged m = merge_corners(f);
     bool all_known = true;
     int N = 0;
@@ -1322,15 +1326,18 @@ __device__ __forceinline__ float4 combine_eq1_lean(const Foot &f, const bool (&i
         N += kn ? 1 : 0;
         Sw = __fadd_rn(Sw, kn ? m.dw[k] : 0.0f);
         const float one = kn ? 1.0f : 0.0f, wk = kn ? m.dw[k] : 0.0f;
-        sp01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(one, one), sp01);   // Sp += p (exact product)
-        sp23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(one, one), sp23);
-        sq01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(wk, wk), sq01);     // WC: sum dw * p
-        sq23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(wk, wk), sq23);
+        if (WC) {
+            sq01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(wk, wk), sq01);   // sum dw * p
+            sq23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(wk, wk), sq23);
+        } else {
+            sp01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(one, one), sp01);   // Sp += p (exact product)
+            sp23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(one, one), sp23);
+        }
     }
     const float4 bl = blend4f(pv, f.w);   // sum over the known corners of w_k p_k
     const float2 a01 = f2unpack(sp01), a23 = f2unpack(sp23);
     float4 c;
-    if (wc) {
+    if (WC) {
         const float2 q01 = f2unpack(sq01), q23 = f2unpack(sq23);
         const float r = 1.0f / Sw;
         c = all_known ? bl : make_float4(q01.x * r, q01.y * r, q23.x * r, q23.y * r);
@@ -1339,7 +1346,12 @@ __device__ __forceinline__ float4 combine_eq1_lean(const Foot &f, const bool (&i
         c = make_float4(fmaf(rest, a01.x, bl.x), fmaf(rest, a01.y, bl.y), fmaf(rest, a23.x, bl.z),
                         fmaf(rest, a23.y, bl.w));
     }
-    if (N == 1 && !all_known) c = make_float4(a01.x, a01.y, a23.x, a23.y);
+    if (!WC && N == 1 && !all_known) c = make_float4(a01.x, a01.y, a23.x, a23.y);
+    if (WC && N == 1 && !all_known) {   // N = 1: the known texel itself (Sp of the general path)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (m.first[k] && m.dw[k] != 0.0f && in[k]) c = pv[k];
+    }
     return c;
 }
 
@@ -1511,7 +1523,7 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
                     in[k] = test64(dl, dh, t);
                     pv[k] = in[k] ? fs.xch[t] : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
-                o.color = combine_eq1_lean(f, in, pv, fb == FB_WC);
+                o.color = fb == FB_WC ? combine_eq1_lean<true>(f, in, pv) : combine_eq1_lean<false>(f, in, pv);
             }
             o.rec = (uint32_t)evals | ((uint32_t)n << 8) | (32u << 16) |
                   ((uint32_t)(PATH_FB_STF + fb) << 22) | ((uint32_t)wave_mag << 25);
@@ -1589,8 +1601,11 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
 // window fits 8x8 (they need a fallback) take the lean fallback; partial waves and wider
 // windows take the general path.  Warps stride over groups of 32 records (one
 // coalesced 128-B load + ballot each).
+#ifndef CTF_REST_MINB
+#define CTF_REST_MINB 3  // rest kernel: resident CTAs per SM (85 registers: the general path fits)
+#endif
 template <bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, CTF_BC1_MINB) ctf_collab_bc1_rest_kernel(const KArgs a, unsigned nrec) {
+__global__ void __launch_bounds__(kWarps * 32, CTF_REST_MINB) ctf_collab_bc1_rest_kernel(const KArgs a, unsigned nrec) {
     __shared__ WarpSmem smem[kWarps];
     __shared__ FastSmem fsm[kWarps];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -1603,18 +1618,53 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_BC1_MINB) ctf_collab_bc1_rest
         const unsigned wi0 = g * 32u;
         const uint32_t r = (wi0 + lane < nrec) ? a.rec[wi0 + lane] : 0u;
         unsigned todo = __ballot_sync(FULL, r == kSlowMark);
-        while (todo) {
-            const unsigned wi = wi0 + (unsigned)(__ffs(todo) - 1);
-            todo &= todo - 1u;
-            const unsigned fr = wi / (unsigned)a.wpf, rem = wi - fr * (unsigned)a.wpf;
-            const int wy = (int)(rem / (unsigned)a.nwx), wx = (int)rem - wy * a.nwx;
-            const int px = wx * 8 + lx, py = wy * 4 + ly;
-            const bool inframe = px < a.Wf && py < a.Hf;
-            const unsigned pix = fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)px;
-            float2 uv = make_float2(__int_as_float(0x7fc00000), 0.f);
-            uint2 gr = make_uint2(0u, 0u);
+        if (!todo) continue;
+        // wave coordinates of the group's first record (one division per group), then
+        // of record wi0 + b by carrying b across wave-rows and frames
+        const unsigned fr0 = wi0 / (unsigned)a.wpf, rem0 = wi0 - fr0 * (unsigned)a.wpf;
+        const int wy0 = (int)(rem0 / (unsigned)a.nwx), wx00 = (int)rem0 - wy0 * a.nwx;
+        auto locate = [&](unsigned b, unsigned &fr, int &wy, int &wx) {
+            fr = fr0;
+            wy = wy0;
+            wx = wx00 + (int)b;
+            while (wx >= a.nwx) {
+                wx -= a.nwx;
+                if (++wy == a.nwy) { wy = 0; ++fr; }
+            }
+        };
+        // the next marked wave's inputs are loaded before the current one is processed
+        auto fetch = [&](unsigned b, float2 &uv, uint2 &gr, unsigned &fr, int &px, int &py, bool &inframe,
+                         unsigned &pix) {
+            int wy, wx;
+            locate(b, fr, wy, wx);
+            px = wx * 8 + lx;
+            py = wy * 4 + ly;
+            inframe = px < a.Wf && py < a.Hf;
+            pix = fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)px;
+            uv = make_float2(__int_as_float(0x7fc00000), 0.f);
+            gr = make_uint2(0u, 0u);
             ld_stream_f2_if(uv, a.uv + pix, inframe);
             ld_stream_u2_if(gr, a.grad + pix, inframe & (a.grad != nullptr));
+        };
+        float2 uv_n;
+        uint2 gr_n;
+        unsigned fr_n, pix_n;
+        int px_n, py_n;
+        bool in_n;
+        unsigned b_n = (unsigned)(__ffs(todo) - 1);
+        fetch(b_n, uv_n, gr_n, fr_n, px_n, py_n, in_n, pix_n);
+        while (todo) {
+            const unsigned wi = wi0 + b_n;
+            const float2 uv = uv_n;
+            const uint2 gr = gr_n;
+            const unsigned fr = fr_n, pix = pix_n;
+            const int px = px_n, py = py_n;
+            const bool inframe = in_n;
+            todo &= todo - 1u;
+            if (todo) {
+                b_n = (unsigned)(__ffs(todo) - 1);
+                fetch(b_n, uv_n, gr_n, fr_n, px_n, py_n, in_n, pix_n);
+            }
             __syncwarp();
             const bool active = inframe && !isnan(uv.x);
             const unsigned A = __ballot_sync(FULL, active);
