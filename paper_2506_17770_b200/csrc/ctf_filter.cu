@@ -57,6 +57,7 @@ struct KArgs {
     unsigned nchunks;
     unsigned ipc;                   // work items per CTA (claimed dynamically by its warps)
     float Wflt, Hflt;
+    int Wm1, Hm1;                   // texture W - 1, H - 1 (clamp-to-edge bounds)
     int fallback;
     int variant;                    // COLLAB kernel: VAR_LIST / VAR_BOX / VAR_MASK16 / VAR_MASK11
     uint32_t flags, frame_index, seed_lo, seed_hi;
@@ -105,10 +106,43 @@ __device__ __forceinline__ Foot footprint(float2 uv, const KArgs &a) {
     f.s = __fsub_rn(fx, flx);
     f.t = __fsub_rn(fy, fly);
     f.xa = max(x0, 0);
-    f.xb = min(x0 + 1, a.tex.W - 1);
+    f.xb = min(x0 + 1, a.Wm1);
     f.ya = max(y0, 0);
-    f.yb = min(y0 + 1, a.tex.H - 1);
+    f.yb = min(y0 + 1, a.Hm1);
     make_weights(f);
+    return f;
+}
+
+// The same footprint with the x / y pairs in packed fp32 (FFMA2 / FADD2): every lane of a
+// packed op is the scalar IEEE op, so the result equals footprint() bit for bit.
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ Foot footprint2(float2 uv, const KArgs &a) {
+    Foot f;
+    const uint64_t fxy = ffma2(f2pack(__saturatef(uv.x), __saturatef(uv.y)), f2pack(a.Wflt, a.Hflt),
+                               f2pack(-0.5f, -0.5f));
+    const uint64_t r = fadd2_rm(fxy, f2pack(12582912.0f, 12582912.0f));        // floor on the 2^23 grid
+    const uint64_t st = ffma2(fadd2(r, f2pack(-12582912.0f, -12582912.0f)), f2pack(-1.0f, -1.0f), fxy);
+    const float2 rr = f2unpack(r), stf = f2unpack(st);
+    const int x0 = __float_as_int(rr.x) - 0x4B400000, y0 = __float_as_int(rr.y) - 0x4B400000;
+    f.s = stf.x;
+    f.t = stf.y;
+    f.xa = max(x0, 0);
+    f.xb = min(x0 + 1, a.Wm1);
+    f.ya = max(y0, 0);
+    f.yb = min(y0 + 1, a.Hm1);
+    // {1 - s, s} and {1 - t, t} (one rounding each, as R-3), then the four products
+    const uint64_t S = ffma2(f2pack(f.s, f.s), f2pack(-1.0f, 1.0f), f2pack(1.0f, 0.0f));
+    const uint64_t T = ffma2(f2pack(f.t, f.t), f2pack(-1.0f, 1.0f), f2pack(1.0f, 0.0f));
+    const float2 tt = f2unpack(T);
+    const float2 w01 = f2unpack(fmul2(S, f2pack(tt.x, tt.x))), w23 = f2unpack(fmul2(S, f2pack(tt.y, tt.y)));
+    f.w[0] = w01.x;
+    f.w[1] = w01.y;
+    f.w[2] = w23.x;
+    f.w[3] = w23.y;
     return f;
 }
 
@@ -1365,9 +1399,8 @@ struct LeanOut {
 
 template <bool DBG, bool FALLBACK>
 __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float2 uv, uint2 gr, int px, int py,
-                                             uint32_t frame) {
+                                             uint32_t frame, bool has_grad, bool force) {
     const unsigned lane = lane_id(), lt = lanemask_lt(), lanebit = 1u << lane;
-    const bool has_grad = a.grad != nullptr;
     LeanOut o;
     o.color = make_float4(0.f, 0.f, 0.f, 0.f);
     o.rec = 0u;
@@ -1384,8 +1417,8 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
         mag_lane = rx <= 1.0f && ry <= 1.0f;
     }
     const bool wave_mag = has_grad && __all_sync(FULL, mag_lane);
-    // ---- a2: footprint
-    const Foot f = footprint(uv, a);
+    // ---- a2: footprint (packed fp32; = footprint())
+    const Foot f = footprint2(uv, a);
     // ---- a3: AABB origin and window
     const int minx = __reduce_min_sync(FULL, f.xa), miny = __reduce_min_sync(FULL, f.ya);
     const unsigned dx = (unsigned)(f.xb - minx), dy = (unsigned)(f.yb - miny);
@@ -1421,7 +1454,7 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
             if ((wh & lanebit) && rh < 32) fs.bit_of_rank[rh] = (uint8_t)(32u + lane);
         }
         // ---- a4: exact iff n <= a = 32 (always for a 32-bit window)
-        const bool exact = n <= 32 && !(a.flags & FLAG_FORCE_FALLBACK);
+        const bool exact = n <= 32 && !force;
         if (!FALLBACK && !exact) {
             o.done = false;   // left to the second kernel
             return o;
@@ -1532,7 +1565,9 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
     return o;
 }
 
-template <bool DBG>
+// GRAD: grad != NULL (magnified class); FORCE: CTF_FLAG_FORCE_FALLBACK (every live wave
+// goes to the rest kernel) — compile-time, so the hot loop tests neither.
+template <bool DBG, bool GRAD, bool FORCE>
 __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_kernel(const KArgs a) {
     __shared__ FastSmem fsm[kWarps];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -1553,7 +1588,7 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
         const unsigned w0 = (unsigned)fr * (unsigned)a.wpf + (unsigned)(wy * a.nwx + wx0);
         unsigned pix = (unsigned)fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)(wx0 * 8 + lx);
         int px = wx0 * 8 + lx;
-        const bool has_grad = a.grad != nullptr;
+        constexpr bool has_grad = GRAD;
         float2 uv_n = make_float2(__int_as_float(0x7fc00000), 0.f);
         uint2 gr_n = make_uint2(0u, 0u);
         ld_stream_f2_if(uv_n, a.uv + pix, rowok & (px < a.Wf));
@@ -1571,8 +1606,8 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
             const bool active = inframe && !isnan(uv.x);
             const unsigned A = __ballot_sync(FULL, active);
             uint32_t rec;
-            if (A == FULL) {
-                const LeanOut o = lean_wave<DBG, false>(a, fs, uv, gr, px, py, frame);
+            if (!FORCE && A == FULL) {
+                const LeanOut o = lean_wave<DBG, false>(a, fs, uv, gr, px, py, frame, GRAD, false);
                 rec = o.done ? o.rec : kSlowMark;
                 if (o.done) {
                     st_stream_f4(a.out + pix, o.color);
@@ -1671,7 +1706,7 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_REST_MINB) ctf_collab_bc1_res
             const uint32_t frame = a.frame_index + fr;
             LeanOut o;
             o.done = false;
-            if (A == FULL) o = lean_wave<DBG, true>(a, fs, uv, gr, px, py, frame);
+            if (A == FULL) o = lean_wave<DBG, true>(a, fs, uv, gr, px, py, frame, a.grad != nullptr, a.flags & FLAG_FORCE_FALLBACK);
             if (!o.done) {
                 const WaveOut go = wave_general<FMT_BC1, MODE_COLLAB, DBG>(a, NoWeights{}, s, mc, uv, gr, active, A,
                                                                            __popc(A), px, py, frame);
@@ -1750,7 +1785,9 @@ static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, 
 // same work split as the general BC1 kernel
 template <bool DBG>
 static cudaError_t launch_fast(KArgs k, cudaStream_t stream) {
-    auto kern = ctf_collab_bc1_kernel<DBG>;
+    const bool grad = k.grad != nullptr, force = (k.flags & FLAG_FORCE_FALLBACK) != 0;
+    auto kern = grad ? (force ? ctf_collab_bc1_kernel<DBG, true, true> : ctf_collab_bc1_kernel<DBG, true, false>)
+                     : (force ? ctf_collab_bc1_kernel<DBG, false, true> : ctf_collab_bc1_kernel<DBG, false, false>);
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -1836,6 +1873,8 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.nchunks = (unsigned)((long long)k.cpf * a.frames);
     k.Wflt = (float)a.W;
     k.Hflt = (float)a.H;
+    k.Wm1 = a.W - 1;
+    k.Hm1 = a.H - 1;
     k.fallback = a.fallback;
     k.variant = a.mode >= 4 ? a.mode - 3 : VAR_LIST;   // BOX / MASK16 / MASK11 run in the COLLAB kernel
     k.flags = a.flags;
