@@ -222,9 +222,10 @@ int ctf_filter_frames_host(const ctf_texture *tex, const float *uv_host, const u
  * Kernel launches one call above issues (for launch accounting): format / mode / filter
  * as in ctf_texture / ctf_params, `frames` frames, `batched` != 0 for ctf_filter_batch
  * (one pass over all frames) else ctf_filter_frame once per frame.  The BC1 COLLAB
- * bilinear path is two kernels per pass (the lean kernel, then the general path over
- * the waves it left: partial coverage, windows wider than 8x8); every other path is
- * one.  Returns -1 for an invalid format / mode / filter.
+ * bilinear path is three kernels per pass (the lean exact kernel; the lean fallback
+ * kernel over the full waves it left; the general path over partial waves and windows
+ * wider than 8x8); every other path is one.  Returns -1 for an invalid format / mode /
+ * filter.
  */
 int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int batched);
 int ctf_abi_version(void);

@@ -50,6 +50,10 @@ __device__ __forceinline__ void ld_stream_u2_if(uint2 &r, const uint2 *p, bool p
                  "@q ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];\n\t}"
                  : "+r"(r.x), "+r"(r.y) : "l"(p), "r"((unsigned)pred));
 }
+__device__ __forceinline__ void ld_u32_if(uint32_t &r, const uint32_t *p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cg.u32 %0, [%1];\n\t}"
+                 : "+r"(r) : "l"(p), "r"((unsigned)pred));
+}
 __device__ __forceinline__ void st_stream_f4(float4 *p, float4 v) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");

@@ -1267,12 +1267,17 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : 
 //              done once per texel instead of once per read;
 //   filter   : exact: blend4f (FFMA2), bit-identical to every other exact path;
 //              fallback: one-tap / WC / Eq. 1 (combine_eq1f, as the general path).
-// The remaining waves (partial coverage; windows wider than 8x8, e.g. minified waves)
-// are marked in their record with kSlowMark and finished by ctf_collab_bc1_rest_kernel
-// through the general path (wave_general): the record buffer is the work list, so no
-// workspace is needed, and the lean kernel contains no call (a call makes ptxas guard
-// every warp collective with a divergence check).
-constexpr uint32_t kSlowMark = 0xFFFFFFFFu;   // never a COLLAB record (path <= 4, n <= 128)
+// The waves the lean kernel does not finish are marked in their record and finished by
+// two more kernels that use the record buffer as their work list (no workspace):
+//   kFbMark   full waves whose window fits 8x8 but need a fallback (n > 32) ->
+//             the same lean code with the fallback enabled (64 registers, no spills);
+//   kSlowMark partial waves and wider windows (minified waves) -> the general path
+//             (wave_general, 80 registers).
+// The lean kernel itself contains no call and no fallback code (a call or a divergent
+// region before a warp collective makes ptxas guard every collective of the loop with a
+// divergence check).
+constexpr uint32_t kSlowMark = 0xFFFFFFFFu;   // neither is a COLLAB record (path <= 4, n <= 128)
+constexpr uint32_t kFbMark = 0xFFFFFFFEu;
 
 struct FastSmem {
     float4 xch[64];           // exact: rank -> produced value; fallback: window position -> produced value
@@ -1286,9 +1291,6 @@ struct FastSmem {
 // 64-bit window masks held as two words (hi = 0 for a 32-bit window)
 __device__ __forceinline__ uint32_t bit_lo(uint32_t t) { return t < 32u ? 1u << t : 0u; }
 __device__ __forceinline__ uint32_t bit_hi(uint32_t t) { return t >= 32u ? 1u << (t - 32u) : 0u; }
-__device__ __forceinline__ bool test64(uint32_t lo, uint32_t hi, uint32_t t) {
-    return ((t < 32u ? lo : hi) >> (t & 31u)) & 1u;
-}
 __device__ __forceinline__ int rank64(uint32_t lo, uint32_t hi, uint32_t t) {   // set bits below t
     return t < 32u ? __popc(lo & ((1u << t) - 1u)) : __popc(lo) + __popc(hi & ((1u << (t - 32u)) - 1u));
 }
@@ -1316,56 +1318,65 @@ __device__ __forceinline__ Merged merge_corners(const Foot &f) {
     return m;
 }
 
-// C+ spare-lane pick (R-18 v) over served lane g's footprint, straight-line: the distinct
-// nonzero-weight texels not planned, chosen ~ merged weight with u2 (first cumulative
-// sum > u2 * sum, else the last candidate); -1 when there is none.  = cplus_pick().
-template <typename Planned>
-__device__ __forceinline__ int cplus_pick_lean(const Foot &g, float u2, Planned planned) {
-    const Merged m = merge_corners(g);
-    bool cand[4];
-    float wsum = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        cand[k] = m.first[k] && m.dw[k] != 0.0f && !planned(corner_x(g, k), corner_y(g, k));
-        wsum = __fadd_rn(wsum, cand[k] ? m.dw[k] : 0.0f);
-    }
-    const float target = __fmul_rn(u2, wsum);
-    float cum = 0.0f;
-    int pick = -1, lastc = -1;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        cum = __fadd_rn(cum, cand[k] ? m.dw[k] : 0.0f);
-        pick = (pick < 0 && cand[k] && cum > target) ? k : pick;
-        lastc = cand[k] ? k : lastc;
-    }
-    return pick < 0 ? lastc : pick;
+// Corner masks (bit k = corner k of a footprint) read from a window bitmask (lo, hi):
+// corners 0 / 1 sit at t0 and t0 + dxs, corners 2 / 3 at t2 and t2 + dxs (one 64-bit
+// shift per footprint row).
+__device__ __forceinline__ unsigned corner_bits(uint32_t lo, uint32_t hi, uint32_t t0, uint32_t t2, uint32_t dxs) {
+    const uint64_t D = ((uint64_t)hi << 32) | lo;
+    const uint32_t r0 = (uint32_t)(D >> t0), r2 = (uint32_t)(D >> t2);
+    return (r0 & 1u) | (((r0 >> dxs) & 1u) << 1) | ((r2 & 1u) << 2) | (((r2 >> dxs) & 1u) << 3);
+}
+// bit k = corner k is the first occurrence of its texel and its merged weight is nonzero
+__device__ __forceinline__ unsigned contrib_bits(const Foot &f, const Merged &m) {
+    const unsigned ddx = f.xb != f.xa, ddy = f.yb != f.ya;
+    const unsigned first = 1u | (ddx << 1) | (ddy << 2) | ((ddx & ddy) << 3);
+    const unsigned nz = (m.dw[0] != 0.0f ? 1u : 0u) | (m.dw[1] != 0.0f ? 2u : 0u) | (m.dw[2] != 0.0f ? 4u : 0u) |
+                        (m.dw[3] != 0.0f ? 8u : 0u);
+    return first & nz;
 }
 
-// One-tap / WC stand-in / Eq. 1 from per-corner values pv[k] (0 where the texel was not
-// produced; in[k] = produced), straight-line.  Same operations in the same order as
-// combine_eq1f over distinct_corners (adding / fma-ing exact zeros changes nothing), so
-// the special cases hold bit for bit and the rest matches it exactly.
+// C+ spare-lane pick (R-18 v) over served lane g's footprint: the distinct nonzero-weight
+// texels not planned (PL = planned corner mask), chosen ~ merged weight with u2 (first
+// cumulative sum > u2 * sum, else the last candidate); -1 when there is none.  The sums
+// run in corner order from 0 with one rounding per candidate, exactly as cplus_pick().
+__device__ __forceinline__ int cplus_pick_bits(const Foot &g, float u2, unsigned PL) {
+    const Merged m = merge_corners(g);
+    const unsigned cand = contrib_bits(g, m) & ~PL;
+    float ps[4], wsum = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        wsum = __fadd_rn(wsum, ((cand >> k) & 1u) ? m.dw[k] : 0.0f);
+        ps[k] = wsum;
+    }
+    const float target = __fmul_rn(u2, wsum);
+    const unsigned gt = cand & ((ps[0] > target ? 1u : 0u) | (ps[1] > target ? 2u : 0u) |
+                                (ps[2] > target ? 4u : 0u) | (ps[3] > target ? 8u : 0u));
+    return cand == 0u ? -1 : gt != 0u ? __ffs(gt) - 1 : 31 - __clz(cand);
+}
+
+// One-tap-free Eq. 1 / WC stand-in from the four corner values pv[k] (0 where the texel
+// was not produced; IN = produced corner mask).  Same operations in the same order as
+// combine_eq1f over distinct_corners — fma by an exact 0 / 1 adds nothing / exactly p —
+// so the special cases (all known -> exact bilinear; N = 1 -> that texel) hold bit for
+// bit and the rest equals it.
 template <bool WC>
-__device__ __forceinline__ float4 combine_eq1_lean(const Foot &f, const bool (&in)[4], const float4 (&pv)[4]) {
+__device__ __forceinline__ float4 combine_eq1_bits(const Foot &f, unsigned IN, const float4 (&pv)[4]) {
     const Merged m = merge_corners(f);
-    bool all_known = true;
-    int N = 0;
+    const unsigned C = contrib_bits(f, m), Kn = C & IN;
+    const bool all_known = (C & ~IN) == 0u;
+    const int N = __popc(Kn);
     float Sw = 0.0f;
     uint64_t sp01 = f2pack(0.f, 0.f), sp23 = f2pack(0.f, 0.f), sq01 = f2pack(0.f, 0.f), sq23 = f2pack(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const bool contrib = m.first[k] && m.dw[k] != 0.0f;
-        const bool kn = contrib && in[k];
-        all_known = all_known && (!contrib || in[k]);
-        N += kn ? 1 : 0;
-        Sw = __fadd_rn(Sw, kn ? m.dw[k] : 0.0f);
+        const bool kn = (Kn >> k) & 1u;
         const float one = kn ? 1.0f : 0.0f, wk = kn ? m.dw[k] : 0.0f;
+        Sw = __fadd_rn(Sw, wk);
+        sp01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(one, one), sp01);   // Sp += p (exact product)
+        sp23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(one, one), sp23);
         if (WC) {
             sq01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(wk, wk), sq01);   // sum dw * p
             sq23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(wk, wk), sq23);
-        } else {
-            sp01 = ffma2(f2pack(pv[k].x, pv[k].y), f2pack(one, one), sp01);   // Sp += p (exact product)
-            sp23 = ffma2(f2pack(pv[k].z, pv[k].w), f2pack(one, one), sp23);
         }
     }
     const float4 bl = blend4f(pv, f.w);   // sum over the known corners of w_k p_k
@@ -1380,34 +1391,21 @@ __device__ __forceinline__ float4 combine_eq1_lean(const Foot &f, const bool (&i
         c = make_float4(fmaf(rest, a01.x, bl.x), fmaf(rest, a01.y, bl.y), fmaf(rest, a23.x, bl.z),
                         fmaf(rest, a23.y, bl.w));
     }
-    if (!WC && N == 1 && !all_known) c = make_float4(a01.x, a01.y, a23.x, a23.y);
-    if (WC && N == 1 && !all_known) {   // N = 1: the known texel itself (Sp of the general path)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (m.first[k] && m.dw[k] != 0.0f && in[k]) c = pv[k];
-    }
+    if (N == 1 && !all_known) c = make_float4(a01.x, a01.y, a23.x, a23.y);
     return c;
 }
 
-// One FULL wave (32 active lanes) through the lean path.  Returns done = false when the
-// window does not fit 8x8, or (FALLBACK = false) when the wave needs a fallback.
+// One FULL wave (32 active lanes) through the lean exact path.  Returns done = false with
+// rec = kFbMark when the wave needs a fallback or its window only fits a 128-bit shape
+// (16x8, 8x16, 32x4), or kSlowMark when no window fits (general path).
 struct LeanOut {
     float4 color;
     uint32_t rec, prod, selbits;
-    bool done;
+    bool done;   // else rec = the mark for the kernel that finishes the wave
 };
 
-template <bool DBG, bool FALLBACK>
-__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float2 uv, uint2 gr, int px, int py,
-                                             uint32_t frame, bool has_grad, bool force) {
-    const unsigned lane = lane_id(), lt = lanemask_lt(), lanebit = 1u << lane;
-    LeanOut o;
-    o.color = make_float4(0.f, 0.f, 0.f, 0.f);
-    o.rec = 0u;
-    o.prod = INVALID_ID;
-    o.selbits = 0u;
-    o.done = false;
-    // ---- a1: magnified class (R-20), as in the general path
+// magnified class of a full wave (R-20), as in the general path
+__device__ __forceinline__ bool wave_magnified(uint2 gr, bool has_grad) {
     bool mag_lane = true;
     if (has_grad) {
         const float rx = fma_f32_f16((unsigned short)(gr.x & 0xffffu), (unsigned short)(gr.x & 0xffffu),
@@ -1416,7 +1414,20 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
                                      fma_f32_f16((unsigned short)(gr.y >> 16), (unsigned short)(gr.y >> 16), 0.0f));
         mag_lane = rx <= 1.0f && ry <= 1.0f;
     }
-    const bool wave_mag = has_grad && __all_sync(FULL, mag_lane);
+    return has_grad && __all_sync(FULL, mag_lane);
+}
+
+template <bool DBG>
+__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float2 uv, uint2 gr, bool has_grad) {
+    const unsigned lane = lane_id(), lt = lanemask_lt(), lanebit = 1u << lane;
+    LeanOut o;
+    o.color = make_float4(0.f, 0.f, 0.f, 0.f);
+    o.rec = kFbMark;
+    o.prod = INVALID_ID;
+    o.selbits = 0u;
+    o.done = false;
+    // ---- a1: magnified class
+    const bool wave_mag = wave_magnified(gr, has_grad);
     // ---- a2: footprint (packed fp32; = footprint())
     const Foot f = footprint2(uv, a);
     // ---- a3: AABB origin and window
@@ -1427,141 +1438,241 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
     if (__all_sync(FULL, (dx | (dy << 1)) < 8u)) K = 1;                      // 8x4
     else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; lgP = 2u; }   // 4x8
     else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                        // 8x8
-    if (K != 0) {
-        o.done = true;
-        const uint32_t pmask = (1u << lgP) - 1u;
-        const uint32_t t0 = ((uint32_t)(f.ya - miny) << lgP) + (uint32_t)(f.xa - minx);
-        const uint32_t t2 = t0 + ((uint32_t)(f.yb - f.ya) << lgP);
-        const uint32_t dxs = (uint32_t)(f.xb - f.xa);
-        const uint32_t pat = 1u + dxs + dxs;   // bits t and t + dxs (same window row)
-        int n, r0, r2;
-        if (K == 1) {
-            const uint32_t wm = __reduce_or_sync(FULL, (pat << t0) | (pat << t2));
-            n = __popc(wm);
-            r0 = __popc(wm & ((1u << t0) - 1u));
-            r2 = __popc(wm & ((1u << t2) - 1u));
-            if (wm & lanebit) fs.bit_of_rank[__popc(wm & lt)] = (uint8_t)lane;
-        } else {
-            const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
-            const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
-            const uint32_t wh = __reduce_or_sync(FULL, (uint32_t)(m >> 32));
-            const int nl = __popc(wl);
-            n = nl + __popc(wh);
-            r0 = rank64(wl, wh, t0);
-            r2 = rank64(wl, wh, t2);
-            if (wl & lanebit) fs.bit_of_rank[__popc(wl & lt)] = (uint8_t)lane;
-            const int rh = nl + __popc(wh & lt);
-            if ((wh & lanebit) && rh < 32) fs.bit_of_rank[rh] = (uint8_t)(32u + lane);
-        }
-        // ---- a4: exact iff n <= a = 32 (always for a 32-bit window)
-        const bool exact = n <= 32 && !force;
-        if (!FALLBACK && !exact) {
-            o.done = false;   // left to the second kernel
-            return o;
-        }
-        __syncwarp();
-        bool produced;
-        int qx = 0, qy = 0;
-        const int fb = a.fallback;
-        if (exact) {
-            // ---- a5: lane r < n produces U[r]
-            produced = (int)lane < n;
-            const uint32_t e = fs.bit_of_rank[lane];
-            qx = minx + (int)(e & pmask);
-            qy = miny + (int)(e >> lgP);
-        } else {
-            // ---- a7 plan: every lane's STF texel; C+ dedupes it
-            // and spreads the spare lanes over the wave with Eq. 2
-            const uint4 rn = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo,
-                                           a.seed_hi);
-            const int ksel = stf_corner(f, rn);
-            qx = corner_x(f, ksel);
-            qy = corner_y(f, ksel);
-            o.selbits = (uint32_t)ksel;
-            produced = true;
-            if (fb == FB_CPLUS) {
-                const uint32_t tp = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
-                const uint32_t pl = __reduce_or_sync(FULL, bit_lo(tp));   // planned set P
-                const uint32_t ph = __reduce_or_sync(FULL, bit_hi(tp));
-                const int npl = __popc(pl), np = npl + __popc(ph);
-                if (pl & lanebit) fs.bit_of_rank[__popc(pl & lt)] = (uint8_t)lane;
-                if (ph & lanebit) fs.bit_of_rank[npl + __popc(ph & lt)] = (uint8_t)(32u + lane);
-                __syncwarp();
-                const bool spare = (int)lane >= np;
-                const int l = spare ? eq2_lane_rank((int)lane, np, 32) : (int)lane;   // h(., A) = id
-                Foot g;
-                g.xa = __shfl_sync(FULL, f.xa, l);
-                g.xb = __shfl_sync(FULL, f.xb, l);
-                g.ya = __shfl_sync(FULL, f.ya, l);
-                g.yb = __shfl_sync(FULL, f.yb, l);
-                g.s = __shfl_sync(FULL, f.s, l);
-                g.t = __shfl_sync(FULL, f.t, l);
-                make_weights(g);
-                const int pick = cplus_pick_lean(g, unit24(rn.z), [&](int x, int y) {
-                    return test64(pl, ph, ((uint32_t)(y - miny) << lgP) + (uint32_t)(x - minx));
-                });
-                const uint32_t e = fs.bit_of_rank[lane & 31u];
-                if (!spare) {   // planned rank `lane` < n_p
-                    qx = minx + (int)(e & pmask);
-                    qy = miny + (int)(e >> lgP);
-                } else {
-                    o.selbits |= (1u << 5) | ((uint32_t)l << 8);
-                    produced = pick >= 0;
-                    qx = produced ? corner_x(g, pick) : qx;
-                    qy = produced ? corner_y(g, pick) : qy;
-                    o.selbits |= produced ? (((uint32_t)pick << 2) | (1u << 4)) : 0u;
-                }
-            }
-        }
-        // ---- the single texel-production site (<= 1 evaluation per lane)
-        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (produced) {
-            val = rgba8_unorm(bc1_decode(a.tex, qx, qy));
-            if (DBG) o.prod = (uint32_t)(qy * a.tex.W + qx);
-        }
-        if (exact) {
-            if (produced) fs.xch[lane] = val;
-            __syncwarp();
-            // ---- a6: gather (ranks rho_k; the wave is full so h(r, A) = r) + blend
-            const float4 p[4] = {fs.xch[r0], fs.xch[r0 + (int)dxs], fs.xch[r2], fs.xch[r2 + (int)dxs]};
-            o.color = blend4f(p, f.w);
-            o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
-            if (DBG && a.dbg_unread) {
-                const unsigned bad = __reduce_add_sync(
-                    FULL, (unsigned)(r0 >= n) + (unsigned)(r0 + (int)dxs >= n) + (unsigned)(r2 >= n) +
-                              (unsigned)(r2 + (int)dxs >= n));
-                if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
-            }
-        } else {
-            // ---- a7 finish: one-tap (STF), WC stand-in or Eq. 1 (C, C+) over the
-            // produced set D of the wave
-            const int evals = fb == FB_CPLUS ? __popc(__ballot_sync(FULL, produced)) : 32;
-            if (fb == FB_STF) {
-                o.color = val;
-            } else {
-                const uint32_t tq = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
-                const uint32_t dl = __reduce_or_sync(FULL, produced ? bit_lo(tq) : 0u);
-                const uint32_t dh = __reduce_or_sync(FULL, produced ? bit_hi(tq) : 0u);
-                // one publisher per produced texel (the decode is deterministic); the
-                // values are indexed by window position
-                const unsigned peers = __match_any_sync(FULL, produced ? tq : 0xFFFFFFFFu);
-                if (produced && (unsigned)(__ffs(peers) - 1) == lane) fs.xch[tq] = val;
-                __syncwarp();
-                bool in[4];
-                float4 pv[4];
+    if (K == 0) {   // a 128-bit window (fallback kernel) or none (general kernel)
+        const bool w128 = __all_sync(FULL, dx < 16u && dy < 8u) || __all_sync(FULL, dx < 8u && dy < 16u) ||
+                          __all_sync(FULL, dx < 32u && dy < 4u);
+        o.rec = w128 ? kFbMark : kSlowMark;
+        return o;
+    }
+    const uint32_t pmask = (1u << lgP) - 1u;
+    const uint32_t t0 = ((uint32_t)(f.ya - miny) << lgP) + (uint32_t)(f.xa - minx);
+    const uint32_t t2 = t0 + ((uint32_t)(f.yb - f.ya) << lgP);
+    const uint32_t dxs = (uint32_t)(f.xb - f.xa);
+    const uint32_t pat = 1u + dxs + dxs;   // bits t and t + dxs (same window row)
+    int n, r0, r2;
+    if (K == 1) {
+        const uint32_t wm = __reduce_or_sync(FULL, (pat << t0) | (pat << t2));
+        n = __popc(wm);
+        r0 = __popc(wm & ((1u << t0) - 1u));
+        r2 = __popc(wm & ((1u << t2) - 1u));
+        if (wm & lanebit) fs.bit_of_rank[__popc(wm & lt)] = (uint8_t)lane;
+    } else {
+        const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
+        const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
+        const uint32_t wh = __reduce_or_sync(FULL, (uint32_t)(m >> 32));
+        const int nl = __popc(wl);
+        n = nl + __popc(wh);
+        r0 = rank64(wl, wh, t0);
+        r2 = rank64(wl, wh, t2);
+        if (wl & lanebit) fs.bit_of_rank[__popc(wl & lt)] = (uint8_t)lane;
+        const int rh = nl + __popc(wh & lt);
+        if ((wh & lanebit) && rh < 32) fs.bit_of_rank[rh] = (uint8_t)(32u + lane);
+    }
+    // ---- a4: exact iff n <= a = 32 (always for a 32-bit window)
+    if (n > 32) return o;   // fallback kernel
+    o.done = true;
+    __syncwarp();
+    // ---- a5: lane r < n produces U[r] (h(r, A) = r); one decode site, fp32 once
+    const bool produced = (int)lane < n;
+    const uint32_t e = fs.bit_of_rank[lane];
+    const int qx = minx + (int)(e & pmask), qy = miny + (int)(e >> lgP);
+    if (produced) {
+        fs.xch[lane] = rgba8_unorm(bc1_decode(a.tex, qx, qy));
+        if (DBG) o.prod = (uint32_t)(qy * a.tex.W + qx);
+    }
+    __syncwarp();
+    // ---- a6: gather (ranks rho_k) + blend
+    const float4 p[4] = {fs.xch[r0], fs.xch[r0 + (int)dxs], fs.xch[r2], fs.xch[r2 + (int)dxs]};
+    o.color = blend4f(p, f.w);
+    o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
+    if (DBG && a.dbg_unread) {
+        const unsigned bad = __reduce_add_sync(FULL, (unsigned)(r0 >= n) + (unsigned)(r0 + (int)dxs >= n) +
+                                                         (unsigned)(r2 >= n) + (unsigned)(r2 + (int)dxs >= n));
+        if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
+    }
+    return o;
+}
+
+// ---------------------------------------- lean fallback over windows up to 128 bits
+// Window masks as 4 words; the pitch 2^lgP <= 32 keeps every window row inside one word.
+struct W128 {
+    uint32_t w[4];
+    __device__ __forceinline__ uint32_t word(uint32_t k) const { return k == 0 ? w[0] : k == 1 ? w[1] : k == 2 ? w[2] : w[3]; }
+    __device__ __forceinline__ int count() const { return __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]); }
+    __device__ __forceinline__ int below(uint32_t k) const {   // set bits in words < k
+        return (k > 0 ? __popc(w[0]) : 0) + (k > 1 ? __popc(w[1]) : 0) + (k > 2 ? __popc(w[2]) : 0);
+    }
+    __device__ __forceinline__ int rank(uint32_t t) const {
+        return below(t >> 5) + __popc(word(t >> 5) & ((1u << (t & 31u)) - 1u));
+    }
+    // corners 0 / 1 at t0, t0 + dxs; 2 / 3 at t2, t2 + dxs
+    __device__ __forceinline__ unsigned corners(uint32_t t0, uint32_t t2, uint32_t dxs) const {
+        const uint32_t a = word(t0 >> 5) >> (t0 & 31u), b = word(t2 >> 5) >> (t2 & 31u);
+        return (a & 1u) | (((a >> dxs) & 1u) << 1) | ((b & 1u) << 2) | (((b >> dxs) & 1u) << 3);
+    }
+    // lane j holds bit j of every word: rank -> bit position for ranks < 32
+    __device__ __forceinline__ void push(uint8_t *tbl, unsigned lane, unsigned lt) const {
+        int pre = 0;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t t = ((uint32_t)(corner_y(f, k) - miny) << lgP) +
-                                       (uint32_t)(corner_x(f, k) - minx);
-                    in[k] = test64(dl, dh, t);
-                    pv[k] = in[k] ? fs.xch[t] : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-                o.color = fb == FB_WC ? combine_eq1_lean<true>(f, in, pv) : combine_eq1_lean<false>(f, in, pv);
-            }
-            o.rec = (uint32_t)evals | ((uint32_t)n << 8) | (32u << 16) |
-                  ((uint32_t)(PATH_FB_STF + fb) << 22) | ((uint32_t)wave_mag << 25);
+        for (int k = 0; k < 4; ++k) {
+            const int r = pre + __popc(w[k] & lt);
+            if (((w[k] >> lane) & 1u) && r < 32) tbl[r] = (uint8_t)(32u * k + lane);
+            pre += __popc(w[k]);
         }
     }
+};
+// OR-reduce of per-lane bits: `m` (pattern at bit t, t + 1, ...) placed at window position t
+__device__ __forceinline__ W128 reduce_w128(int K, uint32_t t, uint32_t pat, bool on, uint32_t t2 = 0xFFFFFFFFu) {
+    W128 r;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        uint32_t m = 0u;
+        if (k < K) {   // warp-uniform
+            if (on && (t >> 5) == (uint32_t)k) m |= pat << (t & 31u);
+            if (on && (t2 >> 5) == (uint32_t)k) m |= pat << (t2 & 31u);
+            m = __reduce_or_sync(FULL, m);
+        }
+        r.w[k] = m;
+    }
+    return r;
+}
+
+struct FbSmem {
+    float4 xch[128];          // exact: rank -> value; fallback: window position -> value
+    uint8_t bit_of_rank[32];  // rank -> window bit (0..127)
+};
+
+// One FULL wave whose window fits 128 bits, exact or fallback (STF / WC / C / C+), the
+// same results as the general path (records, producers, selections bit for bit).
+template <bool DBG>
+__device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const Foot &f, int minx, int miny, int K,
+                                             unsigned lgP, bool wave_mag, int px, int py, uint32_t frame, bool force) {
+    const unsigned lane = lane_id(), lt = lanemask_lt();
+    LeanOut o;
+    o.prod = INVALID_ID;
+    o.selbits = 0u;
+    o.done = true;
+    const uint32_t pmask = (1u << lgP) - 1u;
+    const uint32_t t0 = ((uint32_t)(f.ya - miny) << lgP) + (uint32_t)(f.xa - minx);
+    const uint32_t t2 = t0 + ((uint32_t)(f.yb - f.ya) << lgP);
+    const uint32_t dxs = (uint32_t)(f.xb - f.xa);
+    const W128 U = reduce_w128(K, t0, 1u + dxs + dxs, true, t2);   // the unique set (List)
+    const int n = U.count();
+    const bool exact = n <= 32 && !force;
+    const int fb = a.fallback;
+    bool produced;
+    int qx, qy;
+    if (exact) {
+        U.push(fs.bit_of_rank, lane, lt);
+        __syncwarp();
+        produced = (int)lane < n;
+        const uint32_t e = fs.bit_of_rank[lane];
+        qx = minx + (int)(e & pmask);
+        qy = miny + (int)(e >> lgP);
+    } else {
+        // ---- a7 plan: every lane's STF texel; C+ dedupes it and spreads the
+        // spare lanes over the wave with Eq. 2
+        const uint4 rn = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo, a.seed_hi);
+        const int ksel = stf_corner(f, rn);
+        qx = corner_x(f, ksel);
+        qy = corner_y(f, ksel);
+        o.selbits = (uint32_t)ksel;
+        produced = true;
+        if (fb == FB_CPLUS) {
+            const uint32_t tp = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
+            const W128 P = reduce_w128(K, tp, 1u, true);   // planned set
+            const int np = P.count();
+            P.push(fs.bit_of_rank, lane, lt);
+            __syncwarp();
+            const bool spare = (int)lane >= np;
+            const int l = spare ? eq2_lane_rank((int)lane, np, 32) : (int)lane;   // h(., A) = id
+            Foot g;
+            g.xa = __shfl_sync(FULL, f.xa, l);
+            g.xb = __shfl_sync(FULL, f.xb, l);
+            g.ya = __shfl_sync(FULL, f.ya, l);
+            g.yb = __shfl_sync(FULL, f.yb, l);
+            g.s = __shfl_sync(FULL, f.s, l);
+            g.t = __shfl_sync(FULL, f.t, l);
+            make_weights(g);
+            const uint32_t tg0 = ((uint32_t)(g.ya - miny) << lgP) + (uint32_t)(g.xa - minx);
+            const uint32_t tg2 = tg0 + ((uint32_t)(g.yb - g.ya) << lgP);
+            const int pick = cplus_pick_bits(g, unit24(rn.z), P.corners(tg0, tg2, (uint32_t)(g.xb - g.xa)));
+            const uint32_t e = fs.bit_of_rank[lane];
+            if (!spare) {   // planned rank `lane` < n_p
+                qx = minx + (int)(e & pmask);
+                qy = miny + (int)(e >> lgP);
+            } else {
+                o.selbits |= (1u << 5) | ((uint32_t)l << 8);
+                produced = pick >= 0;
+                qx = produced ? corner_x(g, pick) : qx;
+                qy = produced ? corner_y(g, pick) : qy;
+                o.selbits |= produced ? (((uint32_t)pick << 2) | (1u << 4)) : 0u;
+            }
+        }
+    }
+    // ---- the single texel-production site (<= 1 evaluation per lane)
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (produced) {
+        val = rgba8_unorm(bc1_decode(a.tex, qx, qy));
+        if (DBG) o.prod = (uint32_t)(qy * a.tex.W + qx);
+    }
+    if (exact) {
+        if (produced) fs.xch[lane] = val;
+        __syncwarp();
+        const int r0 = U.rank(t0), r2 = U.rank(t2);
+        const float4 p[4] = {fs.xch[r0], fs.xch[r0 + (int)dxs], fs.xch[r2], fs.xch[r2 + (int)dxs]};
+        o.color = blend4f(p, f.w);
+        o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
+        return o;
+    }
+    // ---- a7 finish: one-tap (STF), WC stand-in or Eq. 1 (C, C+) over the produced set D
+    const int evals = fb == FB_CPLUS ? __popc(__ballot_sync(FULL, produced)) : 32;
+    if (fb == FB_STF) {
+        o.color = val;
+    } else {
+        const uint32_t tq = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
+        const W128 D = reduce_w128(K, tq, 1u, produced);
+        // values indexed by window position, zero where nothing was produced; one
+        // publisher per produced texel (the decode is deterministic)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < K) fs.xch[32 * k + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const unsigned peers = __match_any_sync(FULL, produced ? tq : 0xFFFFFFFFu);
+        __syncwarp();
+        if (produced && (unsigned)(__ffs(peers) - 1) == lane) fs.xch[tq] = val;
+        __syncwarp();
+        const float4 pv[4] = {fs.xch[t0], fs.xch[t0 + dxs], fs.xch[t2], fs.xch[t2 + dxs]};
+        const unsigned IN = D.corners(t0, t2, dxs);
+        o.color = fb == FB_WC ? combine_eq1_bits<true>(f, IN, pv) : combine_eq1_bits<false>(f, IN, pv);
+    }
+    o.rec = (uint32_t)evals | ((uint32_t)(n & 0xFF) << 8) | (32u << 16) | ((uint32_t)(PATH_FB_STF + fb) << 22) |
+            ((uint32_t)wave_mag << 25);
+    return o;
+}
+
+template <bool DBG>
+__device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv, uint2 gr, int px, int py,
+                                           uint32_t frame, bool has_grad, bool force) {
+    const bool wave_mag = wave_magnified(gr, has_grad);
+    const Foot f = footprint2(uv, a);
+    const int minx = __reduce_min_sync(FULL, f.xa), miny = __reduce_min_sync(FULL, f.ya);
+    const unsigned dx = (unsigned)(f.xb - minx), dy = (unsigned)(f.yb - miny);
+    // the window shapes of wave_box(), in its order (one instantiation: small code)
+    int K = 0;
+    unsigned lgP = 3u;
+    if (__all_sync(FULL, dx < 8u && dy < 4u)) { K = 1; lgP = 3u; }
+    else if (__all_sync(FULL, dx < 4u && dy < 8u)) { K = 1; lgP = 2u; }
+    else if (__all_sync(FULL, dx < 8u && dy < 8u)) { K = 2; lgP = 3u; }
+    else if (__all_sync(FULL, dx < 16u && dy < 8u)) { K = 4; lgP = 4u; }
+    else if (__all_sync(FULL, dx < 8u && dy < 16u)) { K = 4; lgP = 3u; }
+    else if (__all_sync(FULL, dx < 32u && dy < 4u)) { K = 4; lgP = 5u; }
+    if (K != 0) return fb_wave_k<DBG>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
+    LeanOut o;
+    o.done = false;   // general path
+    o.color = make_float4(0.f, 0.f, 0.f, 0.f);
+    o.rec = kSlowMark;
+    o.prod = INVALID_ID;
+    o.selbits = 0u;
     return o;
 }
 
@@ -1607,8 +1718,8 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
             const unsigned A = __ballot_sync(FULL, active);
             uint32_t rec;
             if (!FORCE && A == FULL) {
-                const LeanOut o = lean_wave<DBG, false>(a, fs, uv, gr, px, py, frame, GRAD, false);
-                rec = o.done ? o.rec : kSlowMark;
+                const LeanOut o = lean_wave<DBG>(a, fs, uv, gr, GRAD);
+                rec = o.rec;
                 if (o.done) {
                     st_stream_f4(a.out + pix, o.color);
                     if (DBG) {
@@ -1624,7 +1735,7 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
                     if (a.dbg_sel) a.dbg_sel[pix] = 0u;
                 }
             } else {
-                rec = kSlowMark;   // partial wave: second kernel
+                rec = kSlowMark;   // partial wave: general kernel
             }
             if (lane == (unsigned)(wx - wx0)) myrec = rec;
         }
@@ -1632,28 +1743,67 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
     }
 }
 
-// Second pass over the waves the lean kernel marked with kSlowMark: full waves whose
-// window fits 8x8 (they need a fallback) take the lean fallback; partial waves and wider
-// windows take the general path.  Warps stride over groups of 32 records (one
-// coalesced 128-B load + ballot each).
+// Second / third pass over the marked waves.  FALLBACK: the kFbMark waves through the lean
+// fallback (fb_wave) — and, with CTF_REST_MERGED, the kSlowMark waves through the general
+// path out of line; else (third kernel) the kSlowMark waves through the general path.
+// Warps stride over groups of 32 records (one coalesced 128-B load + ballot each).
 #ifndef CTF_REST_MINB
-#define CTF_REST_MINB 3  // rest kernel: resident CTAs per SM (85 registers: the general path fits)
+#define CTF_REST_MINB 3  // general kernel: resident CTAs per SM (80 registers: the general path fits)
 #endif
+#ifndef CTF_FB_MINB
+#define CTF_FB_MINB 4  // fallback kernel: resident CTAs per SM (64 registers)
+#endif
+constexpr int kScanGroups = 8;   // record groups loaded per warp step in the rest kernels
+#ifndef CTF_REST_MERGED
+#define CTF_REST_MERGED 0  // 1: the fallback kernel also runs the general path (out of line); no third kernel
+#endif
+// the general path for one wave; OUT_OF_LINE keeps its register demand out of the
+// fallback kernel's allocation (it spills instead; those waves are rare)
 template <bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, CTF_REST_MINB) ctf_collab_bc1_rest_kernel(const KArgs a, unsigned nrec) {
-    __shared__ WarpSmem smem[kWarps];
-    __shared__ FastSmem fsm[kWarps];
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    WarpSmem &s = smem[warp];
-    FastSmem &fs = fsm[warp];
-    const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
+static __device__ __noinline__ WaveOut general_wave_noinline(const KArgs &a, WarpSmem &s, float2 uv, uint2 gr,
+                                                             bool active, unsigned A, int px, int py, uint32_t frame) {
     const MlpCtx mc{nullptr, nullptr, nullptr, nullptr, 0u};
+    return wave_general<FMT_BC1, MODE_COLLAB, DBG>(a, NoWeights{}, s, mc, uv, gr, active, A, __popc(A), px, py, frame);
+}
+template <bool DBG, bool OUT_OF_LINE>
+__device__ __forceinline__ WaveOut general_wave(const KArgs &a, WarpSmem &s, float2 uv, uint2 gr, bool active,
+                                                unsigned A, int px, int py, uint32_t frame) {
+    if constexpr (OUT_OF_LINE) {
+        return general_wave_noinline<DBG>(a, s, uv, gr, active, A, px, py, frame);
+    } else {
+        const MlpCtx mc{nullptr, nullptr, nullptr, nullptr, 0u};
+        return wave_general<FMT_BC1, MODE_COLLAB, DBG>(a, NoWeights{}, s, mc, uv, gr, active, A, __popc(A), px, py,
+                                                       frame);
+    }
+}
+template <bool DBG, bool FALLBACK>
+__global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : CTF_REST_MINB)
+    ctf_collab_bc1_rest_kernel(const KArgs a, unsigned nrec) {
+    __shared__ WarpSmem smem[(FALLBACK && !CTF_REST_MERGED) ? 1 : kWarps];
+    __shared__ FbSmem fsm[FALLBACK ? kWarps : 1];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    WarpSmem &s = smem[(FALLBACK && !CTF_REST_MERGED) ? 0 : warp];
+    FbSmem &fs = fsm[FALLBACK ? warp : 0];
+    const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
+    // groups of 32 records (marked waves cluster: fine groups balance better), kScanGroups
+    // groups per warp step loaded together (the scan is latency-bound where nothing is marked)
     const unsigned ngroups = (nrec + 31u) / 32u, gwarps = gridDim.x * kWarps;
-    for (unsigned g = blockIdx.x * kWarps + warp; g < ngroups; g += gwarps) {
-        const unsigned wi0 = g * 32u;
-        const uint32_t r = (wi0 + lane < nrec) ? a.rec[wi0 + lane] : 0u;
-        unsigned todo = __ballot_sync(FULL, r == kSlowMark);
+    for (unsigned g0 = blockIdx.x * kWarps + warp; g0 < ngroups; g0 += kScanGroups * gwarps) {
+      uint32_t rs[kScanGroups];
+#pragma unroll
+      for (int j = 0; j < kScanGroups; ++j) {   // volatile: all loads issue before the first use
+          const unsigned gj = g0 + (unsigned)j * gwarps;
+          rs[j] = 0u;
+          ld_u32_if(rs[j], a.rec + gj * 32u + lane, gj < ngroups && gj * 32u + lane < nrec);
+      }
+#pragma unroll 1
+      for (int j = 0; j < kScanGroups; ++j) {
+        const unsigned g = g0 + (unsigned)j * gwarps;
+        const uint32_t r = rs[j];
+        unsigned todo = FALLBACK ? __ballot_sync(FULL, r == kFbMark || (CTF_REST_MERGED && r == kSlowMark))
+                                 : __ballot_sync(FULL, r == kSlowMark);
         if (!todo) continue;
+        const unsigned wi0 = g * 32u;
         // wave coordinates of the group's first record (one division per group), then
         // of record wi0 + b by carrying b across wave-rows and frames
         const unsigned fr0 = wi0 / (unsigned)a.wpf, rem0 = wi0 - fr0 * (unsigned)a.wpf;
@@ -1706,10 +1856,14 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_REST_MINB) ctf_collab_bc1_res
             const uint32_t frame = a.frame_index + fr;
             LeanOut o;
             o.done = false;
-            if (A == FULL) o = lean_wave<DBG, true>(a, fs, uv, gr, px, py, frame, a.grad != nullptr, a.flags & FLAG_FORCE_FALLBACK);
+            if (FALLBACK && A == FULL)
+                o = fb_wave<DBG>(a, fs, uv, gr, px, py, frame, a.grad != nullptr, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
             if (!o.done) {
-                const WaveOut go = wave_general<FMT_BC1, MODE_COLLAB, DBG>(a, NoWeights{}, s, mc, uv, gr, active, A,
-                                                                           __popc(A), px, py, frame);
+                if (FALLBACK && !CTF_REST_MERGED) {   // (defensive) no 128-bit window: general kernel
+                    if (lane == 0) a.rec[wi] = kSlowMark;
+                    continue;
+                }
+                const WaveOut go = general_wave<DBG, FALLBACK && CTF_REST_MERGED>(a, s, uv, gr, active, A, px, py, frame);
                 o.color = go.color;
                 o.rec = go.rec;
                 o.prod = go.prod;
@@ -1722,6 +1876,7 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_REST_MINB) ctf_collab_bc1_res
             }
             if (lane == 0) a.rec[wi] = o.rec;
         }
+      }
     }
 }
 #endif
@@ -1804,16 +1959,21 @@ static cudaError_t launch_fast(KArgs k, cudaStream_t stream) {
     kern<<<(unsigned)grid, kWarps * 32, 0, stream>>>(k);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // second pass over the marked waves: at most one resident wave of CTAs
-    auto rest = ctf_collab_bc1_rest_kernel<DBG>;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rest, kWarps * 32, 0);
-    if (e != cudaSuccess) return e;
+    // the marked waves: lean fallback kernel, then the general kernel; each at most one
+    // resident wave of CTAs
     const unsigned nrec = (unsigned)((long long)k.wpf * (k.nchunks / (unsigned)k.cpf));
     const long long groups = ((long long)nrec + 31) / 32;
-    long long g2 = (long long)sms * (per_sm > 0 ? per_sm : 1);
-    if (g2 * kWarps > groups) g2 = (groups + kWarps - 1) / kWarps;
-    rest<<<(unsigned)(g2 < 1 ? 1 : g2), kWarps * 32, 0, stream>>>(k, nrec);
-    return cudaGetLastError();
+    for (int pass = 0; pass < (CTF_REST_MERGED ? 1 : 2); ++pass) {
+        auto rest = pass == 0 ? ctf_collab_bc1_rest_kernel<DBG, true> : ctf_collab_bc1_rest_kernel<DBG, false>;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rest, kWarps * 32, 0);
+        if (e != cudaSuccess) return e;
+        long long g2 = (long long)sms * (per_sm > 0 ? per_sm : 1);
+        if (g2 * kWarps > groups) g2 = (groups + kWarps - 1) / kWarps;
+        rest<<<(unsigned)(g2 < 1 ? 1 : g2), kWarps * 32, 0, stream>>>(k, nrec);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 #endif
 
@@ -1842,7 +2002,7 @@ static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::typ
 #endif
 #if CTF_TU_FMT == 1
 int launches_per_pass(int fmt, int mode, int filter) {
-    return (CTF_FAST && fmt == FMT_BC1 && mode == MODE_COLLAB && filter == 0) ? 2 : 1;
+    return (CTF_FAST && fmt == FMT_BC1 && mode == MODE_COLLAB && filter == 0) ? (CTF_REST_MERGED ? 2 : 3) : 1;
 }
 
 cudaError_t launch_filter_bc1(const LaunchArgs &a, cudaStream_t stream) {

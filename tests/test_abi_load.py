@@ -74,7 +74,7 @@ def test_validation_errors_without_gpu():
     tex.width, tex.height = 8192, 8192
     assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EUNSUPPORTED
     lib.ctf_launches_per_call.argtypes = [ctypes.c_int32] * 4 + [ctypes.c_int]
-    # BC1 COLLAB bilinear: lean kernel + rest kernel per pass; everything else one kernel
-    assert lib.ctf_launches_per_call(1, 3, 0, 64, 1) == 2 and lib.ctf_launches_per_call(1, 3, 0, 64, 0) == 128
+    # BC1 COLLAB bilinear: exact, fallback and general kernels per pass; everything else one kernel
+    assert lib.ctf_launches_per_call(1, 3, 0, 64, 1) == 3 and lib.ctf_launches_per_call(1, 3, 0, 64, 0) == 192
     assert lib.ctf_launches_per_call(1, 0, 0, 64, 1) == 1 and lib.ctf_launches_per_call(2, 3, 0, 8, 0) == 8
     assert lib.ctf_launches_per_call(3, 3, 0, 1, 1) == -1
