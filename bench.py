@@ -369,8 +369,11 @@ def main():
     rec = torch.empty((F, nwy, nwx), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
+    wspace = ctf.workspace_for(tex, mode, 0, Wf, Hf, F, dev)   # work lists (ctf_params.workspace_dev)
+
     def step():
-        ctf.filter_batch(tex, uv, grad, mode, fb, 0, args.seed, frame_base, out=out, rec=rec, stream=stream)
+        ctf.filter_batch(tex, uv, grad, mode, fb, 0, args.seed, frame_base, out=out, rec=rec, stream=stream,
+                         workspace=wspace)
 
     for _ in range(max(args.warmup, 0)):
         step()

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define CTF_ABI_VERSION 3
+#define CTF_ABI_VERSION 4
 
 typedef enum {
     CTF_OK = 0,
@@ -122,6 +122,14 @@ typedef struct {
     uint64_t seed;         /* RNG key (R-11: Philox4x32-10, ctr = (x, y, frame, 0))         */
     int32_t filter;        /* ctf_filter (ABI 2); 0 = bilinear                             */
     int32_t max_evals;     /* exact-path evaluations per lane: 0 or 1, or 2 (bicubic only)  */
+    void *workspace_dev;   /* optional device scratch (ABI 4), >= ctf_filter_workspace_bytes()
+                              bytes, 16-byte aligned, owned by the caller, contents need no
+                              initialisation; used by the BC1 COLLAB bilinear path for
+                              compact work lists of its fallback / general waves (no record
+                              scans, balanced second passes).  NULL: the record buffer doubles
+                              as the work list.  Results are identical either way.  Calls
+                              that share a workspace must be ordered (same stream).        */
+    uint64_t workspace_bytes;
 } ctf_params;
 
 /* Optional per-pixel debug outputs (only with CTF_FLAG_DEBUG; any may be NULL). */
@@ -217,6 +225,9 @@ int ctf_filter_frames_host(const ctf_texture *tex, const float *uv_host, const u
                            int32_t Wf, int32_t Hf, int32_t frames, int32_t chunk_frames,
                            const ctf_params *p, float *out_host, uint32_t *rec_host,
                            void *workspace_dev, size_t workspace_bytes, void *stream);
+
+/* Bytes of ctf_params.workspace_dev for `frames` frames of Wf x Hf (8 bytes per wave + 256). */
+size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames);
 
 /*
  * Kernel launches one call above issues (for launch accounting): format / mode / filter

@@ -68,6 +68,9 @@ ctf::LaunchArgs make_args(const ctf_texture *tex, const float *uv, const uint16_
     a.seed = p->seed;
     a.filter = p->filter;
     a.max_evals = p->max_evals < 1 ? 1 : p->max_evals;
+    if (p->workspace_dev && p->workspace_bytes >= ctf_filter_workspace_bytes(Wf, Hf, frames) &&
+        ((uintptr_t)p->workspace_dev & 15u) == 0)
+        a.lists = static_cast<uint32_t *>(p->workspace_dev);
     if (dbg && (p->flags & CTF_FLAG_DEBUG)) {
         a.dbg_pid = dbg->produced_id_dev;
         a.dbg_sel = dbg->selection_dev;
@@ -83,6 +86,12 @@ ctf::LaunchArgs make_args(const ctf_texture *tex, const float *uv, const uint16_
 extern "C" {
 
 int ctf_abi_version(void) { return CTF_ABI_VERSION; }
+
+size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames) {
+    if (Wf <= 0 || Hf <= 0 || frames <= 0) return 0;
+    const size_t waves = (size_t)((Wf + 7) / 8) * (size_t)((Hf + 3) / 4) * (size_t)frames;
+    return 256 + 8 * waves;
+}
 
 int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int batched) {
     if ((format != CTF_FMT_BC1 && format != CTF_FMT_LATENT_MLP) || mode < 0 || mode > CTF_MODE_MASK11 || filter < 0 ||
@@ -210,6 +219,8 @@ int ctf_filter_frames_host(const ctf_texture *tex, const float *uv_host, const u
         if (!good) { rc = CTF_ECUDA; break; }
         ctf_params pc = *p;
         pc.frame_index = p->frame_index + (uint32_t)f0;
+        pc.workspace_dev = nullptr;   // the chunks run on two streams: no shared work lists
+        pc.workspace_bytes = 0;
         rc = ctf_filter_batch(tex, S.uv, S.grad, Wf, Hf, nf, &pc, S.out, S.rec, nullptr, comp);
         if (rc != CTF_OK) break;
         good = cudaEventRecord(ev_k[b], comp) == cudaSuccess && cudaStreamWaitEvent(d2h, ev_k[b], 0) == cudaSuccess;

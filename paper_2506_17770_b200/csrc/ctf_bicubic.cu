@@ -162,7 +162,7 @@ template <int FMT>
 __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
     ctf_bicubic_kernel(const BArgs a, const typename WeightsOf<FMT>::type mw, const int MODE) {
     __shared__ BSmem smem[kBWarps];
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     BSmem &s = smem[warp];
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned lt = lanemask_lt();

@@ -54,6 +54,18 @@ __device__ __forceinline__ void ld_u32_if(uint32_t &r, const uint32_t *p, bool p
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cg.u32 %0, [%1];\n\t}"
                  : "+r"(r) : "l"(p), "r"((unsigned)pred));
 }
+// predicated global atomic add / store without a branch (a divergent branch anywhere in a
+// loop makes ptxas guard the loop's warp collectives with divergence checks)
+__device__ __forceinline__ uint32_t atom_add_if(uint32_t *p, uint32_t v, bool pred) {
+    uint32_t old = 0u;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q atom.global.add.u32 %0, [%1], %2;\n\t}"
+                 : "+r"(old) : "l"(p), "r"(v), "r"((unsigned)pred) : "memory");
+    return old;
+}
+__device__ __forceinline__ void st_u32_if(uint32_t *p, uint32_t v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.u32 [%0], %1;\n\t}"
+                 ::"l"(p), "r"(v), "r"((unsigned)pred) : "memory");
+}
 __device__ __forceinline__ void st_stream_f4(float4 *p, float4 v) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");

@@ -51,6 +51,8 @@ struct KArgs {
     float4 *out;
     uint32_t *rec;
     uint32_t *dbg_pid, *dbg_sel, *dbg_unread;
+    uint32_t *lists;                // optional work lists (BC1 COLLAB): counts [0], [1]; lists at [64], [64 + nrec]
+    unsigned nrec;                  // waves in the batch
     unsigned fpx;                   // pixels per frame (all pixel indices < 2^32, validated on the host)
     int Wf, Hf, nwx, nwy, wpf;
     int cpr, cpf;                   // work items (runs of kChunk waves) per wave-row / per frame
@@ -1152,7 +1154,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : 
     ctf_filter_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ WarpSmem smem[kWarps];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent-MLP COLLAB: batch buffers
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     WarpSmem &s = smem[warp];
     constexpr bool kBatchMlp = FMT == FMT_MLP && MODE == MODE_COLLAB;
     MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
@@ -1516,7 +1518,7 @@ struct W128 {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int r = pre + __popc(w[k] & lt);
-            if (((w[k] >> lane) & 1u) && r < 32) tbl[r] = (uint8_t)(32u * k + lane);
+            st_shared_u8_if(tbl + (r & 31), 32u * k + lane, ((w[k] >> lane) & 1u) && r < 32);
             pre += __popc(w[k]);
         }
     }
@@ -1610,12 +1612,15 @@ __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const F
             }
         }
     }
-    // ---- the single texel-production site (<= 1 evaluation per lane)
-    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (produced) {
-        val = rgba8_unorm(bc1_decode(a.tex, qx, qy));
-        if (DBG) o.prod = (uint32_t)(qy * a.tex.W + qx);
+    // ---- the single texel-production site (<= 1 evaluation per lane).  The
+    // decoder runs on every lane (SIMT: same cost), non-producers on the window origin,
+    // so no divergent region precedes the warp collectives below.
+    if (!produced) {
+        qx = minx;
+        qy = miny;
     }
+    const float4 val = rgba8_unorm(bc1_decode(a.tex, qx, qy));
+    if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
     if (exact) {
         if (produced) fs.xch[lane] = val;
         __syncwarp();
@@ -1681,7 +1686,7 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
 template <bool DBG, bool GRAD, bool FORCE>
 __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_kernel(const KArgs a) {
     __shared__ FastSmem fsm[kWarps];
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     FastSmem &fs = fsm[warp];
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned per_warp = a.ipc / kWarps;
@@ -1739,7 +1744,18 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
             }
             if (lane == (unsigned)(wx - wx0)) myrec = rec;
         }
-        if (lane < (unsigned)(wx1 - wx0)) a.rec[w0 + lane] = myrec;
+        const bool inrun = lane < (unsigned)(wx1 - wx0);
+        if (inrun) a.rec[w0 + lane] = myrec;
+        // this run's fallback / general waves (lane = wave of the run)
+        const unsigned mfb = __ballot_sync(FULL, inrun && myrec == kFbMark);
+        const unsigned msl = __ballot_sync(FULL, inrun && myrec == kSlowMark);
+        if (a.lists && (mfb | msl)) {   // append the run's marked waves to the work lists (predicated)
+            const unsigned b0 = __shfl_sync(FULL, atom_add_if(a.lists + 0, (unsigned)__popc(mfb), lane == 0 && mfb), 0);
+            const unsigned b1 = __shfl_sync(FULL, atom_add_if(a.lists + 1, (unsigned)__popc(msl), lane == 0 && msl), 0);
+            const unsigned lt = lanemask_lt();
+            st_u32_if(a.lists + 64u + b0 + __popc(mfb & lt), w0 + lane, (mfb >> lane) & 1u);
+            st_u32_if(a.lists + 64u + a.nrec + b1 + __popc(msl & lt), w0 + lane, (msl >> lane) & 1u);
+        }
     }
 }
 
@@ -1781,11 +1797,84 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : CTF_REST
     ctf_collab_bc1_rest_kernel(const KArgs a, unsigned nrec) {
     __shared__ WarpSmem smem[(FALLBACK && !CTF_REST_MERGED) ? 1 : kWarps];
     __shared__ FbSmem fsm[FALLBACK ? kWarps : 1];
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     WarpSmem &s = smem[(FALLBACK && !CTF_REST_MERGED) ? 0 : warp];
     FbSmem &fs = fsm[FALLBACK ? warp : 0];
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
-    // groups of 32 records (marked waves cluster: fine groups balance better), kScanGroups
+    // one marked wave: lean fallback (FALLBACK) or the general path
+    auto process = [&](unsigned wi, float2 uv, uint2 gr, unsigned fr, int px, int py, bool inframe, unsigned pix) {
+        __syncwarp();
+        const bool active = inframe && !isnan(uv.x);
+        const unsigned A = __ballot_sync(FULL, active);
+        const uint32_t frame = a.frame_index + fr;
+        LeanOut o;
+        o.done = false;
+        if (FALLBACK && A == FULL)
+            o = fb_wave<DBG>(a, fs, uv, gr, px, py, frame, a.grad != nullptr, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
+        if (!o.done) {
+            if (FALLBACK && !CTF_REST_MERGED) {   // (defensive) no 128-bit window: general kernel
+                if (lane == 0) {
+                    a.rec[wi] = kSlowMark;
+                    if (a.lists) a.lists[64u + a.nrec + atomicAdd(a.lists + 1, 1u)] = wi;
+                }
+                return;
+            }
+            const WaveOut go = general_wave<DBG, FALLBACK && CTF_REST_MERGED>(a, s, uv, gr, active, A, px, py, frame);
+            o.color = go.color;
+            o.rec = go.rec;
+            o.prod = go.prod;
+            o.selbits = go.selbits;
+        }
+        if (inframe) st_stream_f4(a.out + pix, o.color);
+        if (DBG && inframe) {
+            if (a.dbg_pid) a.dbg_pid[pix] = o.prod;
+            if (a.dbg_sel) a.dbg_sel[pix] = o.selbits;
+        }
+        if (lane == 0) a.rec[wi] = o.rec;
+    };
+    if (a.lists) {
+        // ---- work-list mode: the waves the lean kernel appended, one per warp step
+        // (balanced over the whole grid), the next one's inputs loaded ahead
+        const unsigned n = __shfl_sync(FULL, a.lists[FALLBACK ? 0 : 1], 0);   // provably uniform
+        const uint32_t *L = a.lists + 64u + (FALLBACK ? 0u : a.nrec);
+        const unsigned tw = gridDim.x * kWarps;
+        unsigned i = blockIdx.x * kWarps + warp;
+        if (i >= n) return;
+        auto fetch_wi = [&](unsigned wi, float2 &uv, uint2 &gr, unsigned &fr, int &px, int &py, bool &inframe,
+                            unsigned &pix) {
+            fr = wi / (unsigned)a.wpf;
+            const unsigned rem = wi - fr * (unsigned)a.wpf;
+            const int wy = (int)(rem / (unsigned)a.nwx), wx = (int)rem - wy * a.nwx;
+            px = wx * 8 + lx;
+            py = wy * 4 + ly;
+            inframe = px < a.Wf && py < a.Hf;
+            pix = fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)px;
+            uv = make_float2(__int_as_float(0x7fc00000), 0.f);
+            gr = make_uint2(0u, 0u);
+            ld_stream_f2_if(uv, a.uv + pix, inframe);
+            ld_stream_u2_if(gr, a.grad + pix, inframe & (a.grad != nullptr));
+        };
+        unsigned wi_n = __shfl_sync(FULL, L[i], 0), fr_n, pix_n;
+        float2 uv_n;
+        uint2 gr_n;
+        int px_n, py_n;
+        bool in_n;
+        fetch_wi(wi_n, uv_n, gr_n, fr_n, px_n, py_n, in_n, pix_n);
+        for (; i < n; i += tw) {
+            const unsigned wi = wi_n, fr = fr_n, pix = pix_n;
+            const float2 uv = uv_n;
+            const uint2 gr = gr_n;
+            const int px = px_n, py = py_n;
+            const bool inframe = in_n;
+            if (i + tw < n) {
+                wi_n = __shfl_sync(FULL, L[i + tw], 0);
+                fetch_wi(wi_n, uv_n, gr_n, fr_n, px_n, py_n, in_n, pix_n);
+            }
+            process(wi, uv, gr, fr, px, py, inframe, pix);
+        }
+        return;
+    }
+    // ---- record-scan mode: groups of 32 records (marked waves cluster: fine groups balance better), kScanGroups
     // groups per warp step loaded together (the scan is latency-bound where nothing is marked)
     const unsigned ngroups = (nrec + 31u) / 32u, gwarps = gridDim.x * kWarps;
     for (unsigned g0 = blockIdx.x * kWarps + warp; g0 < ngroups; g0 += kScanGroups * gwarps) {
@@ -1850,31 +1939,7 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : CTF_REST
                 b_n = (unsigned)(__ffs(todo) - 1);
                 fetch(b_n, uv_n, gr_n, fr_n, px_n, py_n, in_n, pix_n);
             }
-            __syncwarp();
-            const bool active = inframe && !isnan(uv.x);
-            const unsigned A = __ballot_sync(FULL, active);
-            const uint32_t frame = a.frame_index + fr;
-            LeanOut o;
-            o.done = false;
-            if (FALLBACK && A == FULL)
-                o = fb_wave<DBG>(a, fs, uv, gr, px, py, frame, a.grad != nullptr, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
-            if (!o.done) {
-                if (FALLBACK && !CTF_REST_MERGED) {   // (defensive) no 128-bit window: general kernel
-                    if (lane == 0) a.rec[wi] = kSlowMark;
-                    continue;
-                }
-                const WaveOut go = general_wave<DBG, FALLBACK && CTF_REST_MERGED>(a, s, uv, gr, active, A, px, py, frame);
-                o.color = go.color;
-                o.rec = go.rec;
-                o.prod = go.prod;
-                o.selbits = go.selbits;
-            }
-            if (inframe) st_stream_f4(a.out + pix, o.color);
-            if (DBG && inframe) {
-                if (a.dbg_pid) a.dbg_pid[pix] = o.prod;
-                if (a.dbg_sel) a.dbg_sel[pix] = o.selbits;
-            }
-            if (lane == 0) a.rec[wi] = o.rec;
+            process(wi, uv, gr, fr, px, py, inframe, pix);
         }
       }
     }
@@ -1940,6 +2005,10 @@ static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, 
 // same work split as the general BC1 kernel
 template <bool DBG>
 static cudaError_t launch_fast(KArgs k, cudaStream_t stream) {
+    if (k.lists) {   // work-list counters (the lists need no initialisation)
+        const cudaError_t e0 = cudaMemsetAsync(k.lists, 0, 2 * sizeof(uint32_t), stream);
+        if (e0 != cudaSuccess) return e0;
+    }
     const bool grad = k.grad != nullptr, force = (k.flags & FLAG_FORCE_FALLBACK) != 0;
     auto kern = grad ? (force ? ctf_collab_bc1_kernel<DBG, true, true> : ctf_collab_bc1_kernel<DBG, true, false>)
                      : (force ? ctf_collab_bc1_kernel<DBG, false, true> : ctf_collab_bc1_kernel<DBG, false, false>);
@@ -2022,6 +2091,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.dbg_pid = a.dbg_pid;
     k.dbg_sel = a.dbg_sel;
     k.dbg_unread = a.dbg_unread;
+    k.lists = a.lists;
     k.Wf = a.Wf;
     k.Hf = a.Hf;
     k.nwx = (a.Wf + 7) / 8;
@@ -2031,6 +2101,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.cpr = (k.nwx + kChunk - 1) / kChunk;
     k.cpf = k.cpr * k.nwy;
     k.nchunks = (unsigned)((long long)k.cpf * a.frames);
+    k.nrec = (unsigned)((long long)k.wpf * a.frames);
     k.Wflt = (float)a.W;
     k.Hflt = (float)a.H;
     k.Wm1 = a.W - 1;

@@ -30,6 +30,9 @@ struct LaunchArgs {
     int max_evals;          // exact-path evaluations per lane (1 or 2)
     // debug
     uint32_t *dbg_pid, *dbg_sel, *dbg_unread;
+    // optional work lists (ctf_params.workspace_dev): [0] = #fallback waves, [1] = #general
+    // waves, fallback list at [64], general list at [64 + waves]
+    uint32_t *lists;
 };
 
 cudaError_t launch_filter_bc1(const LaunchArgs &a, cudaStream_t stream);  // ctf_filter.cu, CTF_TU_FMT=1

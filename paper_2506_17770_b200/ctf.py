@@ -39,7 +39,7 @@ class ctf_texture(ctypes.Structure):
 class ctf_params(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("fallback", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("frame_index", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("filter", ctypes.c_int32),
-                ("max_evals", ctypes.c_int32)]
+                ("max_evals", ctypes.c_int32), ("workspace_dev", ctypes.c_void_p), ("workspace_bytes", ctypes.c_uint64)]
 
 
 class ctf_debug(ctypes.Structure):
@@ -64,7 +64,7 @@ class ctf_frame_stats(ctypes.Structure):
 
 
 EXPORTS = ["ctf_filter_frame", "ctf_filter_batch", "ctf_stats", "ctf_host_workspace_bytes",
-           "ctf_filter_frames_host", "ctf_launches_per_call", "ctf_abi_version"]
+           "ctf_filter_frames_host", "ctf_filter_workspace_bytes", "ctf_launches_per_call", "ctf_abi_version"]
 
 _lib = None
 
@@ -85,6 +85,8 @@ def load_library(path: Path | str | None = None):
     lib.ctf_stats.argtypes = [V, I32, I32, I32, V, V, ctypes.POINTER(ctf_frame_stats), V]
     lib.ctf_host_workspace_bytes.argtypes = [I32, I32, I32, ctypes.c_int]
     lib.ctf_host_workspace_bytes.restype = ctypes.c_size_t
+    lib.ctf_filter_workspace_bytes.argtypes = [I32, I32, I32]
+    lib.ctf_filter_workspace_bytes.restype = ctypes.c_size_t
     lib.ctf_filter_frames_host.argtypes = [PT, V, V, I32, I32, I32, I32, PP, V, V, V, ctypes.c_size_t, V]
     lib.ctf_launches_per_call.argtypes = [I32, I32, I32, I32, ctypes.c_int]
     for fn in ("ctf_filter_frame", "ctf_filter_batch", "ctf_stats", "ctf_filter_frames_host",
@@ -152,13 +154,31 @@ def num_waves(wf: int, hf: int) -> int:
     return ((wf + 7) // 8) * ((hf + 3) // 4)
 
 
+def workspace_for(tex: Texture, mode: int, filt: int, wf: int, hf: int, frames: int, device) -> torch.Tensor | None:
+    """Device scratch for ctf_params.workspace_dev (the BC1 COLLAB bilinear work lists), or None
+    where the path does not use one."""
+    if tex.fmt != FMT_BC1 or mode != MODE_COLLAB or filt != FILTER_BILINEAR:
+        return None
+    nbytes = load_library().ctf_filter_workspace_bytes(wf, hf, frames)
+    return torch.empty(nbytes, device=device, dtype=torch.uint8)
+
+
+def _set_workspace(p: ctf_params, ws: torch.Tensor | None):
+    if ws is not None:
+        p.workspace_dev = ws.data_ptr()
+        p.workspace_bytes = ws.numel() * ws.element_size()
+
+
 def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS,
                  flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
                  rec: torch.Tensor | None = None, debug: dict | None = None,
-                 stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR, max_evals: int = 1):
+                 stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR, max_evals: int = 1,
+                 workspace: torch.Tensor | bool | None = True):
     """uv: float32 [F][Hf][Wf][2] (or [Hf][Wf][2]); grad: float16 [..][4] or None.
     Returns (out float32 [..][4], rec int32 [F][nwy][nwx]).  `debug` may hold tensors
-    'produced_id', 'selection' (int32, pixel-shaped) and 'unread' (int32 [1])."""
+    'produced_id', 'selection' (int32, pixel-shaped) and 'unread' (int32 [1]).
+    workspace: True = allocate the path's scratch (workspace_for) for this call, a tensor =
+    use it, None / False = none (the record buffer doubles as the work list)."""
     lib = load_library()
     single = uv.dim() == 3
     uv4 = uv.unsqueeze(0) if single else uv
@@ -172,6 +192,8 @@ def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
     if rec is None:
         rec = torch.empty((frames, (hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
     p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
+    ws = workspace_for(tex, mode, filter, wf, hf, frames, uv.device) if workspace is True else (workspace if isinstance(workspace, torch.Tensor) else None)
+    _set_workspace(p, ws)
     dbg = None
     if debug is not None:
         dbg = ctf_debug(_ptr(debug.get("produced_id")), _ptr(debug.get("selection")), _ptr(debug.get("unread")))
@@ -188,8 +210,9 @@ def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
 def filter_frame(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS,
                  flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
                  rec: torch.Tensor | None = None, debug: dict | None = None,
-                 stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR, max_evals: int = 1):
-    """One frame through ctf_filter_frame.  uv float32 [Hf][Wf][2]."""
+                 stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR, max_evals: int = 1,
+                 workspace: torch.Tensor | bool | None = True):
+    """One frame through ctf_filter_frame.  uv float32 [Hf][Wf][2]; workspace as filter_batch."""
     lib = load_library()
     hf, wf = uv.shape[0], uv.shape[1]
     if out is None:
@@ -197,6 +220,8 @@ def filter_frame(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
     if rec is None:
         rec = torch.empty(((hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
     p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
+    ws = workspace_for(tex, mode, filter, wf, hf, 1, uv.device) if workspace is True else (workspace if isinstance(workspace, torch.Tensor) else None)
+    _set_workspace(p, ws)
     dbg = None
     if debug is not None:
         dbg = ctf_debug(_ptr(debug.get("produced_id")), _ptr(debug.get("selection")), _ptr(debug.get("unread")))

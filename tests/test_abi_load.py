@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     lib.ctf_abi_version.restype = ctypes.c_int
-    assert lib.ctf_abi_version() == 3
+    assert lib.ctf_abi_version() == 4
 
 
 def test_binding_declares_all_exports():

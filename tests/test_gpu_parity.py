@@ -258,3 +258,26 @@ def test_release_kernel_matches_oracle(ctf, mode, fb, fl):
     out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, fl, 21, 2)
     np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
     assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
+
+
+@pytest.mark.parametrize("fb,fl", [(3, 0), (2, 0), (1, 0), (0, 0), (3, 2)])
+def test_workspace_lists_equal_record_scan(ctf, fb, fl):
+    """BC1 COLLAB: the workspace work lists and the record-scan second passes give identical
+    records, colours and debug outputs (mixed scene: exact, fallback, partial, minified waves)."""
+    tex = bc1_tex(512, 512, 5, "image")
+    uv, g = synthetic.perspective_plane(333, 141, 512, 512, synthetic.PLANE_C4)
+    dt = to_dev_tex(ctf, tex)
+    uvd, gd = torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda()
+    res = []
+    for ws in (True, None):
+        dbg = {"produced_id": torch.zeros(uv.shape[:2], dtype=torch.int32, device="cuda"),
+               "selection": torch.zeros(uv.shape[:2], dtype=torch.int32, device="cuda"),
+               "unread": torch.zeros(1, dtype=torch.int32, device="cuda")}
+        out, rec = ctf.filter_frame(dt, uvd, gd, 3, fb, fl, seed=11, debug=dbg, workspace=ws)
+        out2, rec2 = ctf.filter_frame(dt, uvd, gd, 3, fb, fl, seed=11, workspace=ws)   # release kernels
+        res.append([t.cpu().numpy().view(np.uint32) for t in (out, rec, dbg["produced_id"], dbg["selection"], out2, rec2)])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+    import oracle
+    o = oracle.filter_frame(tex, uv, g, 3, fb, fl, seed=11)
+    np.testing.assert_array_equal(res[0][1], o["rec"])
