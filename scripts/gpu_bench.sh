@@ -9,12 +9,12 @@ fi
 timeout 900 python bench.py --steps ${STEPS:-20} --warmup 3 --cpu-seconds ${CPUS:-12} > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 tail -5 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
 # launch list of the same command (cold-cache, serialised: compare shares)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:ctf_ -c 40 --csv --log-file gpurun_out/launches_$TAG.csv \
-    python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch_bench_$TAG.json 2>&1
-tail -3 gpurun_out/launches_$TAG.csv
-# one full capture of the dominant kernel (16-frame batch)
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ctf_filter_kernel -s 3 -c 1 \
-    -o gpurun_out/prof_$TAG python bench.py --frames 16 --warmup 3 --profile-launches 1 > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:ctf_ -c 60 --csv --log-file gpurun_out/launches_$TAG.csv \
+    python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu --no-configs > gpurun_out/ncu_launch_bench_$TAG.json 2>&1
+python scripts/launch_shares.py gpurun_out/launches_$TAG.csv
+# one full capture of the three BC1 COLLAB kernels of one 64-frame step (the bench step)
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ctf_collab_bc1 -s 3 -c 3 \
+    -o gpurun_out/prof_$TAG python bench.py --warmup 1 --profile-launches 1 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -3 gpurun_out/ncu_full_$TAG.log
 if [ "${MLPPROF:-0}" = "1" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctf_filter_kernel -s 1 -c 1 \
