@@ -53,6 +53,8 @@ struct KArgs {
     uint32_t *dbg_pid, *dbg_sel, *dbg_unread;
     uint32_t *lists;                // optional work lists (BC1 COLLAB): counts [0], [1]; lists at [64], [64 + nrec]
     unsigned nrec;                  // waves in the batch
+    uint32_t wpf_m, nwx_m;          // magic multipliers: n / wpf, n / nwx (udiv_magic)
+    int wpf_s, nwx_s;
     unsigned fpx;                   // pixels per frame (all pixel indices < 2^32, validated on the host)
     int Wf, Hf, nwx, nwy, wpf;
     int cpr, cpf;                   // work items (runs of kChunk waves) per wave-row / per frame
@@ -73,6 +75,16 @@ struct WarpSmem {
     uint8_t lane_of_t[128]; // AABB position -> a lane that produced it (fallback, mask path)
     uint8_t rank_of[128];   // slow collect: (lane*4 + corner) -> rank
 };
+
+// n / d for n < 2^31 with a host-computed magic pair (m, s): s = floor(log2 d),
+// m = ceil(2^(32+s) / d) (0 when d is a power of two), q = umulhi(n, m) >> s.  Exact: with
+// m = 2^(32+s)/d + e (0 <= e < 1) the excess n e / 2^(32+s) stays below 1/d whenever
+// n < 2^(32+s)/d, which holds for n < 2^31 because d < 2^(s+1).
+__device__ __forceinline__ unsigned udiv_magic(unsigned n, uint32_t m, int s) { return (m ? __umulhi(n, m) : n) >> s; }
+static inline void udiv_magic_host(unsigned d, uint32_t &m, int &s) {
+    s = 31 - __builtin_clz(d);
+    m = (d & (d - 1u)) == 0u ? 0u : (uint32_t)(((1ull << (32 + s)) + d - 1u) / d);
+}
 
 // Per-lane footprint of one pixel (a2).
 struct Foot {
@@ -1496,16 +1508,30 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
 }
 
 // ---------------------------------------- lean fallback over windows up to 128 bits
-// Window masks as 4 words; the pitch 2^lgP <= 32 keeps every window row inside one word.
-struct W128 {
-    uint32_t w[4];
-    __device__ __forceinline__ uint32_t word(uint32_t k) const { return k == 0 ? w[0] : k == 1 ? w[1] : k == 2 ? w[2] : w[3]; }
-    __device__ __forceinline__ int count() const { return __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]); }
-    __device__ __forceinline__ int below(uint32_t k) const {   // set bits in words < k
-        return (k > 0 ? __popc(w[0]) : 0) + (k > 1 ? __popc(w[1]) : 0) + (k > 2 ? __popc(w[2]) : 0);
+// Window masks as NW (2 or 4) words; the pitch 2^lgP <= 32 keeps every window row inside one
+// word.  NW = 2 covers the 8x4 / 4x8 / 8x8 windows (most fallback waves), NW = 4 the
+// 16x8 / 8x16 / 32x4 ones.
+template <int NW>
+struct WMaskN {
+    uint32_t w[NW];
+    __device__ __forceinline__ uint32_t word(uint32_t k) const {
+        if constexpr (NW == 2) return k == 0 ? w[0] : w[1];
+        else return k == 0 ? w[0] : k == 1 ? w[1] : k == 2 ? w[2] : w[3];
     }
-    __device__ __forceinline__ int rank(uint32_t t) const {
-        return below(t >> 5) + __popc(word(t >> 5) & ((1u << (t & 31u)) - 1u));
+    __device__ __forceinline__ int count() const {
+        int c = 0;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) c += __popc(w[k]);
+        return c;
+    }
+    __device__ __forceinline__ int rank(uint32_t t) const {   // set bits below t
+        int c = 0;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const uint32_t kk = (uint32_t)k;
+            c += __popc(w[k] & ((t >> 5) > kk ? 0xFFFFFFFFu : (t >> 5) == kk ? (1u << (t & 31u)) - 1u : 0u));
+        }
+        return c;
     }
     // corners 0 / 1 at t0, t0 + dxs; 2 / 3 at t2, t2 + dxs
     __device__ __forceinline__ unsigned corners(uint32_t t0, uint32_t t2, uint32_t dxs) const {
@@ -1516,18 +1542,19 @@ struct W128 {
     __device__ __forceinline__ void push(uint8_t *tbl, unsigned lane, unsigned lt) const {
         int pre = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < NW; ++k) {
             const int r = pre + __popc(w[k] & lt);
             st_shared_u8_if(tbl + (r & 31), 32u * k + lane, ((w[k] >> lane) & 1u) && r < 32);
             pre += __popc(w[k]);
         }
     }
 };
-// OR-reduce of per-lane bits: `m` (pattern at bit t, t + 1, ...) placed at window position t
-__device__ __forceinline__ W128 reduce_w128(int K, uint32_t t, uint32_t pat, bool on, uint32_t t2 = 0xFFFFFFFFu) {
-    W128 r;
+// OR-reduce of per-lane bit patterns placed at window positions t (and t2), words < K
+template <int NW>
+__device__ __forceinline__ WMaskN<NW> reduce_wn(int K, uint32_t t, uint32_t pat, bool on, uint32_t t2 = 0xFFFFFFFFu) {
+    WMaskN<NW> r;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < NW; ++k) {
         uint32_t m = 0u;
         if (k < K) {   // warp-uniform
             if (on && (t >> 5) == (uint32_t)k) m |= pat << (t & 31u);
@@ -1546,7 +1573,7 @@ struct FbSmem {
 
 // One FULL wave whose window fits 128 bits, exact or fallback (STF / WC / C / C+), the
 // same results as the general path (records, producers, selections bit for bit).
-template <bool DBG>
+template <bool DBG, int NW>
 __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const Foot &f, int minx, int miny, int K,
                                              unsigned lgP, bool wave_mag, int px, int py, uint32_t frame, bool force) {
     const unsigned lane = lane_id(), lt = lanemask_lt();
@@ -1558,7 +1585,7 @@ __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const F
     const uint32_t t0 = ((uint32_t)(f.ya - miny) << lgP) + (uint32_t)(f.xa - minx);
     const uint32_t t2 = t0 + ((uint32_t)(f.yb - f.ya) << lgP);
     const uint32_t dxs = (uint32_t)(f.xb - f.xa);
-    const W128 U = reduce_w128(K, t0, 1u + dxs + dxs, true, t2);   // the unique set (List)
+    const WMaskN<NW> U = reduce_wn<NW>(K, t0, 1u + dxs + dxs, true, t2);   // the unique set (List)
     const int n = U.count();
     const bool exact = n <= 32 && !force;
     const int fb = a.fallback;
@@ -1582,7 +1609,7 @@ __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const F
         produced = true;
         if (fb == FB_CPLUS) {
             const uint32_t tp = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
-            const W128 P = reduce_w128(K, tp, 1u, true);   // planned set
+            const WMaskN<NW> P = reduce_wn<NW>(K, tp, 1u, true);   // planned set
             const int np = P.count();
             P.push(fs.bit_of_rank, lane, lt);
             __syncwarp();
@@ -1636,11 +1663,11 @@ __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const F
         o.color = val;
     } else {
         const uint32_t tq = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
-        const W128 D = reduce_w128(K, tq, 1u, produced);
+        const WMaskN<NW> D = reduce_wn<NW>(K, tq, 1u, produced);
         // values indexed by window position, zero where nothing was produced; one
         // publisher per produced texel (the decode is deterministic)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < NW; ++k)
             if (k < K) fs.xch[32 * k + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
         const unsigned peers = __match_any_sync(FULL, produced ? tq : 0xFFFFFFFFu);
         __syncwarp();
@@ -1671,7 +1698,8 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
     else if (__all_sync(FULL, dx < 16u && dy < 8u)) { K = 4; lgP = 4u; }
     else if (__all_sync(FULL, dx < 8u && dy < 16u)) { K = 4; lgP = 3u; }
     else if (__all_sync(FULL, dx < 32u && dy < 4u)) { K = 4; lgP = 5u; }
-    if (K != 0) return fb_wave_k<DBG>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
+    if (K == 1 || K == 2) return fb_wave_k<DBG, 2>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
+    if (K == 4) return fb_wave_k<DBG, 4>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
     LeanOut o;
     o.done = false;   // general path
     o.color = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1842,9 +1870,9 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : CTF_REST
         if (i >= n) return;
         auto fetch_wi = [&](unsigned wi, float2 &uv, uint2 &gr, unsigned &fr, int &px, int &py, bool &inframe,
                             unsigned &pix) {
-            fr = wi / (unsigned)a.wpf;
+            fr = udiv_magic(wi, a.wpf_m, a.wpf_s);
             const unsigned rem = wi - fr * (unsigned)a.wpf;
-            const int wy = (int)(rem / (unsigned)a.nwx), wx = (int)rem - wy * a.nwx;
+            const int wy = (int)udiv_magic(rem, a.nwx_m, a.nwx_s), wx = (int)rem - wy * a.nwx;
             px = wx * 8 + lx;
             py = wy * 4 + ly;
             inframe = px < a.Wf && py < a.Hf;
@@ -2102,6 +2130,8 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.cpf = k.cpr * k.nwy;
     k.nchunks = (unsigned)((long long)k.cpf * a.frames);
     k.nrec = (unsigned)((long long)k.wpf * a.frames);
+    udiv_magic_host((unsigned)k.wpf, k.wpf_m, k.wpf_s);
+    udiv_magic_host((unsigned)k.nwx, k.nwx_m, k.nwx_s);
     k.Wflt = (float)a.W;
     k.Hflt = (float)a.H;
     k.Wm1 = a.W - 1;
