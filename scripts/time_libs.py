@@ -14,7 +14,7 @@ import paper_2506_17770_b200.ctf as ctf  # noqa: E402
 from paper_2506_17770_b200 import dist as cdist  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--frames", type=int, default=32)
+ap.add_argument("--frames", type=int, default=64)
 ap.add_argument("--mode", type=int, default=3)
 ap.add_argument("--fb", type=int, default=3)
 ap.add_argument("--rounds", type=int, default=5)
