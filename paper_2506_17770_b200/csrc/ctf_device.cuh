@@ -76,6 +76,11 @@ __device__ __forceinline__ void st_shared_u32_if(uint32_t *p, uint32_t v, bool p
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
                  ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v), "r"((unsigned)pred) : "memory");
 }
+__device__ __forceinline__ void st_shared_f4_if(float4 *p, float4 v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n\t}"
+                 ::"r"((unsigned)__cvta_generic_to_shared(p)), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"((unsigned)pred)
+                 : "memory");
+}
 __device__ __forceinline__ void st_shared_u8_if(uint8_t *p, uint32_t v, bool pred) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u8 [%0], %1;\n\t}"
                  ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v), "r"((unsigned)pred) : "memory");

@@ -1469,7 +1469,7 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
         n = __popc(wm);
         r0 = __popc(wm & ((1u << t0) - 1u));
         r2 = __popc(wm & ((1u << t2) - 1u));
-        if (wm & lanebit) fs.bit_of_rank[__popc(wm & lt)] = (uint8_t)lane;
+        st_shared_u8_if(fs.bit_of_rank + __popc(wm & lt), lane, wm & lanebit);
     } else {
         const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
         const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
@@ -1478,22 +1478,22 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
         n = nl + __popc(wh);
         r0 = rank64(wl, wh, t0);
         r2 = rank64(wl, wh, t2);
-        if (wl & lanebit) fs.bit_of_rank[__popc(wl & lt)] = (uint8_t)lane;
+        st_shared_u8_if(fs.bit_of_rank + __popc(wl & lt), lane, wl & lanebit);
         const int rh = nl + __popc(wh & lt);
-        if ((wh & lanebit) && rh < 32) fs.bit_of_rank[rh] = (uint8_t)(32u + lane);
+        st_shared_u8_if(fs.bit_of_rank + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
     }
     // ---- a4: exact iff n <= a = 32 (always for a 32-bit window)
     if (n > 32) return o;   // fallback kernel
     o.done = true;
     __syncwarp();
     // ---- a5: lane r < n produces U[r] (h(r, A) = r); one decode site, fp32 once
+    // (SIMT: the decoder runs on every lane; non-producers decode the window origin and
+    // do not store — predicated, so the loop stays free of divergent regions)
     const bool produced = (int)lane < n;
-    const uint32_t e = fs.bit_of_rank[lane];
+    const uint32_t e = produced ? (uint32_t)fs.bit_of_rank[lane] : 0u;
     const int qx = minx + (int)(e & pmask), qy = miny + (int)(e >> lgP);
-    if (produced) {
-        fs.xch[lane] = rgba8_unorm(bc1_decode(a.tex, qx, qy));
-        if (DBG) o.prod = (uint32_t)(qy * a.tex.W + qx);
-    }
+    st_shared_f4_if(&fs.xch[lane], rgba8_unorm(bc1_decode(a.tex, qx, qy)), produced);
+    if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
     __syncwarp();
     // ---- a6: gather (ranks rho_k) + blend
     const float4 p[4] = {fs.xch[r0], fs.xch[r0 + (int)dxs], fs.xch[r2], fs.xch[r2 + (int)dxs]};
