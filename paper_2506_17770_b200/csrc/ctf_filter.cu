@@ -21,6 +21,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "ctf_device.cuh"
 #include "ctf_internal.h"
@@ -1728,6 +1729,7 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
         const int wx1 = min(wx0 + kChunk, a.nwx);
         const int py = wy * 4 + ly;
         const bool rowok = py < a.Hf;
+        const bool rowok_all = wy * 4 + 4 <= a.Hf;   // warp-uniform: all 4 rows in the frame
         const uint32_t frame = a.frame_index + (uint32_t)fr;
         const unsigned w0 = (unsigned)fr * (unsigned)a.wpf + (unsigned)(wy * a.nwx + wx0);
         unsigned pix = (unsigned)fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)(wx0 * 8 + lx);
@@ -1737,12 +1739,16 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
         uint2 gr_n = make_uint2(0u, 0u);
         ld_stream_f2_if(uv_n, a.uv + pix, rowok & (px < a.Wf));
         ld_stream_u2_if(gr_n, a.grad + pix, rowok & (px < a.Wf) & has_grad);
+        // interior runs (every pixel of the run in the frame, the common case) drop the
+        // per-wave bounds predicates: the loop is instantiated twice
         uint32_t myrec = 0u;
-        for (int wx = wx0; wx < wx1; ++wx, pix += 8u, px += 8) {
-            const bool inframe = rowok & (px < a.Wf);
+        auto run = [&](auto interior_tag) {
+          constexpr bool INTERIOR = decltype(interior_tag)::value;
+          for (int wx = wx0; wx < wx1; ++wx, pix += 8u, px += 8) {
+            const bool inframe = INTERIOR || (rowok & (px < a.Wf));
             const float2 uv = uv_n;
             const uint2 gr = gr_n;
-            const bool pf = (wx + 1 < wx1) & rowok & (px + 8 < a.Wf);
+            const bool pf = INTERIOR ? (wx + 1 < wx1) : ((wx + 1 < wx1) & rowok & (px + 8 < a.Wf));
             ld_stream_f2_if(uv_n, a.uv + (pix + 8u), pf);
             ld_stream_u2_if(gr_n, a.grad + (pix + 8u), pf & has_grad);
             __syncwarp();  // the previous wave's shared-memory reads are done
@@ -1771,7 +1777,10 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
                 rec = kSlowMark;   // partial wave: general kernel
             }
             if (lane == (unsigned)(wx - wx0)) myrec = rec;
-        }
+          }
+        };
+        if (rowok_all && wx1 * 8 <= a.Wf) run(std::true_type{});
+        else run(std::false_type{});
         const bool inrun = lane < (unsigned)(wx1 - wx0);
         if (inrun) a.rec[w0 + lane] = myrec;
         // this run's fallback / general waves (lane = wave of the run)
