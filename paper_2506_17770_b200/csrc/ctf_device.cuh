@@ -130,24 +130,26 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
     return d;
 }
 
-// RGBA8 -> (v / 255.0f) per channel, correctly rounded like the IEEE division of R-9:
-// a byte permute places v under the exponent of 2^23 (exact 2^23 + v), FADD2 removes
-// the 2^23, then q = v * (1/255) is corrected once, q += (v - 255 q) * (1/255) (FFMA2;
-// exact for every v in [0, 255]).  12 instructions per texel, no I2F.
-__device__ __forceinline__ float4 rgba8_unorm(uint32_t v) {
-    uint64_t rg = f2pack(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540)),
-                         __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541)));
-    uint64_t ba = f2pack(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7542)),
-                         __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7543)));
-    const uint64_t mag = f2pack(-8388608.0f, -8388608.0f), r = f2pack(1.0f / 255.0f, 1.0f / 255.0f),
+// (2^23 + v) bit patterns of the four channels -> v / 255, correctly rounded like the IEEE
+// division of R-9: FADD2 removes the 2^23 (exact), then q = v * (1/255) is corrected once,
+// q += (v - 255 q) * (1/255) (FFMA2; exact for every v in [0, 255]).  No I2F.
+__device__ __forceinline__ float4 magic_unorm(uint32_t r, uint32_t g, uint32_t b, uint32_t a) {
+    uint64_t rg = f2pack(__uint_as_float(r), __uint_as_float(g));
+    uint64_t ba = f2pack(__uint_as_float(b), __uint_as_float(a));
+    const uint64_t mag = f2pack(-8388608.0f, -8388608.0f), rc = f2pack(1.0f / 255.0f, 1.0f / 255.0f),
                    n255 = f2pack(-255.0f, -255.0f);
     rg = fadd2(rg, mag);
     ba = fadd2(ba, mag);
-    uint64_t q0 = fmul2(rg, r), q1 = fmul2(ba, r);
-    q0 = ffma2(ffma2(q0, n255, rg), r, q0);
-    q1 = ffma2(ffma2(q1, n255, ba), r, q1);
-    const float2 a = f2unpack(q0), b = f2unpack(q1);
-    return make_float4(a.x, a.y, b.x, b.y);
+    uint64_t q0 = fmul2(rg, rc), q1 = fmul2(ba, rc);
+    q0 = ffma2(ffma2(q0, n255, rg), rc, q0);
+    q1 = ffma2(ffma2(q1, n255, ba), rc, q1);
+    const float2 x = f2unpack(q0), y = f2unpack(q1);
+    return make_float4(x.x, x.y, y.x, y.y);
+}
+// RGBA8 -> v / 255 per channel: a byte permute places each byte under the 2^23 exponent.
+__device__ __forceinline__ float4 rgba8_unorm(uint32_t v) {
+    return magic_unorm(__byte_perm(v, 0x4B000000u, 0x7540), __byte_perm(v, 0x4B000000u, 0x7541),
+                       __byte_perm(v, 0x4B000000u, 0x7542), __byte_perm(v, 0x4B000000u, 0x7543));
 }
 
 // Exact bilinear blend (c8 / R-8): per channel c = fma(w3,p3, fma(w2,p2, fma(w1,p1, w0*p0))),
@@ -219,6 +221,36 @@ template <> struct WeightsOf<2> { using type = MlpWeights; };
 // entry wa*e0 + wb*e1 is one IMAD against M = (wa << 16) | wb (bits 16-31 of the
 // product), then /1, /2 or /3 as (v * {2048, 1024, 683}) >> 11 — exact for v <= 765
 // (checked exhaustively, R-9).
+// Channel products before the final >> 11 (palette value = product >> 11) and alpha.
+struct Bc1Raw {
+    uint32_t r, g, b;
+    bool opaque;
+};
+__device__ __forceinline__ Bc1Raw bc1_raw(const TexArgs &t, int x, int y) {
+    const uint2 b = __ldg(t.bc1 + ((unsigned)(y >> 2) * (unsigned)(t.W >> 2) + (unsigned)(x >> 2)));
+    const uint32_t shift = 2u * ((((unsigned)y & 3u) << 2) | ((unsigned)x & 3u));
+    const uint32_t code = (b.y >> shift) & 3u;
+    const bool four = (b.x & 0xffffu) > (b.x >> 16);
+    uint32_t rp = (b.x >> 11) & 0x001F001Fu;
+    rp = ((rp << 3) | (rp >> 2)) & 0x00FF00FFu;
+    uint32_t gp = (b.x >> 5) & 0x003F003Fu;
+    gp = ((gp << 2) | (gp >> 4)) & 0x00FF00FFu;
+    uint32_t bp = b.x & 0x001F001Fu;
+    bp = ((bp << 3) | (bp >> 2)) & 0x00FF00FFu;
+    const uint32_t i = code | (four ? 4u : 0u);
+    const uint32_t nib = (0x96410541u >> (4u * i)) & 15u;
+    const uint32_t M = ((nib & 3u) << 16) | (nib >> 2);
+    const uint32_t mul = code < 2u ? 2048u : (four ? 683u : 1024u);
+    return {((rp * M) >> 16) * mul, ((gp * M) >> 16) * mul, ((bp * M) >> 16) * mul, four || code != 3u};
+}
+// Texel (x, y) straight to v / 255 per channel (= rgba8_unorm(bc1_decode(...)) bit for bit):
+// the palette bytes land under the 2^23 exponent with one LEA.HI each, no RGBA8 packing.
+__device__ __forceinline__ float4 bc1_decode_unorm(const TexArgs &t, int x, int y) {
+    const Bc1Raw q = bc1_raw(t, x, y);
+    return magic_unorm((q.r >> 11) + 0x4B000000u, (q.g >> 11) + 0x4B000000u, (q.b >> 11) + 0x4B000000u,
+                       q.opaque ? 0x4B0000FFu : 0x4B000000u);
+}
+
 __device__ __forceinline__ uint32_t bc1_decode(const TexArgs &t, int x, int y) {
     const uint2 b = __ldg(t.bc1 + ((unsigned)(y >> 2) * (unsigned)(t.W >> 2) + (unsigned)(x >> 2)));
     const uint32_t shift = 2u * ((((unsigned)y & 3u) << 2) | ((unsigned)x & 3u));

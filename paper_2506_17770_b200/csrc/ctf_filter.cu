@@ -1493,7 +1493,7 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
     const bool produced = (int)lane < n;
     const uint32_t e = produced ? (uint32_t)fs.bit_of_rank[lane] : 0u;
     const int qx = minx + (int)(e & pmask), qy = miny + (int)(e >> lgP);
-    st_shared_f4_if(&fs.xch[lane], rgba8_unorm(bc1_decode(a.tex, qx, qy)), produced);
+    st_shared_f4_if(&fs.xch[lane], bc1_decode_unorm(a.tex, qx, qy), produced);
     if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
     __syncwarp();
     // ---- a6: gather (ranks rho_k) + blend
@@ -1647,7 +1647,7 @@ __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const F
         qx = minx;
         qy = miny;
     }
-    const float4 val = rgba8_unorm(bc1_decode(a.tex, qx, qy));
+    const float4 val = bc1_decode_unorm(a.tex, qx, qy);
     if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
     if (exact) {
         if (produced) fs.xch[lane] = val;
