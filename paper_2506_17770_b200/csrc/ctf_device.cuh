@@ -251,6 +251,32 @@ __device__ __forceinline__ float4 bc1_decode_unorm(const TexArgs &t, int x, int 
                        q.opaque ? 0x4B0000FFu : 0x4B000000u);
 }
 
+// The same with the per-index constants from a shared-memory table (one LDS.128 instead of
+// ~10 instructions of table-in-register arithmetic): entry i = code | four << 2 holds
+// {M, mul, alpha bits under 2^23, 0}; fill it with bc1_lut_entry(i).
+__device__ __forceinline__ uint4 bc1_lut_entry(uint32_t i) {
+    const uint32_t code = i & 3u;
+    const bool four = i >= 4u;
+    const uint32_t nib = (0x96410541u >> (4u * i)) & 15u;
+    return make_uint4(((nib & 3u) << 16) | (nib >> 2), code < 2u ? 2048u : (four ? 683u : 1024u),
+                      (four || code != 3u) ? 0x4B0000FFu : 0x4B000000u, 0u);
+}
+__device__ __forceinline__ float4 bc1_decode_unorm_lut(const TexArgs &t, int x, int y, const uint4 *lut) {
+    const uint2 b = __ldg(t.bc1 + ((unsigned)(y >> 2) * (unsigned)(t.W >> 2) + (unsigned)(x >> 2)));
+    const uint32_t shift = 2u * ((((unsigned)y & 3u) << 2) | ((unsigned)x & 3u));
+    const uint32_t code = (b.y >> shift) & 3u;
+    const bool four = (b.x & 0xffffu) > (b.x >> 16);
+    const uint4 e = lut[code | (four ? 4u : 0u)];
+    uint32_t rp = (b.x >> 11) & 0x001F001Fu;
+    rp = ((rp << 3) | (rp >> 2)) & 0x00FF00FFu;
+    uint32_t gp = (b.x >> 5) & 0x003F003Fu;
+    gp = ((gp << 2) | (gp >> 4)) & 0x00FF00FFu;
+    uint32_t bp = b.x & 0x001F001Fu;
+    bp = ((bp << 3) | (bp >> 2)) & 0x00FF00FFu;
+    return magic_unorm((((rp * e.x) >> 16) * e.y >> 11) + 0x4B000000u, (((gp * e.x) >> 16) * e.y >> 11) + 0x4B000000u,
+                       (((bp * e.x) >> 16) * e.y >> 11) + 0x4B000000u, e.z);
+}
+
 __device__ __forceinline__ uint32_t bc1_decode(const TexArgs &t, int x, int y) {
     const uint2 b = __ldg(t.bc1 + ((unsigned)(y >> 2) * (unsigned)(t.W >> 2) + (unsigned)(x >> 2)));
     const uint32_t shift = 2u * ((((unsigned)y & 3u) << 2) | ((unsigned)x & 3u));

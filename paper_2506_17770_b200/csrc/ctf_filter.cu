@@ -1433,7 +1433,8 @@ __device__ __forceinline__ bool wave_magnified(uint2 gr, bool has_grad) {
 }
 
 template <bool DBG>
-__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float2 uv, uint2 gr, bool has_grad) {
+__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, const uint4 *lut, float2 uv, uint2 gr,
+                                             bool has_grad) {
     const unsigned lane = lane_id(), lt = lanemask_lt(), lanebit = 1u << lane;
     LeanOut o;
     o.color = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1493,7 +1494,7 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, float
     const bool produced = (int)lane < n;
     const uint32_t e = produced ? (uint32_t)fs.bit_of_rank[lane] : 0u;
     const int qx = minx + (int)(e & pmask), qy = miny + (int)(e >> lgP);
-    st_shared_f4_if(&fs.xch[lane], bc1_decode_unorm(a.tex, qx, qy), produced);
+    st_shared_f4_if(&fs.xch[lane], bc1_decode_unorm_lut(a.tex, qx, qy, lut), produced);
     if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
     __syncwarp();
     // ---- a6: gather (ranks rho_k) + blend
@@ -1715,6 +1716,9 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
 template <bool DBG, bool GRAD, bool FORCE>
 __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_kernel(const KArgs a) {
     __shared__ FastSmem fsm[kWarps];
+    __shared__ uint4 bc1_lut[8];   // BC1 per-index constants (bc1_lut_entry)
+    if (threadIdx.x < 8) bc1_lut[threadIdx.x] = bc1_lut_entry(threadIdx.x);
+    __syncthreads();
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     FastSmem &fs = fsm[warp];
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
@@ -1757,7 +1761,7 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
             const unsigned A = __ballot_sync(FULL, active);
             uint32_t rec;
             if (!FORCE && A == FULL) {
-                const LeanOut o = lean_wave<DBG>(a, fs, uv, gr, GRAD);
+                const LeanOut o = lean_wave<DBG>(a, fs, bc1_lut, uv, gr, GRAD);
                 rec = o.rec;
                 if (o.done) {
                     st_stream_f4(a.out + pix, o.color);
