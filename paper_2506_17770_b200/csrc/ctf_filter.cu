@@ -1570,6 +1570,7 @@ __device__ __forceinline__ WMaskN<NW> reduce_wn(int K, uint32_t t, uint32_t pat,
 
 struct FbSmem {
     float4 xch[128];          // exact: rank -> value; fallback: window position -> value
+    uint4 lut[8];             // BC1 per-index constants (bc1_lut_entry), per warp
     uint8_t bit_of_rank[32];  // rank -> window bit (0..127)
 };
 
@@ -1648,7 +1649,7 @@ __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const F
         qx = minx;
         qy = miny;
     }
-    const float4 val = bc1_decode_unorm(a.tex, qx, qy);
+    const float4 val = bc1_decode_unorm_lut(a.tex, qx, qy, fs.lut);
     if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
     if (exact) {
         if (produced) fs.xch[lane] = val;
@@ -1841,6 +1842,10 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : CTF_REST
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     WarpSmem &s = smem[(FALLBACK && !CTF_REST_MERGED) ? 0 : warp];
     FbSmem &fs = fsm[FALLBACK ? warp : 0];
+    if (FALLBACK) {
+        if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
+        __syncwarp();
+    }
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     // one marked wave: lean fallback (FALLBACK) or the general path
     auto process = [&](unsigned wi, float2 uv, uint2 gr, unsigned fr, int px, int py, bool inframe, unsigned pix) {
