@@ -281,3 +281,22 @@ def test_workspace_lists_equal_record_scan(ctf, fb, fl):
     import oracle
     o = oracle.filter_frame(tex, uv, g, 3, fb, fl, seed=11)
     np.testing.assert_array_equal(res[0][1], o["rec"])
+
+
+@pytest.mark.parametrize("center,mag,theta", [((0.0, 0.0), 1.1, 20.0), ((1.0, 0.5), 1.3, 45.0),
+                                              ((0.5, 1.0), 0.45, 10.0), ((0.0, 1.0), 2.5, 70.0)])
+def test_full_waves_at_texture_borders(ctf, center, mag, theta):
+    """FULL waves (every lane covered) straddling the texture border: clamp-duplicate corners
+    and merged weights in the lean exact / fallback kernels (n > 32 at m ~ 1, 128-bit windows
+    at m < 1), all fallbacks, with and without the work-list workspace."""
+    tex = bc1_tex(64, 64, 9, "image")
+    uv, g = synthetic.rotated_quad(96, 48, 64, 64, mag, theta, center=center, jitter_seed=2)
+    for mode, fb, fl in [(3, 0, 0), (3, 1, 0), (3, 2, 0), (3, 3, 0), (3, 3, 2), (3, 2, 2)]:
+        o = run_oracle(tex, uv, g, mode, fb, fl, seed=5, frame_index=3)
+        gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=5, frame_index=3)
+        assert_parity(gg, o, f"c={center} m={mag} fb={fb} flags={fl}")
+        dt = to_dev_tex(ctf, tex)
+        out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, fl, 5, 3,
+                                    workspace=None)
+        assert np.array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), gg["out"].view(np.uint32))
