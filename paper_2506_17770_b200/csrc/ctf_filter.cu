@@ -149,15 +149,12 @@ __device__ __forceinline__ Foot footprint2(float2 uv, const KArgs &a) {
     f.xb = min(x0 + 1, a.Wm1);
     f.ya = max(y0, 0);
     f.yb = min(y0 + 1, a.Hm1);
-    // {1 - s, s} and {1 - t, t} (one rounding each, as R-3), then the four products
-    const uint64_t S = ffma2(f2pack(f.s, f.s), f2pack(-1.0f, 1.0f), f2pack(1.0f, 0.0f));
-    const uint64_t T = ffma2(f2pack(f.t, f.t), f2pack(-1.0f, 1.0f), f2pack(1.0f, 0.0f));
-    const float2 tt = f2unpack(T);
-    const float2 w01 = f2unpack(fmul2(S, f2pack(tt.x, tt.x))), w23 = f2unpack(fmul2(S, f2pack(tt.y, tt.y)));
-    f.w[0] = w01.x;
-    f.w[1] = w01.y;
-    f.w[2] = w23.x;
-    f.w[3] = w23.y;
+    // {1 - s, 1 - t} in one FADD2 (one rounding each, as R-3), then the four products
+    const float2 om = f2unpack(fsub2(f2pack(1.0f, 1.0f), st));
+    f.w[0] = __fmul_rn(om.x, om.y);
+    f.w[1] = __fmul_rn(f.s, om.y);
+    f.w[2] = __fmul_rn(om.x, f.t);
+    f.w[3] = __fmul_rn(f.s, f.t);
     return f;
 }
 
