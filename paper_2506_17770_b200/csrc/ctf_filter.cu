@@ -1292,7 +1292,8 @@ constexpr uint32_t kSlowMark = 0xFFFFFFFFu;   // neither is a COLLAB record (pat
 constexpr uint32_t kFbMark = 0xFFFFFFFEu;
 
 struct FastSmem {
-    float4 xch[64];           // exact: rank -> produced value; fallback: window position -> produced value
+    float4 xch[32];           // rank -> produced value (exact waves, n <= 32)
+    uint4 lut[8];             // BC1 per-index constants (bc1_lut_entry), per warp
     uint8_t bit_of_rank[32];  // rank -> window bit (0..63)
 };
 
@@ -1714,11 +1715,10 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
 template <bool DBG, bool GRAD, bool FORCE>
 __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_kernel(const KArgs a) {
     __shared__ FastSmem fsm[kWarps];
-    __shared__ uint4 bc1_lut[8];   // BC1 per-index constants (bc1_lut_entry)
-    if (threadIdx.x < 8) bc1_lut[threadIdx.x] = bc1_lut_entry(threadIdx.x);
-    __syncthreads();
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     FastSmem &fs = fsm[warp];
+    if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
+    __syncwarp();
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned per_warp = a.ipc / kWarps;
     for (unsigned k = warp;; k += kWarps) {
@@ -1759,7 +1759,7 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
             const unsigned A = __ballot_sync(FULL, active);
             uint32_t rec;
             if (!FORCE && A == FULL) {
-                const LeanOut o = lean_wave<DBG>(a, fs, bc1_lut, uv, gr, GRAD);
+                const LeanOut o = lean_wave<DBG>(a, fs, fs.lut, uv, gr, GRAD);
                 rec = o.rec;
                 if (o.done) {
                     st_stream_f4(a.out + pix, o.color);
