@@ -1298,7 +1298,7 @@ struct FastSmem {
 };
 
 #ifndef CTF_FAST_MINB
-#define CTF_FAST_MINB 6  // resident CTAs per SM (40 registers, no spills)
+#define CTF_FAST_MINB 7  // resident CTAs per SM (32 registers, no spills)
 #endif
 
 // 64-bit window masks held as two words (hi = 0 for a 32-bit window)
