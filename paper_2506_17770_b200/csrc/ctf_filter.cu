@@ -1131,8 +1131,18 @@ __device__ __forceinline__ WaveOut wave_general(const KArgs &a, const typename W
                 for (int k = 0; k < 4; ++k) src[k] = active ? (int)s.lane_of_rank[rho[k] & 31] : (int)lane;
             }
             Texel<FMT> p[4];
+#if CTF_MLP_TC
+            if constexpr (kBatchMlp) {
+                // the tensor-core decoder left every lane's texel in its scratch row: one
+                // LDS.128 per corner instead of four 32-bit shuffles
 #pragma unroll
-            for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
+                for (int k = 0; k < 4; ++k) p[k].v = mc.tsc->out[src[k]];
+            } else
+#endif
+            {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) p[k] = Texel<FMT>::shfl(val, src[k]);
+            }
             if (active) color = blend4<FMT>(p, f.w);
             if (DBG && a.dbg_unread) {
                 unsigned bad = 0;

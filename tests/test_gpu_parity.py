@@ -300,3 +300,27 @@ def test_full_waves_at_texture_borders(ctf, center, mag, theta):
                                     workspace=None)
         assert np.array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
         assert np.array_equal(out.cpu().numpy().view(np.uint32), gg["out"].view(np.uint32))
+
+
+def test_exact_waves_with_128bit_windows(ctf):
+    """FULL exact waves whose footprint AABB only fits a 16x8 or 32x4 window (n <= 32): they
+    leave the lean exact kernel and take the fallback kernel's exact branch (4-word masks)."""
+    W = H = 64
+    tex = bc1_tex(W, H, 6, "image")
+    uv = np.zeros((8, 24, 2), np.float32)
+    lx = np.arange(8)
+    for wx, (step, row) in enumerate([(2, 5.0), (4, 20.0), (3, 40.0)]):   # 16-wide, 32-wide, 24-wide
+        for ly in range(4):
+            uv[ly, wx * 8 + lx, 0] = (step * lx + 0.5) / W
+            uv[ly, wx * 8 + lx, 1] = (row + 0.25) / H
+            uv[4 + ly, wx * 8 + lx, 0] = (step * lx + 0.5 + ly % 2) / W       # two rows of footprints
+            uv[4 + ly, wx * 8 + lx, 1] = (row + 0.25 + (ly // 2) * 3.0) / H
+    import oracle
+    for mode, fb, fl in [(3, 3, 0), (3, 0, 0), (3, 2, 2)]:
+        o = run_oracle(tex, uv, None, mode, fb, fl, seed=9)
+        gg = run_gpu(ctf, tex, uv, None, mode, fb, fl, seed=9)
+        assert_parity(gg, o, f"fb={fb} flags={fl}")
+    o = oracle.filter_frame(tex, uv, None, 3, 3, 0, 9)
+    n = (o["rec"] >> 8) & 255
+    path = (o["rec"] >> 22) & 7
+    assert (path[0] == 0).all() and (n[0] == 32).all()   # the first wave row is exact with n = 32
