@@ -124,7 +124,7 @@ typedef struct {
     int32_t max_evals;     /* exact-path evaluations per lane: 0 or 1, or 2 (bicubic only)  */
     void *workspace_dev;   /* optional device scratch (ABI 4), >= ctf_filter_workspace_bytes()
                               bytes, 16-byte aligned, owned by the caller, contents need no
-                              initialisation; used by the BC1 COLLAB bilinear path for
+                              initialisation; used by the COLLAB bilinear path for
                               compact work lists of its fallback / general waves (no record
                               scans, balanced second passes).  NULL: the record buffer doubles
                               as the work list.  Results are identical either way.  Calls
@@ -232,11 +232,11 @@ size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames);
 /*
  * Kernel launches one call above issues (for launch accounting): format / mode / filter
  * as in ctf_texture / ctf_params, `frames` frames, `batched` != 0 for ctf_filter_batch
- * (one pass over all frames) else ctf_filter_frame once per frame.  The BC1 COLLAB
- * bilinear path is three kernels per pass (the lean exact kernel; the lean fallback
- * kernel over the full waves it left; the general path over partial waves and windows
- * wider than 8x8); every other path is one.  Returns -1 for an invalid format / mode /
- * filter.
+ * (one pass over all frames) else ctf_filter_frame once per frame.  The COLLAB bilinear
+ * path is three kernels per pass for BC1 (the lean exact kernel; the lean fallback kernel
+ * over the full waves it left; the general path over partial waves and windows wider than
+ * 8x8) and two for the latent MLP (lean exact kernel + general path); every other path is
+ * one.  Returns -1 for an invalid format / mode / filter.
  */
 int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int batched);
 int ctf_abi_version(void);

@@ -1274,8 +1274,7 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : 
     }
 }
 
-#if CTF_TU_FMT == 1
-// ------------------------------------------- BC1 COLLAB (List) kernel: the lean path
+// ---------------------------------------------- COLLAB (List) kernels: the lean path
 // On a magnified frame nearly every wave is FULL (32 active lanes) with a footprint
 // bounding box that fits an 8x4 / 4x8 window (one 32-bit mask) or an 8x8 window (two
 // words).  Those waves run the straight-line code below, exact or fallback:
@@ -1440,9 +1439,12 @@ __device__ __forceinline__ bool wave_magnified(uint2 gr, bool has_grad) {
     return has_grad && __all_sync(FULL, mag_lane);
 }
 
-template <bool DBG>
-__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, const uint4 *lut, float2 uv, uint2 gr,
-                                             bool has_grad) {
+// FMT_MLP: the wave's produced texels go through the tensor-core decoder together
+// (mlp_decode_tc, rows = lanes); its fallback and 128-bit-window waves go to the general
+// kernel (kSlowMark) — there is no lean fallback for the latent-MLP format.
+template <bool DBG, int FMT>
+__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, const uint4 *lut, const MlpCtx &mc,
+                                             float2 uv, uint2 gr, bool has_grad) {
     const unsigned lane = lane_id(), lt = lanemask_lt(), lanebit = 1u << lane;
     LeanOut o;
     o.color = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1463,6 +1465,10 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, const
     else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; lgP = 2u; }   // 4x8
     else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                        // 8x8
     if (K == 0) {   // a 128-bit window (fallback kernel) or none (general kernel)
+        if (FMT != FMT_BC1) {
+            o.rec = kSlowMark;
+            return o;
+        }
         const bool w128 = __all_sync(FULL, dx < 16u && dy < 8u) || __all_sync(FULL, dx < 8u && dy < 16u) ||
                           __all_sync(FULL, dx < 32u && dy < 4u);
         o.rec = w128 ? kFbMark : kSlowMark;
@@ -1493,7 +1499,10 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, const
         st_shared_u8_if(fs.bit_of_rank + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
     }
     // ---- a4: exact iff n <= a = 32 (always for a 32-bit window)
-    if (n > 32) return o;   // fallback kernel
+    if (n > 32) {   // fallback kernel (BC1) / general kernel (latent MLP)
+        if (FMT != FMT_BC1) o.rec = kSlowMark;
+        return o;
+    }
     o.done = true;
     __syncwarp();
     // ---- a5: lane r < n produces U[r] (h(r, A) = r); one decode site, fp32 once
@@ -1502,11 +1511,19 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, const
     const bool produced = (int)lane < n;
     const uint32_t e = produced ? (uint32_t)fs.bit_of_rank[lane] : 0u;
     const int qx = minx + (int)(e & pmask), qy = miny + (int)(e >> lgP);
-    st_shared_f4_if(&fs.xch[lane], bc1_decode_unorm_lut(a.tex, qx, qy, lut), produced);
+    const float4 *xv;   // rank -> produced value
+    if constexpr (FMT == FMT_BC1) {
+        st_shared_f4_if(&fs.xch[lane], bc1_decode_unorm_lut(a.tex, qx, qy, lut), produced);
+        xv = fs.xch;
+    } else {
+        // rows = lanes = ranks; the decoder leaves every row's texel in its scratch
+        mlp_decode_tc(a.tex, *mc.tw, *mc.tsc, produced, qx, qy, lane_id());
+        xv = mc.tsc->out;
+    }
     if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
     __syncwarp();
     // ---- a6: gather (ranks rho_k) + blend
-    const float4 p[4] = {fs.xch[r0], fs.xch[r0 + (int)dxs], fs.xch[r2], fs.xch[r2 + (int)dxs]};
+    const float4 p[4] = {xv[r0], xv[r0 + (int)dxs], xv[r2], xv[r2 + (int)dxs]};
     o.color = blend4f(p, f.w);
     o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
     if (DBG && a.dbg_unread) {
@@ -1722,13 +1739,24 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
 
 // GRAD: grad != NULL (magnified class); FORCE: CTF_FLAG_FORCE_FALLBACK (every live wave
 // goes to the rest kernel) — compile-time, so the hot loop tests neither.
-template <bool DBG, bool GRAD, bool FORCE>
-__global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_kernel(const KArgs a) {
+template <bool DBG, bool GRAD, bool FORCE, int FMT>
+__global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? CTF_FAST_MINB : CTF_MLP_COLLAB_MINB)
+    ctf_collab_lean_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ FastSmem fsm[kWarps];
+    extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent MLP: TcWeights + per-warp TcScratch
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     FastSmem &fs = fsm[warp];
-    if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
-    __syncwarp();
+    MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
+    if constexpr (FMT == FMT_BC1) {
+        if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
+        __syncwarp();
+    } else {
+        TcWeights &tw = *reinterpret_cast<TcWeights *>(dyn_smem);
+        fill_tc_weights(mw, tw);
+        mc.tw = &tw;
+        mc.tsc = &reinterpret_cast<TcScratch *>(dyn_smem + sizeof(TcWeights))[warp];
+        __syncthreads();
+    }
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned per_warp = a.ipc / kWarps;
     for (unsigned k = warp;; k += kWarps) {
@@ -1769,7 +1797,7 @@ __global__ void __launch_bounds__(kWarps * 32, CTF_FAST_MINB) ctf_collab_bc1_ker
             const unsigned A = __ballot_sync(FULL, active);
             uint32_t rec;
             if (!FORCE && A == FULL) {
-                const LeanOut o = lean_wave<DBG>(a, fs, fs.lut, uv, gr, GRAD);
+                const LeanOut o = lean_wave<DBG, FMT>(a, fs, fs.lut, mc, uv, gr, GRAD);
                 rec = o.rec;
                 if (o.done) {
                     st_stream_f4(a.out + pix, o.color);
@@ -1841,17 +1869,28 @@ __device__ __forceinline__ WaveOut general_wave(const KArgs &a, WarpSmem &s, flo
                                                        frame);
     }
 }
-template <bool DBG, bool FALLBACK>
-__global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : CTF_REST_MINB)
-    ctf_collab_bc1_rest_kernel(const KArgs a, unsigned nrec) {
+template <bool DBG, bool FALLBACK, int FMT>
+__global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == FMT_BC1 ? CTF_REST_MINB : CTF_MLP_COLLAB_MINB))
+    ctf_collab_rest_kernel(const KArgs a, unsigned nrec, const typename WeightsOf<FMT>::type mw) {
+    static_assert(FMT == FMT_BC1 || !FALLBACK, "no lean fallback for the latent-MLP format");
+    if (a.lists && a.lists[FALLBACK ? 0 : 1] == 0u) return;   // empty work list (same value in every thread)
     __shared__ WarpSmem smem[(FALLBACK && !CTF_REST_MERGED) ? 1 : kWarps];
     __shared__ FbSmem fsm[FALLBACK ? kWarps : 1];
+    extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent MLP: TcWeights + per-warp TcScratch
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     WarpSmem &s = smem[(FALLBACK && !CTF_REST_MERGED) ? 0 : warp];
     FbSmem &fs = fsm[FALLBACK ? warp : 0];
+    MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
     if (FALLBACK) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
         __syncwarp();
+    }
+    if constexpr (FMT != FMT_BC1) {
+        TcWeights &tw = *reinterpret_cast<TcWeights *>(dyn_smem);
+        fill_tc_weights(mw, tw);
+        mc.tw = &tw;
+        mc.tsc = &reinterpret_cast<TcScratch *>(dyn_smem + sizeof(TcWeights))[warp];
+        __syncthreads();
     }
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     // one marked wave: lean fallback (FALLBACK) or the general path
@@ -1872,7 +1911,11 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : CTF_REST
                 }
                 return;
             }
-            const WaveOut go = general_wave<DBG, FALLBACK && CTF_REST_MERGED>(a, s, uv, gr, active, A, px, py, frame);
+            WaveOut go;
+            if constexpr (FMT == FMT_BC1)
+                go = general_wave<DBG, FALLBACK && CTF_REST_MERGED>(a, s, uv, gr, active, A, px, py, frame);
+            else
+                go = wave_general<FMT, MODE_COLLAB, DBG>(a, mw, s, mc, uv, gr, active, A, __popc(A), px, py, frame);
             o.color = go.color;
             o.rec = go.rec;
             o.prod = go.prod;
@@ -1997,7 +2040,6 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : CTF_REST
       }
     }
 }
-#endif
 
 template <int FMT, int MODE, bool DBG>
 static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
@@ -2051,60 +2093,87 @@ static cudaError_t launch_one(KArgs k, const typename WeightsOf<FMT>::type &mw, 
     return cudaGetLastError();
 }
 
-#if CTF_TU_FMT == 1
 #ifndef CTF_FAST
-#define CTF_FAST 1  // BC1 COLLAB List runs the lean kernel (0: the general kernel, for A/B timing)
+#define CTF_FAST 1  // COLLAB List runs the lean kernels (0: the general kernel, for A/B timing)
 #endif
-// same work split as the general BC1 kernel
-template <bool DBG>
-static cudaError_t launch_fast(KArgs k, cudaStream_t stream) {
+// dynamic shared memory of the latent-MLP kernels (tensor-core weights + per-warp scratch),
+// with a carveout that holds the register-limited number of CTAs
+template <typename Kern>
+static cudaError_t mlp_smem_setup(Kern kern, size_t dyn, int dev) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    int max_smem = 0;
+    e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    const int regs_ctas = 65536 / (fa.numRegs * kWarps * 32);
+    const size_t per_cta = dyn + fa.sharedSizeBytes + 1024;   // + the driver's reserved 1 KB
+    const int pct = (int)((100 * per_cta * (size_t)(regs_ctas > 0 ? regs_ctas : 1) + max_smem - 1) / max_smem);
+    return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+}
+
+// The lean COLLAB (List) pass: the lean exact kernel, then (BC1) the lean fallback kernel
+// and the general kernel over the waves it marked / appended to the work lists; (latent
+// MLP) the general kernel over them.  Same work split as the general BC1 kernel.
+template <int FMT, bool DBG>
+static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
     if (k.lists) {   // work-list counters (the lists need no initialisation)
         const cudaError_t e0 = cudaMemsetAsync(k.lists, 0, 2 * sizeof(uint32_t), stream);
         if (e0 != cudaSuccess) return e0;
     }
     const bool grad = k.grad != nullptr, force = (k.flags & FLAG_FORCE_FALLBACK) != 0;
-    auto kern = grad ? (force ? ctf_collab_bc1_kernel<DBG, true, true> : ctf_collab_bc1_kernel<DBG, true, false>)
-                     : (force ? ctf_collab_bc1_kernel<DBG, false, true> : ctf_collab_bc1_kernel<DBG, false, false>);
+    auto kern = grad ? (force ? ctf_collab_lean_kernel<DBG, true, true, FMT> : ctf_collab_lean_kernel<DBG, true, false, FMT>)
+                     : (force ? ctf_collab_lean_kernel<DBG, false, true, FMT> : ctf_collab_lean_kernel<DBG, false, false, FMT>);
+    const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0);
+    if (dyn > 0 && (e = mlp_smem_setup(kern, dyn, dev)) != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, dyn);
     if (e != cudaSuccess) return e;
     const long long slots = (long long)sms * (per_sm > 0 ? per_sm : 1);
-    long long ipw = ((long long)k.nchunks + slots * kWarps * CTF_BC1_ROUNDS / 2) / (slots * kWarps * CTF_BC1_ROUNDS);
-    ipw = ipw < 1 ? 1 : ipw > CTF_BC1_MAX_IPW ? CTF_BC1_MAX_IPW : ipw;
+    long long ipw;
+    if (FMT == FMT_BC1) {   // many short-lived CTAs; the block scheduler balances
+        ipw = ((long long)k.nchunks + slots * kWarps * CTF_BC1_ROUNDS / 2) / (slots * kWarps * CTF_BC1_ROUNDS);
+        ipw = ipw < 1 ? 1 : ipw > CTF_BC1_MAX_IPW ? CTF_BC1_MAX_IPW : ipw;
+    } else {                // latent MLP: one CTA per slot (each CTA stages the MLP weights once)
+        ipw = ((long long)k.nchunks + slots * kWarps - 1) / (slots * kWarps);
+        if (ipw < 1) ipw = 1;
+    }
     k.ipc = (unsigned)(ipw * kWarps);
     long long grid = ((long long)k.nchunks + k.ipc - 1) / k.ipc;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kWarps * 32, 0, stream>>>(k);
+    kern<<<(unsigned)grid, kWarps * 32, dyn, stream>>>(k, mw);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // the marked waves: lean fallback kernel, then the general kernel; each at most one
-    // resident wave of CTAs
+    // the marked waves, each pass at most one resident wave of CTAs
     const unsigned nrec = (unsigned)((long long)k.wpf * (k.nchunks / (unsigned)k.cpf));
     const long long groups = ((long long)nrec + 31) / 32;
-    for (int pass = 0; pass < (CTF_REST_MERGED ? 1 : 2); ++pass) {
-        auto rest = pass == 0 ? ctf_collab_bc1_rest_kernel<DBG, true> : ctf_collab_bc1_rest_kernel<DBG, false>;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rest, kWarps * 32, 0);
+    const int first = FMT == FMT_BC1 ? 0 : 1;   // pass 0: lean fallback (BC1); pass 1: general
+    for (int pass = first; pass < (CTF_REST_MERGED ? 1 : 2); ++pass) {
+        auto rest = ctf_collab_rest_kernel<DBG, false, FMT>;
+        if constexpr (FMT == FMT_BC1)
+            if (pass == 0) rest = ctf_collab_rest_kernel<DBG, true, FMT_BC1>;
+        if (dyn > 0 && (e = mlp_smem_setup(rest, dyn, dev)) != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rest, kWarps * 32, dyn);
         if (e != cudaSuccess) return e;
         long long g2 = (long long)sms * (per_sm > 0 ? per_sm : 1);
         if (g2 * kWarps > groups) g2 = (groups + kWarps - 1) / kWarps;
-        rest<<<(unsigned)(g2 < 1 ? 1 : g2), kWarps * 32, 0, stream>>>(k, nrec);
+        rest<<<(unsigned)(g2 < 1 ? 1 : g2), kWarps * 32, dyn, stream>>>(k, nrec, mw);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
 }
-#endif
 
 template <int FMT, int MODE>
 static cudaError_t launch_dbg(const KArgs &k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
-#if CTF_TU_FMT == 1
-    if (CTF_FAST && FMT == FMT_BC1 && MODE == MODE_COLLAB && k.variant == VAR_LIST)
-        return (k.flags & FLAG_DEBUG) ? launch_fast<true>(k, stream) : launch_fast<false>(k, stream);
-#endif
+    if (CTF_FAST && MODE == MODE_COLLAB && k.variant == VAR_LIST)
+        return (k.flags & FLAG_DEBUG) ? launch_fast<FMT, true>(k, mw, stream) : launch_fast<FMT, false>(k, mw, stream);
     return (k.flags & FLAG_DEBUG) ? launch_one<FMT, MODE, true>(k, mw, stream)
                                   : launch_one<FMT, MODE, false>(k, mw, stream);
 }
@@ -2124,7 +2193,8 @@ static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::typ
 #endif
 #if CTF_TU_FMT == 1
 int launches_per_pass(int fmt, int mode, int filter) {
-    return (CTF_FAST && fmt == FMT_BC1 && mode == MODE_COLLAB && filter == 0) ? (CTF_REST_MERGED ? 2 : 3) : 1;
+    if (!CTF_FAST || mode != MODE_COLLAB || filter != 0) return 1;
+    return fmt == FMT_BC1 ? (CTF_REST_MERGED ? 2 : 3) : 2;   // latent MLP: lean exact + general
 }
 
 cudaError_t launch_filter_bc1(const LaunchArgs &a, cudaStream_t stream) {

@@ -155,9 +155,9 @@ def num_waves(wf: int, hf: int) -> int:
 
 
 def workspace_for(tex: Texture, mode: int, filt: int, wf: int, hf: int, frames: int, device) -> torch.Tensor | None:
-    """Device scratch for ctf_params.workspace_dev (the BC1 COLLAB bilinear work lists), or None
+    """Device scratch for ctf_params.workspace_dev (the COLLAB bilinear work lists), or None
     where the path does not use one."""
-    if tex.fmt != FMT_BC1 or mode != MODE_COLLAB or filt != FILTER_BILINEAR:
+    if mode != MODE_COLLAB or filt != FILTER_BILINEAR:
         return None
     nbytes = load_library().ctf_filter_workspace_bytes(wf, hf, frames)
     return torch.empty(nbytes, device=device, dtype=torch.uint8)

@@ -76,5 +76,6 @@ def test_validation_errors_without_gpu():
     lib.ctf_launches_per_call.argtypes = [ctypes.c_int32] * 4 + [ctypes.c_int]
     # BC1 COLLAB bilinear: exact, fallback and general kernels per pass; everything else one kernel
     assert lib.ctf_launches_per_call(1, 3, 0, 64, 1) == 3 and lib.ctf_launches_per_call(1, 3, 0, 64, 0) == 192
-    assert lib.ctf_launches_per_call(1, 0, 0, 64, 1) == 1 and lib.ctf_launches_per_call(2, 3, 0, 8, 0) == 8
+    assert lib.ctf_launches_per_call(1, 0, 0, 64, 1) == 1 and lib.ctf_launches_per_call(2, 3, 0, 8, 0) == 16
+    assert lib.ctf_launches_per_call(2, 4, 0, 8, 1) == 1   # Box: the general kernel
     assert lib.ctf_launches_per_call(3, 3, 0, 1, 1) == -1
