@@ -1750,18 +1750,32 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? CTF_FAST_MINB : 
     if constexpr (FMT == FMT_BC1) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
         __syncwarp();
-    } else {
+    }
+    __shared__ unsigned s_next;   // latent MLP: the CTA's warps claim its items dynamically
+    if constexpr (FMT != FMT_BC1) {
         TcWeights &tw = *reinterpret_cast<TcWeights *>(dyn_smem);
         fill_tc_weights(mw, tw);
         mc.tw = &tw;
         mc.tsc = &reinterpret_cast<TcScratch *>(dyn_smem + sizeof(TcWeights))[warp];
+        if (threadIdx.x == 0) s_next = kWarps;
         __syncthreads();
     }
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned per_warp = a.ipc / kWarps;
-    for (unsigned k = warp;; k += kWarps) {
-        const unsigned c = (blockIdx.x * kWarps + (k % kWarps)) + (k / kWarps) * gridDim.x * kWarps;
-        if (k / kWarps >= per_warp || c >= a.nchunks) break;
+    for (unsigned k = warp;;) {
+        // BC1: warp (b, w) takes items b*kWarps + w + j*gridDim.x*kWarps (static); latent MLP:
+        // CTA b owns items b + k*gridDim.x and its warps claim k from a shared counter
+        // (decode cost varies with n: dynamic claims balance the warps of a CTA)
+        const unsigned c = FMT == FMT_BC1 ? (blockIdx.x * kWarps + (k % kWarps)) + (k / kWarps) * gridDim.x * kWarps
+                                          : blockIdx.x + k * gridDim.x;
+        if ((FMT == FMT_BC1 ? k / kWarps >= per_warp : k >= a.ipc) || c >= a.nchunks) break;
+        if constexpr (FMT == FMT_BC1) {
+            k += kWarps;
+        } else {
+            unsigned nx = 0u;
+            if (lane == 0) nx = atomicAdd(&s_next, 1u);
+            k = __shfl_sync(FULL, nx, 0);
+        }
         const int fr = (int)(c / (unsigned)a.cpf);
         const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
         const int wy = rr / a.cpr;
