@@ -803,6 +803,14 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
                  : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// four 8x8 b16 matrices from shared memory, lane i addressing row i % 8 of matrix i / 8;
+// register j of lane t = matrix j, row t / 4, columns 2 (t % 4), +1: the mma fragment layout
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void *p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"((unsigned)__cvta_generic_to_shared(p))
+                 : "memory");
+}
 // d += A * B with A = Ah + Al, B = Bh + Bl, dropping Al * Bl (3xFP16)
 __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t bh0,
                                      uint32_t bh1, uint32_t bl0, uint32_t bl1) {
@@ -860,16 +868,20 @@ __device__ __forceinline__ float4 mlp_decode_tc(const TexArgs &t, const TcWeight
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
         if (mt >= nmt) break;
-        const int r0 = 16 * mt + g;
-        uint32_t ah[4] = {sm.ah[r0][q], sm.ah[r0 + 8][q], sm.ah[r0][q + 4], sm.ah[r0 + 8][q + 4]};
-        uint32_t al[4] = {sm.al[r0][q], sm.al[r0 + 8][q], sm.al[r0][q + 4], sm.al[r0 + 8][q + 4]};
+        // fragments by ldmatrix: lane i addresses row (i & 7) of matrix mi = i >> 3
+        const int mi = (int)(lane >> 3), mr = (int)(lane & 7);
+        uint32_t ah[4], al[4];   // rows 16mt + (mi & 1) * 8 + mr, words (mi >> 1) * 4 ..
+        ldsm_x4(ah, &sm.ah[16 * mt + (mi & 1) * 8 + mr][(mi >> 1) * 4]);
+        ldsm_x4(al, &sm.al[16 * mt + (mi & 1) * 8 + mr][(mi >> 1) * 4]);
         // layer 1: 12 (16) -> 32, ReLU; C fragments become layer-2 A fragments (k-tiles of 16)
         uint32_t a2h[2][4], a2l[2][4];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
-            const int n = 8 * nt + g, c = 8 * nt + 2 * q;
+            const int c = 8 * nt + 2 * q;
             float d[4] = {tw.b1[c], tw.b1[c + 1], tw.b1[c], tw.b1[c + 1]};
-            mma3(d, ah, al, tw.w1h[n][q], tw.w1h[n][q + 4], tw.w1l[n][q], tw.w1l[n][q + 4]);
+            uint32_t b[4];   // {hi b0, hi b1, lo b0, lo b1} of W1 rows 8nt..8nt+7
+            ldsm_x4(b, &((mi & 2) ? tw.w1l : tw.w1h)[8 * nt + mr][(mi & 1) * 4]);
+            mma3(d, ah, al, b[0], b[1], b[2], b[3]);
             const int kt = nt >> 1, hi = nt & 1;
             split2(fmaxf(d[0], 0.f), fmaxf(d[1], 0.f), a2h[kt][2 * hi], a2l[kt][2 * hi]);
             split2(fmaxf(d[2], 0.f), fmaxf(d[3], 0.f), a2h[kt][2 * hi + 1], a2l[kt][2 * hi + 1]);
@@ -878,12 +890,14 @@ __device__ __forceinline__ float4 mlp_decode_tc(const TexArgs &t, const TcWeight
         uint32_t a3h[2][4], a3l[2][4];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
-            const int n = 8 * nt + g, c = 8 * nt + 2 * q;
+            const int c = 8 * nt + 2 * q;
             float d[4] = {tw.b2[c], tw.b2[c + 1], tw.b2[c], tw.b2[c + 1]};
 #pragma unroll
-            for (int kt = 0; kt < 2; ++kt)
-                mma3(d, a2h[kt], a2l[kt], tw.w2h[n][8 * kt + q], tw.w2h[n][8 * kt + q + 4], tw.w2l[n][8 * kt + q],
-                     tw.w2l[n][8 * kt + q + 4]);
+            for (int kt = 0; kt < 2; ++kt) {
+                uint32_t b[4];
+                ldsm_x4(b, &((mi & 2) ? tw.w2l : tw.w2h)[8 * nt + mr][8 * kt + (mi & 1) * 4]);
+                mma3(d, a2h[kt], a2l[kt], b[0], b[1], b[2], b[3]);
+            }
             const int kt = nt >> 1, hi = nt & 1;
             split2(fmaxf(d[0], 0.f), fmaxf(d[1], 0.f), a3h[kt][2 * hi], a3l[kt][2 * hi]);
             split2(fmaxf(d[2], 0.f), fmaxf(d[3], 0.f), a3h[kt][2 * hi + 1], a3l[kt][2 * hi + 1]);
@@ -893,9 +907,11 @@ __device__ __forceinline__ float4 mlp_decode_tc(const TexArgs &t, const TcWeight
             const int c = 2 * q;
             float d[4] = {tw.b3[c], tw.b3[c + 1], tw.b3[c], tw.b3[c + 1]};
 #pragma unroll
-            for (int kt = 0; kt < 2; ++kt)
-                mma3(d, a3h[kt], a3l[kt], tw.w3h[g][8 * kt + q], tw.w3h[g][8 * kt + q + 4], tw.w3l[g][8 * kt + q],
-                     tw.w3l[g][8 * kt + q + 4]);
+            for (int kt = 0; kt < 2; ++kt) {
+                uint32_t b[4];
+                ldsm_x4(b, &((mi & 2) ? tw.w3l : tw.w3h)[mr][8 * kt + (mi & 1) * 4]);
+                mma3(d, a3h[kt], a3l[kt], b[0], b[1], b[2], b[3]);
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) out[mt][i] = fminf(fmaxf(d[i], 0.f), 1.f);
         }
