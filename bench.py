@@ -42,7 +42,7 @@ UNIT = "Gpix/s"
 # the timed ABI call: BC1 COLLAB runs the lean exact kernel, then the lean fallback kernel and
 # the general kernel over the waves it marked (fallback / partial or wider windows); the
 # roofline times the whole call
-KERNEL_NAME = "ctf_collab_bc1_kernel + 2 x ctf_collab_bc1_rest_kernel (one ctf_filter_batch call)"
+KERNEL_NAME = "ctf_collab_lean_kernel + 2 x ctf_collab_rest_kernel (one ctf_filter_batch call)"
 MODES = {"collab": 3, "4tap": 0, "stf": 1, "wc": 2}
 FALLBACKS = {"stf": 0, "wc": 1, "c": 2, "cplus": 3}
 MLP_FMA_PER_EVAL = 32 * 12 + 32 * 32 + 4 * 32   # 1536 FMA per latent-MLP texel (R-10)

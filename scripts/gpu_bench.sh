@@ -13,11 +13,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:c
     python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu --no-configs > gpurun_out/ncu_launch_bench_$TAG.json 2>&1
 python scripts/launch_shares.py gpurun_out/launches_$TAG.csv
 # one full capture of the three BC1 COLLAB kernels of one 64-frame step (the bench step)
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ctf_collab_bc1 -s 3 -c 3 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ctf_collab_ -s 3 -c 3 \
     -o gpurun_out/prof_$TAG python bench.py --warmup 1 --profile-launches 1 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -3 gpurun_out/ncu_full_$TAG.log
 if [ "${MLPPROF:-0}" = "1" ]; then
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctf_filter_kernel -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ctf_collab_lean_kernel -s 1 -c 1 \
     -o gpurun_out/prof_mlp_$TAG python bench.py --profile-config3 2 > gpurun_out/ncu_mlp_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_mlp_$TAG.log
 fi
