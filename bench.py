@@ -61,7 +61,7 @@ def parse_args():
     ap.add_argument("--mode", choices=list(MODES), default="collab")
     ap.add_argument("--fallback", choices=list(FALLBACKS), default="cplus")
     ap.add_argument("--no-grad", action="store_true")
-    ap.add_argument("--e2e-frames", type=int, default=8)
+    ap.add_argument("--e2e-frames", type=int, default=32)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -71,6 +71,13 @@ __device__ __forceinline__ void st_stream_f4(float4 *p, float4 v) {
                  : "memory");
 }
 
+// shared-memory load from a 32-bit shared address
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
+}
 // predicated shared store without a branch (keeps the warp provably converged)
 __device__ __forceinline__ void st_shared_u32_if(uint32_t *p, uint32_t v, bool pred) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"

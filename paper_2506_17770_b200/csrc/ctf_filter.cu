@@ -1325,6 +1325,20 @@ struct FastSmem {
 #ifndef CTF_FAST_MINB
 #define CTF_FAST_MINB 7  // resident CTAs per SM (32 registers, no spills)
 #endif
+#ifndef CTF_PAIR
+#define CTF_PAIR 1  // BC1 non-debug: two waves share one decode pass (pair_front / pair_decode)
+#endif
+#ifndef CTF_PAIR_MINB
+#define CTF_PAIR_MINB 6  // paired lean kernel: resident CTAs per SM (40 registers)
+#endif
+
+// Shared memory of the paired exact path: wave A's produced texels take jobs 0..nA-1,
+// wave B's jobs nA..nA+nB-1 (xch / bit_of_rank indexed by job).
+struct PairSmem {
+    float4 xch[64];           // job -> produced value
+    uint4 lut[8];             // BC1 per-index constants (bc1_lut_entry), per warp
+    uint8_t bit_of_rank[64];  // job -> window bit (0..63)
+};
 
 // 64-bit window masks held as two words (hi = 0 for a 32-bit window)
 __device__ __forceinline__ uint32_t bit_lo(uint32_t t) { return t < 32u ? 1u << t : 0u; }
@@ -1458,8 +1472,8 @@ __device__ __forceinline__ bool wave_magnified(uint2 gr, bool has_grad) {
 // FMT_MLP: the wave's produced texels go through the tensor-core decoder together
 // (mlp_decode_tc, rows = lanes); its fallback and 128-bit-window waves go to the general
 // kernel (kSlowMark) — there is no lean fallback for the latent-MLP format.
-template <bool DBG, int FMT>
-__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, const uint4 *lut, const MlpCtx &mc,
+template <bool DBG, int FMT, class SM>
+__device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4 *lut, const MlpCtx &mc,
                                              float2 uv, uint2 gr, bool has_grad) {
     const unsigned lane = lane_id(), lt = lanemask_lt(), lanebit = 1u << lane;
     LeanOut o;
@@ -1548,6 +1562,127 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, FastSmem &fs, const
         if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
     }
     return o;
+}
+
+// ------------------------------------------- paired exact path (BC1, non-debug build)
+// Two consecutive waves of a run share one decode pass.  Each wave still evaluates exactly
+// its own unique set U (n texels; its rank r is job base + r, h(r, A) = r up to the
+// offset), so colours, records and evaluation counts equal the one-wave path bit
+// for bit; only the SIMT packing of the evaluations changes: with n ~ 13 per wave (config
+// 5) one 32-lane decode pass serves both waves (two passes when nA + nB > 32).
+struct PairFront {
+    float s, t;        // footprint fractions (the weights are rebuilt from them, as footprint2)
+    uint32_t a0, a2;   // shared addresses of xch[job of the upper-left / lower-left corner]
+    uint32_t dxs16;    // 16 * (xb - xa): the right corners' slots follow the left ones
+    int n;             // produced texels; 0: the wave is not finished here (rec says where)
+    int minx, miny;    // window origin
+    uint32_t rec;
+};
+// steps a1-a4 of lean_wave for one wave; the rank -> window-bit table goes to job base + r
+template <bool GRAD, class SM>
+__device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 uv, uint2 gr, int base, unsigned lane,
+                                                unsigned lt) {
+    const unsigned lanebit = 1u << lane;
+    PairFront o;
+    o.s = o.t = 0.f;
+    o.a0 = o.a2 = o.dxs16 = 0u;
+    o.n = 0;
+    o.minx = o.miny = 0;
+    const unsigned A = __ballot_sync(FULL, !isnan(uv.x));   // interior run: every pixel in the frame
+    if (A != FULL) {   // empty wave: n = 0, zero colour; partial wave: general kernel
+        o.rec = A == 0u ? (1u << 26) : kSlowMark;
+        return o;
+    }
+    const bool wave_mag = wave_magnified(gr, GRAD);
+    const Foot f = footprint2(uv, a);
+    const int minx = __reduce_min_sync(FULL, f.xa), miny = __reduce_min_sync(FULL, f.ya);
+    const unsigned dx = (unsigned)(f.xb - minx), dy = (unsigned)(f.yb - miny);
+    // window P x (32 / P) or 8 x 8, row-major (bit t = dy * P + dx: the rank order is the
+    // row-major order of U for every shape); 6x5 / 5x6 take the 5x5..6x6 AABBs of rotated
+    // magnified waves (~10 % of config-5 waves) off the 64-bit path
+    int K = 0;
+    uint32_t P = 8u, qmul = 32u;   // pitch, ceil(256 / P): t / P = (t * qmul) >> 8 for t < 32 (64 for P = 8)
+    if (__all_sync(FULL, (dx | (dy << 1)) < 8u)) K = 1;                                // 8x4
+    else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; P = 4u; qmul = 64u; }   // 4x8
+    else if (__all_sync(FULL, dx < 6u && dy < 5u)) { K = 1; P = 6u; qmul = 43u; }      // 6x5
+    else if (__all_sync(FULL, dx < 5u && dy < 6u)) { K = 1; P = 5u; qmul = 52u; }      // 5x6
+    else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                                  // 8x8
+    if (K == 0) {
+        const bool w128 = __all_sync(FULL, dx < 16u && dy < 8u) || __all_sync(FULL, dx < 8u && dy < 16u) ||
+                          __all_sync(FULL, dx < 32u && dy < 4u);
+        o.rec = w128 ? kFbMark : kSlowMark;
+        return o;
+    }
+    const uint32_t t0 = (uint32_t)(f.ya - miny) * P + (uint32_t)(f.xa - minx);
+    const uint32_t t2 = t0 + (uint32_t)(f.yb - f.ya) * P;
+    const uint32_t dxs = (uint32_t)(f.xb - f.xa);
+    const uint32_t pat = 1u + dxs + dxs;
+    // push table entry of window bit t: its offset (dy << 3) | dx from the window origin
+    const uint32_t qt = (lane * qmul) >> 8;
+    const uint32_t code = (qt << 3) | (lane - qt * P);
+    uint8_t *bits = fs.bit_of_rank + base;
+    int n, r0, r2;
+    if (K == 1) {
+        const uint32_t wm = __reduce_or_sync(FULL, (pat << t0) | (pat << t2));
+        n = __popc(wm);
+        r0 = __popc(wm & ((1u << t0) - 1u));
+        r2 = __popc(wm & ((1u << t2) - 1u));
+        st_shared_u8_if(bits + __popc(wm & lt), code, wm & lanebit);
+    } else {
+        const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
+        const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
+        const uint32_t wh = __reduce_or_sync(FULL, (uint32_t)(m >> 32));
+        const int nl = __popc(wl);
+        n = nl + __popc(wh);
+        r0 = rank64(wl, wh, t0);
+        r2 = rank64(wl, wh, t2);
+        st_shared_u8_if(bits + __popc(wl & lt), lane, wl & lanebit);
+        const int rh = nl + __popc(wh & lt);
+        st_shared_u8_if(bits + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
+    }
+    if (n > 32) {   // fallback kernel
+        o.rec = kFbMark;
+        return o;
+    }
+    o.s = f.s;
+    o.t = f.t;
+    const uint32_t x0 = (uint32_t)__cvta_generic_to_shared(fs.xch + base);
+    o.a0 = x0 + 16u * (uint32_t)r0;
+    o.a2 = x0 + 16u * (uint32_t)r2;
+    o.dxs16 = 16u * dxs;
+    o.n = n;
+    o.minx = minx;
+    o.miny = miny;
+    o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
+    return o;
+}
+// step a5 for both waves: job j < nA decodes wave A's U[j], job nA + r wave B's U[r]
+template <class SM>
+__device__ __forceinline__ void pair_decode(const KArgs &a, SM &fs, const PairFront &A, const PairFront &B,
+                                            unsigned lane) {
+    const int J = A.n + B.n;
+    for (int j0 = 0; j0 < J; j0 += 32) {   // one pass, two when nA + nB > 32 (warp-uniform)
+        const int j = j0 + (int)lane;
+        const bool produced = j < J, inA = j < A.n;
+        const uint32_t e = produced ? (uint32_t)fs.bit_of_rank[j] : 0u;   // (dy << 3) | dx
+        const int qx = (inA ? A.minx : B.minx) + (int)(e & 7u);
+        const int qy = (inA ? A.miny : B.miny) + (int)(e >> 3);
+        st_shared_f4_if(&fs.xch[j], bc1_decode_unorm_lut(a.tex, qx, qy, fs.lut), produced);
+    }
+}
+// step a6 for one wave: gather + blend (weights as footprint2) and store; the empty wave
+// stores its zero colour
+template <class SM>
+__device__ __forceinline__ void pair_back(const KArgs &a, const SM &fs, const PairFront &w, unsigned pix) {
+    if (w.n > 0) {
+        const float2 om = f2unpack(fsub2(f2pack(1.0f, 1.0f), f2pack(w.s, w.t)));
+        const float wt[4] = {__fmul_rn(om.x, om.y), __fmul_rn(w.s, om.y), __fmul_rn(om.x, w.t), __fmul_rn(w.s, w.t)};
+        const float4 p[4] = {ld_shared_f4(w.a0), ld_shared_f4(w.a0 + w.dxs16), ld_shared_f4(w.a2),
+                             ld_shared_f4(w.a2 + w.dxs16)};
+        st_stream_f4(a.out + pix, blend4f(p, wt));
+    } else if (w.rec == (1u << 26)) {
+        st_stream_f4(a.out + pix, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
 }
 
 // ---------------------------------------- lean fallback over windows up to 128 bits
@@ -1755,13 +1890,18 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
 
 // GRAD: grad != NULL (magnified class); FORCE: CTF_FLAG_FORCE_FALLBACK (every live wave
 // goes to the rest kernel) — compile-time, so the hot loop tests neither.
+template <bool DBG, bool FORCE, int FMT>
+constexpr bool kPaired = CTF_PAIR && FMT == FMT_BC1 && !DBG && !FORCE;
 template <bool DBG, bool GRAD, bool FORCE, int FMT>
-__global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? CTF_FAST_MINB : CTF_MLP_COLLAB_MINB)
+__global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FORCE, FMT> ? CTF_PAIR_MINB : CTF_FAST_MINB)
+                                                               : CTF_MLP_COLLAB_MINB)
     ctf_collab_lean_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
-    __shared__ FastSmem fsm[kWarps];
+    constexpr bool PAIR = kPaired<DBG, FORCE, FMT>;
+    using SmemT = std::conditional_t<PAIR, PairSmem, FastSmem>;
+    __shared__ SmemT fsm[kWarps];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent MLP: TcWeights + per-warp TcScratch
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
-    FastSmem &fs = fsm[warp];
+    SmemT &fs = fsm[warp];
     MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
     if constexpr (FMT == FMT_BC1) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
@@ -1814,6 +1954,35 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? CTF_FAST_MINB : 
         uint32_t myrec = 0u;
         auto run = [&](auto interior_tag) {
           constexpr bool INTERIOR = decltype(interior_tag)::value;
+          if constexpr (INTERIOR && PAIR) {
+            // pairs (A, B) = waves (wx, wx + 1); A's next load is issued after A's front,
+            // B's after B's front, so each covers about one pair of work
+            const unsigned lt_mask = lanemask_lt();
+            float2 uv_b = make_float2(__int_as_float(0x7fc00000), 0.f);
+            uint2 gr_b = make_uint2(0u, 0u);
+            ld_stream_f2_if(uv_b, a.uv + (pix + 8u), wx0 + 1 < wx1);
+            ld_stream_u2_if(gr_b, a.grad + (pix + 8u), (wx0 + 1 < wx1) & has_grad);
+            for (int wx = wx0; wx < wx1; wx += 2, pix += 16u) {
+              const bool hasB = wx + 1 < wx1;
+              const PairFront fa = pair_front<GRAD>(a, fs, uv_n, gr_n, 0, lane, lt_mask);
+              ld_stream_f2_if(uv_n, a.uv + (pix + 16u), wx + 2 < wx1);
+              ld_stream_u2_if(gr_n, a.grad + (pix + 16u), (wx + 2 < wx1) & has_grad);
+              PairFront fb;
+              fb.n = 0;
+              fb.rec = 0u;
+              if (hasB) fb = pair_front<GRAD>(a, fs, uv_b, gr_b, fa.n, lane, lt_mask);
+              ld_stream_f2_if(uv_b, a.uv + (pix + 24u), wx + 3 < wx1);
+              ld_stream_u2_if(gr_b, a.grad + (pix + 24u), (wx + 3 < wx1) & has_grad);
+              __syncwarp();   // bit_of_rank written; the previous pair's xch reads are done
+              pair_decode(a, fs, fa, fb, lane);
+              __syncwarp();
+              pair_back(a, fs, fa, pix);
+              if (hasB) pair_back(a, fs, fb, pix + 8u);
+              if (lane == (unsigned)(wx - wx0)) myrec = fa.rec;
+              if (lane == (unsigned)(wx + 1 - wx0)) myrec = hasB ? fb.rec : myrec;
+            }
+            return;
+          }
           for (int wx = wx0; wx < wx1; ++wx, pix += 8u, px += 8) {
             const bool inframe = INTERIOR || (rowok & (px < a.Wf));
             const float2 uv = uv_n;

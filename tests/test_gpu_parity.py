@@ -324,3 +324,24 @@ def test_exact_waves_with_128bit_windows(ctf):
     n = (o["rec"] >> 8) & 255
     path = (o["rec"] >> 22) & 7
     assert (path[0] == 0).all() and (n[0] == 32).all()   # the first wave row is exact with n = 32
+
+
+@pytest.mark.parametrize("wf,hf,mag,theta,cov", [(104, 40, 1.2, 30.0, "circle"), (104, 36, 0.9, 50.0, None),
+                                                 (24, 8, 2.0, 10.0, None), (8, 12, 1.5, 60.0, "halfplane"),
+                                                 (136, 44, 0.6, 15.0, "circle")])
+def test_release_paired_runs(ctf, wf, hf, mag, theta, cov):
+    """The release BC1 COLLAB kernel pairs consecutive waves of an interior run for one decode
+    pass: odd-length runs (13, 3, 1, 17 waves), pairs mixing exact / fallback / partial /
+    empty waves and nA + nB > 32 (two passes) give the oracle's records and colours, and the
+    debug kernel's (unpaired) colours bit for bit."""
+    import oracle
+    tex = bc1_tex(128, 128, 17, "image")
+    uv, g = synthetic.rotated_quad(wf, hf, 128, 128, mag, theta, coverage=cov, radius=14.0, jitter_seed=6)
+    dt = to_dev_tex(ctf, tex)
+    for mode, fb, fl in [(3, 3, 0), (3, 0, 0), (3, 2, 0)]:
+        o = oracle.filter_frame(tex, uv, g, mode, fb, fl, seed=8, frame_index=1)
+        out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, fl, 8, 1)
+        np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+        assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
+        gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=8, frame_index=1)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), gg["out"].view(np.uint32))
