@@ -105,6 +105,17 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
     }
     return c;
 }
+// The same with the round keys precomputed (k0[r] = k0 + r * 0x9E3779B9, k1[r] likewise):
+// kernel-parameter arrays, so each key is a constant-bank operand of the XOR.
+__device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const uint32_t (&k0)[10], const uint32_t (&k1)[10]) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0[r], lo1, hi0 ^ c.w ^ k1[r], lo0);
+    }
+    return c;
+}
 // uniform in [0,1) on the 2^-24 grid: exact in fp32 (R-11)
 __device__ __forceinline__ float unit24(uint32_t r) { return __uint2float_rn(r >> 8) * 5.9604644775390625e-08f; }
 

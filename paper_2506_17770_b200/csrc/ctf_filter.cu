@@ -66,6 +66,7 @@ struct KArgs {
     int fallback;
     int variant;                    // COLLAB kernel: VAR_LIST / VAR_BOX / VAR_MASK16 / VAR_MASK11
     uint32_t flags, frame_index, seed_lo, seed_hi;
+    uint32_t rk[2][10];             // Philox round keys of (seed_lo, seed_hi) (constant-bank operands)
 };
 enum { VAR_LIST = 0, VAR_BOX = 1, VAR_MASK16 = 2, VAR_MASK11 = 3 };
 
@@ -932,7 +933,11 @@ __device__ __forceinline__ float4 mlp_decode_tc(const TexArgs &t, const TcWeight
 }
 
 // ----------------------------------------------------------------------- kernel
-constexpr int kChunk = 16;  // waves per work item: a run of consecutive waves in one wave-row
+#ifndef CTF_CHUNK
+#define CTF_CHUNK 16
+#endif
+constexpr int kChunk = CTF_CHUNK;  // waves per work item: a run of consecutive waves in one wave-row (<= 32)
+static_assert(kChunk >= 1 && kChunk <= 32, "a run's records are buffered one per lane");
 
 struct MlpCtx {  // latent-MLP COLLAB decoder state (unused by BC1)
     TcWeights *tw;
@@ -1780,7 +1785,7 @@ __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const F
     } else {
         // ---- a7 plan: every lane's STF texel; C+ dedupes it and spreads the
         // spare lanes over the wave with Eq. 2
-        const uint4 rn = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo, a.seed_hi);
+        const uint4 rn = philox4x32_10_rk(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.rk[0], a.rk[1]);
         const int ksel = stf_corner(f, rn);
         qx = corner_x(f, ksel);
         qy = corner_y(f, ksel);
@@ -1970,6 +1975,7 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
               PairFront fb;
               fb.n = 0;
               fb.rec = 0u;
+              __syncwarp();   // A's push-table writes (all of them, also a rejected A's) before B's
               if (hasB) fb = pair_front<GRAD>(a, fs, uv_b, gr_b, fa.n, lane, lt_mask);
               ld_stream_f2_if(uv_b, a.uv + (pix + 24u), wx + 3 < wx1);
               ld_stream_u2_if(gr_b, a.grad + (pix + 24u), (wx + 3 < wx1) & has_grad);
@@ -2436,6 +2442,10 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.frame_index = a.frame_index;
     k.seed_lo = (uint32_t)a.seed;
     k.seed_hi = (uint32_t)(a.seed >> 32);
+    for (int r = 0; r < 10; ++r) {   // the key schedule of philox4x32_10, precomputed
+        k.rk[0][r] = k.seed_lo + (uint32_t)r * 0x9E3779B9u;
+        k.rk[1][r] = k.seed_hi + (uint32_t)r * 0xBB67AE85u;
+    }
 #if CTF_TU_FMT == 1
     return launch_fmt<FMT_BC1>(k, NoWeights{}, a.mode, stream);
 #else
