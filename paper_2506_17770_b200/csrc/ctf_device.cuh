@@ -284,8 +284,15 @@ __device__ __forceinline__ uint4 bc1_lut_entry(uint32_t i) {
     return make_uint4(((nib & 3u) << 16) | (nib >> 2), code < 2u ? 2048u : (four ? 683u : 1024u),
                       (four || code != 3u) ? 0x4B0000FFu : 0x4B000000u, 0u);
 }
+// BC1 block of texel (x, y) (the load of bc1_decode_unorm_lut, issued ahead by the paired path)
+__device__ __forceinline__ uint2 bc1_block(const TexArgs &t, int x, int y) {
+    return __ldg(t.bc1 + ((unsigned)(y >> 2) * (unsigned)(t.W >> 2) + (unsigned)(x >> 2)));
+}
+__device__ __forceinline__ float4 bc1_unorm_from_block(uint2 b, int x, int y, const uint4 *lut);
 __device__ __forceinline__ float4 bc1_decode_unorm_lut(const TexArgs &t, int x, int y, const uint4 *lut) {
-    const uint2 b = __ldg(t.bc1 + ((unsigned)(y >> 2) * (unsigned)(t.W >> 2) + (unsigned)(x >> 2)));
+    return bc1_unorm_from_block(bc1_block(t, x, y), x, y, lut);
+}
+__device__ __forceinline__ float4 bc1_unorm_from_block(uint2 b, int x, int y, const uint4 *lut) {
     const uint32_t shift = 2u * ((((unsigned)y & 3u) << 2) | ((unsigned)x & 3u));
     const uint32_t code = (b.y >> shift) & 3u;
     const bool four = (b.x & 0xffffu) > (b.x >> 16);

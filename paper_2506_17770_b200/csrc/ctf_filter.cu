@@ -1337,12 +1337,13 @@ struct FastSmem {
 #define CTF_PAIR_MINB 6  // paired lean kernel: resident CTAs per SM (40 registers)
 #endif
 
+
 // Shared memory of the paired exact path: wave A's produced texels take jobs 0..nA-1,
 // wave B's jobs nA..nA+nB-1 (xch / bit_of_rank indexed by job).
 struct PairSmem {
     float4 xch[64];           // job -> produced value
     uint4 lut[8];             // BC1 per-index constants (bc1_lut_entry), per warp
-    uint8_t bit_of_rank[64];  // job -> window bit (0..63)
+    uint8_t bit_of_rank[64];  // job -> window offset (dy << 3) | dx
 };
 
 // 64-bit window masks held as two words (hi = 0 for a 32-bit window)
@@ -1585,8 +1586,8 @@ struct PairFront {
 };
 // steps a1-a4 of lean_wave for one wave; the rank -> window-bit table goes to job base + r
 template <bool GRAD, class SM>
-__device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 uv, uint2 gr, int base, unsigned lane,
-                                                unsigned lt) {
+__device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 uv, uint2 gr, int base, uint8_t *bits0,
+                                                unsigned lane, unsigned lt) {
     const unsigned lanebit = 1u << lane;
     PairFront o;
     o.s = o.t = 0.f;
@@ -1625,7 +1626,7 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     // push table entry of window bit t: its offset (dy << 3) | dx from the window origin
     const uint32_t qt = (lane * qmul) >> 8;
     const uint32_t code = (qt << 3) | (lane - qt * P);
-    uint8_t *bits = fs.bit_of_rank + base;
+    uint8_t *bits = bits0 + base;
     int n, r0, r2;
     if (K == 1) {
         const uint32_t wm = __reduce_or_sync(FULL, (pat << t0) | (pat << t2));
@@ -1663,13 +1664,13 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
 }
 // step a5 for both waves: job j < nA decodes wave A's U[j], job nA + r wave B's U[r]
 template <class SM>
-__device__ __forceinline__ void pair_decode(const KArgs &a, SM &fs, const PairFront &A, const PairFront &B,
-                                            unsigned lane) {
+__device__ __forceinline__ void pair_decode(const KArgs &a, SM &fs, const uint8_t *bits, const PairFront &A,
+                                            const PairFront &B, unsigned lane) {
     const int J = A.n + B.n;
     for (int j0 = 0; j0 < J; j0 += 32) {   // one pass, two when nA + nB > 32 (warp-uniform)
         const int j = j0 + (int)lane;
         const bool produced = j < J, inA = j < A.n;
-        const uint32_t e = produced ? (uint32_t)fs.bit_of_rank[j] : 0u;   // (dy << 3) | dx
+        const uint32_t e = produced ? (uint32_t)bits[j] : 0u;   // (dy << 3) | dx
         const int qx = (inA ? A.minx : B.minx) + (int)(e & 7u);
         const int qy = (inA ? A.miny : B.miny) + (int)(e >> 3);
         st_shared_f4_if(&fs.xch[j], bc1_decode_unorm_lut(a.tex, qx, qy, fs.lut), produced);
@@ -1969,18 +1970,18 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
             ld_stream_u2_if(gr_b, a.grad + (pix + 8u), (wx0 + 1 < wx1) & has_grad);
             for (int wx = wx0; wx < wx1; wx += 2, pix += 16u) {
               const bool hasB = wx + 1 < wx1;
-              const PairFront fa = pair_front<GRAD>(a, fs, uv_n, gr_n, 0, lane, lt_mask);
+              const PairFront fa = pair_front<GRAD>(a, fs, uv_n, gr_n, 0, fs.bit_of_rank, lane, lt_mask);
               ld_stream_f2_if(uv_n, a.uv + (pix + 16u), wx + 2 < wx1);
               ld_stream_u2_if(gr_n, a.grad + (pix + 16u), (wx + 2 < wx1) & has_grad);
               PairFront fb;
               fb.n = 0;
               fb.rec = 0u;
               __syncwarp();   // A's push-table writes (all of them, also a rejected A's) before B's
-              if (hasB) fb = pair_front<GRAD>(a, fs, uv_b, gr_b, fa.n, lane, lt_mask);
+              if (hasB) fb = pair_front<GRAD>(a, fs, uv_b, gr_b, fa.n, fs.bit_of_rank, lane, lt_mask);
               ld_stream_f2_if(uv_b, a.uv + (pix + 24u), wx + 3 < wx1);
               ld_stream_u2_if(gr_b, a.grad + (pix + 24u), (wx + 3 < wx1) & has_grad);
               __syncwarp();   // bit_of_rank written; the previous pair's xch reads are done
-              pair_decode(a, fs, fa, fb, lane);
+              pair_decode(a, fs, fs.bit_of_rank, fa, fb, lane);
               __syncwarp();
               pair_back(a, fs, fa, pix);
               if (hasB) pair_back(a, fs, fb, pix + 8u);
