@@ -524,7 +524,7 @@ def main():
             "quality": quality,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * ctf.launches_per_call(1, mode, 0, F, True),
+            "gpu_launches": args.steps * ctf.launches_per_call(1, mode, 0, F, True, workspace=True),
             "clocks": clk,
             "configs": configs,
         }

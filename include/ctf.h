@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define CTF_ABI_VERSION 4
+#define CTF_ABI_VERSION 5
 
 typedef enum {
     CTF_OK = 0,
@@ -231,14 +231,19 @@ size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames);
 
 /*
  * Kernel launches one call above issues (for launch accounting): format / mode / filter
- * as in ctf_texture / ctf_params, `frames` frames, `batched` != 0 for ctf_filter_batch
- * (one pass over all frames) else ctf_filter_frame once per frame.  The COLLAB bilinear
+ * as in ctf_texture / ctf_params, `frames` frames; flags: CTF_LAUNCH_BATCHED for
+ * ctf_filter_batch (one pass over all frames) else ctf_filter_frame once per frame, plus
+ * CTF_LAUNCH_WORKSPACE when ctf_params.workspace_dev holds a workspace.  The COLLAB bilinear
  * path is three kernels per pass for BC1 (the lean exact kernel; the lean fallback kernel
  * over the full waves it left; the general path over partial waves and windows wider than
  * 8x8) and two for the latent MLP (lean exact kernel + general path); every other path is
- * one.  Returns -1 for an invalid format / mode / filter.
+ * one.  A batched BC1 COLLAB bilinear call with a workspace cuts its frames into up to two
+ * groups (three kernels each; the rest passes of a group run on a side stream, overlapping
+ * the next group's lean kernel).  Returns -1 for an invalid format / mode / filter.
  */
-int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int batched);
+#define CTF_LAUNCH_BATCHED 1
+#define CTF_LAUNCH_WORKSPACE 2
+int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int flags);
 int ctf_abi_version(void);
 
 #ifdef __cplusplus

@@ -93,12 +93,14 @@ size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames) {
     return 256 + 8 * waves;
 }
 
-int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int batched) {
+int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int flags) {
     if ((format != CTF_FMT_BC1 && format != CTF_FMT_LATENT_MLP) || mode < 0 || mode > CTF_MODE_MASK11 || filter < 0 ||
         filter > 2)
         return -1;
     const int per_pass = ctf::launches_per_pass(format, mode, filter);
-    return per_pass * (batched ? 1 : (frames > 0 ? frames : 0));
+    if (!(flags & CTF_LAUNCH_BATCHED)) return per_pass * (frames > 0 ? frames : 0);
+    const int groups = (flags & CTF_LAUNCH_WORKSPACE) ? ctf::collab_subbatches(format, mode, filter, frames) : 1;
+    return per_pass * groups;
 }
 
 int ctf_filter_batch(const ctf_texture *tex, const float *uv_dev, const uint16_t *grad_dev, int32_t Wf, int32_t Hf,

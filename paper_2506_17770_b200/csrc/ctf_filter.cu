@@ -21,6 +21,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <type_traits>
 
 #include "ctf_device.cuh"
@@ -32,6 +33,11 @@ constexpr int kWarps = 8;  // warps per CTA
 #ifndef CTF_BC1_MINB
 #define CTF_BC1_MINB 4  // BC1: resident CTAs per SM (64 registers)
 #endif
+#ifndef CTF_SUBBATCH
+#define CTF_SUBBATCH 2  // BC1 COLLAB with work lists: frame groups whose rest passes overlap the next lean kernel (A/B r01: 2 > 1, 4, 8)
+#endif
+constexpr int kMaxSubbatch = 16;
+static_assert(CTF_SUBBATCH >= 1 && CTF_SUBBATCH <= kMaxSubbatch, "workspace holds kMaxSubbatch counter pairs");
 #ifndef CTF_BC1_ROUNDS
 #define CTF_BC1_ROUNDS 8  // BC1: target CTAs per resident CTA slot
 #endif
@@ -52,7 +58,8 @@ struct KArgs {
     float4 *out;
     uint32_t *rec;
     uint32_t *dbg_pid, *dbg_sel, *dbg_unread;
-    uint32_t *lists;                // optional work lists (BC1 COLLAB): counts [0], [1]; lists at [64], [64 + nrec]
+    uint32_t *lcnt;                 // work-list counters [0] (fallback), [1] (general) when lists != NULL
+    uint32_t *lists;                // optional work lists (BC1 COLLAB): fallback at [0], general at [nrec]
     unsigned nrec;                  // waves in the batch
     uint32_t wpf_m, nwx_m;          // magic multipliers: n / wpf, n / nwx (udiv_magic)
     int wpf_s, nwx_s;
@@ -2033,11 +2040,11 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
         const unsigned mfb = __ballot_sync(FULL, inrun && myrec == kFbMark);
         const unsigned msl = __ballot_sync(FULL, inrun && myrec == kSlowMark);
         if (a.lists && (mfb | msl)) {   // append the run's marked waves to the work lists (predicated)
-            const unsigned b0 = __shfl_sync(FULL, atom_add_if(a.lists + 0, (unsigned)__popc(mfb), lane == 0 && mfb), 0);
-            const unsigned b1 = __shfl_sync(FULL, atom_add_if(a.lists + 1, (unsigned)__popc(msl), lane == 0 && msl), 0);
+            const unsigned b0 = __shfl_sync(FULL, atom_add_if(a.lcnt + 0, (unsigned)__popc(mfb), lane == 0 && mfb), 0);
+            const unsigned b1 = __shfl_sync(FULL, atom_add_if(a.lcnt + 1, (unsigned)__popc(msl), lane == 0 && msl), 0);
             const unsigned lt = lanemask_lt();
-            st_u32_if(a.lists + 64u + b0 + __popc(mfb & lt), w0 + lane, (mfb >> lane) & 1u);
-            st_u32_if(a.lists + 64u + a.nrec + b1 + __popc(msl & lt), w0 + lane, (msl >> lane) & 1u);
+            st_u32_if(a.lists + b0 + __popc(mfb & lt), w0 + lane, (mfb >> lane) & 1u);
+            st_u32_if(a.lists + a.nrec + b1 + __popc(msl & lt), w0 + lane, (msl >> lane) & 1u);
         }
     }
 }
@@ -2079,7 +2086,7 @@ template <bool DBG, bool FALLBACK, int FMT>
 __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == FMT_BC1 ? CTF_REST_MINB : CTF_MLP_COLLAB_MINB))
     ctf_collab_rest_kernel(const KArgs a, unsigned nrec, const typename WeightsOf<FMT>::type mw) {
     static_assert(FMT == FMT_BC1 || !FALLBACK, "no lean fallback for the latent-MLP format");
-    if (a.lists && a.lists[FALLBACK ? 0 : 1] == 0u) return;   // empty work list (same value in every thread)
+    if (a.lists && a.lcnt[FALLBACK ? 0 : 1] == 0u) return;   // empty work list (same value in every thread)
     __shared__ WarpSmem smem[(FALLBACK && !CTF_REST_MERGED) ? 1 : kWarps];
     __shared__ FbSmem fsm[FALLBACK ? kWarps : 1];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent MLP: TcWeights + per-warp TcScratch
@@ -2113,7 +2120,7 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
             if (FALLBACK && !CTF_REST_MERGED) {   // (defensive) no 128-bit window: general kernel
                 if (lane == 0) {
                     a.rec[wi] = kSlowMark;
-                    if (a.lists) a.lists[64u + a.nrec + atomicAdd(a.lists + 1, 1u)] = wi;
+                    if (a.lists) a.lists[a.nrec + atomicAdd(a.lcnt + 1, 1u)] = wi;
                 }
                 return;
             }
@@ -2137,8 +2144,8 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
     if (a.lists) {
         // ---- work-list mode: the waves the lean kernel appended, one per warp step
         // (balanced over the whole grid), the next one's inputs loaded ahead
-        const unsigned n = __shfl_sync(FULL, a.lists[FALLBACK ? 0 : 1], 0);   // provably uniform
-        const uint32_t *L = a.lists + 64u + (FALLBACK ? 0u : a.nrec);
+        const unsigned n = __shfl_sync(FULL, a.lcnt[FALLBACK ? 0 : 1], 0);   // provably uniform
+        const uint32_t *L = a.lists + (FALLBACK ? 0u : a.nrec);
         const unsigned tw = gridDim.x * kWarps;
         unsigned i = blockIdx.x * kWarps + warp;
         if (i >= n) return;
@@ -2323,21 +2330,16 @@ static cudaError_t mlp_smem_setup(Kern kern, size_t dyn, int dev) {
 // The lean COLLAB (List) pass: the lean exact kernel, then (BC1) the lean fallback kernel
 // and the general kernel over the waves it marked / appended to the work lists; (latent
 // MLP) the general kernel over them.  Same work split as the general BC1 kernel.
+// the lean exact kernel over k's frames
 template <int FMT, bool DBG>
-static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
-    if (k.lists) {   // work-list counters (the lists need no initialisation)
-        const cudaError_t e0 = cudaMemsetAsync(k.lists, 0, 2 * sizeof(uint32_t), stream);
-        if (e0 != cudaSuccess) return e0;
-    }
+static cudaError_t launch_lean(KArgs &k, const typename WeightsOf<FMT>::type &mw, int dev, int sms,
+                               cudaStream_t stream) {
     const bool grad = k.grad != nullptr, force = (k.flags & FLAG_FORCE_FALLBACK) != 0;
     auto kern = grad ? (force ? ctf_collab_lean_kernel<DBG, true, true, FMT> : ctf_collab_lean_kernel<DBG, true, false, FMT>)
                      : (force ? ctf_collab_lean_kernel<DBG, false, true, FMT> : ctf_collab_lean_kernel<DBG, false, false, FMT>);
     const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaError_t e;
     if (dyn > 0 && (e = mlp_smem_setup(kern, dyn, dev)) != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, dyn);
     if (e != cudaSuccess) return e;
@@ -2354,26 +2356,107 @@ static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw,
     long long grid = ((long long)k.nchunks + k.ipc - 1) / k.ipc;
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, kWarps * 32, dyn, stream>>>(k, mw);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    // the marked waves, each pass at most one resident wave of CTAs
+    return cudaGetLastError();
+}
+
+// the marked waves of k's frames: pass 0 lean fallback (BC1), pass 1 general; each pass at
+// most one resident wave of CTAs
+template <int FMT, bool DBG>
+static cudaError_t launch_rest(const KArgs &k, const typename WeightsOf<FMT>::type &mw, int dev, int sms,
+                               cudaStream_t stream) {
+    const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
     const unsigned nrec = (unsigned)((long long)k.wpf * (k.nchunks / (unsigned)k.cpf));
     const long long groups = ((long long)nrec + 31) / 32;
-    const int first = FMT == FMT_BC1 ? 0 : 1;   // pass 0: lean fallback (BC1); pass 1: general
+    const int first = FMT == FMT_BC1 ? 0 : 1;
+    cudaError_t e;
     for (int pass = first; pass < (CTF_REST_MERGED ? 1 : 2); ++pass) {
         auto rest = ctf_collab_rest_kernel<DBG, false, FMT>;
         if constexpr (FMT == FMT_BC1)
             if (pass == 0) rest = ctf_collab_rest_kernel<DBG, true, FMT_BC1>;
+        int per_sm = 0;
         if (dyn > 0 && (e = mlp_smem_setup(rest, dyn, dev)) != cudaSuccess) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rest, kWarps * 32, dyn);
         if (e != cudaSuccess) return e;
         long long g2 = (long long)sms * (per_sm > 0 ? per_sm : 1);
         if (g2 * kWarps > groups) g2 = (groups + kWarps - 1) / kWarps;
         rest<<<(unsigned)(g2 < 1 ? 1 : g2), kWarps * 32, dyn, stream>>>(k, nrec, mw);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+// Sub-batches (BC1 with work lists, >= 2 frames): the batch is cut into S groups of frames;
+// the lean kernels run in order on the caller's stream and each group's two rest passes on a
+// high-priority side stream as soon as its lean kernel is done, so they overlap the next
+// group's lean kernel (the rest passes are latency-bound at low occupancy, the lean kernel
+// issue-bound: together they fill more issue slots).  Per group the workspace holds its two
+// counters (all groups' counters first, one memset) and its two lists.
+static int subbatches(int frames) {
+    if (CTF_SUBBATCH <= 1 || frames < 2) return 1;
+    return frames < CTF_SUBBATCH ? frames : CTF_SUBBATCH;
+}
+struct SideStreams {   // per device, created on first use; enqueues are serialised by mu
+    std::mutex mu;
+    cudaStream_t side[64] = {};
+    cudaEvent_t ev[64][kMaxSubbatch + 1] = {};
+};
+static SideStreams g_side;
+static cudaError_t side_setup(int dev) {
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (g_side.side[dev]) return cudaSuccess;
+    int least = 0, greatest = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&g_side.side[dev], cudaStreamNonBlocking, greatest);
+    for (int i = 0; e == cudaSuccess && i <= kMaxSubbatch; ++i)
+        e = cudaEventCreateWithFlags(&g_side.ev[dev][i], cudaEventDisableTiming);
+    return e;
+}
+
+template <int FMT, bool DBG>
+static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    const int F = (int)(k.nchunks / (unsigned)k.cpf);
+    const int S = (FMT == FMT_BC1 && k.lists) ? subbatches(F) : 1;
+    if (S == 1) {
+        if (k.lists) {   // work-list counters (the lists need no initialisation)
+            k.lcnt = k.lists;
+            k.lists += 64;
+            if ((e = cudaMemsetAsync(k.lcnt, 0, 2 * sizeof(uint32_t), stream)) != cudaSuccess) return e;
+        }
+        if ((e = launch_lean<FMT, DBG>(k, mw, dev, sms, stream)) != cudaSuccess) return e;
+        return launch_rest<FMT, DBG>(k, mw, dev, sms, stream);
+    }
+    std::lock_guard<std::mutex> lock(g_side.mu);
+    if ((e = side_setup(dev)) != cudaSuccess) return e;
+    cudaStream_t side = g_side.side[dev];
+    uint32_t *cnt = k.lists, *lists = k.lists + 64;
+    if ((e = cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t) * S, stream)) != cudaSuccess) return e;
+    for (int g = 0; g < S; ++g) {
+        const int f0 = (int)((long long)F * g / S), f1 = (int)((long long)F * (g + 1) / S);
+        const size_t px0 = (size_t)f0 * k.fpx, w0 = (size_t)f0 * (size_t)k.wpf;
+        KArgs kg = k;
+        kg.uv = k.uv + px0;
+        kg.grad = k.grad ? k.grad + px0 : nullptr;
+        kg.out = k.out + px0;
+        kg.rec = k.rec + w0;
+        if (k.dbg_pid) kg.dbg_pid = k.dbg_pid + px0;
+        if (k.dbg_sel) kg.dbg_sel = k.dbg_sel + px0;
+        kg.frame_index = k.frame_index + (uint32_t)f0;
+        kg.nchunks = (unsigned)k.cpf * (unsigned)(f1 - f0);
+        kg.nrec = (unsigned)(k.wpf * (f1 - f0));
+        kg.lcnt = cnt + 2 * g;
+        kg.lists = lists + 2 * w0;
+        if ((e = launch_lean<FMT, DBG>(kg, mw, dev, sms, stream)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(g_side.ev[dev][g], stream)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(side, g_side.ev[dev][g], 0)) != cudaSuccess) return e;
+        if ((e = launch_rest<FMT, DBG>(kg, mw, dev, sms, side)) != cudaSuccess) return e;
+    }
+    if ((e = cudaEventRecord(g_side.ev[dev][kMaxSubbatch], side)) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(stream, g_side.ev[dev][kMaxSubbatch], 0);
 }
 
 template <int FMT, int MODE>
@@ -2402,6 +2485,10 @@ int launches_per_pass(int fmt, int mode, int filter) {
     if (!CTF_FAST || mode != MODE_COLLAB || filter != 0) return 1;
     return fmt == FMT_BC1 ? (CTF_REST_MERGED ? 2 : 3) : 2;   // latent MLP: lean exact + general
 }
+int collab_subbatches(int fmt, int mode, int filter, int frames) {   // frame groups of one batched call with a workspace
+    if (!CTF_FAST || fmt != FMT_BC1 || mode != MODE_COLLAB || filter != 0) return 1;
+    return subbatches(frames);
+}
 
 cudaError_t launch_filter_bc1(const LaunchArgs &a, cudaStream_t stream) {
 #else
@@ -2421,6 +2508,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.dbg_sel = a.dbg_sel;
     k.dbg_unread = a.dbg_unread;
     k.lists = a.lists;
+    k.lcnt = nullptr;
     k.Wf = a.Wf;
     k.Hf = a.Hf;
     k.nwx = (a.Wf + 7) / 8;

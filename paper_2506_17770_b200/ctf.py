@@ -142,9 +142,10 @@ class Texture:
         return Texture(FMT_LATENT_MLP, width, height, lat, w)
 
 
-def launches_per_call(fmt: int, mode: int, filt: int = 0, frames: int = 1, batched: bool = True) -> int:
+def launches_per_call(fmt: int, mode: int, filt: int = 0, frames: int = 1, batched: bool = True,
+                      workspace: bool = False) -> int:
     """Kernel launches one filter call issues (ctf_launches_per_call)."""
-    n = load_library().ctf_launches_per_call(fmt, mode, filt, frames, int(batched))
+    n = load_library().ctf_launches_per_call(fmt, mode, filt, frames, int(batched) | (2 if workspace else 0))
     if n < 0:
         raise CtfError("ctf_launches_per_call", CTF_EINVAL)
     return n

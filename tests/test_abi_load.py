@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     lib.ctf_abi_version.restype = ctypes.c_int
-    assert lib.ctf_abi_version() == 4
+    assert lib.ctf_abi_version() == 5
 
 
 def test_binding_declares_all_exports():
@@ -79,3 +79,7 @@ def test_validation_errors_without_gpu():
     assert lib.ctf_launches_per_call(1, 0, 0, 64, 1) == 1 and lib.ctf_launches_per_call(2, 3, 0, 8, 0) == 16
     assert lib.ctf_launches_per_call(2, 4, 0, 8, 1) == 1   # Box: the general kernel
     assert lib.ctf_launches_per_call(3, 3, 0, 1, 1) == -1
+    # batched BC1 COLLAB with a workspace: up to two frame groups of three kernels
+    assert lib.ctf_launches_per_call(1, 3, 0, 64, 3) == 6 and lib.ctf_launches_per_call(1, 3, 0, 3, 3) == 6
+    assert lib.ctf_launches_per_call(1, 3, 0, 1, 3) == 3 and lib.ctf_launches_per_call(2, 3, 0, 64, 3) == 2
+    assert lib.ctf_launches_per_call(1, 3, 1, 64, 3) == 1   # bicubic: one kernel

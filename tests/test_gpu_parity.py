@@ -345,3 +345,34 @@ def test_release_paired_runs(ctf, wf, hf, mag, theta, cov):
         assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
         gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=8, frame_index=1)
         assert np.array_equal(out.cpu().numpy().view(np.uint32), gg["out"].view(np.uint32))
+
+
+@pytest.mark.parametrize("nf", [2, 3, 5])
+def test_frame_groups_with_workspace(ctf, nf):
+    """A batched BC1 COLLAB call with a workspace runs its frames in groups whose rest passes
+    go to a side stream: records, colours and debug outputs equal the record-scan path (no
+    workspace, one group) bit for bit and the per-frame oracle, for every fallback."""
+    import oracle
+    tex = bc1_tex(128, 128, 4, "image")
+    frames = [synthetic.rotated_quad(64, 28, 128, 128, 0.8 + 0.35 * f, 17.0 * f, coverage="circle" if f % 2 else None,
+                                     radius=12.0, jitter_seed=f) for f in range(nf)]
+    uv = torch.from_numpy(np.stack([f[0] for f in frames])).cuda()
+    g = torch.from_numpy(np.stack([f[1] for f in frames])).cuda()
+    dt = to_dev_tex(ctf, tex)
+    for fb, fl in [(3, 0), (0, 0), (2, 2)]:
+        res = []
+        for ws in (True, None):
+            dbg = {"produced_id": torch.zeros(uv.shape[:3], dtype=torch.int32, device="cuda"),
+                   "selection": torch.zeros(uv.shape[:3], dtype=torch.int32, device="cuda"),
+                   "unread": torch.zeros(1, dtype=torch.int32, device="cuda")}
+            out, rec = ctf.filter_batch(dt, uv, g, 3, fb, fl, 6, 40, debug=dbg, workspace=ws)
+            out2, rec2 = ctf.filter_batch(dt, uv, g, 3, fb, fl, 6, 40, workspace=ws)   # release kernels
+            torch.cuda.synchronize()
+            res.append([t.cpu().numpy().view(np.uint32) for t in (out, rec, dbg["produced_id"], dbg["selection"],
+                                                                   out2, rec2)])
+        for a, b in zip(*res):
+            assert np.array_equal(a, b)
+        for f in range(nf):
+            o = oracle.filter_frame(tex, frames[f][0], frames[f][1], 3, fb, fl, seed=6, frame_index=40 + f)
+            np.testing.assert_array_equal(res[0][1][f], o["rec"])
+            assert np.abs(res[0][0][f].view(np.float32).astype(np.float64) - o["out"]).max() <= ATOL
