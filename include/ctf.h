@@ -182,10 +182,15 @@ int ctf_filter_frame(const ctf_texture *tex, const float *uv_dev, const uint16_t
                      uint32_t *rec_dev, const ctf_debug *dbg, void *stream);
 
 /*
- * Filter `frames` consecutive frames in ONE launch (persistent kernel over all waves).
- * uv_dev/grad_dev/out_dev/rec_dev (and debug buffers) hold `frames` frames back to back;
- * frame f is filtered with frame_index = p->frame_index + f.  Same semantics as
- * `frames` calls of ctf_filter_frame.
+ * Filter `frames` consecutive frames in one pass over all waves (one kernel per path step;
+ * ctf_launches_per_call counts them).  uv_dev/grad_dev/out_dev/rec_dev (and debug buffers)
+ * hold `frames` frames back to back; frame f is filtered with frame_index =
+ * p->frame_index + f.  Same results as `frames` calls of ctf_filter_frame.
+ * Stream semantics: all work is ordered after earlier work on `stream` and later work on
+ * `stream` sees its results.  BC1 COLLAB bilinear with a workspace and >= 2 frames forks
+ * part of the work to a library-owned high-priority stream of the current device and joins
+ * it back into `stream` with events before returning (legal under CUDA graph capture);
+ * concurrent calls from several host threads are serialised while they enqueue.
  */
 int ctf_filter_batch(const ctf_texture *tex, const float *uv_dev, const uint16_t *grad_dev,
                      int32_t Wf, int32_t Hf, int32_t frames, const ctf_params *p,
