@@ -3,7 +3,7 @@
 usage: python scripts/ncu_traffic.py gpurun_out/prof_TAG.ncu-rep [frames width height]
 
 The report must hold the kernels of ONE ctf_filter_batch call (scripts/gpu_bench.sh captures
-`-k regex:ctf_collab_ -s 3 -c 3`: the lean exact kernel and the two rest passes of one step).
+`-k regex:ctf_collab_ -s 6 -c 6`: per frame group the lean exact kernel and the two rest passes).
 DRAM bytes are summed over those launches; bench.py reads the total as the per-call traffic.
 """
 import json
@@ -32,7 +32,8 @@ def main():
     for r in rows:
         name = r["Kernel Name"][0].split("(")[0].strip()
         b_r, b_w = scaled(r["dram__bytes_read.sum"]), scaled(r["dram__bytes_write.sum"])
-        per[name] = [b_r, b_w]
+        prev = per.get(name, [0.0, 0.0])
+        per[name] = [prev[0] + b_r, prev[1] + b_w]   # the frame groups' launches of one kernel summed
         rd += b_r
         wr += b_w
         ms += scaled(r["gpu__time_duration.sum"]) * 1e3
