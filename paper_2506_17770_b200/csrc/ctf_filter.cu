@@ -1340,6 +1340,9 @@ struct FastSmem {
 #ifndef CTF_PAIR
 #define CTF_PAIR 1  // BC1 non-debug: two waves share one decode pass (pair_front / pair_decode)
 #endif
+#ifndef CTF_PAIR_MLP
+#define CTF_PAIR_MLP 1  // latent MLP non-debug: two waves share one tensor-core decode
+#endif
 #ifndef CTF_PAIR_MINB
 #define CTF_PAIR_MINB 6  // paired lean kernel: resident CTAs per SM (40 registers)
 #endif
@@ -1577,7 +1580,7 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4
     return o;
 }
 
-// ------------------------------------------- paired exact path (BC1, non-debug build)
+// ------------------------------------------- paired exact path (non-debug build)
 // Two consecutive waves of a run share one decode pass.  Each wave still evaluates exactly
 // its own unique set U (n texels; its rank r is job base + r, h(r, A) = r up to the
 // offset), so colours, records and evaluation counts equal the one-wave path bit
@@ -1592,7 +1595,7 @@ struct PairFront {
     uint32_t rec;
 };
 // steps a1-a4 of lean_wave for one wave; the rank -> window-bit table goes to job base + r
-template <bool GRAD, class SM>
+template <bool GRAD, int FMT, class SM>
 __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 uv, uint2 gr, int base, uint8_t *bits0,
                                                 unsigned lane, unsigned lt) {
     const unsigned lanebit = 1u << lane;
@@ -1620,7 +1623,11 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     else if (__all_sync(FULL, dx < 6u && dy < 5u)) { K = 1; P = 6u; qmul = 43u; }      // 6x5
     else if (__all_sync(FULL, dx < 5u && dy < 6u)) { K = 1; P = 5u; qmul = 52u; }      // 5x6
     else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                                  // 8x8
-    if (K == 0) {
+    if (K == 0) {   // a 128-bit window (fallback kernel, BC1) or none (general kernel)
+        if (FMT != FMT_BC1) {
+            o.rec = kSlowMark;
+            return o;
+        }
         const bool w128 = __all_sync(FULL, dx < 16u && dy < 8u) || __all_sync(FULL, dx < 8u && dy < 16u) ||
                           __all_sync(FULL, dx < 32u && dy < 4u);
         o.rec = w128 ? kFbMark : kSlowMark;
@@ -1653,8 +1660,8 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
         const int rh = nl + __popc(wh & lt);
         st_shared_u8_if(bits + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
     }
-    if (n > 32) {   // fallback kernel
-        o.rec = kFbMark;
+    if (n > 32) {   // fallback kernel (BC1) / general kernel (latent MLP)
+        o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
         return o;
     }
     o.s = f.s;
@@ -1670,9 +1677,11 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     return o;
 }
 // step a5 for both waves: job j < nA decodes wave A's U[j], job nA + r wave B's U[r]
-template <class SM>
+// (latent MLP: the jobs of a pass are the rows of one tensor-core decode, mlp_decode_tc,
+// which runs one 16-row M tile when the pass has <= 16 jobs)
+template <int FMT, class SM>
 __device__ __forceinline__ void pair_decode(const KArgs &a, SM &fs, const uint8_t *bits, const PairFront &A,
-                                            const PairFront &B, unsigned lane) {
+                                            const PairFront &B, unsigned lane, const MlpCtx &mc) {
     const int J = A.n + B.n;
     for (int j0 = 0; j0 < J; j0 += 32) {   // one pass, two when nA + nB > 32 (warp-uniform)
         const int j = j0 + (int)lane;
@@ -1680,7 +1689,12 @@ __device__ __forceinline__ void pair_decode(const KArgs &a, SM &fs, const uint8_
         const uint32_t e = produced ? (uint32_t)bits[j] : 0u;   // (dy << 3) | dx
         const int qx = (inA ? A.minx : B.minx) + (int)(e & 7u);
         const int qy = (inA ? A.miny : B.miny) + (int)(e >> 3);
-        st_shared_f4_if(&fs.xch[j], bc1_decode_unorm_lut(a.tex, qx, qy, fs.lut), produced);
+        if constexpr (FMT == FMT_BC1) {
+            st_shared_f4_if(&fs.xch[j], bc1_decode_unorm_lut(a.tex, qx, qy, fs.lut), produced);
+        } else {
+            const float4 v = mlp_decode_tc(a.tex, *mc.tw, *mc.tsc, produced, qx, qy, lane);
+            st_shared_f4_if(&fs.xch[j], v, produced);
+        }
     }
 }
 // step a6 for one wave: gather + blend (weights as footprint2) and store; the empty wave
@@ -1904,7 +1918,7 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
 // GRAD: grad != NULL (magnified class); FORCE: CTF_FLAG_FORCE_FALLBACK (every live wave
 // goes to the rest kernel) — compile-time, so the hot loop tests neither.
 template <bool DBG, bool FORCE, int FMT>
-constexpr bool kPaired = CTF_PAIR && FMT == FMT_BC1 && !DBG && !FORCE;
+constexpr bool kPaired = CTF_PAIR && !DBG && !FORCE && (FMT == FMT_BC1 || CTF_PAIR_MLP);
 template <bool DBG, bool GRAD, bool FORCE, int FMT>
 __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FORCE, FMT> ? CTF_PAIR_MINB : CTF_FAST_MINB)
                                                                : CTF_MLP_COLLAB_MINB)
@@ -1977,18 +1991,18 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
             ld_stream_u2_if(gr_b, a.grad + (pix + 8u), (wx0 + 1 < wx1) & has_grad);
             for (int wx = wx0; wx < wx1; wx += 2, pix += 16u) {
               const bool hasB = wx + 1 < wx1;
-              const PairFront fa = pair_front<GRAD>(a, fs, uv_n, gr_n, 0, fs.bit_of_rank, lane, lt_mask);
+              const PairFront fa = pair_front<GRAD, FMT>(a, fs, uv_n, gr_n, 0, fs.bit_of_rank, lane, lt_mask);
               ld_stream_f2_if(uv_n, a.uv + (pix + 16u), wx + 2 < wx1);
               ld_stream_u2_if(gr_n, a.grad + (pix + 16u), (wx + 2 < wx1) & has_grad);
               PairFront fb;
               fb.n = 0;
               fb.rec = 0u;
               __syncwarp();   // A's push-table writes (all of them, also a rejected A's) before B's
-              if (hasB) fb = pair_front<GRAD>(a, fs, uv_b, gr_b, fa.n, fs.bit_of_rank, lane, lt_mask);
+              if (hasB) fb = pair_front<GRAD, FMT>(a, fs, uv_b, gr_b, fa.n, fs.bit_of_rank, lane, lt_mask);
               ld_stream_f2_if(uv_b, a.uv + (pix + 24u), wx + 3 < wx1);
               ld_stream_u2_if(gr_b, a.grad + (pix + 24u), (wx + 3 < wx1) & has_grad);
               __syncwarp();   // bit_of_rank written; the previous pair's xch reads are done
-              pair_decode(a, fs, fs.bit_of_rank, fa, fb, lane);
+              pair_decode<FMT>(a, fs, fs.bit_of_rank, fa, fb, lane, mc);
               __syncwarp();
               pair_back(a, fs, fa, pix);
               if (hasB) pair_back(a, fs, fb, pix + 8u);

@@ -376,3 +376,21 @@ def test_frame_groups_with_workspace(ctf, nf):
             o = oracle.filter_frame(tex, frames[f][0], frames[f][1], 3, fb, fl, seed=6, frame_index=40 + f)
             np.testing.assert_array_equal(res[0][1][f], o["rec"])
             assert np.abs(res[0][0][f].view(np.float32).astype(np.float64) - o["out"]).max() <= ATOL
+
+
+@pytest.mark.parametrize("wf,hf,mag,theta", [(104, 40, 1.5, 25.0), (136, 44, 0.9, 60.0)])
+def test_release_paired_runs_latent_mlp(ctf, wf, hf, mag, theta):
+    """The release latent-MLP COLLAB kernel decodes two waves' texels in one tensor-core pass
+    (one 16-row tile when nA + nB <= 16): records and colours equal the oracle's and the
+    debug kernel's (one wave per decode) colours bit for bit, on odd runs with partial waves."""
+    import oracle
+    tex = mlp_tex(64, 64, 5)
+    uv, g = synthetic.rotated_quad(wf, hf, 64, 64, mag, theta, coverage="circle", radius=15.0, jitter_seed=3)
+    dt = to_dev_tex(ctf, tex)
+    for mode, fb, fl in [(3, 3, 0), (3, 0, 0)]:
+        o = oracle.filter_frame(tex, uv, g, mode, fb, fl, seed=12, frame_index=2)
+        out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, fl, 12, 2)
+        np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+        assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
+        gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=12, frame_index=2)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), gg["out"].view(np.uint32))
