@@ -232,7 +232,7 @@ constexpr int kMlpWeights = 32 * 12 + 32 + 32 * 32 + 32 + 4 * 32 + 4;  // 1604 (
 // Latent-MLP weights travel BY VALUE in the kernel parameter block (constant bank 0):
 // every lane reads the same weight at the same time, so FFMA takes it straight from
 // the constant cache with no load instruction.  BC1 kernels get an empty struct.
-struct MlpWeights {
+struct alignas(16) MlpWeights {   // 16-B aligned in the kernel parameter block (vector constant loads)
     float v[kMlpWeights];
 };
 struct NoWeights {};
