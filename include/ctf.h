@@ -186,11 +186,7 @@ int ctf_filter_frame(const ctf_texture *tex, const float *uv_dev, const uint16_t
  * ctf_launches_per_call counts them).  uv_dev/grad_dev/out_dev/rec_dev (and debug buffers)
  * hold `frames` frames back to back; frame f is filtered with frame_index =
  * p->frame_index + f.  Same results as `frames` calls of ctf_filter_frame.
- * Stream semantics: all work is ordered after earlier work on `stream` and later work on
- * `stream` sees its results.  BC1 COLLAB bilinear with a workspace and >= 2 frames forks
- * part of the work to a library-owned high-priority stream of the current device and joins
- * it back into `stream` with events before returning (legal under CUDA graph capture);
- * concurrent calls from several host threads are serialised while they enqueue.
+ * All work is enqueued on `stream` (no library-owned streams, events or allocations).
  */
 int ctf_filter_batch(const ctf_texture *tex, const float *uv_dev, const uint16_t *grad_dev,
                      int32_t Wf, int32_t Hf, int32_t frames, const ctf_params *p,
@@ -237,14 +233,13 @@ size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames);
 /*
  * Kernel launches one call above issues (for launch accounting): format / mode / filter
  * as in ctf_texture / ctf_params, `frames` frames; flags: CTF_LAUNCH_BATCHED for
- * ctf_filter_batch (one pass over all frames) else ctf_filter_frame once per frame, plus
- * CTF_LAUNCH_WORKSPACE when ctf_params.workspace_dev holds a workspace.  The COLLAB bilinear
- * path is three kernels per pass for BC1 (the lean exact kernel; the lean fallback kernel
- * over the full waves it left; the general path over partial waves and windows wider than
- * 8x8) and two for the latent MLP (lean exact kernel + general path); every other path is
- * one.  A batched BC1 COLLAB bilinear call with a workspace cuts its frames into up to two
- * groups (three kernels each; the rest passes of a group run on a side stream, overlapping
- * the next group's lean kernel).  Returns -1 for an invalid format / mode / filter.
+ * ctf_filter_batch (one pass over all frames) else ctf_filter_frame once per frame
+ * (CTF_LAUNCH_WORKSPACE, a workspace in ctf_params, does not change the count).  The COLLAB
+ * bilinear path is three kernels per pass for BC1 (the lean exact kernel; the lean fallback
+ * kernel over the full waves it left; the general path over partial waves and windows wider
+ * than 8x8) and two for the latent MLP (lean exact kernel + general path); every other path
+ * is one (a workspace adds an 8-byte cudaMemsetAsync of the work-list counters, not counted).
+ * Returns -1 for an invalid format / mode / filter.
  */
 #define CTF_LAUNCH_BATCHED 1
 #define CTF_LAUNCH_WORKSPACE 2

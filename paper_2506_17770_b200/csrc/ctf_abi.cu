@@ -98,9 +98,7 @@ int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t 
         filter > 2)
         return -1;
     const int per_pass = ctf::launches_per_pass(format, mode, filter);
-    if (!(flags & CTF_LAUNCH_BATCHED)) return per_pass * (frames > 0 ? frames : 0);
-    const int groups = (flags & CTF_LAUNCH_WORKSPACE) ? ctf::collab_subbatches(format, mode, filter, frames) : 1;
-    return per_pass * groups;
+    return per_pass * ((flags & CTF_LAUNCH_BATCHED) ? 1 : (frames > 0 ? frames : 0));
 }
 
 int ctf_filter_batch(const ctf_texture *tex, const float *uv_dev, const uint16_t *grad_dev, int32_t Wf, int32_t Hf,

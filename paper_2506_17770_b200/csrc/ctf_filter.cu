@@ -21,7 +21,6 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
-#include <mutex>
 #include <type_traits>
 
 #include "ctf_device.cuh"
@@ -33,11 +32,6 @@ constexpr int kWarps = 8;  // warps per CTA
 #ifndef CTF_BC1_MINB
 #define CTF_BC1_MINB 4  // BC1: resident CTAs per SM (64 registers)
 #endif
-#ifndef CTF_SUBBATCH
-#define CTF_SUBBATCH 2  // BC1 COLLAB with work lists: frame groups whose rest passes overlap the next lean kernel (A/B r01: 2 > 1, 4, 8)
-#endif
-constexpr int kMaxSubbatch = 16;
-static_assert(CTF_SUBBATCH >= 1 && CTF_SUBBATCH <= kMaxSubbatch, "workspace holds kMaxSubbatch counter pairs");
 #ifndef CTF_BC1_ROUNDS
 #define CTF_BC1_ROUNDS 8  // BC1: target CTAs per resident CTA slot
 #endif
@@ -2399,33 +2393,6 @@ static cudaError_t launch_rest(const KArgs &k, const typename WeightsOf<FMT>::ty
     return cudaSuccess;
 }
 
-// Sub-batches (BC1 with work lists, >= 2 frames): the batch is cut into S groups of frames;
-// the lean kernels run in order on the caller's stream and each group's two rest passes on a
-// high-priority side stream as soon as its lean kernel is done, so they overlap the next
-// group's lean kernel (the rest passes are latency-bound at low occupancy, the lean kernel
-// issue-bound: together they fill more issue slots).  Per group the workspace holds its two
-// counters (all groups' counters first, one memset) and its two lists.
-static int subbatches(int frames) {
-    if (CTF_SUBBATCH <= 1 || frames < 2) return 1;
-    return frames < CTF_SUBBATCH ? frames : CTF_SUBBATCH;
-}
-struct SideStreams {   // per device, created on first use; enqueues are serialised by mu
-    std::mutex mu;
-    cudaStream_t side[64] = {};
-    cudaEvent_t ev[64][kMaxSubbatch + 1] = {};
-};
-static SideStreams g_side;
-static cudaError_t side_setup(int dev) {
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    if (g_side.side[dev]) return cudaSuccess;
-    int least = 0, greatest = 0;
-    cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&g_side.side[dev], cudaStreamNonBlocking, greatest);
-    for (int i = 0; e == cudaSuccess && i <= kMaxSubbatch; ++i)
-        e = cudaEventCreateWithFlags(&g_side.ev[dev][i], cudaEventDisableTiming);
-    return e;
-}
-
 template <int FMT, bool DBG>
 static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
     int dev = 0, sms = 0;
@@ -2433,44 +2400,13 @@ static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw,
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    const int F = (int)(k.nchunks / (unsigned)k.cpf);
-    const int S = (FMT == FMT_BC1 && k.lists) ? subbatches(F) : 1;
-    if (S == 1) {
-        if (k.lists) {   // work-list counters (the lists need no initialisation)
-            k.lcnt = k.lists;
-            k.lists += 64;
-            if ((e = cudaMemsetAsync(k.lcnt, 0, 2 * sizeof(uint32_t), stream)) != cudaSuccess) return e;
-        }
-        if ((e = launch_lean<FMT, DBG>(k, mw, dev, sms, stream)) != cudaSuccess) return e;
-        return launch_rest<FMT, DBG>(k, mw, dev, sms, stream);
+    if (k.lists) {   // work-list counters (the lists need no initialisation)
+        k.lcnt = k.lists;
+        k.lists += 64;
+        if ((e = cudaMemsetAsync(k.lcnt, 0, 2 * sizeof(uint32_t), stream)) != cudaSuccess) return e;
     }
-    std::lock_guard<std::mutex> lock(g_side.mu);
-    if ((e = side_setup(dev)) != cudaSuccess) return e;
-    cudaStream_t side = g_side.side[dev];
-    uint32_t *cnt = k.lists, *lists = k.lists + 64;
-    if ((e = cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t) * S, stream)) != cudaSuccess) return e;
-    for (int g = 0; g < S; ++g) {
-        const int f0 = (int)((long long)F * g / S), f1 = (int)((long long)F * (g + 1) / S);
-        const size_t px0 = (size_t)f0 * k.fpx, w0 = (size_t)f0 * (size_t)k.wpf;
-        KArgs kg = k;
-        kg.uv = k.uv + px0;
-        kg.grad = k.grad ? k.grad + px0 : nullptr;
-        kg.out = k.out + px0;
-        kg.rec = k.rec + w0;
-        if (k.dbg_pid) kg.dbg_pid = k.dbg_pid + px0;
-        if (k.dbg_sel) kg.dbg_sel = k.dbg_sel + px0;
-        kg.frame_index = k.frame_index + (uint32_t)f0;
-        kg.nchunks = (unsigned)k.cpf * (unsigned)(f1 - f0);
-        kg.nrec = (unsigned)(k.wpf * (f1 - f0));
-        kg.lcnt = cnt + 2 * g;
-        kg.lists = lists + 2 * w0;
-        if ((e = launch_lean<FMT, DBG>(kg, mw, dev, sms, stream)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(g_side.ev[dev][g], stream)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(side, g_side.ev[dev][g], 0)) != cudaSuccess) return e;
-        if ((e = launch_rest<FMT, DBG>(kg, mw, dev, sms, side)) != cudaSuccess) return e;
-    }
-    if ((e = cudaEventRecord(g_side.ev[dev][kMaxSubbatch], side)) != cudaSuccess) return e;
-    return cudaStreamWaitEvent(stream, g_side.ev[dev][kMaxSubbatch], 0);
+    if ((e = launch_lean<FMT, DBG>(k, mw, dev, sms, stream)) != cudaSuccess) return e;
+    return launch_rest<FMT, DBG>(k, mw, dev, sms, stream);
 }
 
 template <int FMT, int MODE>
@@ -2498,10 +2434,6 @@ static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::typ
 int launches_per_pass(int fmt, int mode, int filter) {
     if (!CTF_FAST || mode != MODE_COLLAB || filter != 0) return 1;
     return fmt == FMT_BC1 ? (CTF_REST_MERGED ? 2 : 3) : 2;   // latent MLP: lean exact + general
-}
-int collab_subbatches(int fmt, int mode, int filter, int frames) {   // frame groups of one batched call with a workspace
-    if (!CTF_FAST || fmt != FMT_BC1 || mode != MODE_COLLAB || filter != 0) return 1;
-    return subbatches(frames);
 }
 
 cudaError_t launch_filter_bc1(const LaunchArgs &a, cudaStream_t stream) {

@@ -12,8 +12,8 @@ tail -5 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:ctf_ -c 60 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu --no-configs > gpurun_out/ncu_launch_bench_$TAG.json 2>&1
 python scripts/launch_shares.py gpurun_out/launches_$TAG.csv
-# one full capture of the six BC1 COLLAB kernels (two frame groups) of one 64-frame step (the bench step)
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ctf_collab_ -s 6 -c 6 \
+# one full capture of the three BC1 COLLAB kernels of one 64-frame step (the bench step)
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ctf_collab_ -s 3 -c 3 \
     -o gpurun_out/prof_$TAG python bench.py --warmup 1 --profile-launches 1 > gpurun_out/ncu_full_$TAG.log 2>&1
 tail -3 gpurun_out/ncu_full_$TAG.log
 if [ "${MLPPROF:-0}" = "1" ]; then

@@ -3,7 +3,7 @@
 usage: python scripts/ncu_traffic.py gpurun_out/prof_TAG.ncu-rep [frames width height]
 
 The report must hold the kernels of ONE ctf_filter_batch call (scripts/gpu_bench.sh captures
-`-k regex:ctf_collab_ -s 6 -c 6`: per frame group the lean exact kernel and the two rest passes).
+`-k regex:ctf_collab_ -s 3 -c 3`: the lean exact kernel and the two rest passes).
 DRAM bytes are summed over those launches; bench.py reads the total as the per-call traffic.
 """
 import json

@@ -79,7 +79,6 @@ def test_validation_errors_without_gpu():
     assert lib.ctf_launches_per_call(1, 0, 0, 64, 1) == 1 and lib.ctf_launches_per_call(2, 3, 0, 8, 0) == 16
     assert lib.ctf_launches_per_call(2, 4, 0, 8, 1) == 1   # Box: the general kernel
     assert lib.ctf_launches_per_call(3, 3, 0, 1, 1) == -1
-    # batched BC1 COLLAB with a workspace: up to two frame groups of three kernels
-    assert lib.ctf_launches_per_call(1, 3, 0, 64, 3) == 6 and lib.ctf_launches_per_call(1, 3, 0, 3, 3) == 6
-    assert lib.ctf_launches_per_call(1, 3, 0, 1, 3) == 3 and lib.ctf_launches_per_call(2, 3, 0, 64, 3) == 2
+    # the workspace flag does not change the count
+    assert lib.ctf_launches_per_call(1, 3, 0, 64, 3) == 3 and lib.ctf_launches_per_call(2, 3, 0, 64, 3) == 2
     assert lib.ctf_launches_per_call(1, 3, 1, 64, 3) == 1   # bicubic: one kernel

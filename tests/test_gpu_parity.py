@@ -348,10 +348,10 @@ def test_release_paired_runs(ctf, wf, hf, mag, theta, cov):
 
 
 @pytest.mark.parametrize("nf", [2, 3, 5])
-def test_frame_groups_with_workspace(ctf, nf):
-    """A batched BC1 COLLAB call with a workspace runs its frames in groups whose rest passes
-    go to a side stream: records, colours and debug outputs equal the record-scan path (no
-    workspace, one group) bit for bit and the per-frame oracle, for every fallback."""
+def test_multi_frame_work_lists(ctf, nf):
+    """A batched BC1 COLLAB call with a workspace (work lists over all frames of the batch):
+    records, colours and debug outputs equal the record-scan path (no workspace) bit for bit
+    and the per-frame oracle, for every fallback."""
     import oracle
     tex = bc1_tex(128, 128, 4, "image")
     frames = [synthetic.rotated_quad(64, 28, 128, 128, 0.8 + 0.35 * f, 17.0 * f, coverage="circle" if f % 2 else None,
