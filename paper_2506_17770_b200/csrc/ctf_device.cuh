@@ -19,7 +19,19 @@ enum { FLAG_DEBUG = 1u, FLAG_FORCE_FALLBACK = 2u };
 enum { PATH_EXACT = 0, PATH_FB_STF = 1, PATH_FB_WC = 2, PATH_FB_C = 3, PATH_FB_CPLUS = 4,
        PATH_4TAP = 5, PATH_STF = 6, PATH_WC = 7 };
 
-__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+#ifndef CTF_LANEID_SREG
+#define CTF_LANEID_SREG 1
+#endif
+// the lane index: %laneid is one S2R when ptxas rematerialises it (threadIdx.x & 31 is two)
+__device__ __forceinline__ unsigned lane_id() {
+#if CTF_LANEID_SREG
+    unsigned l;
+    asm("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+#else
+    return threadIdx.x & 31u;
+#endif
+}
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
