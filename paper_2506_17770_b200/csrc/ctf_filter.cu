@@ -1898,6 +1898,12 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
     else if (__all_sync(FULL, dx < 16u && dy < 8u)) { K = 4; lgP = 4u; }
     else if (__all_sync(FULL, dx < 8u && dy < 16u)) { K = 4; lgP = 3u; }
     else if (__all_sync(FULL, dx < 32u && dy < 4u)) { K = 4; lgP = 5u; }
+    // Mask sampling: exact also needs the AABB inside the fixed grid; a wave outside
+    // it takes the fallback exactly like a forced one
+    if (a.variant >= VAR_MASK16) {
+        const unsigned lim = a.variant == VAR_MASK16 ? 16u : 11u;
+        force = force || !__all_sync(FULL, dx < lim && dy < lim);
+    }
     if (K == 1 || K == 2) return fb_wave_k<DBG, 2>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
     if (K == 4) return fb_wave_k<DBG, 4>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
     LeanOut o;
@@ -2411,7 +2417,10 @@ static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw,
 
 template <int FMT, int MODE>
 static cudaError_t launch_dbg(const KArgs &k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
-    if (CTF_FAST && MODE == MODE_COLLAB && k.variant == VAR_LIST)
+    // List and Mask 16x16 / 11x11 share the lean kernels: every lean exact window is <= 8x8,
+    // inside both grids, so there Mask's success test is List's; the lean fallback kernel adds
+    // the grid test for its wider windows.  Box (another producer mapping) runs the general kernel.
+    if (CTF_FAST && MODE == MODE_COLLAB && k.variant != VAR_BOX)
         return (k.flags & FLAG_DEBUG) ? launch_fast<FMT, true>(k, mw, stream) : launch_fast<FMT, false>(k, mw, stream);
     return (k.flags & FLAG_DEBUG) ? launch_one<FMT, MODE, true>(k, mw, stream)
                                   : launch_one<FMT, MODE, false>(k, mw, stream);
@@ -2432,7 +2441,8 @@ static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::typ
 #endif
 #if CTF_TU_FMT == 1
 int launches_per_pass(int fmt, int mode, int filter) {
-    if (!CTF_FAST || mode != MODE_COLLAB || filter != 0) return 1;
+    if (!CTF_FAST || (mode != MODE_COLLAB && mode != MODE_COLLAB + 2 && mode != MODE_COLLAB + 3) || filter != 0)
+        return 1;   // List (3), Mask16 (5), Mask11 (6) run the lean kernels
     return fmt == FMT_BC1 ? (CTF_REST_MERGED ? 2 : 3) : 2;   // latent MLP: lean exact + general
 }
 

@@ -316,7 +316,7 @@ def test_exact_waves_with_128bit_windows(ctf):
             uv[4 + ly, wx * 8 + lx, 0] = (step * lx + 0.5 + ly % 2) / W       # two rows of footprints
             uv[4 + ly, wx * 8 + lx, 1] = (row + 0.25 + (ly // 2) * 3.0) / H
     import oracle
-    for mode, fb, fl in [(3, 3, 0), (3, 0, 0), (3, 2, 2)]:
+    for mode, fb, fl in [(3, 3, 0), (3, 0, 0), (3, 2, 2), (5, 3, 0), (6, 3, 0), (5, 1, 0)]:
         o = run_oracle(tex, uv, None, mode, fb, fl, seed=9)
         gg = run_gpu(ctf, tex, uv, None, mode, fb, fl, seed=9)
         assert_parity(gg, o, f"fb={fb} flags={fl}")
@@ -394,3 +394,45 @@ def test_release_paired_runs_latent_mlp(ctf, wf, hf, mag, theta):
         assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
         gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=12, frame_index=2)
         assert np.array_equal(out.cpu().numpy().view(np.uint32), gg["out"].view(np.uint32))
+
+
+def anisotropic_quad(wf, hf, tex_w, tex_h, sx, sy, theta_deg, center=(0.5, 0.5)):
+    """uv of a plane stretched by (sx, sy) texels per pixel and rotated by theta: thin slanted
+    footprints whose AABB is wide while n stays <= 32 (a linear map, no RNG)."""
+    yy, xx = np.mgrid[0:hf, 0:wf].astype(np.float64)
+    px, py = xx + 0.5 - wf / 2, yy + 0.5 - hf / 2
+    c, s = np.cos(np.radians(theta_deg)), np.sin(np.radians(theta_deg))
+    tx, ty = c * sx * px - s * sy * py, s * sx * px + c * sy * py
+    uv = np.stack([(tx + 0.37) / tex_w + center[0], (ty + 0.21) / tex_h + center[1]], -1).astype(np.float32)
+    g = np.zeros((hf, wf, 4), np.float16)
+    g[..., 0], g[..., 1], g[..., 2], g[..., 3] = c * sx, s * sx, -s * sy, c * sy
+    return uv, g
+
+
+@pytest.mark.parametrize("sx,sy,theta,center", [(1.4, 0.05, 10.0, (0.5, 0.5)), (1.5, 0.2, 15.0, (0.5, 0.5)),
+                                                (1.3, 0.1, 5.0, (0.5, 0.5)), (2.6, 0.05, 0.0, (0.5, 0.0))])
+def test_mask_variants_in_the_lean_kernels(ctf, sx, sy, theta, center):
+    """Mask 16x16 / 11x11 run the lean kernels: FULL waves with n <= 32 whose AABB exceeds the
+    grid (wide thin footprints; at the clamped top edge one texel row, so n <= 32 up to 32
+    wide) must fall back in the lean fallback kernel exactly where the oracle's Mask test does,
+    with and without the work-list workspace, debug and release builds."""
+    import oracle
+    W = H = 128
+    tex = bc1_tex(W, H, 7, "image")
+    uv, g = anisotropic_quad(64, 32, W, H, sx, sy, theta, center)
+    lst = oracle.filter_frame(tex, uv, g, 3, 3, 0, 4)["rec"]
+    rejected = 0
+    for mode in (5, 6):
+        for fb in (3, 2, 0):
+            o = run_oracle(tex, uv, g, mode, fb, 0, seed=4, frame_index=1)
+            gg = run_gpu(ctf, tex, uv, g, mode, fb, 0, seed=4, frame_index=1)
+            assert_parity(gg, o, f"mode={mode} fb={fb}")
+            assert gg["unread"] == 0
+            dt = to_dev_tex(ctf, tex)
+            out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, 0, 4, 1,
+                                        workspace=None)
+            np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+            assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
+        m = oracle.filter_frame(tex, uv, g, mode, 3, 0, 4)["rec"]
+        rejected += int(((((lst >> 22) & 7) == 0) & (((m >> 22) & 7) != 0)).sum())
+    assert rejected > 0   # the scene exercises Mask's grid test on List-exact waves
