@@ -1482,7 +1482,13 @@ __device__ __forceinline__ bool wave_magnified(uint2 gr, bool has_grad) {
 // FMT_MLP: the wave's produced texels go through the tensor-core decoder together
 // (mlp_decode_tc, rows = lanes); its fallback and 128-bit-window waves go to the general
 // kernel (kSlowMark) — there is no lean fallback for the latent-MLP format.
-template <bool DBG, int FMT, class SM>
+// BOX: Box Sampling: exact iff the AABB area w*h <= a = 32; job j < w*h decodes
+// AABB texel (j mod w, j div w) (LaneIdxToCoord), a corner reads its AABB-local
+// index (CoordToLaneIdx); n (unique texels) goes to the record only.  The lean
+// windows are <= 8 wide and tall, so j div w = trunc((j + 1/2) / w) in fp32 is exact.
+__device__ __forceinline__ int box_row(unsigned j, int w) { return (int)__fdividef((float)j + 0.5f, (float)w); }
+
+template <bool DBG, int FMT, class SM, bool BOX = false>
 __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4 *lut, const MlpCtx &mc,
                                              float2 uv, uint2 gr, bool has_grad) {
     const unsigned lane = lane_id(), lt = lanemask_lt(), lanebit = 1u << lane;
@@ -1525,7 +1531,7 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4
         n = __popc(wm);
         r0 = __popc(wm & ((1u << t0) - 1u));
         r2 = __popc(wm & ((1u << t2) - 1u));
-        st_shared_u8_if(fs.bit_of_rank + __popc(wm & lt), lane, wm & lanebit);
+        if (!BOX) st_shared_u8_if(fs.bit_of_rank + __popc(wm & lt), lane, wm & lanebit);
     } else {
         const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
         const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
@@ -1534,13 +1540,23 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4
         n = nl + __popc(wh);
         r0 = rank64(wl, wh, t0);
         r2 = rank64(wl, wh, t2);
-        st_shared_u8_if(fs.bit_of_rank + __popc(wl & lt), lane, wl & lanebit);
-        const int rh = nl + __popc(wh & lt);
-        st_shared_u8_if(fs.bit_of_rank + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
+        if (!BOX) {
+            st_shared_u8_if(fs.bit_of_rank + __popc(wl & lt), lane, wl & lanebit);
+            const int rh = nl + __popc(wh & lt);
+            st_shared_u8_if(fs.bit_of_rank + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
+        }
     }
-    // ---- a4: exact iff n <= a = 32 (always for a 32-bit window)
-    if (n > 32) {   // fallback kernel (BC1) / general kernel (latent MLP)
-        if (FMT != FMT_BC1) o.rec = kSlowMark;
+    int evals = n;   // jobs: n (List), the AABB area (Box)
+    if constexpr (BOX) {
+        const int bw = (int)__reduce_max_sync(FULL, dx) + 1, bh = (int)__reduce_max_sync(FULL, dy) + 1;
+        evals = bw * bh;
+        if (evals > 32) return o;   // Box fallback (lean fallback kernel)
+        const int jq = box_row(lane, bw);
+        st_shared_u8_if(fs.bit_of_rank + lane, ((uint32_t)jq << lgP) | (lane - (uint32_t)(jq * bw)), (int)lane < evals);
+        r0 = (f.ya - miny) * bw + (f.xa - minx);
+        r2 = r0 + (f.yb - f.ya) * bw;
+    } else if (n > 32) {   // ---- a4: exact iff n <= a = 32 (always for a 32-bit window)
+        if (FMT != FMT_BC1) o.rec = kSlowMark;   // fallback kernel (BC1) / general kernel (latent MLP)
         return o;
     }
     o.done = true;
@@ -1548,7 +1564,7 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4
     // ---- a5: lane r < n produces U[r] (h(r, A) = r); one decode site, fp32 once
     // (SIMT: the decoder runs on every lane; non-producers decode the window origin and
     // do not store — predicated, so the loop stays free of divergent regions)
-    const bool produced = (int)lane < n;
+    const bool produced = (int)lane < evals;
     const uint32_t e = produced ? (uint32_t)fs.bit_of_rank[lane] : 0u;
     const int qx = minx + (int)(e & pmask), qy = miny + (int)(e >> lgP);
     const float4 *xv;   // rank -> produced value
@@ -1565,10 +1581,10 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4
     // ---- a6: gather (ranks rho_k) + blend
     const float4 p[4] = {xv[r0], xv[r0 + (int)dxs], xv[r2], xv[r2 + (int)dxs]};
     o.color = blend4f(p, f.w);
-    o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
+    o.rec = ((uint32_t)n << 8) | (uint32_t)evals | (32u << 16) | ((uint32_t)wave_mag << 25);
     if (DBG && a.dbg_unread) {
-        const unsigned bad = __reduce_add_sync(FULL, (unsigned)(r0 >= n) + (unsigned)(r0 + (int)dxs >= n) +
-                                                         (unsigned)(r2 >= n) + (unsigned)(r2 + (int)dxs >= n));
+        const unsigned bad = __reduce_add_sync(FULL, (unsigned)(r0 >= evals) + (unsigned)(r0 + (int)dxs >= evals) +
+                                                         (unsigned)(r2 >= evals) + (unsigned)(r2 + (int)dxs >= evals));
         if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
     }
     return o;
@@ -1589,7 +1605,7 @@ struct PairFront {
     uint32_t rec;
 };
 // steps a1-a4 of lean_wave for one wave; the rank -> window-bit table goes to job base + r
-template <bool GRAD, int FMT, class SM>
+template <bool GRAD, int FMT, class SM, bool BOX = false>
 __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 uv, uint2 gr, int base, uint8_t *bits0,
                                                 unsigned lane, unsigned lt) {
     const unsigned lanebit = 1u << lane;
@@ -1641,7 +1657,7 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
         n = __popc(wm);
         r0 = __popc(wm & ((1u << t0) - 1u));
         r2 = __popc(wm & ((1u << t2) - 1u));
-        st_shared_u8_if(bits + __popc(wm & lt), code, wm & lanebit);
+        if (!BOX) st_shared_u8_if(bits + __popc(wm & lt), code, wm & lanebit);
     } else {
         const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
         const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
@@ -1650,11 +1666,25 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
         n = nl + __popc(wh);
         r0 = rank64(wl, wh, t0);
         r2 = rank64(wl, wh, t2);
-        st_shared_u8_if(bits + __popc(wl & lt), lane, wl & lanebit);
-        const int rh = nl + __popc(wh & lt);
-        st_shared_u8_if(bits + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
+        if (!BOX) {
+            st_shared_u8_if(bits + __popc(wl & lt), lane, wl & lanebit);
+            const int rh = nl + __popc(wh & lt);
+            st_shared_u8_if(bits + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
+        }
     }
-    if (n > 32) {   // fallback kernel (BC1) / general kernel (latent MLP)
+    int evals = n;   // jobs: n (List), the AABB area (Box, see lean_wave)
+    if constexpr (BOX) {
+        const int bw = (int)__reduce_max_sync(FULL, dx) + 1, bh = (int)__reduce_max_sync(FULL, dy) + 1;
+        evals = bw * bh;
+        if (evals > 32) {   // Box fallback (lean fallback kernel)
+            o.rec = kFbMark;
+            return o;
+        }
+        const int jq = box_row(lane, bw);
+        st_shared_u8_if(bits + lane, ((uint32_t)jq << 3) | (lane - (uint32_t)(jq * bw)), (int)lane < evals);
+        r0 = (f.ya - miny) * bw + (f.xa - minx);
+        r2 = r0 + (f.yb - f.ya) * bw;
+    } else if (n > 32) {   // fallback kernel (BC1) / general kernel (latent MLP)
         o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
         return o;
     }
@@ -1664,10 +1694,10 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     o.a0 = x0 + 16u * (uint32_t)r0;
     o.a2 = x0 + 16u * (uint32_t)r2;
     o.dxs16 = 16u * dxs;
-    o.n = n;
+    o.n = evals;
     o.minx = minx;
     o.miny = miny;
-    o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
+    o.rec = ((uint32_t)n << 8) | (uint32_t)evals | (32u << 16) | ((uint32_t)wave_mag << 25);
     return o;
 }
 // step a5 for both waves: job j < nA decodes wave A's U[j], job nA + r wave B's U[r]
@@ -1903,6 +1933,10 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
     if (a.variant >= VAR_MASK16) {
         const unsigned lim = a.variant == VAR_MASK16 ? 16u : 11u;
         force = force || !__all_sync(FULL, dx < lim && dy < lim);
+    } else if (a.variant == VAR_BOX) {   // Box: exact iff the AABB area <= 32 (its own producer mapping)
+        const int area = (int)(__reduce_max_sync(FULL, dx) + 1u) * (int)(__reduce_max_sync(FULL, dy) + 1u);
+        if (area <= 32) K = 0;   // -> general path
+        force = true;
     }
     if (K == 1 || K == 2) return fb_wave_k<DBG, 2>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
     if (K == 4) return fb_wave_k<DBG, 4>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
@@ -1919,7 +1953,7 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
 // goes to the rest kernel) — compile-time, so the hot loop tests neither.
 template <bool DBG, bool FORCE, int FMT>
 constexpr bool kPaired = CTF_PAIR && !DBG && !FORCE && (FMT == FMT_BC1 || CTF_PAIR_MLP);
-template <bool DBG, bool GRAD, bool FORCE, int FMT>
+template <bool DBG, bool GRAD, bool FORCE, int FMT, bool BOX = false>
 __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FORCE, FMT> ? CTF_PAIR_MINB : CTF_FAST_MINB)
                                                                : CTF_MLP_COLLAB_MINB)
     ctf_collab_lean_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
@@ -1991,14 +2025,14 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
             ld_stream_u2_if(gr_b, a.grad + (pix + 8u), (wx0 + 1 < wx1) & has_grad);
             for (int wx = wx0; wx < wx1; wx += 2, pix += 16u) {
               const bool hasB = wx + 1 < wx1;
-              const PairFront fa = pair_front<GRAD, FMT>(a, fs, uv_n, gr_n, 0, fs.bit_of_rank, lane, lt_mask);
+              const PairFront fa = pair_front<GRAD, FMT, SmemT, BOX>(a, fs, uv_n, gr_n, 0, fs.bit_of_rank, lane, lt_mask);
               ld_stream_f2_if(uv_n, a.uv + (pix + 16u), wx + 2 < wx1);
               ld_stream_u2_if(gr_n, a.grad + (pix + 16u), (wx + 2 < wx1) & has_grad);
               PairFront fb;
               fb.n = 0;
               fb.rec = 0u;
               __syncwarp();   // A's push-table writes (all of them, also a rejected A's) before B's
-              if (hasB) fb = pair_front<GRAD, FMT>(a, fs, uv_b, gr_b, fa.n, fs.bit_of_rank, lane, lt_mask);
+              if (hasB) fb = pair_front<GRAD, FMT, SmemT, BOX>(a, fs, uv_b, gr_b, fa.n, fs.bit_of_rank, lane, lt_mask);
               ld_stream_f2_if(uv_b, a.uv + (pix + 24u), wx + 3 < wx1);
               ld_stream_u2_if(gr_b, a.grad + (pix + 24u), (wx + 3 < wx1) & has_grad);
               __syncwarp();   // bit_of_rank written; the previous pair's xch reads are done
@@ -2024,7 +2058,7 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
             const unsigned A = __ballot_sync(FULL, active);
             uint32_t rec;
             if (!FORCE && A == FULL) {
-                const LeanOut o = lean_wave<DBG, FMT>(a, fs, fs.lut, mc, uv, gr, GRAD);
+                const LeanOut o = lean_wave<DBG, FMT, SmemT, BOX>(a, fs, fs.lut, mc, uv, gr, GRAD);
                 rec = o.rec;
                 if (o.done) {
                     st_stream_f4(a.out + pix, o.color);
@@ -2351,6 +2385,10 @@ static cudaError_t launch_lean(KArgs &k, const typename WeightsOf<FMT>::type &mw
     const bool grad = k.grad != nullptr, force = (k.flags & FLAG_FORCE_FALLBACK) != 0;
     auto kern = grad ? (force ? ctf_collab_lean_kernel<DBG, true, true, FMT> : ctf_collab_lean_kernel<DBG, true, false, FMT>)
                      : (force ? ctf_collab_lean_kernel<DBG, false, true, FMT> : ctf_collab_lean_kernel<DBG, false, false, FMT>);
+    if constexpr (FMT == FMT_BC1) {   // Box (forced: every live wave goes to the general path anyway)
+        if (k.variant == VAR_BOX && !force)
+            kern = grad ? ctf_collab_lean_kernel<DBG, true, false, FMT, true> : ctf_collab_lean_kernel<DBG, false, false, FMT, true>;
+    }
     const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
     int per_sm = 0;
     cudaError_t e;
@@ -2419,8 +2457,8 @@ template <int FMT, int MODE>
 static cudaError_t launch_dbg(const KArgs &k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
     // List and Mask 16x16 / 11x11 share the lean kernels: every lean exact window is <= 8x8,
     // inside both grids, so there Mask's success test is List's; the lean fallback kernel adds
-    // the grid test for its wider windows.  Box (another producer mapping) runs the general kernel.
-    if (CTF_FAST && MODE == MODE_COLLAB && k.variant != VAR_BOX)
+    // the grid test for its wider windows.  Box (BC1) has its own lean exact instantiation.
+    if (CTF_FAST && MODE == MODE_COLLAB && (k.variant != VAR_BOX || FMT == FMT_BC1))
         return (k.flags & FLAG_DEBUG) ? launch_fast<FMT, true>(k, mw, stream) : launch_fast<FMT, false>(k, mw, stream);
     return (k.flags & FLAG_DEBUG) ? launch_one<FMT, MODE, true>(k, mw, stream)
                                   : launch_one<FMT, MODE, false>(k, mw, stream);
@@ -2441,8 +2479,9 @@ static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::typ
 #endif
 #if CTF_TU_FMT == 1
 int launches_per_pass(int fmt, int mode, int filter) {
-    if (!CTF_FAST || (mode != MODE_COLLAB && mode != MODE_COLLAB + 2 && mode != MODE_COLLAB + 3) || filter != 0)
-        return 1;   // List (3), Mask16 (5), Mask11 (6) run the lean kernels
+    if (!CTF_FAST || mode < MODE_COLLAB || mode > MODE_COLLAB + 3 || (mode == MODE_COLLAB + 1 && fmt != FMT_BC1) ||
+        filter != 0)
+        return 1;   // List (3), Mask16 (5), Mask11 (6) and BC1 Box (4) run the lean kernels
     return fmt == FMT_BC1 ? (CTF_REST_MERGED ? 2 : 3) : 2;   // latent MLP: lean exact + general
 }
 

@@ -82,3 +82,21 @@ def test_validation_errors_without_gpu():
     # the workspace flag does not change the count
     assert lib.ctf_launches_per_call(1, 3, 0, 64, 3) == 3 and lib.ctf_launches_per_call(2, 3, 0, 64, 3) == 2
     assert lib.ctf_launches_per_call(1, 3, 1, 64, 3) == 1   # bicubic: one kernel
+
+
+def test_workspace_and_launch_accounting_per_mode():
+    """Host logic: which modes take the lean kernels' work-list workspace and how many launches
+    a call makes (List / Mask / BC1 Box: lean exact + lean fallback + general; latent-MLP Box
+    and every other mode: one general kernel)."""
+    import torch
+    import paper_2506_17770_b200.ctf as ctf
+    bc1 = ctf.Texture.bc1(torch.zeros(8 * 64, dtype=torch.uint8), 32, 32, device="cpu")
+    mlp = ctf.Texture(ctf.FMT_LATENT_MLP, 32, 32, torch.zeros(8 * 8 * 8, dtype=torch.float16))
+    for mode in range(7):
+        lean_bc1 = mode in (ctf.MODE_COLLAB, ctf.MODE_BOX, ctf.MODE_MASK16, ctf.MODE_MASK11)
+        lean_mlp = mode in (ctf.MODE_COLLAB, ctf.MODE_MASK16, ctf.MODE_MASK11)
+        assert (ctf.workspace_for(bc1, mode, 0, 64, 32, 2, "cpu") is not None) == lean_bc1, mode
+        assert (ctf.workspace_for(mlp, mode, 0, 64, 32, 2, "cpu") is not None) == lean_mlp, mode
+        assert ctf.launches_per_call(ctf.FMT_BC1, mode, 0, 1) == (3 if lean_bc1 else 1), mode
+        assert ctf.launches_per_call(ctf.FMT_LATENT_MLP, mode, 0, 1) == (2 if lean_mlp else 1), mode
+        assert ctf.workspace_for(bc1, mode, 1, 64, 32, 2, "cpu") is None   # bicubic: no work lists

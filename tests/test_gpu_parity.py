@@ -247,7 +247,8 @@ def test_abi_errors(ctf):
     assert e.value.code == ctf.CTF_EINVAL
 
 
-@pytest.mark.parametrize("mode,fb,fl", [(3, 3, 0), (3, 2, 0), (3, 0, 2), (0, 0, 0), (2, 0, 0)])
+@pytest.mark.parametrize("mode,fb,fl", [(3, 3, 0), (3, 2, 0), (3, 0, 2), (0, 0, 0), (2, 0, 0), (4, 3, 0), (4, 1, 0),
+                                        (5, 3, 0), (6, 2, 0)])
 def test_release_kernel_matches_oracle(ctf, mode, fb, fl):
     """The non-debug kernel instantiation (what bench.py runs) against the oracle."""
     import oracle
@@ -316,7 +317,7 @@ def test_exact_waves_with_128bit_windows(ctf):
             uv[4 + ly, wx * 8 + lx, 0] = (step * lx + 0.5 + ly % 2) / W       # two rows of footprints
             uv[4 + ly, wx * 8 + lx, 1] = (row + 0.25 + (ly // 2) * 3.0) / H
     import oracle
-    for mode, fb, fl in [(3, 3, 0), (3, 0, 0), (3, 2, 2), (5, 3, 0), (6, 3, 0), (5, 1, 0)]:
+    for mode, fb, fl in [(3, 3, 0), (3, 0, 0), (3, 2, 2), (5, 3, 0), (6, 3, 0), (5, 1, 0), (4, 3, 0), (4, 2, 0)]:
         o = run_oracle(tex, uv, None, mode, fb, fl, seed=9)
         gg = run_gpu(ctf, tex, uv, None, mode, fb, fl, seed=9)
         assert_parity(gg, o, f"fb={fb} flags={fl}")
@@ -411,8 +412,9 @@ def anisotropic_quad(wf, hf, tex_w, tex_h, sx, sy, theta_deg, center=(0.5, 0.5))
 
 @pytest.mark.parametrize("sx,sy,theta,center", [(1.4, 0.05, 10.0, (0.5, 0.5)), (1.5, 0.2, 15.0, (0.5, 0.5)),
                                                 (1.3, 0.1, 5.0, (0.5, 0.5)), (2.6, 0.05, 0.0, (0.5, 0.0))])
-def test_mask_variants_in_the_lean_kernels(ctf, sx, sy, theta, center):
-    """Mask 16x16 / 11x11 run the lean kernels: FULL waves with n <= 32 whose AABB exceeds the
+def test_mask_and_box_variants_in_the_lean_kernels(ctf, sx, sy, theta, center):
+    """Box and Mask 16x16 / 11x11 run the lean kernels (Box: AABB-order producers, AABB-area
+    evaluations; both exact and fallback decided by its area test); Mask: FULL waves with n <= 32 whose AABB exceeds the
     grid (wide thin footprints; at the clamped top edge one texel row, so n <= 32 up to 32
     wide) must fall back in the lean fallback kernel exactly where the oracle's Mask test does,
     with and without the work-list workspace, debug and release builds."""
@@ -422,7 +424,7 @@ def test_mask_variants_in_the_lean_kernels(ctf, sx, sy, theta, center):
     uv, g = anisotropic_quad(64, 32, W, H, sx, sy, theta, center)
     lst = oracle.filter_frame(tex, uv, g, 3, 3, 0, 4)["rec"]
     rejected = 0
-    for mode in (5, 6):
+    for mode in (4, 5, 6):
         for fb in (3, 2, 0):
             o = run_oracle(tex, uv, g, mode, fb, 0, seed=4, frame_index=1)
             gg = run_gpu(ctf, tex, uv, g, mode, fb, 0, seed=4, frame_index=1)
@@ -434,5 +436,7 @@ def test_mask_variants_in_the_lean_kernels(ctf, sx, sy, theta, center):
             np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
             assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
         m = oracle.filter_frame(tex, uv, g, mode, 3, 0, 4)["rec"]
+        if mode == 4:
+            continue
         rejected += int(((((lst >> 22) & 7) == 0) & (((m >> 22) & 7) != 0)).sum())
     assert rejected > 0   # the scene exercises Mask's grid test on List-exact waves
