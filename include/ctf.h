@@ -124,7 +124,7 @@ typedef struct {
     int32_t max_evals;     /* exact-path evaluations per lane: 0 or 1, or 2 (bicubic only)  */
     void *workspace_dev;   /* optional device scratch (ABI 4), >= ctf_filter_workspace_bytes()
                               bytes, 16-byte aligned, owned by the caller, contents need no
-                              initialisation; used by the COLLAB / MASK16 / MASK11 (and BC1 BOX) bilinear paths for
+                              initialisation; used by the COLLAB / BOX / MASK16 / MASK11 bilinear paths for
                               compact work lists of its fallback / general waves (no record
                               scans, balanced second passes).  NULL: the record buffer doubles
                               as the work list.  Results are identical either way.  Calls

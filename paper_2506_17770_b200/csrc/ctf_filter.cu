@@ -1550,7 +1550,10 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4
     if constexpr (BOX) {
         const int bw = (int)__reduce_max_sync(FULL, dx) + 1, bh = (int)__reduce_max_sync(FULL, dy) + 1;
         evals = bw * bh;
-        if (evals > 32) return o;   // Box fallback (lean fallback kernel)
+        if (evals > 32) {   // Box fallback: lean fallback kernel (BC1) / general kernel (latent MLP)
+            if (FMT != FMT_BC1) o.rec = kSlowMark;
+            return o;
+        }
         const int jq = box_row(lane, bw);
         st_shared_u8_if(fs.bit_of_rank + lane, ((uint32_t)jq << lgP) | (lane - (uint32_t)(jq * bw)), (int)lane < evals);
         r0 = (f.ya - miny) * bw + (f.xa - minx);
@@ -1676,8 +1679,8 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     if constexpr (BOX) {
         const int bw = (int)__reduce_max_sync(FULL, dx) + 1, bh = (int)__reduce_max_sync(FULL, dy) + 1;
         evals = bw * bh;
-        if (evals > 32) {   // Box fallback (lean fallback kernel)
-            o.rec = kFbMark;
+        if (evals > 32) {   // Box fallback: lean fallback kernel (BC1) / general kernel (latent MLP)
+            o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
             return o;
         }
         const int jq = box_row(lane, bw);
@@ -2385,10 +2388,8 @@ static cudaError_t launch_lean(KArgs &k, const typename WeightsOf<FMT>::type &mw
     const bool grad = k.grad != nullptr, force = (k.flags & FLAG_FORCE_FALLBACK) != 0;
     auto kern = grad ? (force ? ctf_collab_lean_kernel<DBG, true, true, FMT> : ctf_collab_lean_kernel<DBG, true, false, FMT>)
                      : (force ? ctf_collab_lean_kernel<DBG, false, true, FMT> : ctf_collab_lean_kernel<DBG, false, false, FMT>);
-    if constexpr (FMT == FMT_BC1) {   // Box (forced: every live wave goes to the general path anyway)
-        if (k.variant == VAR_BOX && !force)
-            kern = grad ? ctf_collab_lean_kernel<DBG, true, false, FMT, true> : ctf_collab_lean_kernel<DBG, false, false, FMT, true>;
-    }
+    if (k.variant == VAR_BOX && !force)   // Box (forced: every live wave goes to the general path anyway)
+        kern = grad ? ctf_collab_lean_kernel<DBG, true, false, FMT, true> : ctf_collab_lean_kernel<DBG, false, false, FMT, true>;
     const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
     int per_sm = 0;
     cudaError_t e;
@@ -2457,8 +2458,8 @@ template <int FMT, int MODE>
 static cudaError_t launch_dbg(const KArgs &k, const typename WeightsOf<FMT>::type &mw, cudaStream_t stream) {
     // List and Mask 16x16 / 11x11 share the lean kernels: every lean exact window is <= 8x8,
     // inside both grids, so there Mask's success test is List's; the lean fallback kernel adds
-    // the grid test for its wider windows.  Box (BC1) has its own lean exact instantiation.
-    if (CTF_FAST && MODE == MODE_COLLAB && (k.variant != VAR_BOX || FMT == FMT_BC1))
+    // the grid test for its wider windows.  Box has its own lean exact instantiation.
+    if (CTF_FAST && MODE == MODE_COLLAB)
         return (k.flags & FLAG_DEBUG) ? launch_fast<FMT, true>(k, mw, stream) : launch_fast<FMT, false>(k, mw, stream);
     return (k.flags & FLAG_DEBUG) ? launch_one<FMT, MODE, true>(k, mw, stream)
                                   : launch_one<FMT, MODE, false>(k, mw, stream);
@@ -2479,9 +2480,8 @@ static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::typ
 #endif
 #if CTF_TU_FMT == 1
 int launches_per_pass(int fmt, int mode, int filter) {
-    if (!CTF_FAST || mode < MODE_COLLAB || mode > MODE_COLLAB + 3 || (mode == MODE_COLLAB + 1 && fmt != FMT_BC1) ||
-        filter != 0)
-        return 1;   // List (3), Mask16 (5), Mask11 (6) and BC1 Box (4) run the lean kernels
+    if (!CTF_FAST || mode < MODE_COLLAB || mode > MODE_COLLAB + 3 || filter != 0)
+        return 1;   // List (3), Box (4), Mask16 (5), Mask11 (6) run the lean kernels
     return fmt == FMT_BC1 ? (CTF_REST_MERGED ? 2 : 3) : 2;   // latent MLP: lean exact + general
 }
 

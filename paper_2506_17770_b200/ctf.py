@@ -158,8 +158,7 @@ def num_waves(wf: int, hf: int) -> int:
 def workspace_for(tex: Texture, mode: int, filt: int, wf: int, hf: int, frames: int, device) -> torch.Tensor | None:
     """Device scratch for ctf_params.workspace_dev (the work lists of the lean COLLAB / Mask
     bilinear kernels), or None where the path does not use one."""
-    lean = (MODE_COLLAB, MODE_MASK16, MODE_MASK11) + ((MODE_BOX,) if tex.fmt == FMT_BC1 else ())
-    if mode not in lean or filt != FILTER_BILINEAR:
+    if mode not in (MODE_COLLAB, MODE_BOX, MODE_MASK16, MODE_MASK11) or filt != FILTER_BILINEAR:
         return None
     nbytes = load_library().ctf_filter_workspace_bytes(wf, hf, frames)
     return torch.empty(nbytes, device=device, dtype=torch.uint8)

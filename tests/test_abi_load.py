@@ -77,7 +77,7 @@ def test_validation_errors_without_gpu():
     # BC1 COLLAB bilinear: exact, fallback and general kernels per pass; everything else one kernel
     assert lib.ctf_launches_per_call(1, 3, 0, 64, 1) == 3 and lib.ctf_launches_per_call(1, 3, 0, 64, 0) == 192
     assert lib.ctf_launches_per_call(1, 0, 0, 64, 1) == 1 and lib.ctf_launches_per_call(2, 3, 0, 8, 0) == 16
-    assert lib.ctf_launches_per_call(2, 4, 0, 8, 1) == 1   # Box: the general kernel
+    assert lib.ctf_launches_per_call(2, 4, 0, 8, 1) == 2   # Box: lean exact + general (latent MLP)
     assert lib.ctf_launches_per_call(3, 3, 0, 1, 1) == -1
     # the workspace flag does not change the count
     assert lib.ctf_launches_per_call(1, 3, 0, 64, 3) == 3 and lib.ctf_launches_per_call(2, 3, 0, 64, 3) == 2
@@ -86,15 +86,15 @@ def test_validation_errors_without_gpu():
 
 def test_workspace_and_launch_accounting_per_mode():
     """Host logic: which modes take the lean kernels' work-list workspace and how many launches
-    a call makes (List / Mask / BC1 Box: lean exact + lean fallback + general; latent-MLP Box
-    and every other mode: one general kernel)."""
+    a call makes (List / Box / Mask: lean exact + lean fallback + general for BC1, lean exact +
+    general for the latent MLP; every other mode: one general kernel)."""
     import torch
     import paper_2506_17770_b200.ctf as ctf
     bc1 = ctf.Texture.bc1(torch.zeros(8 * 64, dtype=torch.uint8), 32, 32, device="cpu")
     mlp = ctf.Texture(ctf.FMT_LATENT_MLP, 32, 32, torch.zeros(8 * 8 * 8, dtype=torch.float16))
     for mode in range(7):
         lean_bc1 = mode in (ctf.MODE_COLLAB, ctf.MODE_BOX, ctf.MODE_MASK16, ctf.MODE_MASK11)
-        lean_mlp = mode in (ctf.MODE_COLLAB, ctf.MODE_MASK16, ctf.MODE_MASK11)
+        lean_mlp = lean_bc1
         assert (ctf.workspace_for(bc1, mode, 0, 64, 32, 2, "cpu") is not None) == lean_bc1, mode
         assert (ctf.workspace_for(mlp, mode, 0, 64, 32, 2, "cpu") is not None) == lean_mlp, mode
         assert ctf.launches_per_call(ctf.FMT_BC1, mode, 0, 1) == (3 if lean_bc1 else 1), mode

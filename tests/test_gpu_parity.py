@@ -159,6 +159,22 @@ def test_latent_mlp_texture(ctf, mode, fb, fl):
     assert_parity(run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=6), run_oracle(tex, uv, g, mode, fb, fl, seed=6))
 
 
+@pytest.mark.parametrize("mode", [3, 4, 5, 6])
+def test_latent_mlp_release_lean_kernels(ctf, mode):
+    """Latent MLP, release build (paired tensor-core decode) for List / Box / Mask: FULL waves
+    (no coverage mask) at m ~ 1.3-1.6 rotated (exact and n > 32 / area > 32 waves) and a
+    magnified interior, against the oracle."""
+    import oracle
+    tex = mlp_tex(64, 64, 3)
+    dt = to_dev_tex(ctf, tex)
+    for mag, theta in ((1.3, 30.0), (1.6, 45.0), (3.0, 10.0)):
+        uv, g = synthetic.rotated_quad(64, 32, 64, 64, mag, theta)
+        o = oracle.filter_frame(tex, uv, g, mode, 3, 0, 8, 2)
+        out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, 3, 0, 8, 2)
+        np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"], err_msg=f"m={mag}")
+        assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
+
+
 def test_batch_equals_frames(ctf):
     """ctf_filter_batch over 3 frames == per-frame oracle with frame_index + f."""
     tex = bc1_tex(128, 128, 3, "image")
