@@ -9,6 +9,7 @@ latent grid + MLP weights).  The recipe is stated in DESIGN.md §"Inputs".
 """
 from .scenes import (  # noqa: F401
     rotated_quad,
+    affine_quad,
     perspective_plane,
     camera_path_frame,
     camera_path_frame_torch,

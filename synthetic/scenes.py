@@ -96,6 +96,22 @@ def rotated_quad(wf: int, hf: int, tex_w: int, tex_h: int, mag: float, theta_deg
     return _pack(u, v, c / mag * ones, -s / mag * ones, s / mag * ones, c / mag * ones, covered)
 
 
+def affine_quad(wf: int, hf: int, tex_w: int, tex_h: int, jac, center=(0.5, 0.5)):
+    """A general affine mapping (anisotropic / sheared quad): texel offset d = J (p + 1/2 - frame/2),
+    uv = center + d / (W, H).  `jac` = [[du/dx, du/dy], [dv/dx, dv/dy]] in texel units per pixel,
+    i.e. column 0 is the texel step of one pixel along screen x, column 1 along screen y.
+    grad = (du/dx, dv/dx, du/dy, dv/dy), constant."""
+    J = np.asarray(jac, np.float64)
+    px, py = _pixel_grid(wf, hf)
+    dx = px + 0.5 - wf / 2.0
+    dy = py + 0.5 - hf / 2.0
+    u = center[0] + (J[0, 0] * dx + J[0, 1] * dy) / tex_w
+    v = center[1] + (J[1, 0] * dx + J[1, 1] * dy) / tex_h
+    ones = np.ones_like(u)
+    return _pack(u, v, J[0, 0] * ones, J[1, 0] * ones, J[0, 1] * ones, J[1, 1] * ones,
+                 np.ones_like(u, dtype=bool))
+
+
 def _plane_uv(px, py, wf, hf, p: PlaneParams, cam_height: float):
     """Continuous pixel position -> (u, v, hit) for the ground plane z = 0."""
     t_half = np.tan(np.deg2rad(p.fov_deg) / 2.0)

@@ -452,3 +452,273 @@ def test_box_produces_whole_aabb_and_is_exact():
     area = bw * (max(ys) - min(ys) + 1)
     expect = [(min(ys) + i // bw) * W + min(xs) + i % bw for i in range(area)]
     assert [int(pid[l]) for l in act[:area]] == expect
+
+
+# ------------------------- Eq. 1's general case vs the WC renormalisation --
+# P:477 reads Eq. 1's second term as estimating "the missing texel values as an unweighted
+# average of the known ones".  So when every unknown footprint texel EQUALS the unweighted
+# mean of the known ones, Eq. 1 reproduces exact bilinear — whatever the known set is — and a
+# weight-renormalising estimator (Sum w p / Sum w) does not.  Conversely the renormalisation is
+# exact when the unknown texels equal the WEIGHTED mean of the known ones (our WC reading,
+# R-16), and Eq. 1 is not.  The footprint lies in one BC1 block whose 4-colour palette
+# (c0 = pure red, c1 = pure blue) gives red/blue = code0 (255, 0), code1 (0, 255),
+# code2 (170, 85), code3 (85, 170) — hand-decoded from R-9.
+_PAL = {0: (255, 0), 1: (0, 255), 2: (170, 85), 3: (85, 170)}
+
+
+def _one_block_texture(codes_at):
+    """16x16 BC1 texture; block (0,0) has c0 = 0xF800 (red), c1 = 0x001F (blue) and the given
+    codes at texel (x, y) (code 0 elsewhere); every other block is code 0."""
+    W = H = 16
+    codes = [[0] * 4 for _ in range(4)]
+    for (x, y), c in codes_at.items():
+        codes[y][x] = c
+    nb = (W // 4) * (H // 4)
+    c0 = np.full(nb, 0xF800)
+    c1 = np.full(nb, 0x001F)
+    idx = np.zeros(nb, np.uint32)
+    idx[0] = codes_word(codes)
+    return {"format": 1, "width": W, "height": H, "bc1": blocks_from(c0, c1, idx)}, W, H
+
+
+def _probe_wave(W, H, s, t):
+    """Lane 0 at fractional position (1 + s, 1 + t) in texel space (footprint = texels (1,1),
+    (2,1), (1,2), (2,2), all weights nonzero); lanes 1 and 2 at the CENTRES of texels (1,1)
+    and (2,1): with s = t = 0 their STF draw is the upper-left corner for every uniform (the
+    strict u < s test, R-12), so they deterministically produce the upper row of lane 0's
+    footprint; lane 0's own STF draw is random (any corner); the other 29 lanes are uncovered."""
+    uv = np.full((4, 8, 2), np.nan, np.float32)
+    uv[0, 0] = ((1.5 + s) / W, (1.5 + t) / H)
+    uv[0, 1] = (1.5 / W, 1.5 / H)
+    uv[0, 2] = (2.5 / W, 1.5 / H)
+    return uv
+
+
+def _bilinear_red_blue(codes, s, t):
+    """Plain bilinear of the four hand-decoded palette values (UL, UR, LL, LR)."""
+    w = [(1 - s) * (1 - t), s * (1 - t), (1 - s) * t, s * t]
+    return np.array([sum(wk * _PAL[c][ch] for wk, c in zip(w, codes)) / 255.0 for ch in (0, 1)])
+
+
+@pytest.mark.parametrize("fb", [FB_C, FB_CPLUS])
+def test_eq1_unknown_equal_to_unweighted_mean_gives_bilinear(fb):
+    """UL = code0 (255, 0), UR = code3 (85, 170), LL = LR = code2 (170, 85).  If lane 0 draws
+    the upper row, K = {UL, UR} and both unknowns equal mean(K) = (170, 85); if it draws LL or
+    LR, K = {UL, UR, code2} and the unknown one equals mean(K) = (170, 85) again.  Eq. 1 must
+    then give exact bilinear in every case; the WC renormalisation must not."""
+    codes = (0, 3, 2, 2)
+    tex, W, H = _one_block_texture({(1, 1): 0, (2, 1): 3, (1, 2): 2, (2, 2): 2})
+    s, t = 0.3, 0.6
+    uv = _probe_wave(W, H, s, t)
+    s32, t32 = (np.float32(uv[0, 0, 0]) * np.float32(W) - np.float32(0.5)) - 1, \
+               (np.float32(uv[0, 0, 1]) * np.float32(H) - np.float32(0.5)) - 1
+    expect = _bilinear_red_blue(codes, float(s32), float(t32))
+    wc_off = 0
+    for seed in range(12):
+        r = filter_frame(tex, uv, None, M_COLLAB, fb, FL_FORCE_FALLBACK, seed=seed)
+        assert decode_record(r["rec"])["path"][0, 0] == (3 if fb == FB_C else 4)
+        got = r["out"][0, 0]
+        np.testing.assert_allclose(got[[0, 2]], expect, atol=1e-12)
+        np.testing.assert_allclose(got[[1, 3]], [0.0, 1.0], atol=1e-12)
+        wc = filter_frame(tex, uv, None, M_COLLAB, FB_WC, FL_FORCE_FALLBACK, seed=seed)["out"][0, 0]
+        wc_off += int(np.abs(wc[[0, 2]] - expect).max() > 1e-3)
+    assert wc_off == 12
+
+
+def test_wc_unknown_equal_to_weighted_mean_gives_bilinear():
+    """UL = code0 (255, 0), UR = code1 (0, 255), LL = LR = code2 (170, 85), s = 1/3: the
+    weighted mean of the upper row (1 - s)UL + sUR = (170, 85) equals the unknowns, so the
+    renormalisation Sum w p / Sum w (R-16) reproduces bilinear for any known set containing
+    the upper row; Eq. 1 (unweighted mean) does not."""
+    codes = (0, 1, 2, 2)
+    tex, W, H = _one_block_texture({(1, 1): 0, (2, 1): 1, (1, 2): 2, (2, 2): 2})
+    uv = _probe_wave(W, H, 1.0 / 3.0, 0.55)
+    s32 = float((np.float32(uv[0, 0, 0]) * np.float32(W) - np.float32(0.5)) - 1)
+    t32 = float((np.float32(uv[0, 0, 1]) * np.float32(H) - np.float32(0.5)) - 1)
+    expect = _bilinear_red_blue(codes, s32, t32)
+    for seed in range(12):
+        wc = filter_frame(tex, uv, None, M_COLLAB, FB_WC, FL_FORCE_FALLBACK, seed=seed)["out"][0, 0]
+        np.testing.assert_allclose(wc[[0, 2]], expect, atol=1e-6)
+        c = filter_frame(tex, uv, None, M_COLLAB, FB_C, FL_FORCE_FALLBACK, seed=seed)["out"][0, 0]
+        assert np.abs(c[[0, 2]] - expect).max() > 1e-3
+
+
+def test_eq1_general_case_closed_form_on_random_known_sets():
+    """Eq. 1 written out for one lane from the hand-decoded palette: the lane of _probe_wave on a
+    texture where all four footprint texels differ; for every seed the result equals
+    Sum_K w p + (1 - Sum_K w) mean_K(p) where K is read back as the set of produced ids (the
+    estimator is a function of K only)."""
+    codes = (0, 1, 3, 2)
+    tex, W, H = _one_block_texture({(1, 1): 0, (2, 1): 1, (1, 2): 3, (2, 2): 2})
+    uv = _probe_wave(W, H, 0.3, 0.6)
+    s = float((np.float32(uv[0, 0, 0]) * np.float32(W) - np.float32(0.5)) - 1)
+    t = float((np.float32(uv[0, 0, 1]) * np.float32(H) - np.float32(0.5)) - 1)
+    w = [(1 - s) * (1 - t), s * (1 - t), (1 - s) * t, s * t]
+    ids = [1 * W + 1, 1 * W + 2, 2 * W + 1, 2 * W + 2]
+    seen = set()
+    for seed in range(40):
+        r = filter_frame(tex, uv, None, M_COLLAB, FB_C, FL_FORCE_FALLBACK, seed=seed)
+        prod = set(int(p) for p in r["produced_id"].reshape(-1) if p != 0xFFFFFFFF)
+        K = [k for k in range(4) if ids[k] in prod]
+        seen.add(tuple(K))
+        if len(K) in (1, 4):
+            continue
+        Sw = sum(w[k] for k in K)
+        for ch_i, ch in ((0, 0), (2, 1)):
+            vals = [_PAL[codes[k]][ch] / 255.0 for k in K]
+            e = sum(w[k] * v for k, v in zip(K, vals)) + (1 - Sw) * sum(vals) / len(K)
+            assert abs(r["out"][0, 0, ch_i] - e) < 1e-12
+    assert len(seen) >= 2     # the upper row plus at least one lower corner over the seeds
+
+
+# --------------------------- R-20 magnified class on an anisotropic Jacobian (P:72-73) --
+@pytest.mark.parametrize("theta", [0.0, 25.0])
+@pytest.mark.parametrize("cols,expect", [(((0.9, 0.3), (0.9, -0.3)), 1),    # |J_x|^2 = |J_y|^2 = 0.9
+                                         (((0.9, 0.9), (0.3, -0.3)), 0)])   # |J_x|^2 = 1.62
+def test_magnified_class_anisotropic(cols, expect, theta):
+    """Magnification per screen axis: a wave is magnified iff one pixel step along screen x and
+    along screen y each moves <= 1 texel (R-20).  The truth is taken by brute force from the uv
+    buffer itself (finite differences of neighbouring pixels, independent of `grad`).  The two
+    Jacobians are transposes of each other's classes: the row norms are (1.62, 0.18) where the
+    column norms are (0.9, 0.9) and vice versa, so reading J transposed flips the class."""
+    th = np.deg2rad(theta)
+    R = np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
+    J = R @ np.array(cols, np.float64).T              # columns = screen-x / screen-y texel steps
+    W = H = 256
+    tex = bc1_tex(W, H, 2, "image")
+    uv, g = synthetic.affine_quad(24, 8, W, H, J)
+    du_x = (uv[:, 1:, :].astype(np.float64) - uv[:, :-1, :]) * (W, H)
+    du_y = (uv[1:, :, :].astype(np.float64) - uv[:-1, :, :]) * (W, H)
+    step2 = max(float((du_x ** 2).sum(-1).max()), float((du_y ** 2).sum(-1).max()))
+    truth = int(step2 <= 1.0)
+    assert truth == expect
+    for mode in (M_COLLAB, M_4TAP):
+        d = decode_record(filter_frame(tex, uv, g, mode, FB_C, seed=1)["rec"])
+        assert np.all(d["magnified"] == truth)
+
+
+# ----------------------------------- Eq. 2 on partial waves (P:508-515, R-18 iv) --
+def test_eq2_partial_waves_exhaustive():
+    """P:514-515's guarantees carried to a active lanes (a - 1 in place of 31): for every
+    a in [1, 32] and n_p in [0, a - 1], the spare ranks c in [n_p, a - 1] map to DISTINCT
+    served ranks in [0, a - 1], including 0 and a - 1 whenever a - n_p >= 2; a single spare
+    rank maps to 0."""
+    for a in range(1, 33):
+        for n in range(0, a):
+            ls = [oracle.eq2(c, n, a) for c in range(n, a)]
+            assert all(0 <= l <= a - 1 for l in ls), (a, n, ls)
+            assert len(set(ls)) == len(ls), (a, n, ls)
+            if a - n >= 2:
+                assert min(ls) == 0 and max(ls) == a - 1, (a, n, ls)
+            else:
+                assert ls == [0]
+
+
+def test_cplus_spread_on_partial_waves():
+    """C+ on a coverage-masked frame (circle): in every partial fallback wave the served lanes
+    recorded in `selection` (b8-12) are active lanes, pairwise distinct, and include the first
+    and last active lane whenever at least two lanes are spare (P:514-515 with edge remapping,
+    P:1378-1380)."""
+    W = H = 256
+    tex = bc1_tex(W, H, 8, "image")
+    uv, g = synthetic.rotated_quad(64, 32, W, H, 1.3, 33.0, coverage="circle", radius=14.0, jitter_seed=4)
+    r = filter_frame(tex, uv, g, M_COLLAB, FB_CPLUS, FL_FORCE_FALLBACK, seed=3)
+    d = decode_record(r["rec"])
+    checked = 0
+    for wy in range(d["a"].shape[0]):
+        for wx in range(d["a"].shape[1]):
+            a = int(d["a"][wy, wx])
+            if a == 0 or a == 32:
+                continue
+            lanes_uv = uv[wy * 4:wy * 4 + 4, wx * 8:wx * 8 + 8].reshape(-1, 2)
+            act = [l for l in range(32) if not np.isnan(lanes_uv[l, 0])]
+            sel = r["selection"][wy * 4:wy * 4 + 4, wx * 8:wx * 8 + 8].reshape(-1)
+            spare = [l for l in act if (sel[l] >> 5) & 1]
+            served = [int((sel[l] >> 8) & 31) for l in spare]
+            assert all(l in act for l in served)
+            assert len(set(served)) == len(served)
+            if len(spare) >= 2:
+                assert act[0] in served and act[-1] in served
+                checked += 1
+    assert checked >= 5
+
+
+def test_magnified_class_boundary_m_equals_one():
+    """m = 1 (one texel per pixel, J = I or a rotation of it at 90°) is still magnification: the
+    paper's magnification studies start at m = 1.0 (P:1632, P:1643 '[1.0, 2.5]'), and minified
+    waves are those with a pixel BELOW 1.  fp16 1.0 and 0.0 are exact."""
+    W = H = 128
+    tex = bc1_tex(W, H, 2, "image")
+    for J in ([[1.0, 0.0], [0.0, 1.0]], [[0.0, -1.0], [1.0, 0.0]]):
+        uv, g = synthetic.affine_quad(16, 8, W, H, J)
+        d = decode_record(filter_frame(tex, uv, g, M_COLLAB, FB_C, seed=1)["rec"])
+        assert np.all(d["magnified"] == 1)
+    uv, g = synthetic.affine_quad(16, 8, W, H, [[1.01, 0.0], [0.0, 1.0]])
+    assert np.all(decode_record(filter_frame(tex, uv, g, M_COLLAB, FB_C, seed=1)["rec"])["magnified"] == 0)
+
+
+def test_eq1_counts_only_nonzero_weight_texels():
+    """the known set holds the unique texels 'with nonzero filter weights'.  Lane 0
+    sits on a texel row (t = 0, s = 1/2: weights UL = UR = 1/2, LL = LR = 0); lanes 1 and 2
+    (texel centres) produce UL and the zero-weight LL.  When lane 0 draws UL, its only known
+    nonzero-weight texel is UL, so N = 1 and the result is exactly that texel —
+    the known zero-weight LL must not enter N or the mean; when it draws UR, everything with
+    nonzero weight is known and the result is exact bilinear."""
+    tex, W, H = _one_block_texture({(1, 1): 0, (2, 1): 1, (1, 2): 3, (2, 2): 2})
+    uv = np.full((4, 8, 2), np.nan, np.float32)
+    uv[0, 0] = (2.0 / W, 1.5 / H)          # fx = 1.5, fy = 1.0: s = 1/2, t = 0
+    uv[0, 1] = (1.5 / W, 1.5 / H)          # centre of (1,1) = UL
+    uv[0, 2] = (1.5 / W, 2.5 / H)          # centre of (1,2) = LL (zero weight for lane 0)
+    picks = set()
+    for seed in range(16):
+        r = filter_frame(tex, uv, None, M_COLLAB, FB_C, FL_FORCE_FALLBACK, seed=seed)
+        corner = int(r["selection"][0, 0] & 3)
+        picks.add(corner)
+        got = r["out"][0, 0][[0, 2]] * 255.0
+        if corner == 0:
+            np.testing.assert_allclose(got, _PAL[0], atol=1e-9)
+        else:
+            assert corner == 1
+            np.testing.assert_allclose(got, [0.5 * _PAL[0][c] + 0.5 * _PAL[1][c] for c in (0, 1)], atol=1e-9)
+    assert picks == {0, 1}
+
+
+def test_mask_grid_limits_on_a_16_wide_wave():
+    """A full wave whose footprints tile a 16 x 2 texel strip (n = 32 = a): List and the 16 x 16
+    mask resolve it exactly (the AABB fits the 16-wide grid), the 11 x 11 mask
+    cannot (AABB wider than 11) and falls back."""
+    W = H = 64
+    tex = bc1_tex(W, H, 3, "image")
+    uv = np.empty((4, 8, 2), np.float32)
+    for lane in range(32):
+        k = min(lane // 2, 14)             # footprint columns {k, k+1}, k = 0..14
+        uv[lane // 8, lane % 8] = ((20 + k + 1.0) / W, (30 + 1.0) / H)   # fx = 20.5 + k, fy = 30.5
+    expect = {M_COLLAB: 0, 5: 0, 6: 3}
+    for mode, path in expect.items():
+        d = decode_record(filter_frame(tex, uv, None, mode, FB_C, seed=1)["rec"])
+        assert (d["n"][0, 0], d["a"][0, 0], d["path"][0, 0]) == (32, 32, path), mode
+
+
+def test_cplus_extra_texels_come_from_the_served_lanes_footprint():
+    """R-18 (i): a spare lane c serving lane l (Eq. 2) produces a texel of l's footprint with
+    nonzero weight that is not planned (P:503-506 'its filter footprint ... spread out')."""
+    W = H = 256
+    tex = bc1_tex(W, H, 8, "image")
+    uv, g = synthetic.rotated_quad(64, 32, W, H, 1.4, 41.0, jitter_seed=1)
+    r = filter_frame(tex, uv, g, M_COLLAB, FB_CPLUS, FL_FORCE_FALLBACK, seed=5)
+    n_extra = 0
+    for wy in range(8):
+        for wx in range(8):
+            sel = r["selection"][wy * 4:wy * 4 + 4, wx * 8:wx * 8 + 8].reshape(-1)
+            pid = r["produced_id"][wy * 4:wy * 4 + 4, wx * 8:wx * 8 + 8].reshape(-1)
+            luv = uv[wy * 4:wy * 4 + 4, wx * 8:wx * 8 + 8].reshape(-1, 2)
+            for c in range(32):
+                if not ((sel[c] >> 4) & 1):
+                    continue
+                l = int((sel[c] >> 8) & 31)
+                ids, st = oracle.footprint(float(luv[l, 0]), float(luv[l, 1]), W, H)
+                w = [(1 - st[0]) * (1 - st[1]), st[0] * (1 - st[1]), (1 - st[0]) * st[1], st[0] * st[1]]
+                assert int(pid[c]) in {int(i) for i, wi in zip(ids, w) if wi != 0}
+                assert int(ids[(sel[c] >> 2) & 3]) == int(pid[c])
+                n_extra += 1
+    assert n_extra > 100
