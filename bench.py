@@ -5,12 +5,17 @@ Headline workload (BASELINE.json configs[4], "config 5"): a batch of 64 4K
 (3840x2160) frames of the animated camera path over the perspective ground
 plane (synthetic.camera_path_frame: magnification ~0.5-9.4), BC1-style 4096^2
 texture, CTF_MODE_COLLAB with the C+ fallback, per-pixel uv + fp16 Jacobian in,
-RGBA fp32 + per-wave records out.  One step = one ctf_filter_batch call (one
-persistent-kernel launch) over the rank's 64 frames.  Inputs are resident in
-HBM before timing; the batch (17 GB of I/O) is far larger than L2, so no L2
-flush is needed between steps.  Multi-GPU: weak scaling — every rank filters
-its own 64 frames (distinct RNG frame indices); NCCL carries only the
-max-over-ranks time and one all_gather of statistics (paper_2506_17770_b200.dist).
+RGBA fp32 + per-wave records out.  One step = one ctf_filter_batch call over
+the rank's share of the 64 frames.  Inputs are resident in HBM before timing;
+the batch (17 GB of I/O) is far larger than L2, so no L2 flush is needed
+between steps.  Multi-GPU: the path shards with no data
+exchange (waves never read another wave's pixels).  Default
+--split frames: rank g filters frames [g*64/G, (g+1)*64/G) of the fixed batch
+(strong scaling, RNG frame indices = global frame numbers, so the results equal
+the 1-GPU run bit for bit); --split strip: every rank filters its wave-row
+strip of all 64 frames (ctf_params.row0); --split weak: every rank its own 64
+frames.  NCCL carries only the max-over-ranks time and one all_gather of
+statistics, reduced in rank order (paper_2506_17770_b200.dist).
 
 At N = 1 the line also carries "configs": the other §8 configurations
 (1: 64x64 launch latency, 2: 1080p, 3: 4K latent-MLP COLLAB vs 4-tap,
@@ -54,7 +59,11 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--frames", type=int, default=64, help="frames per rank per step")
+    ap.add_argument("--frames", type=int, default=64, help="frames in the batch (per rank with --split weak)")
+    ap.add_argument("--split", choices=["frames", "strip", "weak"], default="frames",
+                    help="multi-GPU partition (SURVEY §8(e)): frames = contiguous frame blocks of the fixed "
+                         "batch (strong), strip = wave-row strips of every frame (strong), weak = every rank "
+                         "its own batch of --frames frames")
     ap.add_argument("--width", type=int, default=3840)
     ap.add_argument("--height", type=int, default=2160)
     ap.add_argument("--tex", type=int, default=4096)
@@ -351,29 +360,42 @@ def main():
         torch.cuda.synchronize()
         return 0
 
-    F, Wf, Hf, T = args.frames, args.width, args.height, args.tex
+    Wf, Hf, T = args.width, args.height, args.tex
     mode, fb = MODES[args.mode], FALLBACKS[args.fallback]
     blocks = synthetic.bc1_texture(T, T, args.seed, "image")
-    tex = ctf.Texture.bc1(blocks, T, T, device=dev)
-    path_frames, frame_base = cdist.weak_frames(F, rank)
-    uv = torch.empty((F, Hf, Wf, 2), dtype=torch.float32, device=dev)
-    grad = None if args.no_grad else torch.empty((F, Hf, Wf, 4), dtype=torch.float16, device=dev)
+    tex = ctf.Texture.bc1(blocks, T, T, device=dev)   # every rank builds the same texture from the seed
+    # this rank's share of the work; each rank generates only its own inputs
+    row0, Hr = 0, Hf
+    if args.split == "weak":
+        path_frames, frame_base = cdist.weak_frames(args.frames, rank)
+        F_total = ws * args.frames
+    else:
+        F_total = args.frames
+        if args.split == "frames":
+            shard = cdist.frame_shard(F_total, ws, rank)
+            path_frames, frame_base = list(shard), shard.start
+        else:
+            path_frames, frame_base = list(range(F_total)), 0
+            row0, Hr = cdist.strip_shard(Hf, ws, rank)
+    F = len(path_frames)
+    uv = torch.empty((F, Hr, Wf, 2), dtype=torch.float32, device=dev)
+    grad = None if args.no_grad else torch.empty((F, Hr, Wf, 4), dtype=torch.float16, device=dev)
     for i, f in enumerate(path_frames):
         u, g = synthetic.camera_path_frame_torch(f, Wf, Hf, T, T, device=dev)
-        uv[i].copy_(u)
+        uv[i].copy_(u[row0:row0 + Hr])
         if grad is not None:
-            grad[i].copy_(g)
+            grad[i].copy_(g[row0:row0 + Hr])
         del u, g
-    out = torch.empty((F, Hf, Wf, 4), dtype=torch.float32, device=dev)
-    nwy, nwx = (Hf + 3) // 4, (Wf + 7) // 8
+    out = torch.empty((F, Hr, Wf, 4), dtype=torch.float32, device=dev)
+    nwy, nwx = (Hr + 3) // 4, (Wf + 7) // 8
     rec = torch.empty((F, nwy, nwx), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
-    wspace = ctf.workspace_for(tex, mode, 0, Wf, Hf, F, dev)   # work lists (ctf_params.workspace_dev)
+    wspace = ctf.workspace_for(tex, mode, 0, Wf, Hr, F, dev)   # work lists (ctf_params.workspace_dev)
 
     def step():
         ctf.filter_batch(tex, uv, grad, mode, fb, 0, args.seed, frame_base, out=out, rec=rec, stream=stream,
-                         workspace=wspace)
+                         workspace=wspace, row0=row0)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -407,11 +429,11 @@ def main():
     elapsed_ms = cdist.max_over_ranks(t0.elapsed_time(t1), device=dev)
     kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_per_step = elapsed_ms / args.steps
-    value = ws * F * Wf * Hf / (ms_per_step / 1e3) / 1e9
+    value = F_total * Wf * Hf / (ms_per_step / 1e3) / 1e9   # whole job: every rank's pixels / max-over-ranks time
 
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / mean launch time
     nwaves = nwy * nwx
-    bytes_per_launch = F * (Wf * Hf * (8 + (0 if grad is None else 8) + 16) + nwaves * 4)
+    bytes_per_launch = F * (Wf * Hr * (8 + (0 if grad is None else 8) + 16) + nwaves * 4)
     k_ms = statistics.mean(kernel_ms)
     achieved = bytes_per_launch / (k_ms / 1e3) / 1e9
     peak, sm_mhz, peak_src = measured_peaks()
@@ -419,10 +441,15 @@ def main():
 
     # quality + statistics (off the timed path): 4-tap reference, ctf_stats, NCCL all_gather
     ref = torch.empty_like(out)
-    ctf.filter_batch(tex, uv, grad, 0, 0, 0, args.seed, frame_base, out=ref, rec=torch.empty_like(rec), stream=stream)
-    st = ctf.stats(rec, Wf, Hf, F, out, ref, stream=stream)
+    ctf.filter_batch(tex, uv, grad, 0, 0, 0, args.seed, frame_base, out=ref, rec=torch.empty_like(rec), stream=stream,
+                     row0=row0)
+    per_frame = []   # per-frame records, reduced in global frame order on every rank (dist.reduce_frame_stats)
+    for i in range(F):
+        st = ctf.stats(rec[i], Wf, Hr, 1, out[i], ref[i], stream=stream)
+        st["frame"], st["row0"] = frame_base + i, row0
+        per_frame.append(st)
     del ref
-    tot = cdist.reduce_stats(st, device=dev)
+    tot = cdist.reduce_frame_stats(per_frame)
     mse = tot["sum_sq_err"] / max(1, 4 * tot["pixels_active"])
     quality = {
         "texel_evals_per_px": tot["texel_evals"] / max(1, tot["pixels_active"]),
@@ -441,11 +468,11 @@ def main():
         E = min(args.e2e_frames, F)
         uv_h = uv[:E].cpu().pin_memory()
         g_h = None if grad is None else grad[:E].cpu().pin_memory()
-        out_h = torch.empty((E, Hf, Wf, 4), dtype=torch.float32).pin_memory()
+        out_h = torch.empty((E, Hr, Wf, 4), dtype=torch.float32).pin_memory()
         rec_h = torch.empty((E, nwy, nwx), dtype=torch.int32).pin_memory()
         chunk = 1  # one frame per chunk: the copy engines overlap H2D(c+1), kernel(c), D2H(c-1)
-        pipe = ctf.HostPipeline(Wf, Hf, chunk, grad is not None, device=dev)
-        pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream)  # warm
+        pipe = ctf.HostPipeline(Wf, Hr, chunk, grad is not None, device=dev)
+        pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream, row0=row0)  # warm
         if ws > 1:
             tdist.barrier()
         torch.cuda.synchronize()
@@ -453,12 +480,12 @@ def main():
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         for _ in range(args.e2e_steps):
-            pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream)
+            pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream, row0=row0)
         a1.record(stream)
         torch.cuda.synchronize()
         e_ms = cdist.max_over_ranks(a0.elapsed_time(a1) / args.e2e_steps, device=dev)
-        h2d_b = E * Wf * Hf * (8 + (0 if grad is None else 8))
-        d2h_b = E * (Wf * Hf * 16 + nwaves * 4)
+        h2d_b = E * Wf * Hr * (8 + (0 if grad is None else 8))
+        d2h_b = E * (Wf * Hr * 16 + nwaves * 4)
         # the link bound: each direction's pinned-copy bandwidth, measured alone
         bw = {}
         for name, (src, dst) in {"h2d": (out_h, out), "d2h": (out, out_h)}.items():
@@ -474,7 +501,8 @@ def main():
             torch.cuda.synchronize()
             bw[name] = 5 * n / (b0.elapsed_time(b1) / 1e3) / 1e9
         link_ms = max(h2d_b / bw["h2d"], d2h_b / bw["d2h"]) / 1e6
-        e2e = {"value": ws * E * Wf * Hf / (e_ms / 1e3) / 1e9, "unit": UNIT,
+        e2e_px = cdist.sum_over_ranks(E * Wf * Hr, device=dev)
+        e2e = {"value": e2e_px / (e_ms / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "frames_per_step": E,
                "chunk_frames": chunk, "ms_per_step": e_ms,
                "pcie_gbs": {"h2d": bw["h2d"], "d2h": bw["d2h"]},
@@ -502,7 +530,7 @@ def main():
             c0 = time.perf_counter()
             oracle.filter_frame(otex, u_np, g_np, mode, fb, 0, args.seed, frame_base + i, debug=False)
             secs += time.perf_counter() - c0
-            px += Wf * Hf
+            px += Wf * Hr
             nfr += 1
         cpu = {"value": px / secs / 1e9, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
                "sample": f"{nfr} full 4K frames of the batch (every 8th first), {secs:.1f} s of oracle time"}
@@ -510,13 +538,19 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if args.split == "weak" else "strong",
+            "per_gpu_value": value / ws,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "config5: 64-frame 4K camera path over a perspective plane, BC1 4096^2, "
                                    "COLLAB + C+ fallback, uv f32x2 + grad f16x4 in, RGBA f32 out",
-                       "frames_per_rank_per_step": F, "width": Wf, "height": Hf, "tex": T, "mode": args.mode,
+                       "frames_per_step": F_total, "frames_per_rank": F, "rows_per_rank": Hr,
+                       "width": Wf, "height": Hf, "tex": T, "mode": args.mode,
                        "fallback": args.fallback, "grad": grad is not None,
-                       "l2": "inputs (17 GB/step) >> L2, no flush needed", "parallelism": f"frames x{ws} (weak)"},
+                       "l2": "inputs (17 GB/step) >> L2, no flush needed",
+                       "parallelism": {"frames": f"frame blocks of the {F_total}-frame batch x{ws} (strong)",
+                                       "strip": f"wave-row strips of every frame x{ws} (strong)",
+                                       "weak": f"{args.frames} frames per rank x{ws} (weak)"}[args.split]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": KERNEL_NAME, "kernel_ms": k_ms,

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define CTF_ABI_VERSION 5
+#define CTF_ABI_VERSION 6
 
 typedef enum {
     CTF_OK = 0,
@@ -67,10 +67,12 @@ typedef struct {
                                 LATENT_MLP: fp16 latents [(H/4)][(W/4)][8].                 */
     const float *mlp_dev;    /* LATENT_MLP: 1604 fp32 = W1[32][12] b1[32] W2[32][32] b2[32]
                                 W3[4][32] b3[4]; NULL for BC1.                               */
-    const float *mlp_host;   /* LATENT_MLP, optional: HOST copy of the same 1604 weights.  The
-                                kernel receives the weights by value in its parameter block
-                                (constant bank); without this copy every launch first copies
-                                them from mlp_dev synchronously.  NULL for BC1.              */
+    const float *mlp_host;   /* LATENT_MLP, REQUIRED (ABI 6): HOST copy of the same 1604
+                                weights.  The kernels receive the weights by value in their
+                                parameter block (constant bank), so a launch reads them from
+                                here and never copies from the device (no hidden
+                                synchronisation; calls stay asynchronous and capturable in a
+                                CUDA graph).  NULL with LATENT_MLP -> CTF_EINVAL.  NULL for BC1. */
 } ctf_texture;
 
 /* Filter modes (P:606-609 naming: method + fallback in parentheses). */
@@ -130,6 +132,13 @@ typedef struct {
                               as the work list.  Results are identical either way.  Calls
                               that share a workspace must be ordered (same stream).        */
     uint64_t workspace_bytes;
+    int32_t row0;          /* (ABI 6) frame row of the first buffer row, a multiple of 4, >= 0:
+                              the buffers hold rows [row0, row0 + Hf) of a taller frame (strip
+                              sharding).  Only the RNG counter uses the frame row
+                              (ctr = (x, row0 + y, frame, 0)); waves never read outside their
+                              8x4 pixels, so a strip's results equal the same rows
+                              of the whole frame bit for bit.  0 for whole frames.          */
+    int32_t reserved_;     /* must be 0                                                     */
 } ctf_params;
 
 /* Optional per-pixel debug outputs (only with CTF_FLAG_DEBUG; any may be NULL). */

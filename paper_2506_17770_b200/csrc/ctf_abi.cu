@@ -19,7 +19,9 @@ int validate(const ctf_texture *tex, const float *uv, const uint16_t *grad, int3
     if (tex->width <= 0 || tex->height <= 0 || (tex->width & 3) || (tex->height & 3)) return CTF_EINVAL;
     if (tex->addr != CTF_ADDR_CLAMP) return CTF_EINVAL;
     if (!tex->data_dev) return CTF_EINVAL;
-    if (tex->format == CTF_FMT_LATENT_MLP && !tex->mlp_dev) return CTF_EINVAL;
+    if (tex->format == CTF_FMT_LATENT_MLP && (!tex->mlp_dev || !tex->mlp_host)) return CTF_EINVAL;
+    if (p->row0 < 0 || (p->row0 & 3) || p->reserved_ != 0) return CTF_EINVAL;
+    if ((int64_t)p->row0 + Hf > (1LL << 30)) return CTF_EUNSUPPORTED;
     if (p->mode < CTF_MODE_BILINEAR_4TAP || p->mode > CTF_MODE_MASK11) return CTF_EINVAL;
     if (p->fallback < CTF_FB_STF || p->fallback > CTF_FB_CPLUS) return CTF_EINVAL;
     if (p->filter < CTF_FILTER_BILINEAR || p->filter > CTF_FILTER_CATMULL_ROM) return CTF_EINVAL;
@@ -65,6 +67,7 @@ ctf::LaunchArgs make_args(const ctf_texture *tex, const float *uv, const uint16_
     a.fallback = p->fallback;
     a.flags = p->flags;
     a.frame_index = p->frame_index;
+    a.row0 = p->row0;
     a.seed = p->seed;
     a.filter = p->filter;
     a.max_evals = p->max_evals < 1 ? 1 : p->max_evals;

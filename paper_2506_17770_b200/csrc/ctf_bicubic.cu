@@ -45,6 +45,7 @@ struct BArgs {
     float Wflt, Hflt;
     int filter, E, fallback, variant;
     uint32_t flags, frame_index, seed_lo, seed_hi;
+    int row0;                       // RNG counter y = row0 + py (strip sharding)
 };
 
 struct BSmem {
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                 path = PATH_4TAP;
             } else if (MODE == MODE_STF) {
                 // R-27 positivized STF: one draw per lobe, c = W+ p+ - W- p-
-                const uint4 rnd = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo, a.seed_hi);
+                const uint4 rnd = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)(py + a.row0), frame, 0u), a.seed_lo, a.seed_hi);
                 float Wp = 0.0f, Wn = 0.0f;
                 int lastp = 0, lastn = 0;
 #pragma unroll
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
 
             if (run_fb >= 0) {
                 // ---- a7: fallbacks; one-tap plan (R-26)
-                const uint4 rnd = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.seed_lo, a.seed_hi);
+                const uint4 rnd = philox4x32_10(make_uint4((uint32_t)px, (uint32_t)(py + a.row0), frame, 0u), a.seed_lo, a.seed_hi);
                 float Sx, Sy;
                 const int pi = cubic_pick(f.wx, unit24(rnd.x), Sx);
                 const int pj = cubic_pick(f.wy, unit24(rnd.y), Sy);
@@ -574,6 +575,7 @@ cudaError_t launch_bicubic_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.variant = a.mode >= 4 ? a.mode - 3 : BVAR_LIST;
     k.flags = a.flags;
     k.frame_index = a.frame_index;
+    k.row0 = a.row0;
     k.seed_lo = (uint32_t)a.seed;
     k.seed_hi = (uint32_t)(a.seed >> 32);
 #if CTF_TU_FMT == 1

@@ -67,6 +67,7 @@ struct KArgs {
     int fallback;
     int variant;                    // COLLAB kernel: VAR_LIST / VAR_BOX / VAR_MASK16 / VAR_MASK11
     uint32_t flags, frame_index, seed_lo, seed_hi;
+    int row0;                       // frame row of buffer row 0 (strip sharding): RNG counter y = row0 + py
     uint32_t rk[2][10];             // Philox round keys of (seed_lo, seed_hi) (constant-bank operands)
 };
 enum { VAR_LIST = 0, VAR_BOX = 1, VAR_MASK16 = 2, VAR_MASK11 = 3 };
@@ -1107,11 +1108,11 @@ __device__ __forceinline__ WaveOut wave_general(const KArgs &a, const typename W
             pl.produced = false;
             pl.qx = pl.qy = 0;
         } else {
-            pl = fb_plan(fb, f, b, active, A, na, px, py, frame, a.seed_lo, a.seed_hi, a.tex.W, s);
+            pl = fb_plan(fb, f, b, active, A, na, px, py + a.row0, frame, a.seed_lo, a.seed_hi, a.tex.W, s);
         }
         FbAll fball{};
         if constexpr (FMT == FMT_BC1) {
-            if (!exact) fball = fb_all_bc1(fb, f, b, active, A, na, px, py, frame, a, s);
+            if (!exact) fball = fb_all_bc1(fb, f, b, active, A, na, px, py + a.row0, frame, a, s);
         }
         selbits = (FMT == FMT_BC1 && !exact) ? fball.selbits : pl.selbits;
         // ---- the single texel-production site (<= 1 evaluation per lane)
@@ -1834,7 +1835,7 @@ __device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const F
     } else {
         // ---- a7 plan: every lane's STF texel; C+ dedupes it and spreads the
         // spare lanes over the wave with Eq. 2
-        const uint4 rn = philox4x32_10_rk(make_uint4((uint32_t)px, (uint32_t)py, frame, 0u), a.rk[0], a.rk[1]);
+        const uint4 rn = philox4x32_10_rk(make_uint4((uint32_t)px, (uint32_t)(py + a.row0), frame, 0u), a.rk[0], a.rk[1]);
         const int ksel = stf_corner(f, rn);
         qx = corner_x(f, ksel);
         qy = corner_y(f, ksel);
@@ -2524,6 +2525,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.variant = a.mode >= 4 ? a.mode - 3 : VAR_LIST;   // BOX / MASK16 / MASK11 run in the COLLAB kernel
     k.flags = a.flags;
     k.frame_index = a.frame_index;
+    k.row0 = a.row0;
     k.seed_lo = (uint32_t)a.seed;
     k.seed_hi = (uint32_t)(a.seed >> 32);
     for (int r = 0; r < 10; ++r) {   // the key schedule of philox4x32_10, precomputed

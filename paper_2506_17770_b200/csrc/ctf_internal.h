@@ -15,7 +15,7 @@ struct LaunchArgs {
     int fmt, W, H;
     const void *tex_data;   // BC1 blocks or fp16 latents
     const float *mlp;       // device copy of the MLP weights
-    const float *mlp_host;  // optional host copy (passed by value to the kernel)
+    const float *mlp_host;  // host copy (required; passed by value to the kernel)
     // frames
     const float *uv;        // [frames][Hf][Wf][2]
     const uint16_t *grad;   // [frames][Hf][Wf][4] fp16 bits or nullptr
@@ -25,6 +25,7 @@ struct LaunchArgs {
     // parameters
     int mode, fallback;
     uint32_t flags, frame_index;
+    int row0;               // frame row of buffer row 0 (strip sharding; RNG counter only)
     uint64_t seed;
     int filter;             // ctf_filter: 0 bilinear, 1 B-spline, 2 Catmull-Rom
     int max_evals;          // exact-path evaluations per lane (1 or 2)
@@ -48,17 +49,11 @@ inline cudaError_t launch_filter(const LaunchArgs &a, cudaStream_t stream) {
 
 // Latent-MLP weights for the kernel parameter block, repacked from the ABI layout
 // (W1[32][12] b1 W2[32][32] b2 W3[4][32] b3) into the kernels' access order (W1, b1,
-// W2 transposed, b2, W3 transposed, b3).  Source: the caller's host copy, else one
-// synchronous copy from the device.
-inline cudaError_t mlp_weights_by_value(const LaunchArgs &a, cudaStream_t stream, float (&o)[kMlpParams]) {
-    float src[kMlpParams];
-    if (a.mlp_host) {
-        memcpy(src, a.mlp_host, sizeof(src));
-    } else {
-        cudaError_t e = cudaMemcpyAsync(src, a.mlp, sizeof(src), cudaMemcpyDeviceToHost, stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) return e;
-    }
+// W2 transposed, b2, W3 transposed, b3).  Source: the caller's host copy (required by the
+// ABI, validated non-NULL): no device round trip, no synchronisation (include/ctf.h).
+inline cudaError_t mlp_weights_by_value(const LaunchArgs &a, cudaStream_t, float (&o)[kMlpParams]) {
+    if (!a.mlp_host) return cudaErrorInvalidValue;
+    const float *src = a.mlp_host;
     const float *W1 = src, *b1 = W1 + 384, *W2 = b1 + 32, *b2 = W2 + 1024, *W3 = b2 + 32, *b3 = W3 + 128;
     memcpy(o, W1, sizeof(float) * 384);
     memcpy(o + 384, b1, sizeof(float) * 32);

@@ -39,7 +39,8 @@ class ctf_texture(ctypes.Structure):
 class ctf_params(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("fallback", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("frame_index", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("filter", ctypes.c_int32),
-                ("max_evals", ctypes.c_int32), ("workspace_dev", ctypes.c_void_p), ("workspace_bytes", ctypes.c_uint64)]
+                ("max_evals", ctypes.c_int32), ("workspace_dev", ctypes.c_void_p), ("workspace_bytes", ctypes.c_uint64),
+                ("row0", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
 
 
 class ctf_debug(ctypes.Structure):
@@ -170,12 +171,28 @@ def _set_workspace(p: ctf_params, ws: torch.Tensor | None):
         p.workspace_bytes = ws.numel() * ws.element_size()
 
 
+def _call_workspace(tex, mode, filt, wf, hf, frames, device, workspace, stream):
+    """The call's work-list scratch: a caller tensor, None, or (workspace=True) one allocated
+    here.  A scratch allocated here is released when the call returns while the kernels still
+    use it on `stream`; record_stream keeps the caching allocator from reusing the block until
+    the work queued on that stream so far has finished."""
+    if isinstance(workspace, torch.Tensor):
+        return workspace
+    if workspace is not True:
+        return None
+    ws = workspace_for(tex, mode, filt, wf, hf, frames, device)
+    if ws is not None and stream is not None:
+        ws.record_stream(stream)
+    return ws
+
+
 def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS,
                  flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
                  rec: torch.Tensor | None = None, debug: dict | None = None,
                  stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR, max_evals: int = 1,
-                 workspace: torch.Tensor | bool | None = True):
+                 workspace: torch.Tensor | bool | None = True, row0: int = 0):
     """uv: float32 [F][Hf][Wf][2] (or [Hf][Wf][2]); grad: float16 [..][4] or None.
+    row0: frame row of the buffers' first row (strip sharding; a multiple of 4).
     Returns (out float32 [..][4], rec int32 [F][nwy][nwx]).  `debug` may hold tensors
     'produced_id', 'selection' (int32, pixel-shaped) and 'unread' (int32 [1]).
     workspace: True = allocate the path's scratch (workspace_for) for this call, a tensor =
@@ -193,8 +210,8 @@ def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
     if rec is None:
         rec = torch.empty((frames, (hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
     p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
-    ws = workspace_for(tex, mode, filter, wf, hf, frames, uv.device) if workspace is True else (workspace if isinstance(workspace, torch.Tensor) else None)
-    _set_workspace(p, ws)
+    p.row0 = row0
+    _set_workspace(p, _call_workspace(tex, mode, filter, wf, hf, frames, uv.device, workspace, stream))
     dbg = None
     if debug is not None:
         dbg = ctf_debug(_ptr(debug.get("produced_id")), _ptr(debug.get("selection")), _ptr(debug.get("unread")))
@@ -212,8 +229,8 @@ def filter_frame(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
                  flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
                  rec: torch.Tensor | None = None, debug: dict | None = None,
                  stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR, max_evals: int = 1,
-                 workspace: torch.Tensor | bool | None = True):
-    """One frame through ctf_filter_frame.  uv float32 [Hf][Wf][2]; workspace as filter_batch."""
+                 workspace: torch.Tensor | bool | None = True, row0: int = 0):
+    """One frame through ctf_filter_frame.  uv float32 [Hf][Wf][2]; workspace and row0 as filter_batch."""
     lib = load_library()
     hf, wf = uv.shape[0], uv.shape[1]
     if out is None:
@@ -221,8 +238,8 @@ def filter_frame(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
     if rec is None:
         rec = torch.empty(((hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
     p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
-    ws = workspace_for(tex, mode, filter, wf, hf, 1, uv.device) if workspace is True else (workspace if isinstance(workspace, torch.Tensor) else None)
-    _set_workspace(p, ws)
+    p.row0 = row0
+    _set_workspace(p, _call_workspace(tex, mode, filter, wf, hf, 1, uv.device, workspace, stream))
     dbg = None
     if debug is not None:
         dbg = ctf_debug(_ptr(debug.get("produced_id")), _ptr(debug.get("selection")), _ptr(debug.get("unread")))
@@ -257,13 +274,14 @@ class HostPipeline:
     def run(self, tex: Texture, uv_host: torch.Tensor, grad_host: torch.Tensor | None, out_host: torch.Tensor,
             rec_host: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS, flags: int = 0, seed: int = 0,
             frame_index: int = 0, stream: torch.cuda.Stream | None = None, filter: int = FILTER_BILINEAR,
-            max_evals: int = 1):
+            max_evals: int = 1, row0: int = 0):
         lib = load_library()
         for t in (uv_host, grad_host, out_host, rec_host):
             if t is not None and (t.is_cuda or not t.is_contiguous()):
                 raise ValueError("host pipeline expects contiguous CPU (ideally pinned) tensors")
         frames = uv_host.shape[0]
         p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
+        p.row0 = row0
         hp = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
         rc = lib.ctf_filter_frames_host(ctypes.byref(tex.desc), hp(uv_host), hp(grad_host), self.wf, self.hf,
                                         frames, self.chunk, ctypes.byref(p), hp(out_host), hp(rec_host),

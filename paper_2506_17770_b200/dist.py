@@ -27,6 +27,16 @@ def frame_shard(total_frames: int, world: int, rank: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
+def strip_shard(hf: int, world: int, rank: int) -> tuple[int, int]:
+    """Strip sharding of one frame: the ceil(Hf/4) wave-rows are split into
+    `world` contiguous strips (sizes differ by at most one wave-row); returns (row0, rows) in
+    pixels: rank `rank` filters frame rows [row0, row0 + rows), row0 a multiple of 4 (wave rows
+    never straddle two strips, and waves never read another wave's pixels)."""
+    wr = frame_shard((hf + 3) // 4, world, rank)
+    row0 = 4 * wr.start
+    return row0, max(0, min(4 * wr.stop, hf) - row0)
+
+
 def weak_frames(frames_per_rank: int, rank: int, period: int = 64) -> tuple[list[int], int]:
     """Weak scaling: rank r filters its own frames_per_rank frames of the camera path
     (path position f mod period) with distinct RNG frame indices starting at r*frames_per_rank."""
@@ -78,6 +88,32 @@ def reduce_stats(st: dict, device: torch.device | str = "cpu", group=None) -> di
     dist.all_gather(gi, ints, group=group)
     dist.all_gather(gf, flts, group=group)
     return reduce_stats_local([_unpack(a.cpu(), b.cpu()) for a, b in zip(gi, gf)])
+
+
+def reduce_frame_stats(records: list[dict], group=None) -> dict:
+    """Whole-job statistics from per-frame records: every rank contributes the
+    stats of the frames (or frame strips) it filtered, each tagged with 'frame' and 'row0'; the
+    records of all ranks are gathered (all_gather_object) and reduced on every rank in global
+    (frame, row0) order.  With frame sharding the reduction therefore sees exactly the records,
+    in exactly the order, of a 1-GPU run: every total, including the fp64 error sums, is
+    bitwise independent of the number of GPUs.  With strip sharding the integer totals are
+    bitwise identical too; the fp64 error sums of a frame are the sum of its strips' sums."""
+    items = list(records)
+    if dist.is_available() and dist.is_initialized():
+        ws = dist.get_world_size(group)
+        gathered = [None] * ws
+        dist.all_gather_object(gathered, items, group=group)
+        items = [r for part in gathered for r in part]
+    items.sort(key=lambda r: (int(r["frame"]), int(r.get("row0", 0))))
+    return reduce_stats_local(items)
+
+
+def sum_over_ranks(x: int, device: torch.device | str = "cpu", group=None) -> int:
+    if not dist.is_available() or not dist.is_initialized():
+        return int(x)
+    t = torch.tensor([int(x)], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t.item())
 
 
 def max_over_ranks(x: float, device: torch.device | str = "cpu", group=None) -> float:

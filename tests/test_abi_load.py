@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     lib.ctf_abi_version.restype = ctypes.c_int
-    assert lib.ctf_abi_version() == 5
+    assert lib.ctf_abi_version() == 6
 
 
 def test_binding_declares_all_exports():
@@ -73,6 +73,16 @@ def test_validation_errors_without_gpu():
     assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EINVAL
     tex.width, tex.height = 8192, 8192
     assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EUNSUPPORTED
+    tex.width, tex.height = 32, 32
+    # ABI 6: strip origin row0 must be a non-negative multiple of 4; reserved_ must be 0
+    for row0, res in ((2, 0), (-4, 0), (0, 1)):
+        p.row0, p.reserved_ = row0, res
+        assert lib.ctf_filter_frame(ctypes.byref(tex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EINVAL
+    p.row0, p.reserved_ = 0, 0
+    # ABI 6: the latent-MLP format requires the host copy of the weights (no hidden device
+    # round trip / synchronisation in the launch path)
+    mtex = c.ctf_texture(2, 32, 32, 0, 0x1000, 0x1000, None)
+    assert lib.ctf_filter_frame(ctypes.byref(mtex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EINVAL
     lib.ctf_launches_per_call.argtypes = [ctypes.c_int32] * 4 + [ctypes.c_int]
     # BC1 COLLAB bilinear: exact, fallback and general kernels per pass; everything else one kernel
     assert lib.ctf_launches_per_call(1, 3, 0, 64, 1) == 3 and lib.ctf_launches_per_call(1, 3, 0, 64, 0) == 192
