@@ -1511,14 +1511,8 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4
     if (__all_sync(FULL, (dx | (dy << 1)) < 8u)) K = 1;                      // 8x4
     else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; lgP = 2u; }   // 4x8
     else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                        // 8x8
-    if (K == 0) {   // a 128-bit window (fallback kernel) or none (general kernel)
-        if (FMT != FMT_BC1) {
-            o.rec = kSlowMark;
-            return o;
-        }
-        const bool w128 = __all_sync(FULL, dx < 16u && dy < 8u) || __all_sync(FULL, dx < 8u && dy < 16u) ||
-                          __all_sync(FULL, dx < 32u && dy < 4u);
-        o.rec = w128 ? kFbMark : kSlowMark;
+    if (K == 0) {   // a wider window: the wide-window kernel (BC1) / the general kernel (latent MLP)
+        o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
         return o;
     }
     const uint32_t pmask = (1u << lgP) - 1u;
@@ -1619,8 +1613,8 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     o.n = 0;
     o.minx = o.miny = 0;
     const unsigned A = __ballot_sync(FULL, !isnan(uv.x));   // interior run: every pixel in the frame
-    if (A != FULL) {   // empty wave: n = 0, zero colour; partial wave: general kernel
-        o.rec = A == 0u ? (1u << 26) : kSlowMark;
+    if (A != FULL) {   // empty wave: n = 0, zero colour; partial wave: wide-window kernel (BC1)
+        o.rec = A == 0u ? (1u << 26) : (FMT == FMT_BC1 ? kFbMark : kSlowMark);
         return o;
     }
     const bool wave_mag = wave_magnified(gr, GRAD);
@@ -1637,14 +1631,8 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     else if (__all_sync(FULL, dx < 6u && dy < 5u)) { K = 1; P = 6u; qmul = 43u; }      // 6x5
     else if (__all_sync(FULL, dx < 5u && dy < 6u)) { K = 1; P = 5u; qmul = 52u; }      // 5x6
     else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                                  // 8x8
-    if (K == 0) {   // a 128-bit window (fallback kernel, BC1) or none (general kernel)
-        if (FMT != FMT_BC1) {
-            o.rec = kSlowMark;
-            return o;
-        }
-        const bool w128 = __all_sync(FULL, dx < 16u && dy < 8u) || __all_sync(FULL, dx < 8u && dy < 16u) ||
-                          __all_sync(FULL, dx < 32u && dy < 4u);
-        o.rec = w128 ? kFbMark : kSlowMark;
+    if (K == 0) {   // a wider window: the wide-window kernel (BC1) / the general kernel (latent MLP)
+        o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
         return o;
     }
     const uint32_t t0 = (uint32_t)(f.ya - miny) * P + (uint32_t)(f.xa - minx);
@@ -1953,6 +1941,268 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
     return o;
 }
 
+// ------------------------------------------------ wide-window path (shared-memory bitmaps)
+// Every wave the lean exact kernel leaves (n > 32, windows wider than 8x8, partial waves,
+// forced fallbacks) whose footprint AABB fits 32 x 32 texels: the window is a bitmap of 32
+// rows x 32 bits in shared memory, one word per row, and each active lane sets its corners
+// with two shared atomics (ATOMS.OR, one per footprint row) — the cost does not grow with
+// the AABB (no 128-key sort).  The canonical ascending-id order (R-5) is row-major over the
+// window, so a texel's rank is an exclusive scan of the rows' popcounts plus a popc within
+// its row; the atomic's old value tells each lane whether it set a bit first, so every
+// texel has exactly one owner that publishes it.  Bitmaps: U (the needed set: n and the
+// exact ranks), P (the C+ plan), D (the produced set the fallbacks gather from, values
+// indexed by D rank).  Records, producers, selections and colours equal the general path
+// bit for bit (same fp32 operations in the same order).
+struct WideSmem {
+    uint32_t bmU[32], bmP[32], bmD[32];   // window rows (bit c of word r = texel (minx + c, miny + r))
+    float4 xch[32];                       // exact: U rank -> value; fallback: D rank -> value
+    float4 mw[32];                        // per lane: merged corner weights (C+ spare lanes read the served lane's)
+    uint32_t fpos[32];                    // per lane: cx0 | cx1 << 5 | cy0 << 10 | cy1 << 15 | contrib << 20
+    uint16_t tbl[32];                     // rank -> window position (row << 5 | col): exact U ranks / C+ plan
+    uint8_t act[32];                      // active rank -> lane (h(r, A))
+    uint4 lut[8];                         // BC1 per-index constants (bc1_lut_entry)
+};
+
+// exclusive prefix sum over the lanes (lane k holds the count of window row k)
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, unsigned lane) {
+    uint32_t s = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(FULL, s, d);
+        s += lane >= (unsigned)d ? u : 0u;
+    }
+    return s - v;
+}
+// rank of window texel (row r, column c) in a bitmap whose row r word is `word` and whose
+// rows before r hold `base` set bits
+__device__ __forceinline__ int bm_rank(uint32_t base, uint32_t word, int c) {
+    return (int)base + __popc(word & ((1u << c) - 1u));
+}
+
+template <bool DBG>
+__device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float2 uv, uint2 gr, bool inframe, int px,
+                                             int py, uint32_t frame, bool force) {
+    const unsigned lane = lane_id(), lt = lanemask_lt();
+    LeanOut o;
+    o.color = make_float4(0.f, 0.f, 0.f, 0.f);
+    o.prod = INVALID_ID;
+    o.selbits = 0u;
+    o.done = true;
+    const bool active = inframe && !isnan(uv.x);
+    const unsigned A = __ballot_sync(FULL, active);
+    const int na = __popc(A);
+    if (A == 0u) {   // empty wave: n = 0, zero colour
+        o.rec = 1u << 26;
+        return o;
+    }
+    // ---- a1: magnified class over the active lanes (R-20)
+    bool mag_lane = true;
+    if (a.grad) {
+        const float rx = fma_f32_f16((unsigned short)(gr.x & 0xffffu), (unsigned short)(gr.x & 0xffffu),
+                                     fma_f32_f16((unsigned short)(gr.x >> 16), (unsigned short)(gr.x >> 16), 0.0f));
+        const float ry = fma_f32_f16((unsigned short)(gr.y & 0xffffu), (unsigned short)(gr.y & 0xffffu),
+                                     fma_f32_f16((unsigned short)(gr.y >> 16), (unsigned short)(gr.y >> 16), 0.0f));
+        mag_lane = !active || (rx <= 1.0f && ry <= 1.0f);
+    }
+    const bool wave_mag = a.grad != nullptr && __all_sync(FULL, mag_lane);
+    // ---- a2: footprint; a3: AABB (inactive lanes do not count)
+    const Foot f = footprint2(uv, a);
+    const int minx = __reduce_min_sync(FULL, active ? f.xa : INT_MAX);
+    const int miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
+    const int bw = __reduce_max_sync(FULL, active ? f.xb : 0) - minx + 1;
+    const int bh = __reduce_max_sync(FULL, active ? f.yb : 0) - miny + 1;
+    if (bw > 32 || bh > 32) {   // wider than the bitmap: the general path (third kernel)
+        o.done = false;
+        o.rec = kSlowMark;
+        return o;
+    }
+    const int cx0 = (f.xa - minx) & 31, cx1 = (f.xb - minx) & 31, cy0 = (f.ya - miny) & 31, cy1 = (f.yb - miny) & 31;
+    const int ar = __popc(A & lt);   // active rank: lane = h(ar, A)
+    ws.bmU[lane] = 0u;
+    ws.bmP[lane] = 0u;
+    ws.bmD[lane] = 0u;
+    if (active) ws.act[ar] = (uint8_t)lane;
+    __syncwarp();
+    // ---- a3: the needed set U (every corner, zero weights included, R-4)
+    const uint32_t pat = (1u << cx0) | (1u << cx1);
+    uint32_t oU0 = 0u, oU1 = 0u;
+    if (active) {
+        oU0 = atomicOr(&ws.bmU[cy0], pat);
+        oU1 = atomicOr(&ws.bmU[cy1], pat);
+    }
+    __syncwarp();
+    const uint32_t cntU = __popc(ws.bmU[lane]);
+    const int n = (int)__reduce_add_sync(FULL, cntU);
+    // ---- a4: decide (List R-6; Box / Mask R-22)
+    bool exact;
+    if (a.variant == VAR_LIST) exact = n <= na;
+    else if (a.variant == VAR_BOX) exact = bw * bh <= na;
+    else {
+        const int lim = a.variant == VAR_MASK16 ? 16 : 11;
+        exact = bw <= lim && bh <= lim && n <= na;
+    }
+    exact = exact && !force;
+    const uint32_t rec_base = ((uint32_t)na << 16) | ((uint32_t)wave_mag << 25) | ((uint32_t)(na < 32) << 26);
+    if (exact) {
+        int rho[4];
+        bool produced;
+        int qx, qy, evals;
+        if (a.variant != VAR_BOX) {
+            // ranks of the four corners; each texel's first setter publishes rank -> position
+            const uint32_t base = warp_excl_scan(cntU, lane);
+            const uint32_t b0 = __shfl_sync(FULL, base, cy0), b1 = __shfl_sync(FULL, base, cy1);
+            const uint32_t w0 = ws.bmU[cy0], w1 = ws.bmU[cy1];
+            rho[0] = bm_rank(b0, w0, cx0);
+            rho[1] = bm_rank(b0, w0, cx1);
+            rho[2] = bm_rank(b1, w1, cx0);
+            rho[3] = bm_rank(b1, w1, cx1);
+            const bool dx = cx1 != cx0;
+            if (active) {
+                if (!((oU0 >> cx0) & 1u)) ws.tbl[rho[0]] = (uint16_t)((cy0 << 5) | cx0);
+                if (dx && !((oU0 >> cx1) & 1u)) ws.tbl[rho[1]] = (uint16_t)((cy0 << 5) | cx1);
+                if (!((oU1 >> cx0) & 1u)) ws.tbl[rho[2]] = (uint16_t)((cy1 << 5) | cx0);
+                if (dx && !((oU1 >> cx1) & 1u)) ws.tbl[rho[3]] = (uint16_t)((cy1 << 5) | cx1);
+            }
+            __syncwarp();
+            // ---- a5: active rank r < n produces U[r] (lane h(r, A))
+            produced = active && ar < n;
+            const uint32_t e = produced ? (uint32_t)ws.tbl[ar] : 0u;
+            qx = minx + (int)(e & 31u);
+            qy = miny + (int)(e >> 5);
+            evals = n;
+        } else {
+            // Box: active rank i < w*h produces AABB texel (i mod w, i div w) (LaneIdxToCoord,
+            // P:1069-1076); a corner reads its AABB-local index (CoordToLaneIdx)
+            const int area = bw * bh;
+            produced = active && ar < area;
+            const int jq = (int)__fdividef((float)ar + 0.5f, (float)bw);   // exact for bw <= 32, ar < 32
+            qx = minx + (ar - jq * bw);
+            qy = miny + (produced ? jq : 0);
+            rho[0] = cy0 * bw + cx0;
+            rho[1] = cy0 * bw + cx1;
+            rho[2] = cy1 * bw + cx0;
+            rho[3] = cy1 * bw + cx1;
+            evals = area;
+        }
+        if (!produced) {
+            qx = minx;
+            qy = miny;
+        }
+        const float4 val = bc1_decode_unorm_lut(a.tex, qx, qy, ws.lut);
+        if (produced) ws.xch[ar] = val;
+        if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
+        __syncwarp();
+        // ---- a6: gather by rank + blend (the exact-path chain, bit-identical to 4-tap)
+        const float4 p[4] = {ws.xch[rho[0] & 31], ws.xch[rho[1] & 31], ws.xch[rho[2] & 31], ws.xch[rho[3] & 31]};
+        if (active) o.color = blend4f(p, f.w);
+        o.rec = rec_base | ((uint32_t)n << 8) | (uint32_t)evals;
+        if (DBG && a.dbg_unread) {
+            const unsigned bad = __reduce_add_sync(FULL, active ? (unsigned)(rho[0] >= evals) + (unsigned)(rho[1] >= evals) +
+                                                                  (unsigned)(rho[2] >= evals) + (unsigned)(rho[3] >= evals)
+                                                            : 0u);
+            if (lane == 0 && bad) atomicAdd(a.dbg_unread, bad);
+        }
+        __syncwarp();
+        return o;
+    }
+    // ---- a7 fallback: every active lane's STF corner (R-11, R-12)
+    const int fb = a.fallback;
+    const uint4 rn = philox4x32_10_rk(make_uint4((uint32_t)px, (uint32_t)(py + a.row0), frame, 0u), a.rk[0], a.rk[1]);
+    const int ksel = stf_corner(f, rn);
+    o.selbits = active ? (uint32_t)ksel : 0u;
+    int qcx = (ksel & 1) ? cx1 : cx0, qcy = (ksel & 2) ? cy1 : cy0;
+    bool produced = active;   // STF, WC, C: every active lane produces its STF texel
+    if (fb == FB_CPLUS) {
+        // (1) the planned set P: STF texels deduplicated, ranked ascending (R-17)
+        uint32_t oP = 0u;
+        if (active) oP = atomicOr(&ws.bmP[qcy], 1u << qcx);
+        const bool firstP = active && !((oP >> qcx) & 1u);
+        // publish this lane's distinct corners (merged weights, R-14) for the spare lanes
+        const Merged m = merge_corners(f);
+        ws.mw[lane] = make_float4(m.dw[0], m.dw[1], m.dw[2], m.dw[3]);
+        ws.fpos[lane] = (uint32_t)cx0 | ((uint32_t)cx1 << 5) | ((uint32_t)cy0 << 10) | ((uint32_t)cy1 << 15) |
+                        (contrib_bits(f, m) << 20);
+        __syncwarp();
+        const uint32_t cntP = __popc(ws.bmP[lane]);
+        const int np = (int)__reduce_add_sync(FULL, cntP);
+        const uint32_t baseP = warp_excl_scan(cntP, lane);
+        const uint32_t bq = __shfl_sync(FULL, baseP, qcy);
+        if (firstP) ws.tbl[bm_rank(bq, ws.bmP[qcy], qcx)] = (uint16_t)((qcy << 5) | qcx);
+        __syncwarp();
+        produced = false;
+        if (active) {
+            if (ar < np) {   // (2) active rank i < n_p produces planned texel i (lane h(i, A))
+                const uint32_t e = ws.tbl[ar];
+                qcx = (int)(e & 31u);
+                qcy = (int)(e >> 5);
+                produced = true;
+            } else {         // (3) spare lane: serves lane l of Eq. 2 (R-18)
+                const int l = ws.act[eq2_lane_rank(ar, np, na)];
+                o.selbits |= (1u << 5) | ((uint32_t)l << 8);
+                const uint32_t fp = ws.fpos[l];
+                const float4 gw = ws.mw[l];
+                const int gx0 = (int)(fp & 31u), gx1 = (int)((fp >> 5) & 31u), gy0 = (int)((fp >> 10) & 31u),
+                          gy1 = (int)((fp >> 15) & 31u);
+                const uint32_t r0 = ws.bmP[gy0], r1 = ws.bmP[gy1];
+                const unsigned PL = ((r0 >> gx0) & 1u) | (((r0 >> gx1) & 1u) << 1) | (((r1 >> gx0) & 1u) << 2) |
+                                    (((r1 >> gx1) & 1u) << 3);
+                // candidates: l's distinct nonzero-weight texels not planned, picked ~ merged
+                // weight with u2 (the sums and the decision in fp32, as cplus_pick_bits)
+                const unsigned cand = (fp >> 20) & ~PL & 15u;
+                const float dw[4] = {gw.x, gw.y, gw.z, gw.w};
+                float ps[4], wsum = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    wsum = __fadd_rn(wsum, ((cand >> k) & 1u) ? dw[k] : 0.0f);
+                    ps[k] = wsum;
+                }
+                const float target = __fmul_rn(unit24(rn.z), wsum);
+                const unsigned gt = cand & ((ps[0] > target ? 1u : 0u) | (ps[1] > target ? 2u : 0u) |
+                                            (ps[2] > target ? 4u : 0u) | (ps[3] > target ? 8u : 0u));
+                if (cand != 0u) {
+                    const int pick = gt != 0u ? __ffs(gt) - 1 : 31 - __clz(cand);
+                    qcx = (pick & 1) ? gx1 : gx0;
+                    qcy = (pick & 2) ? gy1 : gy0;
+                    produced = true;
+                    o.selbits |= ((uint32_t)pick << 2) | (1u << 4);
+                }
+            }
+        }
+    }
+    // ---- the single texel-production site (<= 1 evaluation per lane)
+    const int qx = produced ? minx + qcx : minx, qy = produced ? miny + qcy : miny;
+    const float4 val = bc1_decode_unorm_lut(a.tex, qx, qy, ws.lut);
+    if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
+    const int evals = fb == FB_CPLUS ? __popc(__ballot_sync(FULL, produced)) : na;
+    o.rec = rec_base | ((uint32_t)(n & 0xFF) << 8) | ((uint32_t)(PATH_FB_STF + fb) << 22) | (uint32_t)(evals & 0xFF);
+    if (fb == FB_STF) {   // one-tap STF
+        if (active) o.color = val;
+        return o;
+    }
+    // ---- a7 finish: the produced set D, values by D rank, Eq. 1 / WC over the known corners
+    uint32_t oD = 0u;
+    if (produced) oD = atomicOr(&ws.bmD[qy - miny], 1u << (qx - minx));
+    const bool firstD = produced && !((oD >> (qx - minx)) & 1u);
+    __syncwarp();
+    const uint32_t cntD = __popc(ws.bmD[lane]);
+    const uint32_t baseD = warp_excl_scan(cntD, lane);
+    const uint32_t bp = __shfl_sync(FULL, baseD, (qy - miny) & 31);
+    if (firstD) ws.xch[bm_rank(bp, ws.bmD[qy - miny], qx - minx)] = val;
+    const uint32_t b0 = __shfl_sync(FULL, baseD, cy0), b1 = __shfl_sync(FULL, baseD, cy1);
+    __syncwarp();
+    const uint32_t d0 = ws.bmD[cy0], d1 = ws.bmD[cy1];
+    const unsigned IN = ((d0 >> cx0) & 1u) | (((d0 >> cx1) & 1u) << 1) | (((d1 >> cx0) & 1u) << 2) |
+                        (((d1 >> cx1) & 1u) << 3);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 pv[4] = {(IN & 1u) ? ws.xch[bm_rank(b0, d0, cx0) & 31] : z,
+                          (IN & 2u) ? ws.xch[bm_rank(b0, d0, cx1) & 31] : z,
+                          (IN & 4u) ? ws.xch[bm_rank(b1, d1, cx0) & 31] : z,
+                          (IN & 8u) ? ws.xch[bm_rank(b1, d1, cx1) & 31] : z};
+    if (active) o.color = fb == FB_WC ? combine_eq1_bits<true>(f, IN, pv) : combine_eq1_bits<false>(f, IN, pv);
+    __syncwarp();
+    return o;
+}
+
 // GRAD: grad != NULL (magnified class); FORCE: CTF_FLAG_FORCE_FALLBACK (every live wave
 // goes to the rest kernel) — compile-time, so the hot loop tests neither.
 template <bool DBG, bool FORCE, int FMT>
@@ -2079,7 +2329,8 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
                     if (a.dbg_sel) a.dbg_sel[pix] = 0u;
                 }
             } else {
-                rec = kSlowMark;   // partial wave: general kernel
+                // partial (or, FORCE, any live) wave: the wide-window kernel (BC1) / the general kernel
+                rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
             }
             if (lane == (unsigned)(wx - wx0)) myrec = rec;
           }
@@ -2140,11 +2391,11 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
     static_assert(FMT == FMT_BC1 || !FALLBACK, "no lean fallback for the latent-MLP format");
     if (a.lists && a.lcnt[FALLBACK ? 0 : 1] == 0u) return;   // empty work list (same value in every thread)
     __shared__ WarpSmem smem[(FALLBACK && !CTF_REST_MERGED) ? 1 : kWarps];
-    __shared__ FbSmem fsm[FALLBACK ? kWarps : 1];
+    __shared__ WideSmem fsm[FALLBACK ? kWarps : 1];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent MLP: TcWeights + per-warp TcScratch
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     WarpSmem &s = smem[(FALLBACK && !CTF_REST_MERGED) ? 0 : warp];
-    FbSmem &fs = fsm[FALLBACK ? warp : 0];
+    WideSmem &fs = fsm[FALLBACK ? warp : 0];
     MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
     if (FALLBACK) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
@@ -2166,10 +2417,9 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
         const uint32_t frame = a.frame_index + fr;
         LeanOut o;
         o.done = false;
-        if (FALLBACK && A == FULL)
-            o = fb_wave<DBG>(a, fs, uv, gr, px, py, frame, a.grad != nullptr, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
+        if (FALLBACK) o = wide_wave<DBG>(a, fs, uv, gr, inframe, px, py, frame, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
         if (!o.done) {
-            if (FALLBACK && !CTF_REST_MERGED) {   // (defensive) no 128-bit window: general kernel
+            if (FALLBACK && !CTF_REST_MERGED) {   // AABB wider than 32 x 32 texels: general kernel
                 if (lane == 0) {
                     a.rec[wi] = kSlowMark;
                     if (a.lists) a.lists[a.nrec + atomicAdd(a.lcnt + 1, 1u)] = wi;
