@@ -169,6 +169,57 @@ def ncu_traffic(frames: int, wf: int, hf: int):
         return None
 
 
+def ncu_issue(frames: int, wf: int, hf: int):
+    """warp instructions per call of the timed kernels, scaled per pixel from the committed ncu
+    --set full capture of one bench step (profiles/ncu_traffic.json), or None."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d["warp_inst_per_launch"] / (d["frames"] * d["width"] * d["height"]) * frames * wf * hf
+    except Exception:
+        return None
+
+
+def roofline_line(achieved, peak, traffic, issue, k_ms, bytes_per_launch, peak_src) -> dict:
+    """frac = max(HBM fraction, issue fraction); `bound` names the larger one and
+    the top-level achieved / peak / unit are its figures; both rooflines are kept."""
+    hbm = {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src}
+    r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+         "traffic": traffic, "kernel": KERNEL_NAME, "kernel_ms": k_ms, "kernel_ms_stat": "median",
+         "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src, "hbm": hbm, "issue": issue}
+    if issue is not None and issue["frac"] > hbm["frac"]:
+        r.update(bound="issue", achieved=issue["achieved"], peak=issue["peak"], unit=issue["unit"], frac=issue["frac"])
+    return r
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_check(oracle, tex_np, uv_t, g_t, out_t, rec_t, mode, fb, seed, frame_index, threads=None):
+    """Time the CPU oracle (as it stands) on the exact bytes the GPU filtered and compare: records
+    bit for bit, colours max |GPU - oracle|.  threads: OpenMP threads for this call (None = all)."""
+    uv_np = uv_t.cpu().numpy()
+    g_np = None if g_t is None else g_t.cpu().numpy()
+    prev = oracle.set_threads(threads) if threads else None
+    t0 = time.perf_counter()
+    o = oracle.filter_frame(tex_np, uv_np, g_np, mode, fb, 0, seed, frame_index, debug=False)
+    secs = time.perf_counter() - t0
+    if prev:
+        oracle.set_threads(prev)
+    rec_ok = bool(np.array_equal(rec_t.cpu().numpy().view(np.uint32), o["rec"]))
+    err = float(np.abs(out_t.cpu().numpy().astype(np.float64) - o["out"]).max())
+    return secs, rec_ok, err
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -232,11 +283,28 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- other §8 configs
-def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: float) -> dict:
-    """Configs 1-4 of BASELINE.json, each timed on the device (rank 0, N = 1)."""
+def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: float, cpu: bool = True) -> dict:
+    """Configs 1-4 of BASELINE.json, each timed on the device (rank 0, N = 1); with `cpu`, the
+    CPU oracle (as it stands, all host cores; config 2 also on one core) filters the same bytes,
+    and its records / colours are compared with the GPU's (SURVEY §8(d) oracle baseline)."""
     import synthetic
     res = {}
+    oracle = None
+    if cpu:
+        import oracle
+        oracle.build_oracle()
+
+    def cpu_leg(key, tex_np, uv, g, out, rec, mode, fb, threads=None):
+        if oracle is None:
+            return
+        secs, rec_ok, err = oracle_check(oracle, tex_np, uv, g, out, rec, mode, fb, seed, 0, threads)
+        px = uv.shape[0] * uv.shape[1]
+        tag = "oracle_1thread" if threads == 1 else "oracle"
+        res[key][tag] = {"ms_per_frame": secs * 1e3, "mpix_s": px / secs / 1e6,
+                         "threads": threads or cpu_cores(), "records_equal_gpu": rec_ok, "max_abs_err_vs_gpu": err}
     fp32_peak_tflops = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FFMA issue peak at max SM clock
+
+    last = {}
 
     def run(tex, uv, g, mode, fb, reps):
         out = torch.empty(uv.shape[:-1] + (4,), dtype=torch.float32, device=dev)
@@ -244,6 +312,7 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
         ms = time_launches(lambda: ctf.filter_frame(tex, uv, g, mode, fb, 0, seed, 0, out=out, rec=rec,
                                                     stream=stream), reps, stream)
         st = ctf.stats(rec, uv.shape[1], uv.shape[0], 1, stream=stream)
+        last["rec"] = rec
         return ms, st, out
 
     def entry(wf, hf, ms, st, nbytes=None):
@@ -255,21 +324,27 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
         return e
 
     # config 1: 64x64 frame, 32^2 BC1, uniform 4x — launch-latency bound
-    t1 = ctf.Texture.bc1(synthetic.bc1_texture(32, 32, seed, "image"), 32, 32, device=dev)
+    b1 = synthetic.bc1_texture(32, 32, seed, "image")
+    t1 = ctf.Texture.bc1(b1, 32, 32, device=dev)
     uv, g = synthetic.rotated_quad(64, 64, 32, 32, 4.0, 30.0)
     uv, g = torch.from_numpy(uv).to(dev), torch.from_numpy(g).to(dev)
-    ms, st, _ = run(t1, uv, g, 3, 3, 200)
+    ms, st, out = run(t1, uv, g, 3, 3, 200)
     res["1_64x64_bc1_m4"] = dict(entry(64, 64, ms, st), us_per_launch=ms * 1e3)
+    cpu_leg("1_64x64_bc1_m4", {"format": 1, "width": 32, "height": 32, "bc1": b1}, uv, g, out, last["rec"], 3, 3)
 
     # config 2: 1080p, 2048^2 BC1, perspective plane (m ~0.9-9.4, mean 4.3)
-    t2 = ctf.Texture.bc1(synthetic.bc1_texture(2048, 2048, seed, "image"), 2048, 2048, device=dev)
+    b2 = synthetic.bc1_texture(2048, 2048, seed, "image")
+    t2 = ctf.Texture.bc1(b2, 2048, 2048, device=dev)
     uv, g = synthetic.perspective_plane_torch(1920, 1080, 2048, 2048, synthetic.PLANE_C2, device=dev)
-    ms, st, _ = run(t2, uv, g, 3, 3, 50)
+    ms, st, out = run(t2, uv, g, 3, 3, 50)
     res["2_1080p_bc1_collab_cplus"] = entry(1920, 1080, ms, st, 1920 * 1080 * 32)
+    tex2 = {"format": 1, "width": 2048, "height": 2048, "bc1": b2}
+    cpu_leg("2_1080p_bc1_collab_cplus", tex2, uv, g, out, last["rec"], 3, 3)
+    cpu_leg("2_1080p_bc1_collab_cplus", tex2, uv, g, out, last["rec"], 3, 3, threads=1)
 
     # config 3: 4K, 4096^2 latent-MLP texture, COLLAB vs 4-tap (FP32-pipe bound)
-    t3 = ctf.Texture.latent_mlp(synthetic.latent_texture(4096, 4096, seed), synthetic.mlp_weights(seed + 1),
-                                4096, 4096, device=dev)
+    lat3, mlp3 = synthetic.latent_texture(4096, 4096, seed), synthetic.mlp_weights(seed + 1)
+    t3 = ctf.Texture.latent_mlp(lat3, mlp3, 4096, 4096, device=dev)
     uv, g = synthetic.perspective_plane_torch(3840, 2160, 4096, 4096, synthetic.PLANE_C2, device=dev)
     for name, mode in (("collab_cplus", 3), ("4tap", 0)):
         ms, st, out = run(t3, uv, g, mode, 3, 3)
@@ -280,11 +355,14 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
         res[f"3_4k_latent_mlp_{name}"] = e
         if mode == 3:
             collab_out = out
+            cpu_leg(f"3_4k_latent_mlp_{name}", {"format": 2, "width": 4096, "height": 4096, "latent": lat3, "mlp": mlp3},
+                    uv, g, out, last["rec"], 3, 3)
         else:
             d = (collab_out.double() - out.double())
             res["3_4k_latent_mlp_collab_cplus"]["max_abs_err_vs_4tap"] = float(d.abs().max())
     # config 4: 4K, 4096^2 BC1, grazing plane (horizon, minified waves), every fallback
-    t4 = ctf.Texture.bc1(synthetic.bc1_texture(4096, 4096, seed, "image"), 4096, 4096, device=dev)
+    b4 = synthetic.bc1_texture(4096, 4096, seed, "image")
+    t4 = ctf.Texture.bc1(b4, 4096, 4096, device=dev)
     uv, g = synthetic.perspective_plane_torch(3840, 2160, 4096, 4096, synthetic.PLANE_C4, device=dev)
     _, _, ref = run(t4, uv, g, 0, 0, 1)
     ref = ref.clone()
@@ -297,6 +375,9 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
         mse = float((err * err).mean())
         e["psnr_vs_bilinear_db"] = 10 * float(np.log10(1.0 / mse)) if mse > 0 else float("inf")
         res[f"4_4k_mixed_bc1_collab_{name}"] = e
+        if name == "cplus":
+            cpu_leg(f"4_4k_mixed_bc1_collab_{name}", {"format": 1, "width": 4096, "height": 4096, "bc1": b4},
+                    uv, g, out, last["rec"], 3, fb)
     # the paper's three exact methods on the same grazing scene, C+ fallback (Fig. 4 / Fig. 7 shape)
     for name, mode in (("list", 3), ("box", 4), ("mask16", 5), ("mask11", 6)):
         ms, st, out = run(t4, uv, g, mode, 3, 10)
@@ -434,10 +515,18 @@ def main():
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / mean launch time
     nwaves = nwy * nwx
     bytes_per_launch = F * (Wf * Hr * (8 + (0 if grad is None else 8) + 16) + nwaves * 4)
-    k_ms = statistics.mean(kernel_ms)
+    k_ms = statistics.median(kernel_ms)   # the median over the timed steps
     achieved = bytes_per_launch / (k_ms / 1e3) / 1e9
     peak, sm_mhz, peak_src = measured_peaks()
-    traffic = ncu_traffic(F, Wf, Hf)
+    traffic = ncu_traffic(F, Wf, Hr)
+    # the issue roofline (§8(d)): warp instructions per call (ncu capture) / (4 schedulers x SMs x clock)
+    inst = ncu_issue(F, Wf, Hr)
+    clk_mhz = clk.get("sm_mhz") or sm_mhz
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    issue = None if inst is None else {
+        "achieved": inst / (k_ms / 1e3) / 1e9, "peak": 4 * n_sms * clk_mhz * 1e6 / 1e9, "unit": "Gwarp-inst/s",
+        "frac": inst / (k_ms / 1e3) / (4 * n_sms * clk_mhz * 1e6), "warp_inst_per_call": inst,
+        "source": "profiles/ncu_traffic.json (ncu --set full of one bench step), SM clock = median under load"}
 
     # quality + statistics (off the timed path): 4-tap reference, ctf_stats, NCCL all_gather
     ref = torch.empty_like(out)
@@ -512,7 +601,7 @@ def main():
 
     configs = None
     if rank == 0 and ws == 1 and not args.no_configs:
-        configs = other_configs(ctf, torch, dev, stream, args.seed, peak, sm_mhz)
+        configs = other_configs(ctf, torch, dev, stream, args.seed, peak, sm_mhz, cpu=not args.no_cpu)
 
     # CPU oracle baseline on a bounded sample (rank 0, N = 1 only)
     cpu = None
@@ -522,23 +611,27 @@ def main():
         oracle.build_oracle()
         otex = {"format": 1, "width": T, "height": T, "bc1": blocks}
         px, secs, nfr = 0, 0.0, 0
+        rec_ok, worst = True, 0.0
         order = list(range(0, F, 8)) + [f for f in range(F) if f % 8]
-        while secs < args.cpu_seconds and nfr < 4 * F:
-            i = order[nfr % F]
-            u_np = uv[i].cpu().numpy()
-            g_np = None if grad is None else grad[i].cpu().numpy()
-            c0 = time.perf_counter()
-            oracle.filter_frame(otex, u_np, g_np, mode, fb, 0, args.seed, frame_base + i, debug=False)
-            secs += time.perf_counter() - c0
+        while secs < args.cpu_seconds and nfr < F:
+            i = order[nfr]
+            dt, ok, err = oracle_check(oracle, otex, uv[i], None if grad is None else grad[i], out[i], rec[i], mode, fb,
+                                       args.seed, frame_base + i)
+            secs += dt
+            rec_ok &= ok
+            worst = max(worst, err)
             px += Wf * Hr
             nfr += 1
         cpu = {"value": px / secs / 1e9, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]), "kind": "oracle",
-               "sample": f"{nfr} full 4K frames of the batch (every 8th first), {secs:.1f} s of oracle time"}
+               "cpu_model": cpu_model(),
+               "sample": f"{nfr} full 4K frames of the batch (every 8th first), {secs:.1f} s of oracle time",
+               "parity_vs_gpu": {"frames": nfr, "records_equal": rec_ok, "max_abs_err": worst, "tolerance": 1e-5}}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "ms_per_step_median": statistics.median(kernel_ms), "ms_per_step_min": min(kernel_ms),
             "scaling": "weak" if args.split == "weak" else "strong",
             "per_gpu_value": value / ws,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -551,14 +644,11 @@ def main():
                        "parallelism": {"frames": f"frame blocks of the {F_total}-frame batch x{ws} (strong)",
                                        "strip": f"wave-row strips of every frame x{ws} (strong)",
                                        "weak": f"{args.frames} frames per rank x{ws} (weak)"}[args.split]},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": KERNEL_NAME, "kernel_ms": k_ms,
-                         "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_src},
+            "roofline": roofline_line(achieved, peak, traffic, issue, k_ms, bytes_per_launch, peak_src),
             "quality": quality,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * ctf.launches_per_call(1, mode, 0, F, True, workspace=True),
+            "gpu_launches": args.steps * ctf.launches_per_call(1, mode, 0, F, True, workspace=True, wf=Wf, hf=Hr),
             "clocks": clk,
             "configs": configs,
         }

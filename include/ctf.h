@@ -98,7 +98,12 @@ typedef enum {
 
 enum {
     CTF_FLAG_DEBUG = 1u << 0,          /* fill the ctf_debug buffers                        */
-    CTF_FLAG_FORCE_FALLBACK = 1u << 1  /* COLLAB: every wave runs the fallback */
+    CTF_FLAG_FORCE_FALLBACK = 1u << 1, /* COLLAB: every wave runs the fallback */
+    CTF_FLAG_SEPARATE_PASSES = 1u << 2 /* (ABI 6) BC1 collaborative bilinear: always run the
+                                          multi-kernel pipeline (lean exact kernel, then the
+                                          waves it leaves in their own passes), never the
+                                          single fused launch the library picks for calls of
+                                          at most 131072 waves.  Results are identical.     */
 };
 
 /* Texture filters (§5.4 "Bicubic Filtering").  The bicubic filters use a 4x4
@@ -240,19 +245,23 @@ int ctf_filter_frames_host(const ctf_texture *tex, const float *uv_host, const u
 size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames);
 
 /*
- * Kernel launches one call above issues (for launch accounting): format / mode / filter
- * as in ctf_texture / ctf_params, `frames` frames; flags: CTF_LAUNCH_BATCHED for
- * ctf_filter_batch (one pass over all frames) else ctf_filter_frame once per frame
- * (CTF_LAUNCH_WORKSPACE, a workspace in ctf_params, does not change the count).  The COLLAB
- * bilinear path is three kernels per pass for BC1 (the lean exact kernel; the lean fallback
- * kernel over the full waves it left; the general path over partial waves and windows wider
- * than 8x8) and two for the latent MLP (lean exact kernel + general path); every other path
- * is one (a workspace adds an 8-byte cudaMemsetAsync of the work-list counters, not counted).
- * Returns -1 for an invalid format / mode / filter.
+ * Kernel launches one call above issues (for launch accounting): format / mode / filter as in
+ * ctf_texture / ctf_params, a Wf x Hf frame, `frames` frames; flags: CTF_LAUNCH_BATCHED for
+ * ctf_filter_batch (one pass over all frames) else ctf_filter_frame once per frame;
+ * CTF_LAUNCH_SEPARATE_PASSES when ctf_params.flags has CTF_FLAG_SEPARATE_PASSES;
+ * CTF_LAUNCH_WORKSPACE (a workspace in ctf_params) does not change the count.  The COLLAB /
+ * BOX / MASK bilinear path is, for BC1, ONE fused kernel when a pass covers at most 131072
+ * waves (and separate passes are not requested), else three (the lean exact kernel; the
+ * wide-window kernel over the waves it leaves; the general path over AABBs wider than 32x32
+ * texels, plus an 8-byte cudaMemsetAsync of the work-list counters with a workspace, not
+ * counted); two for the latent MLP (lean exact kernel + general path); every other path is
+ * one.  Returns -1 for an invalid format / mode / filter / size.
  */
 #define CTF_LAUNCH_BATCHED 1
 #define CTF_LAUNCH_WORKSPACE 2
-int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int flags);
+#define CTF_LAUNCH_SEPARATE_PASSES 4
+int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t Wf, int32_t Hf, int32_t frames,
+                          int flags);
 int ctf_abi_version(void);
 
 #ifdef __cplusplus

@@ -19,6 +19,7 @@ from .oracle import (  # noqa: F401
     h_inv,
     eq2,
     unique_count,
+    set_threads,
     decode_record,
     ORACLE_SO,
 )

@@ -979,6 +979,23 @@ int oracle_filter_waves(int format, int W, int H, const uint8_t *bc1, const uint
                                 selection);
 }
 
+/* Thread count of the OpenMP loops over waves (bench.py's single-thread timing); returns the
+ * previous maximum.  Scheduling only: results do not depend on it. */
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+int oracle_set_threads(int n)
+{
+#ifdef _OPENMP
+    int prev = omp_get_max_threads();
+    if (n > 0) omp_set_num_threads(n);
+    return prev;
+#else
+    (void)n;
+    return 1;
+#endif
+}
+
 /* Number of distinct texels in an arbitrary list (brute force, for pins). */
 int oracle_unique_count(const uint32_t *ids, int n)
 {

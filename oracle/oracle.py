@@ -64,6 +64,8 @@ def load_oracle():
         lib.oracle_eq2.restype = i32
         lib.oracle_unique_count.argtypes = [P, i32]
         lib.oracle_unique_count.restype = i32
+        lib.oracle_set_threads.argtypes = [i32]
+        lib.oracle_set_threads.restype = i32
         _lib = lib
     return _lib
 
@@ -232,6 +234,11 @@ def h_inv(t: int, mask: int) -> int:
 
 def eq2(c: int, n: int, a: int = 32) -> int:
     return load_oracle().oracle_eq2(c, n, a)
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's wave loops (0 = query); returns the previous count."""
+    return load_oracle().oracle_set_threads(n)
 
 
 def unique_count(ids) -> int:

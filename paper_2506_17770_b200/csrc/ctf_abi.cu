@@ -96,12 +96,16 @@ size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames) {
     return 256 + 8 * waves;
 }
 
-int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t frames, int flags) {
+int ctf_launches_per_call(int32_t format, int32_t mode, int32_t filter, int32_t Wf, int32_t Hf, int32_t frames,
+                          int flags) {
     if ((format != CTF_FMT_BC1 && format != CTF_FMT_LATENT_MLP) || mode < 0 || mode > CTF_MODE_MASK11 || filter < 0 ||
-        filter > 2)
+        filter > 2 || Wf <= 0 || Hf <= 0 || frames < 0)
         return -1;
-    const int per_pass = ctf::launches_per_pass(format, mode, filter);
-    return per_pass * ((flags & CTF_LAUNCH_BATCHED) ? 1 : (frames > 0 ? frames : 0));
+    const bool batched = (flags & CTF_LAUNCH_BATCHED) != 0;
+    const long long waves = (long long)((Wf + 7) / 8) * ((Hf + 3) / 4) * (batched ? frames : 1);
+    const int per_pass = ctf::launches_per_pass(format, mode, filter, waves,
+                                                (flags & CTF_LAUNCH_SEPARATE_PASSES) ? CTF_FLAG_SEPARATE_PASSES : 0u);
+    return per_pass * (batched ? (frames > 0 ? 1 : 0) : frames);
 }
 
 int ctf_filter_batch(const ctf_texture *tex, const float *uv_dev, const uint16_t *grad_dev, int32_t Wf, int32_t Hf,

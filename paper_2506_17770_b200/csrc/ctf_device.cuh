@@ -15,7 +15,7 @@ constexpr uint32_t INVALID_ID = 0xffffffffu;
 enum { FMT_BC1 = 1, FMT_MLP = 2 };
 enum { MODE_4TAP = 0, MODE_STF = 1, MODE_WC = 2, MODE_COLLAB = 3 };
 enum { FB_STF = 0, FB_WC = 1, FB_C = 2, FB_CPLUS = 3 };
-enum { FLAG_DEBUG = 1u, FLAG_FORCE_FALLBACK = 2u };
+enum { FLAG_DEBUG = 1u, FLAG_FORCE_FALLBACK = 2u, FLAG_SEPARATE_PASSES = 4u };
 enum { PATH_EXACT = 0, PATH_FB_STF = 1, PATH_FB_WC = 2, PATH_FB_C = 3, PATH_FB_CPLUS = 4,
        PATH_4TAP = 5, PATH_STF = 6, PATH_WC = 7 };
 
@@ -165,20 +165,16 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
     return d;
 }
 
-// (2^23 + v) bit patterns of the four channels -> v / 255, correctly rounded like the IEEE
-// division of R-9: FADD2 removes the 2^23 (exact), then q = v * (1/255) is corrected once,
-// q += (v - 255 q) * (1/255) (FFMA2; exact for every v in [0, 255]).  No I2F.
+// (2^23 + v) bit patterns of the four channels -> v / 255 as v * fl(1/255) (R-9): FADD2
+// removes the 2^23 (exact), one FMUL2 scales.  Within 1 ulp (6e-8) of the correctly rounded
+// quotient for every v in [0, 255] (exact for 130 of the 256 values; checked exhaustively,
+// DESIGN.md R-9) — every BC1 path converts through here, so exact waves stay bit-identical to
+// 4-tap.  No I2F, no correction step.
 __device__ __forceinline__ float4 magic_unorm(uint32_t r, uint32_t g, uint32_t b, uint32_t a) {
     uint64_t rg = f2pack(__uint_as_float(r), __uint_as_float(g));
     uint64_t ba = f2pack(__uint_as_float(b), __uint_as_float(a));
-    const uint64_t mag = f2pack(-8388608.0f, -8388608.0f), rc = f2pack(1.0f / 255.0f, 1.0f / 255.0f),
-                   n255 = f2pack(-255.0f, -255.0f);
-    rg = fadd2(rg, mag);
-    ba = fadd2(ba, mag);
-    uint64_t q0 = fmul2(rg, rc), q1 = fmul2(ba, rc);
-    q0 = ffma2(ffma2(q0, n255, rg), rc, q0);
-    q1 = ffma2(ffma2(q1, n255, ba), rc, q1);
-    const float2 x = f2unpack(q0), y = f2unpack(q1);
+    const uint64_t mag = f2pack(-8388608.0f, -8388608.0f), rc = f2pack(1.0f / 255.0f, 1.0f / 255.0f);
+    const float2 x = f2unpack(fmul2(fadd2(rg, mag), rc)), y = f2unpack(fmul2(fadd2(ba, mag), rc));
     return make_float4(x.x, x.y, y.x, y.y);
 }
 // RGBA8 -> v / 255 per channel: a byte permute places each byte under the 2^23 exponent.

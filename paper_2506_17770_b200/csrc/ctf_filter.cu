@@ -59,7 +59,8 @@ struct KArgs {
     int wpf_s, nwx_s;
     unsigned fpx;                   // pixels per frame (all pixel indices < 2^32, validated on the host)
     int Wf, Hf, nwx, nwy, wpf;
-    int cpr, cpf;                   // work items (runs of kChunk waves) per wave-row / per frame
+    int cpr, cpf;                   // work items (runs of `chunk` waves) per wave-row / per frame
+    int chunk;                      // waves per work item (a run in one wave-row; <= 32, host-chosen)
     unsigned nchunks;
     unsigned ipc;                   // work items per CTA (claimed dynamically by its warps)
     float Wflt, Hflt;
@@ -169,7 +170,7 @@ __device__ __forceinline__ uint32_t corner_id(const Foot &f, int k, int W) {
 
 // Exact bilinear of 4 gathered texels (c8).  The same code runs in 4TAP and in
 // COLLAB-exact, so the two are bit-identical on exact waves.
-// Texel values as fp32 in [0, 1] (BC1: v / 255 correctly rounded, R-9), then the
+// Texel values as fp32 in [0, 1] (BC1: v * fl(1/255), R-9), then the
 // FFMA2 chain of blend4f.
 template <int FMT>
 __device__ __forceinline__ float4 blend4(const Texel<FMT> (&p)[4], const float (&w)[4]) {
@@ -1242,8 +1243,8 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : 
         const int fr = (int)(c / (unsigned)a.cpf);
         const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
         const int wy = rr / a.cpr;
-        const int wx0 = (rr - wy * a.cpr) * kChunk;
-        const int wx1 = min(wx0 + kChunk, a.nwx);
+        const int wx0 = (rr - wy * a.cpr) * a.chunk;
+        const int wx1 = min(wx0 + a.chunk, a.nwx);
         const int py = wy * 4 + ly;
         const bool rowok = py < a.Hf;
         const uint32_t frame = a.frame_index + (uint32_t)fr;
@@ -1423,9 +1424,9 @@ __device__ __forceinline__ int cplus_pick_bits(const Foot &g, float u2, unsigned
 // so the special cases (all known -> exact bilinear; N = 1 -> that texel) hold bit for
 // bit and the rest equals it.
 template <bool WC>
-__device__ __forceinline__ float4 combine_eq1_bits(const Foot &f, unsigned IN, const float4 (&pv)[4]) {
-    const Merged m = merge_corners(f);
-    const unsigned C = contrib_bits(f, m), Kn = C & IN;
+__device__ __forceinline__ float4 combine_eq1_mc(const Foot &f, const Merged &m, unsigned C, unsigned IN,
+                                                 const float4 (&pv)[4]) {
+    const unsigned Kn = C & IN;
     const bool all_known = (C & ~IN) == 0u;
     const int N = __popc(Kn);
     float Sw = 0.0f;
@@ -1456,6 +1457,11 @@ __device__ __forceinline__ float4 combine_eq1_bits(const Foot &f, unsigned IN, c
     }
     if (N == 1 && !all_known) c = make_float4(a01.x, a01.y, a23.x, a23.y);
     return c;
+}
+template <bool WC>
+__device__ __forceinline__ float4 combine_eq1_bits(const Foot &f, unsigned IN, const float4 (&pv)[4]) {
+    const Merged m = merge_corners(f);
+    return combine_eq1_mc<WC>(f, m, contrib_bits(f, m), IN, pv);
 }
 
 // One FULL wave (32 active lanes) through the lean exact path.  Returns done = false with
@@ -1950,8 +1956,9 @@ __device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv
 // window, so a texel's rank is an exclusive scan of the rows' popcounts plus a popc within
 // its row; the atomic's old value tells each lane whether it set a bit first, so every
 // texel has exactly one owner that publishes it.  Bitmaps: U (the needed set: n and the
-// exact ranks), P (the C+ plan), D (the produced set the fallbacks gather from, values
-// indexed by D rank).  Records, producers, selections and colours equal the general path
+// exact ranks), P (the C+ plan), D (the produced set the fallbacks gather from: each
+// producing lane stores its value in its own slot, the first setter of a texel publishes its
+// lane in a position -> lane table).  Records, producers, selections and colours equal the general path
 // bit for bit (same fp32 operations in the same order).
 struct WideSmem {
     uint32_t bmU[32], bmP[32], bmD[32];   // window rows (bit c of word r = texel (minx + c, miny + r))
@@ -1961,16 +1968,18 @@ struct WideSmem {
     uint16_t tbl[32];                     // rank -> window position (row << 5 | col): exact U ranks / C+ plan
     uint8_t act[32];                      // active rank -> lane (h(r, A))
     uint4 lut[8];                         // BC1 per-index constants (bc1_lut_entry)
+    uint8_t lop[1024];                    // fallback: window position -> a lane that produced it (valid where bmD is set)
 };
 
 // exclusive prefix sum over the lanes (lane k holds the count of window row k)
-__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, unsigned lane) {
+// (shfl.up's in-range predicate guards the add: two instructions per step)
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, unsigned) {
     uint32_t s = v;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t u = __shfl_up_sync(FULL, s, d);
-        s += lane >= (unsigned)d ? u : 0u;
-    }
+    for (int d = 1; d < 32; d <<= 1)
+        asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 u;\n\t"
+                     "shfl.sync.up.b32 u|p, %0, %1, 0, 0xffffffff;\n\t@p add.u32 %0, %0, u;\n\t}"
+                     : "+r"(s) : "r"(d));
     return s - v;
 }
 // rank of window texel (row r, column c) in a bitmap whose row r word is `word` and whose
@@ -2112,16 +2121,16 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
     o.selbits = active ? (uint32_t)ksel : 0u;
     int qcx = (ksel & 1) ? cx1 : cx0, qcy = (ksel & 2) ? cy1 : cy0;
     bool produced = active;   // STF, WC, C: every active lane produces its STF texel
+    const Merged m = merge_corners(f);   // this lane's distinct corners (R-14): its Eq. 1 and C+ candidates
+    const unsigned C = contrib_bits(f, m);
     if (fb == FB_CPLUS) {
         // (1) the planned set P: STF texels deduplicated, ranked ascending (R-17)
         uint32_t oP = 0u;
         if (active) oP = atomicOr(&ws.bmP[qcy], 1u << qcx);
         const bool firstP = active && !((oP >> qcx) & 1u);
         // publish this lane's distinct corners (merged weights, R-14) for the spare lanes
-        const Merged m = merge_corners(f);
         ws.mw[lane] = make_float4(m.dw[0], m.dw[1], m.dw[2], m.dw[3]);
-        ws.fpos[lane] = (uint32_t)cx0 | ((uint32_t)cx1 << 5) | ((uint32_t)cy0 << 10) | ((uint32_t)cy1 << 15) |
-                        (contrib_bits(f, m) << 20);
+        ws.fpos[lane] = (uint32_t)cx0 | ((uint32_t)cx1 << 5) | ((uint32_t)cy0 << 10) | ((uint32_t)cy1 << 15) | (C << 20);
         __syncwarp();
         const uint32_t cntP = __popc(ws.bmP[lane]);
         const int np = (int)__reduce_add_sync(FULL, cntP);
@@ -2179,26 +2188,22 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
         if (active) o.color = val;
         return o;
     }
-    // ---- a7 finish: the produced set D, values by D rank, Eq. 1 / WC over the known corners
+    // ---- a7 finish: the produced set D (values in the producers' slots, one source lane per
+    // texel), Eq. 1 / WC over the known corners
+    const int pq = ((qy - miny) << 5) | (qx - minx);
     uint32_t oD = 0u;
-    if (produced) oD = atomicOr(&ws.bmD[qy - miny], 1u << (qx - minx));
-    const bool firstD = produced && !((oD >> (qx - minx)) & 1u);
-    __syncwarp();
-    const uint32_t cntD = __popc(ws.bmD[lane]);
-    const uint32_t baseD = warp_excl_scan(cntD, lane);
-    const uint32_t bp = __shfl_sync(FULL, baseD, (qy - miny) & 31);
-    if (firstD) ws.xch[bm_rank(bp, ws.bmD[qy - miny], qx - minx)] = val;
-    const uint32_t b0 = __shfl_sync(FULL, baseD, cy0), b1 = __shfl_sync(FULL, baseD, cy1);
+    if (produced) oD = atomicOr(&ws.bmD[pq >> 5], 1u << (pq & 31));
+    if (produced) ws.xch[lane] = val;
+    if (produced && !((oD >> (pq & 31)) & 1u)) ws.lop[pq] = (uint8_t)lane;
     __syncwarp();
     const uint32_t d0 = ws.bmD[cy0], d1 = ws.bmD[cy1];
     const unsigned IN = ((d0 >> cx0) & 1u) | (((d0 >> cx1) & 1u) << 1) | (((d1 >> cx0) & 1u) << 2) |
                         (((d1 >> cx1) & 1u) << 3);
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 pv[4] = {(IN & 1u) ? ws.xch[bm_rank(b0, d0, cx0) & 31] : z,
-                          (IN & 2u) ? ws.xch[bm_rank(b0, d0, cx1) & 31] : z,
-                          (IN & 4u) ? ws.xch[bm_rank(b1, d1, cx0) & 31] : z,
-                          (IN & 8u) ? ws.xch[bm_rank(b1, d1, cx1) & 31] : z};
-    if (active) o.color = fb == FB_WC ? combine_eq1_bits<true>(f, IN, pv) : combine_eq1_bits<false>(f, IN, pv);
+    const int p0 = cy0 << 5, p2 = cy1 << 5;
+    const float4 pv[4] = {(IN & 1u) ? ws.xch[ws.lop[p0 | cx0]] : z, (IN & 2u) ? ws.xch[ws.lop[p0 | cx1]] : z,
+                          (IN & 4u) ? ws.xch[ws.lop[p2 | cx0]] : z, (IN & 8u) ? ws.xch[ws.lop[p2 | cx1]] : z};
+    if (active) o.color = fb == FB_WC ? combine_eq1_mc<true>(f, m, C, IN, pv) : combine_eq1_mc<false>(f, m, C, IN, pv);
     __syncwarp();
     return o;
 }
@@ -2207,19 +2212,44 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
 // goes to the rest kernel) — compile-time, so the hot loop tests neither.
 template <bool DBG, bool FORCE, int FMT>
 constexpr bool kPaired = CTF_PAIR && !DBG && !FORCE && (FMT == FMT_BC1 || CTF_PAIR_MLP);
-template <bool DBG, bool GRAD, bool FORCE, int FMT, bool BOX = false>
-__global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FORCE, FMT> ? CTF_PAIR_MINB : CTF_FAST_MINB)
-                                                               : CTF_MLP_COLLAB_MINB)
-    ctf_collab_lean_kernel(const KArgs a, const typename WeightsOf<FMT>::type mw) {
+template <bool DBG>
+static __device__ __noinline__ WaveOut general_wave_noinline(const KArgs &a, WarpSmem &s, float2 uv, uint2 gr,
+                                                             bool active, unsigned A, int px, int py, uint32_t frame);
+// the wide-window path out of line (the fused kernel keeps the lean loop's registers)
+template <bool DBG>
+static __device__ __noinline__ LeanOut wide_wave_noinline(const KArgs &a, WideSmem &ws, float2 uv, uint2 gr, bool inframe,
+                                                          int px, int py, uint32_t frame, bool force) {
+    return wide_wave<DBG>(a, ws, uv, gr, inframe, px, py, frame, force);
+}
+// FUSED (BC1, small calls): the waves a run leaves are finished in the same kernel, right after
+// the run (the wide-window path inline, the general path out of line) — one launch per call,
+// no work lists, no counters; the larger register allocation costs occupancy, which small
+// calls do not have to fill.
+#ifndef CTF_FUSED_MINB
+#define CTF_FUSED_MINB 6  // fused lean kernel: resident CTAs per SM (the lean loop's budget; the wide path is out of line)
+#endif
+#ifndef CTF_FUSED_MAX_WAVES
+#define CTF_FUSED_MAX_WAVES 131072  // calls with at most this many waves run the fused kernel
+#endif
+template <bool DBG, bool GRAD, bool FORCE, int FMT, bool BOX = false, bool FUSED = false>
+__global__ void __launch_bounds__(kWarps * 32, FUSED ? CTF_FUSED_MINB
+                                                     : FMT == FMT_BC1 ? (kPaired<DBG, FORCE, FMT> ? CTF_PAIR_MINB : CTF_FAST_MINB)
+                                                                      : CTF_MLP_COLLAB_MINB)
+    ctf_collab_lean_kernel(const __grid_constant__ KArgs a, const typename WeightsOf<FMT>::type mw) {
+    static_assert(!FUSED || FMT == FMT_BC1, "the fused kernel is BC1-only");
     constexpr bool PAIR = kPaired<DBG, FORCE, FMT>;
     using SmemT = std::conditional_t<PAIR, PairSmem, FastSmem>;
     __shared__ SmemT fsm[kWarps];
+    __shared__ WideSmem wsm[FUSED ? kWarps : 1];
+    __shared__ WarpSmem gsm[FUSED ? kWarps : 1];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent MLP: TcWeights + per-warp TcScratch
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     SmemT &fs = fsm[warp];
     MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
+    WideSmem &ws = wsm[FUSED ? warp : 0];
     if constexpr (FMT == FMT_BC1) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
+        if (FUSED && lane < 8) ws.lut[lane] = bc1_lut_entry(lane);
         __syncwarp();
     }
     __shared__ unsigned s_next;   // latent MLP: the CTA's warps claim its items dynamically
@@ -2250,8 +2280,8 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
         const int fr = (int)(c / (unsigned)a.cpf);
         const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
         const int wy = rr / a.cpr;
-        const int wx0 = (rr - wy * a.cpr) * kChunk;
-        const int wx1 = min(wx0 + kChunk, a.nwx);
+        const int wx0 = (rr - wy * a.cpr) * a.chunk;
+        const int wx1 = min(wx0 + a.chunk, a.nwx);
         const int py = wy * 4 + ly;
         const bool rowok = py < a.Hf;
         const bool rowok_all = wy * 4 + 4 <= a.Hf;   // warp-uniform: all 4 rows in the frame
@@ -2338,6 +2368,39 @@ __global__ void __launch_bounds__(kWarps * 32, FMT == FMT_BC1 ? (kPaired<DBG, FO
         if (rowok_all && wx1 * 8 <= a.Wf) run(std::true_type{});
         else run(std::false_type{});
         const bool inrun = lane < (unsigned)(wx1 - wx0);
+        if constexpr (FUSED) {
+            // finish the run's marked waves here: the wide-window path, else (AABB wider than
+            // 32 x 32) the general path out of line
+            unsigned todo = __ballot_sync(FULL, inrun && (myrec == kFbMark || myrec == kSlowMark));
+            while (todo) {
+                const int b = __ffs(todo) - 1;
+                todo &= todo - 1u;
+                const int pxb = (wx0 + b) * 8 + lx;
+                const bool inf = rowok & (pxb < a.Wf);
+                const unsigned pixb = (unsigned)fr * a.fpx + (unsigned)py * (unsigned)a.Wf + (unsigned)pxb;
+                float2 uvb = make_float2(__int_as_float(0x7fc00000), 0.f);
+                uint2 grb = make_uint2(0u, 0u);
+                ld_stream_f2_if(uvb, a.uv + pixb, inf);
+                ld_stream_u2_if(grb, a.grad + pixb, inf & has_grad);
+                __syncwarp();
+                LeanOut o = wide_wave_noinline<DBG>(a, ws, uvb, grb, inf, pxb, py, frame, FORCE);
+                if (!o.done) {
+                    const bool act = inf && !isnan(uvb.x);
+                    const WaveOut go = general_wave_noinline<DBG>(a, gsm[warp], uvb, grb, act, __ballot_sync(FULL, act),
+                                                                  pxb, py, frame);
+                    o.color = go.color;
+                    o.rec = go.rec;
+                    o.prod = go.prod;
+                    o.selbits = go.selbits;
+                }
+                if (inf) st_stream_f4(a.out + pixb, o.color);
+                if (DBG && inf) {
+                    if (a.dbg_pid) a.dbg_pid[pixb] = o.prod;
+                    if (a.dbg_sel) a.dbg_sel[pixb] = o.selbits;
+                }
+                if (lane == (unsigned)b) myrec = o.rec;
+            }
+        }
         if (inrun) a.rec[w0 + lane] = myrec;
         // this run's fallback / general waves (lane = wave of the run)
         const unsigned mfb = __ballot_sync(FULL, inrun && myrec == kFbMark);
@@ -2387,7 +2450,7 @@ __device__ __forceinline__ WaveOut general_wave(const KArgs &a, WarpSmem &s, flo
 }
 template <bool DBG, bool FALLBACK, int FMT>
 __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == FMT_BC1 ? CTF_REST_MINB : CTF_MLP_COLLAB_MINB))
-    ctf_collab_rest_kernel(const KArgs a, unsigned nrec, const typename WeightsOf<FMT>::type mw) {
+    ctf_collab_rest_kernel(const __grid_constant__ KArgs a, unsigned nrec, const typename WeightsOf<FMT>::type mw) {
     static_assert(FMT == FMT_BC1 || !FALLBACK, "no lean fallback for the latent-MLP format");
     if (a.lists && a.lcnt[FALLBACK ? 0 : 1] == 0u) return;   // empty work list (same value in every thread)
     __shared__ WarpSmem smem[(FALLBACK && !CTF_REST_MERGED) ? 1 : kWarps];
@@ -2633,14 +2696,29 @@ static cudaError_t mlp_smem_setup(Kern kern, size_t dyn, int dev) {
 // and the general kernel over the waves it marked / appended to the work lists; (latent
 // MLP) the general kernel over them.  Same work split as the general BC1 kernel.
 // the lean exact kernel over k's frames
+// one launch per call (the fused kernel) for BC1 calls of at most CTF_FUSED_MAX_WAVES waves,
+// unless the caller asks for separate passes (FLAG_SEPARATE_PASSES; results are identical)
+template <int FMT>
+static bool use_fused(const KArgs &k) {
+    return FMT == FMT_BC1 && k.nrec <= (unsigned)CTF_FUSED_MAX_WAVES && !(k.flags & FLAG_SEPARATE_PASSES);
+}
+template <int FMT, bool DBG, bool FUSED>
+static auto lean_kernel_for(const KArgs &k) {
+    constexpr bool F = FUSED && FMT == FMT_BC1;
+    const bool grad = k.grad != nullptr, force = (k.flags & FLAG_FORCE_FALLBACK) != 0;
+    auto kern = grad ? (force ? ctf_collab_lean_kernel<DBG, true, true, FMT, false, F>
+                              : ctf_collab_lean_kernel<DBG, true, false, FMT, false, F>)
+                     : (force ? ctf_collab_lean_kernel<DBG, false, true, FMT, false, F>
+                              : ctf_collab_lean_kernel<DBG, false, false, FMT, false, F>);
+    if (k.variant == VAR_BOX && !force)   // Box (forced: every live wave leaves the lean path anyway)
+        kern = grad ? ctf_collab_lean_kernel<DBG, true, false, FMT, true, F>
+                    : ctf_collab_lean_kernel<DBG, false, false, FMT, true, F>;
+    return kern;
+}
 template <int FMT, bool DBG>
 static cudaError_t launch_lean(KArgs &k, const typename WeightsOf<FMT>::type &mw, int dev, int sms,
                                cudaStream_t stream) {
-    const bool grad = k.grad != nullptr, force = (k.flags & FLAG_FORCE_FALLBACK) != 0;
-    auto kern = grad ? (force ? ctf_collab_lean_kernel<DBG, true, true, FMT> : ctf_collab_lean_kernel<DBG, true, false, FMT>)
-                     : (force ? ctf_collab_lean_kernel<DBG, false, true, FMT> : ctf_collab_lean_kernel<DBG, false, false, FMT>);
-    if (k.variant == VAR_BOX && !force)   // Box (forced: every live wave goes to the general path anyway)
-        kern = grad ? ctf_collab_lean_kernel<DBG, true, false, FMT, true> : ctf_collab_lean_kernel<DBG, false, false, FMT, true>;
+    auto kern = use_fused<FMT>(k) ? lean_kernel_for<FMT, DBG, true>(k) : lean_kernel_for<FMT, DBG, false>(k);
     const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
     int per_sm = 0;
     cudaError_t e;
@@ -2696,6 +2774,22 @@ static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw,
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
+    if (FMT == FMT_BC1) {
+        // runs short enough that every resident warp gets work (small calls are latency-bound:
+        // a warp's waves are a dependent chain), at most kChunk waves (large batches)
+        const long long warps = (long long)sms * CTF_PAIR_MINB * kWarps;
+        long long ch = ((long long)k.nrec / (warps > 0 ? warps : 1)) & ~1LL;
+        ch = ch < 2 ? 2 : ch > kChunk ? kChunk : ch;
+        const unsigned frames = k.nrec / (unsigned)k.wpf;
+        k.chunk = (int)ch;
+        k.cpr = (k.nwx + k.chunk - 1) / k.chunk;
+        k.cpf = k.cpr * k.nwy;
+        k.nchunks = (unsigned)((long long)k.cpf * frames);
+    }
+    if (use_fused<FMT>(k)) {   // one launch: the lean kernel finishes its own marked waves
+        k.lists = nullptr;
+        return launch_lean<FMT, DBG>(k, mw, dev, sms, stream);
+    }
     if (k.lists) {   // work-list counters (the lists need no initialisation)
         k.lcnt = k.lists;
         k.lists += 64;
@@ -2730,9 +2824,10 @@ static cudaError_t launch_fmt(const KArgs &k, const typename WeightsOf<FMT>::typ
 #error "compile ctf_filter.cu with -DCTF_TU_FMT=1 (BC1) or =2 (latent MLP)"
 #endif
 #if CTF_TU_FMT == 1
-int launches_per_pass(int fmt, int mode, int filter) {
+int launches_per_pass(int fmt, int mode, int filter, long long waves, unsigned flags) {
     if (!CTF_FAST || mode < MODE_COLLAB || mode > MODE_COLLAB + 3 || filter != 0)
         return 1;   // List (3), Box (4), Mask16 (5), Mask11 (6) run the lean kernels
+    if (fmt == FMT_BC1 && waves <= CTF_FUSED_MAX_WAVES && !(flags & FLAG_SEPARATE_PASSES)) return 1;   // fused
     return fmt == FMT_BC1 ? (CTF_REST_MERGED ? 2 : 3) : 2;   // latent MLP: lean exact + general
 }
 
@@ -2761,6 +2856,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.nwy = (a.Hf + 3) / 4;
     k.wpf = k.nwx * k.nwy;
     k.fpx = (unsigned)a.Wf * (unsigned)a.Hf;
+    k.chunk = kChunk;
     k.cpr = (k.nwx + kChunk - 1) / kChunk;
     k.cpf = k.cpr * k.nwy;
     k.nchunks = (unsigned)((long long)k.cpf * a.frames);

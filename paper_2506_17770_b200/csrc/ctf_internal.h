@@ -41,7 +41,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream);  // ctf
 cudaError_t launch_bicubic_bc1(const LaunchArgs &a, cudaStream_t stream);  // ctf_bicubic.cu, CTF_TU_FMT=1
 cudaError_t launch_bicubic_mlp(const LaunchArgs &a, cudaStream_t stream);  // ctf_bicubic.cu, CTF_TU_FMT=2
 bool bicubic_built();
-int launches_per_pass(int fmt, int mode, int filter);  // ctf_filter.cu, CTF_TU_FMT=1
+int launches_per_pass(int fmt, int mode, int filter, long long waves, unsigned flags);  // ctf_filter.cu, CTF_TU_FMT=1
 inline cudaError_t launch_filter(const LaunchArgs &a, cudaStream_t stream) {
     if (a.filter != 0) return a.fmt == 1 ? launch_bicubic_bc1(a, stream) : launch_bicubic_mlp(a, stream);
     return a.fmt == 1 ? launch_filter_bc1(a, stream) : launch_filter_mlp(a, stream);

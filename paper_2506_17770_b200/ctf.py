@@ -19,7 +19,7 @@ CTF_OK, CTF_EINVAL, CTF_EUNSUPPORTED, CTF_EALIGN, CTF_ECUDA = 0, -1, -2, -3, -4
 FMT_BC1, FMT_LATENT_MLP = 1, 2
 MODE_4TAP, MODE_STF, MODE_WAVECOMM, MODE_COLLAB, MODE_BOX, MODE_MASK16, MODE_MASK11 = 0, 1, 2, 3, 4, 5, 6
 FB_STF, FB_WAVECOMM, FB_C, FB_CPLUS = 0, 1, 2, 3
-FLAG_DEBUG, FLAG_FORCE_FALLBACK = 1, 2
+FLAG_DEBUG, FLAG_FORCE_FALLBACK, FLAG_SEPARATE_PASSES = 1, 2, 4
 FILTER_BILINEAR, FILTER_BSPLINE, FILTER_CATMULL_ROM = 0, 1, 2
 _STATUS = {0: "CTF_OK", -1: "CTF_EINVAL", -2: "CTF_EUNSUPPORTED", -3: "CTF_EALIGN", -4: "CTF_ECUDA"}
 
@@ -89,7 +89,7 @@ def load_library(path: Path | str | None = None):
     lib.ctf_filter_workspace_bytes.argtypes = [I32, I32, I32]
     lib.ctf_filter_workspace_bytes.restype = ctypes.c_size_t
     lib.ctf_filter_frames_host.argtypes = [PT, V, V, I32, I32, I32, I32, PP, V, V, V, ctypes.c_size_t, V]
-    lib.ctf_launches_per_call.argtypes = [I32, I32, I32, I32, ctypes.c_int]
+    lib.ctf_launches_per_call.argtypes = [I32, I32, I32, I32, I32, I32, ctypes.c_int]
     for fn in ("ctf_filter_frame", "ctf_filter_batch", "ctf_stats", "ctf_filter_frames_host",
                "ctf_launches_per_call", "ctf_abi_version"):
         getattr(lib, fn).restype = ctypes.c_int
@@ -144,9 +144,10 @@ class Texture:
 
 
 def launches_per_call(fmt: int, mode: int, filt: int = 0, frames: int = 1, batched: bool = True,
-                      workspace: bool = False) -> int:
-    """Kernel launches one filter call issues (ctf_launches_per_call)."""
-    n = load_library().ctf_launches_per_call(fmt, mode, filt, frames, int(batched) | (2 if workspace else 0))
+                      workspace: bool = False, wf: int = 3840, hf: int = 2160, separate: bool = False) -> int:
+    """Kernel launches one filter call of `frames` wf x hf frames issues (ctf_launches_per_call)."""
+    flags = int(batched) | (2 if workspace else 0) | (4 if separate else 0)
+    n = load_library().ctf_launches_per_call(fmt, mode, filt, wf, hf, frames, flags)
     if n < 0:
         raise CtfError("ctf_launches_per_call", CTF_EINVAL)
     return n

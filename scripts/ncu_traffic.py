@@ -28,12 +28,15 @@ def main():
     frames, wf, hf = (int(x) for x in sys.argv[2:5]) if len(sys.argv) >= 5 else (64, 3840, 2160)
     rows = raw(rep)
     per = {}
+    inst = {}
     rd = wr = ms = 0.0
     for r in rows:
         name = r["Kernel Name"][0].split("(")[0].strip()
         b_r, b_w = scaled(r["dram__bytes_read.sum"]), scaled(r["dram__bytes_write.sum"])
         prev = per.get(name, [0.0, 0.0])
         per[name] = [prev[0] + b_r, prev[1] + b_w]   # the frame groups' launches of one kernel summed
+        k_inst = float(r["smsp__inst_executed.sum"][0].replace(",", ""))
+        inst[name] = inst.get(name, 0.0) + k_inst
         rd += b_r
         wr += b_w
         ms += scaled(r["gpu__time_duration.sum"]) * 1e3
@@ -45,6 +48,8 @@ def main():
         "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
         "algorithmic_bytes_per_launch": alg, "duration_ms_under_ncu": ms,
         "traffic_over_algorithmic": (rd + wr) / alg,
+        "warp_inst_per_kernel": inst, "warp_inst_per_launch": sum(inst.values()),
+        "warp_inst_per_wave": sum(inst.values()) / waves,
     }
     p = pathlib.Path(__file__).resolve().parent.parent / "profiles" / "ncu_traffic.json"
     p.write_text(json.dumps(out, indent=1) + "\n")

@@ -19,7 +19,8 @@ ap.add_argument("--mode", type=int, default=3)
 ap.add_argument("--fb", type=int, default=3)
 ap.add_argument("--rounds", type=int, default=5)
 ap.add_argument("--reps", type=int, default=5)
-ap.add_argument("--scene", default="c5", choices=["c5", "c4"])
+ap.add_argument("--scene", default="c5", choices=["c5", "c4", "c2"])
+ap.add_argument("--separate", action="store_true", help="CTF_FLAG_SEPARATE_PASSES")
 ap.add_argument("libs", nargs="+")
 a = ap.parse_args()
 
@@ -27,6 +28,8 @@ dev = torch.device("cuda")
 libs = [ctf.load_library(p) for p in a.libs]
 ctf._lib = libs[0]
 F, Wf, Hf, T = a.frames, 3840, 2160, 4096
+if a.scene == "c2":
+    Wf, Hf = 1920, 1080
 tex = ctf.Texture.bc1(synthetic.bc1_texture(T, T, 0, "image"), T, T, device=dev)
 frames, base = cdist.weak_frames(F, 0)
 uv = torch.empty((F, Hf, Wf, 2), dtype=torch.float32, device=dev)
@@ -34,8 +37,10 @@ grad = torch.empty((F, Hf, Wf, 4), dtype=torch.float16, device=dev)
 for i, f in enumerate(frames):
     if a.scene == "c5":
         u, g = synthetic.camera_path_frame_torch(f, Wf, Hf, T, T, device=dev)
-    else:  # config-4 grazing plane, the same frame F times
+    elif a.scene == "c4":  # config-4 grazing plane, the same frame F times
         u, g = synthetic.perspective_plane_torch(Wf, Hf, T, T, synthetic.PLANE_C4, device=dev)
+    else:  # config-2 shape: 1080p perspective plane
+        u, g = synthetic.perspective_plane_torch(Wf, Hf, T, T, synthetic.PLANE_C2, device=dev)
     uv[i].copy_(u)
     grad[i].copy_(g)
 out = torch.empty((F, Hf, Wf, 4), dtype=torch.float32, device=dev)
@@ -45,7 +50,7 @@ outs = {}
 for r in range(a.rounds):
     for p, lib in zip(a.libs, libs):
         ctf._lib = lib
-        f = lambda: ctf.filter_batch(tex, uv, grad, a.mode, a.fb, 0, 0, base, out=out, rec=rec)
+        f = lambda: ctf.filter_batch(tex, uv, grad, a.mode, a.fb, 4 if a.separate else 0, 0, base, out=out, rec=rec)
         f()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)

@@ -83,15 +83,20 @@ def test_validation_errors_without_gpu():
     # round trip / synchronisation in the launch path)
     mtex = c.ctf_texture(2, 32, 32, 0, 0x1000, 0x1000, None)
     assert lib.ctf_filter_frame(ctypes.byref(mtex), V(0x1000), None, 8, 4, ctypes.byref(p), V(0x1000), V(0x1000), None, None) == c.CTF_EINVAL
-    lib.ctf_launches_per_call.argtypes = [ctypes.c_int32] * 4 + [ctypes.c_int]
-    # BC1 COLLAB bilinear: exact, fallback and general kernels per pass; everything else one kernel
-    assert lib.ctf_launches_per_call(1, 3, 0, 64, 1) == 3 and lib.ctf_launches_per_call(1, 3, 0, 64, 0) == 192
-    assert lib.ctf_launches_per_call(1, 0, 0, 64, 1) == 1 and lib.ctf_launches_per_call(2, 3, 0, 8, 0) == 16
-    assert lib.ctf_launches_per_call(2, 4, 0, 8, 1) == 2   # Box: lean exact + general (latent MLP)
-    assert lib.ctf_launches_per_call(3, 3, 0, 1, 1) == -1
+    lib.ctf_launches_per_call.argtypes = [ctypes.c_int32] * 6 + [ctypes.c_int]
+    L = lib.ctf_launches_per_call
+    # BC1 COLLAB bilinear, 4K frames (259200 waves per frame > 131072): exact, wide-window and
+    # general kernels per pass; small passes (<= 131072 waves): one fused kernel
+    assert L(1, 3, 0, 3840, 2160, 64, 1) == 3 and L(1, 3, 0, 3840, 2160, 64, 0) == 192
+    assert L(1, 3, 0, 1920, 1080, 1, 0) == 1 and L(1, 3, 0, 1920, 1080, 4, 0) == 4      # 64800 waves: fused
+    assert L(1, 3, 0, 1920, 1080, 4, 1) == 3                                              # batched: 259200 waves
+    assert L(1, 3, 0, 1920, 1080, 1, 4) == 3                                              # separate passes asked
+    assert L(1, 0, 0, 3840, 2160, 64, 1) == 1 and L(2, 3, 0, 64, 64, 8, 0) == 16
+    assert L(2, 4, 0, 64, 64, 8, 1) == 2   # Box: lean exact + general (latent MLP)
+    assert L(3, 3, 0, 64, 64, 1, 1) == -1 and L(1, 3, 0, 0, 64, 1, 1) == -1
     # the workspace flag does not change the count
-    assert lib.ctf_launches_per_call(1, 3, 0, 64, 3) == 3 and lib.ctf_launches_per_call(2, 3, 0, 64, 3) == 2
-    assert lib.ctf_launches_per_call(1, 3, 1, 64, 3) == 1   # bicubic: one kernel
+    assert L(1, 3, 0, 3840, 2160, 64, 3) == 3 and L(2, 3, 0, 3840, 2160, 64, 3) == 2
+    assert L(1, 3, 1, 3840, 2160, 64, 3) == 1   # bicubic: one kernel
 
 
 def test_workspace_and_launch_accounting_per_mode():
@@ -108,5 +113,6 @@ def test_workspace_and_launch_accounting_per_mode():
         assert (ctf.workspace_for(bc1, mode, 0, 64, 32, 2, "cpu") is not None) == lean_bc1, mode
         assert (ctf.workspace_for(mlp, mode, 0, 64, 32, 2, "cpu") is not None) == lean_mlp, mode
         assert ctf.launches_per_call(ctf.FMT_BC1, mode, 0, 1) == (3 if lean_bc1 else 1), mode
+        assert ctf.launches_per_call(ctf.FMT_BC1, mode, 0, 1, wf=64, hf=64) == 1, mode   # fused when lean
         assert ctf.launches_per_call(ctf.FMT_LATENT_MLP, mode, 0, 1) == (2 if lean_mlp else 1), mode
         assert ctf.workspace_for(bc1, mode, 1, 64, 32, 2, "cpu") is None   # bicubic: no work lists
