@@ -242,6 +242,32 @@ def time_launches(fn, reps: int, stream) -> float:
     return a.elapsed_time(b) / reps
 
 
+def time_graph(fn, calls: int, stream, replays: int = 10) -> float:
+    """Device time (ms) per call of `calls` calls captured in one CUDA graph and replayed: the
+    per-call cost without host launch overhead (the library enqueues only on the given stream,
+    so its calls are capturable)."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fn(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(calls):
+                fn(s)
+    g.replay()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(replays):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / (replays * calls)
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
     ws, rank, _ = dist_env()
@@ -315,6 +341,21 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
         last["rec"] = rec
         return ms, st, out
 
+    def graph_timing(tex, uv, g, wf, hf, calls):
+        """single-frame calls back to back in a CUDA graph (device time per call, no host
+        launch overhead): the library's one-launch fused path and the separate passes"""
+        out = torch.empty(uv.shape[:-1] + (4,), dtype=torch.float32, device=dev)
+        rec = torch.empty(((uv.shape[0] + 3) // 4, (uv.shape[1] + 7) // 8), dtype=torch.int32, device=dev)
+        ws = ctf.workspace_for(tex, 3, 0, wf, hf, 1, dev)
+        r = {}
+        for key, fl in (("graph_us_per_call", 0), ("graph_us_per_call_separate_passes", ctf.FLAG_SEPARATE_PASSES)):
+            ms_g = time_graph(lambda s: ctf.filter_frame(tex, uv, g, 3, 3, fl, seed, 0, out=out, rec=rec, workspace=ws,
+                                                         stream=s), calls, stream)
+            r[key] = ms_g * 1e3
+        r["graph_gpix_s"] = wf * hf / (r["graph_us_per_call"] / 1e6) / 1e9
+        r["launches_per_call"] = ctf.launches_per_call(1, 3, 0, 1, False, wf=wf, hf=hf)
+        return r
+
     def entry(wf, hf, ms, st, nbytes=None):
         e = {"ms": ms, "gpix_s": wf * hf / (ms / 1e3) / 1e9,
              "texel_evals_per_px": st["texel_evals"] / max(1, st["pixels_active"]),
@@ -330,6 +371,7 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
     uv, g = torch.from_numpy(uv).to(dev), torch.from_numpy(g).to(dev)
     ms, st, out = run(t1, uv, g, 3, 3, 200)
     res["1_64x64_bc1_m4"] = dict(entry(64, 64, ms, st), us_per_launch=ms * 1e3)
+    res["1_64x64_bc1_m4"].update(graph_timing(t1, uv, g, 64, 64, 50))
     cpu_leg("1_64x64_bc1_m4", {"format": 1, "width": 32, "height": 32, "bc1": b1}, uv, g, out, last["rec"], 3, 3)
 
     # config 2: 1080p, 2048^2 BC1, perspective plane (m ~0.9-9.4, mean 4.3)
@@ -338,6 +380,7 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
     uv, g = synthetic.perspective_plane_torch(1920, 1080, 2048, 2048, synthetic.PLANE_C2, device=dev)
     ms, st, out = run(t2, uv, g, 3, 3, 50)
     res["2_1080p_bc1_collab_cplus"] = entry(1920, 1080, ms, st, 1920 * 1080 * 32)
+    res["2_1080p_bc1_collab_cplus"].update(graph_timing(t2, uv, g, 1920, 1080, 50))
     tex2 = {"format": 1, "width": 2048, "height": 2048, "bc1": b2}
     cpu_leg("2_1080p_bc1_collab_cplus", tex2, uv, g, out, last["rec"], 3, 3)
     cpu_leg("2_1080p_bc1_collab_cplus", tex2, uv, g, out, last["rec"], 3, 3, threads=1)
@@ -390,18 +433,23 @@ def other_configs(ctf, torch, dev, stream, seed: int, peak_gbs: float, sm_mhz: f
     # bicubic filters (§5.4, Fig. 13): 4K perspective plane of config 3 with the BC1 texture
     uv, g = synthetic.perspective_plane_torch(3840, 2160, 4096, 4096, synthetic.PLANE_C2, device=dev)
     cov = ~torch.isnan(uv[..., 0])
-    for fname, filt in (("bspline", 1), ("catmull_rom", 2)):
+    # (BC1: both filters; the latent-MLP texture of config 3: Catmull-Rom, where the evaluation
+    # saving — ~0.8 instead of 16 evaluations per pixel — is the whole cost)
+    for fname, filt, tex_b, variants in (
+            ("bspline", 1, t4, None), ("catmull_rom", 2, t4, None),
+            ("catmull_rom_latent_mlp", 2, t3, (("full16", 0, 0, 1), ("list_cplus_e2", 3, 3, 2)))):
         def runb(mode, fb, E, reps):
             out = torch.empty(uv.shape[:-1] + (4,), dtype=torch.float32, device=dev)
             rec = torch.empty(((uv.shape[0] + 3) // 4, (uv.shape[1] + 7) // 8), dtype=torch.int32, device=dev)
-            ms = time_launches(lambda: ctf.filter_frame(t4, uv, g, mode, fb, 0, seed, 0, out=out, rec=rec,
+            ms = time_launches(lambda: ctf.filter_frame(tex_b, uv, g, mode, fb, 0, seed, 0, out=out, rec=rec,
                                                         stream=stream, filter=filt, max_evals=E), reps, stream)
             return ms, ctf.stats(rec, uv.shape[1], uv.shape[0], 1, stream=stream), out
         _, _, full = runb(0, 0, 1, 1)
         full = full.clone()
-        for name, mode, fb, E in (("full16", 0, 0, 1), ("stf_positivized", 1, 0, 1), ("list_cplus_e1", 3, 3, 1),
-                                  ("list_cplus_e2", 3, 3, 2), ("box_cplus_e2", 4, 3, 2)):
-            ms, st, out = runb(mode, fb, E, 3 if mode == 0 else 10)
+        for name, mode, fb, E in variants or (("full16", 0, 0, 1), ("stf_positivized", 1, 0, 1),
+                                              ("list_cplus_e1", 3, 3, 1), ("list_cplus_e2", 3, 3, 2),
+                                              ("box_cplus_e2", 4, 3, 2)):
+            ms, st, out = runb(mode, fb, E, (1 if tex_b is t3 else 3) if mode == 0 else (3 if tex_b is t3 else 10))
             e = entry(3840, 2160, ms, st, 3840 * 2160 * 32)
             err = (out - full)[cov].double()
             mse = float((err * err).mean())

@@ -5,13 +5,16 @@
 // Same wave model as the bilinear kernel (one 8x4 wave per warp), with:
 //   a2  footprint: taps x0-1..x0+2 / y0-1..y0+2 clamped (R-24), weights R-25, clamp
 //       duplicates merged per axis -> an nc x nr grid of distinct cells per lane;
-//   a3  collect: the wave's distinct texels in ascending id by "peeling" — each step one
-//       redux.sync.min over the lanes' next unconsumed cell; a lane learns the rank of each
-//       of its row starts as it is consumed (its cells in a row have consecutive ranks);
-//       stops after E*a + 1 texels (the decision needs no more; R-28);
+//   a3  collect: the wave's distinct texels in ascending id on a 32 x 32 shared-memory bitmap
+//       of the wave's AABB (one word per row; each lane ORs its nc-bit column run into its nr
+//       rows with shared atomics): n = sum of the row popcounts, a texel's rank = exclusive
+//       scan of the row counts + popc within its row (a lane's cells in a row have
+//       consecutive ranks), each texel's first setter publishes rank -> id.  AABBs wider than
+//       32 x 32 (minified waves) "peel" instead: one redux.sync.min per distinct texel;
+//       the record's n saturates at E*a + 1 (R-28);
 //   a4  exact iff n <= E*a (List), AABB area <= E*a (Box), AABB <= MxM and n <= E*a (Mask);
 //   a5  rank r is produced by lane h(r mod a, A) as its (r div a)-th evaluation;
-//   a6  16 shuffles (32 when n > a) + the 16-cell fma chain;
+//   a6  16 shared-memory reads of the produced fp32 values by rank + the 16-cell FFMA2 chain;
 //   a7  fallbacks STF / C / C+ with |w|-proportional one-tap samples (R-26);
 //   STF mode: the positivized two-lobe estimator (R-27).
 // Independent of oracle/.  P:n = PAPER.md line; R-n = DESIGN.md reading.
@@ -51,6 +54,8 @@ struct BArgs {
 struct BSmem {
     uint32_t tbl[72];         // exact: rank -> texel id (<= 2*32 + 1); C+: sorted planned ids
     uint32_t sorted[32];      // fallback gather: sorted (id << 5 | lane) of produced texels
+    uint32_t bm[32];          // collect: AABB bitmap, one word per row
+    float4 xch[64];           // exact: rank -> produced value (fp32)
     uint8_t lane_of_rank[32]; // h(r, A)
 };
 
@@ -120,17 +125,20 @@ __device__ __forceinline__ float sel4(const float (&v)[4], int i) {
 }
 __device__ __forceinline__ int sel4i(const int (&v)[4], int i) { return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3]; }
 
-// the 16-cell blend: acc over cells (r outer, c inner) of (mx[c] * my[r]) * v, then scale.
-// The exact path, the full filter and Eq. 1's "all known" case use this one chain.
-template <int FMT>
+// the 16-cell blend: acc over cells (r outer, c inner) of fma((mx[c] * my[r]), v, acc) with the
+// texel values v in fp32 ([0, 1]: Texel::to_f4, R-9 / R-10), two channels per FFMA2.  The
+// exact path, the full filter and Eq. 1's "all known" case use this one chain, so exact waves
+// equal the full filter bit for bit.
 struct Acc {
-    float c[4];
-    __device__ __forceinline__ Acc() { c[0] = c[1] = c[2] = c[3] = 0.0f; }
-    __device__ __forceinline__ void add(float w, const Texel<FMT> &t) {
-        float v[4];
-        t.expand(v);
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(w, v[ch], c[ch]);
+    uint64_t rg, ba;
+    __device__ __forceinline__ Acc() : rg(0ull), ba(0ull) {}
+    __device__ __forceinline__ void add(float w, const float4 &v) {
+        rg = ffma2(f2pack(v.x, v.y), f2pack(w, w), rg);
+        ba = ffma2(f2pack(v.z, v.w), f2pack(w, w), ba);
+    }
+    __device__ __forceinline__ float4 get() const {
+        const float2 a = f2unpack(rg), b = f2unpack(ba);
+        return make_float4(a.x, a.y, b.x, b.y);
     }
 };
 
@@ -168,7 +176,6 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned lt = lanemask_lt();
     const int W = a.tex.W, H = a.tex.H;
-    const float sc = Texel<FMT>::kScale;
 
     for (unsigned j = 0; j < a.ipw; ++j) {
         const unsigned c = (blockIdx.x * kBWarps + warp) + j * gridDim.x * kBWarps;
@@ -226,16 +233,16 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
             if (MODE == MODE_4TAP) {
                 // the full filter: every lane evaluates its 16 taps (cells; clamp duplicates
                 // are evaluated once per tap in the count, once per cell here)
-                Acc<FMT> acc;
+                Acc acc;
 #pragma unroll 1
                 for (int q = 0; q < 16; ++q) {
                     const int r = q >> 2, cc = q & 3;
                     const bool valid = active && r < f.nr && cc < f.nc;
                     Texel<FMT> v = Texel<FMT>::zero();
                     if (valid) v = produce(a.tex, mw, (uint32_t)(f.xa + cc), (uint32_t)(f.ya + r));
-                    acc.add(__fmul_rn(sel4(f.mx, cc), sel4(f.my, r)), v);
+                    acc.add(__fmul_rn(sel4(f.mx, cc), sel4(f.my, r)), v.to_f4());
                 }
-                color = make_float4(acc.c[0] * sc, acc.c[1] * sc, acc.c[2] * sc, acc.c[3] * sc);
+                color = acc.get();
                 evals = 16 * na;
                 path = PATH_4TAP;
             } else if (MODE == MODE_STF) {
@@ -277,46 +284,86 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                     Texel<FMT> v = Texel<FMT>::zero();
                     if (need)
                         v = produce(a.tex, mw, (uint32_t)(f.xa + sel4i(f.cx, k & 3)), (uint32_t)(f.ya + sel4i(f.ry, k >> 2)));
-                    float e[4];
-                    v.expand(e);
+                    const float4 e = v.to_f4();
                     const float Wl = lobe ? -Wn : Wp;
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) cc4[ch] = need ? fmaf(Wl, e[ch], cc4[ch]) : cc4[ch];
+                    cc4[0] = need ? fmaf(Wl, e.x, cc4[0]) : cc4[0];
+                    cc4[1] = need ? fmaf(Wl, e.y, cc4[1]) : cc4[1];
+                    cc4[2] = need ? fmaf(Wl, e.z, cc4[2]) : cc4[2];
+                    cc4[3] = need ? fmaf(Wl, e.w, cc4[3]) : cc4[3];
                 }
-                color = make_float4(cc4[0] * sc, cc4[1] * sc, cc4[2] * sc, cc4[3] * sc);
+                color = make_float4(cc4[0], cc4[1], cc4[2], cc4[3]);
                 evals = __reduce_add_sync(FULL, active ? (two ? 2 : 1) : 0);
                 path = PATH_STF;
             } else {
-                // ---- a3: collect by peeling (ascending id; ranks of the lane's row starts)
+                // ---- a3: collect (ascending id; ranks of the lane's row starts)
                 const int E = a.E;
                 const int limit = E * na + 1;
-                int r = 0, cc = 0;
-                uint32_t cur = active ? (uint32_t)f.ya * (uint32_t)W + (uint32_t)f.xa : INVALID_ID;
-                int rr[4] = {0, 0, 0, 0};
-                int count = 0;
-                while (count < limit) {
-                    const uint32_t m = __reduce_min_sync(FULL, cur);
-                    if (m == INVALID_ID) break;
-                    if (lane == 0) s.tbl[count] = m;
-                    if (cur == m) {
-                        if (cc == 0) {
-                            rr[0] = r == 0 ? count : rr[0];
-                            rr[1] = r == 1 ? count : rr[1];
-                            rr[2] = r == 2 ? count : rr[2];
-                            rr[3] = r == 3 ? count : rr[3];
-                        }
-                        if (++cc == f.nc) { cc = 0; ++r; }
-                        cur = (r < f.nr) ? (uint32_t)(f.ya + r) * (uint32_t)W + (uint32_t)(f.xa + cc) : INVALID_ID;
-                    }
-                    ++count;
-                }
-                n = count;  // exact when <= E*a, else saturated at E*a + 1 (R-28)
-                // ---- a4: decide
                 const int minx = __reduce_min_sync(FULL, active ? f.xa : INT_MAX);
                 const int miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
                 const int maxx = __reduce_max_sync(FULL, active ? f.xa + f.nc - 1 : INT_MIN);
                 const int maxy = __reduce_max_sync(FULL, active ? f.ya + f.nr - 1 : INT_MIN);
                 const int bw = maxx - minx + 1, bh = maxy - miny + 1;
+                int rr[4] = {0, 0, 0, 0};
+                int count = 0;
+                if (bw <= 32 && bh <= 32) {
+                    // bitmap of the AABB: row r = word r; a lane's cells in a row are the nc
+                    // consecutive bits from xa - minx, so its ranks in that row are consecutive
+                    s.bm[lane] = 0u;
+                    __syncwarp();
+                    const int cx = (f.xa - minx) & 31, cy = (f.ya - miny) & 31;
+                    const uint32_t pat = ((1u << f.nc) - 1u) << cx;
+                    uint32_t old[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (active && r < f.nr) old[r] = atomicOr(&s.bm[(cy + r) & 31], pat);
+                    __syncwarp();
+                    const uint32_t cnt = __popc(s.bm[lane]);
+                    const int nx = (int)__reduce_add_sync(FULL, cnt);
+                    uint32_t base = cnt;   // inclusive scan of the row counts
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t u = __shfl_up_sync(FULL, base, d);
+                        base += lane >= (unsigned)d ? u : 0u;
+                    }
+                    base -= cnt;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t b = __shfl_sync(FULL, base, (cy + r) & 31);
+                        const uint32_t word = s.bm[(cy + r) & 31];
+                        rr[r] = (int)b + __popc(word & ((1u << cx) - 1u));
+                        // the first setter of each texel publishes rank -> id (ranks < E*a + 1 matter)
+                        const uint32_t fresh = active && r < f.nr ? (pat & ~old[r]) : 0u;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const int rank = rr[r] + c;
+                            if (((fresh >> (cx + c)) & 1u) && rank < 72)
+                                s.tbl[rank] = (uint32_t)(f.ya + r) * (uint32_t)W + (uint32_t)(f.xa + c);
+                        }
+                    }
+                    count = nx < limit ? nx : limit;
+                } else {
+                    // wider than the bitmap: peel, one redux.sync.min per distinct texel
+                    int r = 0, cc = 0;
+                    uint32_t cur = active ? (uint32_t)f.ya * (uint32_t)W + (uint32_t)f.xa : INVALID_ID;
+                    while (count < limit) {
+                        const uint32_t m = __reduce_min_sync(FULL, cur);
+                        if (m == INVALID_ID) break;
+                        if (lane == 0) s.tbl[count] = m;
+                        if (cur == m) {
+                            if (cc == 0) {
+                                rr[0] = r == 0 ? count : rr[0];
+                                rr[1] = r == 1 ? count : rr[1];
+                                rr[2] = r == 2 ? count : rr[2];
+                                rr[3] = r == 3 ? count : rr[3];
+                            }
+                            if (++cc == f.nc) { cc = 0; ++r; }
+                            cur = (r < f.nr) ? (uint32_t)(f.ya + r) * (uint32_t)W + (uint32_t)(f.xa + cc) : INVALID_ID;
+                        }
+                        ++count;
+                    }
+                }
+                n = count;  // exact when <= E*a, else saturated at E*a + 1 (R-28)
+                // ---- a4: decide
                 bool ok;
                 if (a.variant == BVAR_BOX) ok = bw * bh <= E * na;
                 else if (a.variant == BVAR_MASK16) ok = bw <= 16 && bh <= 16 && n <= E * na;
@@ -325,15 +372,14 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                 if (a.flags & FLAG_FORCE_FALLBACK) ok = false;
                 __syncwarp();
                 if (ok) {
-                    // ---- a5: produce (<= E per lane)
+                    // ---- a5: produce (<= E per lane): rank i on lane h(i mod a, A), slot i div a;
+                    // the value goes to the shared table by rank (fp32, converted once)
                     const bool box = a.variant == BVAR_BOX;
                     const int total = box ? bw * bh : n;
-                    Texel<FMT> val[2] = {Texel<FMT>::zero(), Texel<FMT>::zero()};
 #pragma unroll 1
                     for (int slot = 0; slot < 2; ++slot) {
                         if (slot * na >= total) break;
                         const int i = ar + slot * na;
-                        Texel<FMT> v = Texel<FMT>::zero();
                         if (active && i < total) {
                             uint32_t tx, ty;
                             if (box) {
@@ -344,14 +390,12 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                                 ty = id / (uint32_t)W;
                                 tx = id - ty * (uint32_t)W;
                             }
-                            v = produce(a.tex, mw, tx, ty);
+                            s.xch[i] = produce(a.tex, mw, tx, ty).to_f4();
                         }
-                        if (slot == 0) val[0] = v; else val[1] = v;
                     }
-                    // ---- a6: gather (16 shuffles, 32 when n > a) + blend
-                    const bool two = total > na;
-                    const bool full = A == FULL;
-                    Acc<FMT> acc;
+                    __syncwarp();
+                    // ---- a6: gather by rank + the 16-cell chain (bit-identical to the full filter)
+                    Acc acc;
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
                         const int rq = q >> 2, cq = q & 3;
@@ -359,18 +403,10 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                         int rank;
                         if (box) rank = (f.ya + rq - miny) * bw + (f.xa + cq - minx);
                         else rank = (rq == 0 ? rr[0] : rq == 1 ? rr[1] : rq == 2 ? rr[2] : rr[3]) + cq;
-                        int slot = 0;
-                        if (rank >= na) { rank -= na; slot = 1; }
-                        int src = (int)lane;
-                        if (valid) src = full ? rank : (int)s.lane_of_rank[rank];
-                        Texel<FMT> v = Texel<FMT>::shfl(val[0], src);
-                        if (two) {
-                            const Texel<FMT> v1 = Texel<FMT>::shfl(val[1], src);
-                            if (slot) v = v1;
-                        }
+                        const float4 v = valid ? s.xch[rank & 63] : make_float4(0.f, 0.f, 0.f, 0.f);
                         acc.add(__fmul_rn(sel4(f.mx, cq), sel4(f.my, rq)), v);
                     }
-                    color = make_float4(acc.c[0] * sc, acc.c[1] * sc, acc.c[2] * sc, acc.c[3] * sc);
+                    color = acc.get();
                     evals = total;
                     path = PATH_EXACT;
                 } else {
@@ -389,11 +425,10 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                 if (run_fb == FB_STF) {
                     Texel<FMT> v = Texel<FMT>::zero();
                     if (active) v = produce(a.tex, mw, (uint32_t)qx, (uint32_t)qy);
-                    float e[4];
-                    v.expand(e);
+                    const float4 e = v.to_f4();
                     const bool neg = (sel4(f.wx, pi) < 0.0f) != (sel4(f.wy, pj) < 0.0f);
-                    const float g = __fmul_rn(__fmul_rn(Sx, Sy), neg ? -sc : sc);
-                    color = make_float4(e[0] * g, e[1] * g, e[2] * g, e[3] * g);
+                    const float g = __fmul_rn(Sx, Sy) * (neg ? -1.0f : 1.0f);
+                    color = make_float4(e.x * g, e.y * g, e.z * g, e.w * g);
                     evals = na;
                 } else {
                     uint32_t prod = active ? (uint32_t)qy * (uint32_t)W + (uint32_t)qx : INVALID_ID;
@@ -460,12 +495,13 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                     }
                     evals = (run_fb == FB_CPLUS) ? __popc(__ballot_sync(FULL, prod != INVALID_ID)) : na;
                     s.sorted[lane] = warp_sort32(prod != INVALID_ID ? ((prod << 5) | lane) : INVALID_ID);
+                    s.xch[lane] = val.to_f4();   // this lane's produced value (fp32), read by lane index
                     __syncwarp();
                     // Eq. 1 over the known cells (R-23 evaluation order, R-28)
                     bool all_known = true;
                     int N = 0;
                     float Sw = 0.0f, Sp[4] = {0.f, 0.f, 0.f, 0.f};
-                    Acc<FMT> acc;
+                    Acc acc;
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
                         const int rq = q >> 2, cq = q & 3;
@@ -481,29 +517,24 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                                 if ((hit >> 5) == id) { known = true; src = (int)(hit & 31u); }
                             }
                         }
-                        Texel<FMT> v = Texel<FMT>::shfl(val, src);
-                        if (!known) v = Texel<FMT>::zero();
+                        const float4 v = known ? s.xch[src] : make_float4(0.f, 0.f, 0.f, 0.f);
                         if (need && !known) all_known = false;
                         if (known) {
                             ++N;
                             Sw = __fadd_rn(Sw, mwq);
-                            float e[4];
-                            v.expand(e);
-#pragma unroll
-                            for (int ch = 0; ch < 4; ++ch) Sp[ch] = __fadd_rn(Sp[ch], e[ch]);
+                            Sp[0] = __fadd_rn(Sp[0], v.x);
+                            Sp[1] = __fadd_rn(Sp[1], v.y);
+                            Sp[2] = __fadd_rn(Sp[2], v.z);
+                            Sp[3] = __fadd_rn(Sp[3], v.w);
                         }
                         acc.add(mwq, v);
                     }
                     __syncwarp();
-                    float cc4[4];
+                    const float4 ac = acc.get();
                     const float rest = (all_known || N == 0) ? 0.0f : __fdividef(__fsub_rn(1.0f, Sw), (float)N);
-#pragma unroll
-                    for (int ch = 0; ch < 4; ++ch) cc4[ch] = fmaf(rest, Sp[ch], acc.c[ch]) * sc;
-                    if (N == 1 && !all_known) {
-#pragma unroll
-                        for (int ch = 0; ch < 4; ++ch) cc4[ch] = Sp[ch] * sc;
-                    }
-                    color = make_float4(cc4[0], cc4[1], cc4[2], cc4[3]);
+                    color = make_float4(fmaf(rest, Sp[0], ac.x), fmaf(rest, Sp[1], ac.y), fmaf(rest, Sp[2], ac.z),
+                                        fmaf(rest, Sp[3], ac.w));
+                    if (N == 1 && !all_known) color = make_float4(Sp[0], Sp[1], Sp[2], Sp[3]);
                 }
             }
             if (!active) color = make_float4(0.f, 0.f, 0.f, 0.f);
