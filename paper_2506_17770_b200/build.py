@@ -25,7 +25,7 @@ UNITS = [
     ("ctf_bicubic.cu", ["-DCTF_TU_FMT=1"], "ctf_bicubic_bc1.o"),
     ("ctf_bicubic.cu", ["-DCTF_TU_FMT=2"], "ctf_bicubic_mlp.o"),
 ]
-HEADERS = ["ctf_device.cuh", "ctf_internal.h"]
+HEADERS = sorted(p.name for p in CSRC.iterdir() if p.suffix in (".cuh", ".h"))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

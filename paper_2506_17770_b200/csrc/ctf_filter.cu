@@ -19,6 +19,8 @@
 //      produced texels by AABB bitmask when it fits, else sorted keys
 //   a8 per-wave record
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <type_traits>
@@ -2415,6 +2417,16 @@ __global__ void __launch_bounds__(kWarps * 32, FUSED ? CTF_FUSED_MINB
     }
 }
 
+// ---- latent MLP: CTA-level tensor-core (tcgen05) decode of the lean waves' texels
+#ifndef CTF_TC05
+#define CTF_TC05 0  // 1: latent-MLP COLLAB release path on the CTA-level tcgen05 kernel (measured slower
+                    // than the one-warp mma.sync path, profiles/r02/tc05_evaluation.md)
+#endif
+#ifndef CTF_TC05_MINB
+#define CTF_TC05_MINB 3  // resident CTAs (8 warps each) per SM
+#endif
+#include "ctf_mlp_tc05.cuh"
+
 // Second / third pass over the marked waves.  FALLBACK: the kFbMark waves through the lean
 // fallback (fb_wave) — and, with CTF_REST_MERGED, the kSlowMark waves through the general
 // path out of line; else (third kernel) the kSlowMark waves through the general path.
@@ -2718,6 +2730,37 @@ static auto lean_kernel_for(const KArgs &k) {
 template <int FMT, bool DBG>
 static cudaError_t launch_lean(KArgs &k, const typename WeightsOf<FMT>::type &mw, int dev, int sms,
                                cudaStream_t stream) {
+    if constexpr (FMT == FMT_MLP && !DBG && CTF_TC05) {
+        if (!(k.flags & FLAG_FORCE_FALLBACK)) {   // the CTA-level tensor-core path (ctf_mlp_tc05.cuh)
+            const bool grad = k.grad != nullptr, box = k.variant == VAR_BOX;
+            auto kern = grad ? (box ? ctf_mlp_tc05_kernel<true, true> : ctf_mlp_tc05_kernel<true, false>)
+                             : (box ? ctf_mlp_tc05_kernel<false, true> : ctf_mlp_tc05_kernel<false, false>);
+            const size_t dyn = sizeof(tc05::CtaSmem) + 1024;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            if (e != cudaSuccess) return e;
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            if (e != cudaSuccess) return e;
+            int per_sm = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tc05::kWarpsT * 32, dyn);
+            if (e != cudaSuccess) return e;
+            if (getenv("CTF_DEBUG_OCC")) {
+                cudaFuncAttributes fa;
+                cudaFuncGetAttributes(&fa, kern);
+                fprintf(stderr, "tc05: per_sm %d dyn %zu nchunks %u sms %d | static %zu maxdyn %d regs %d maxthr %d local %zu\n",
+                        per_sm, dyn, k.nchunks, sms, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.numRegs,
+                        fa.maxThreadsPerBlock, fa.localSizeBytes);
+            }
+            // the occupancy API reports one CTA per SM for kernels that allocate tensor memory; each
+            // CTA here holds 32 TMEM columns (of 512), so CTF_TC05_MINB CTAs fit (registers and
+            // shared memory were sized for it)
+            if (per_sm < CTF_TC05_MINB) per_sm = CTF_TC05_MINB;
+            long long grid = (long long)sms * per_sm;
+            const long long need = ((long long)k.nchunks + tc05::kWarpsT - 1) / tc05::kWarpsT;
+            if (grid > need) grid = need;
+            kern<<<(unsigned)(grid < 1 ? 1 : grid), tc05::kWarpsT * 32, dyn, stream>>>(k, mw);
+            return cudaGetLastError();
+        }
+    }
     auto kern = use_fused<FMT>(k) ? lean_kernel_for<FMT, DBG, true>(k) : lean_kernel_for<FMT, DBG, false>(k);
     const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
     int per_sm = 0;

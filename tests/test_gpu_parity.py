@@ -397,9 +397,11 @@ def test_multi_frame_work_lists(ctf, nf):
 
 @pytest.mark.parametrize("wf,hf,mag,theta", [(104, 40, 1.5, 25.0), (136, 44, 0.9, 60.0)])
 def test_release_paired_runs_latent_mlp(ctf, wf, hf, mag, theta):
-    """The release latent-MLP COLLAB kernel decodes two waves' texels in one tensor-core pass
-    (one 16-row tile when nA + nB <= 16): records and colours equal the oracle's and the
-    debug kernel's (one wave per decode) colours bit for bit, on odd runs with partial waves."""
+    """The release latent-MLP COLLAB kernel decodes the texels of a CTA's waves as the rows of one
+    tcgen05 tile (R-29, CTA-level collaboration): records equal the oracle's, colours are within
+    the parity bar of the oracle and within 1e-6 of the debug kernel's (one wave per mma.sync
+    decode: the same 3xFP16 products, another fp32 accumulation order), on odd runs with partial
+    waves."""
     import oracle
     tex = mlp_tex(64, 64, 5)
     uv, g = synthetic.rotated_quad(wf, hf, 64, 64, mag, theta, coverage="circle", radius=15.0, jitter_seed=3)
@@ -410,7 +412,8 @@ def test_release_paired_runs_latent_mlp(ctf, wf, hf, mag, theta):
         np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
         assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
         gg = run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=12, frame_index=2)
-        assert np.array_equal(out.cpu().numpy().view(np.uint32), gg["out"].view(np.uint32))
+        np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), gg["rec"])
+        assert np.abs(out.cpu().numpy().astype(np.float64) - gg["out"].astype(np.float64)).max() <= 1e-6
 
 
 def anisotropic_quad(wf, hf, tex_w, tex_h, sx, sy, theta_deg, center=(0.5, 0.5)):
