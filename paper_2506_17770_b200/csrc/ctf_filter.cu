@@ -1351,7 +1351,7 @@ struct FastSmem {
 struct PairSmem {
     float4 xch[64];           // job -> produced value
     uint4 lut[8];             // BC1 per-index constants (bc1_lut_entry), per warp
-    uint8_t bit_of_rank[64];  // job -> window offset (dy << 3) | dx
+    uint8_t bit_of_rank[96];  // job -> window offset (dy << 3) | dx; [64, 96): per-lane scratch slots
 };
 
 // 64-bit window masks held as two words (hi = 0 for a 32-bit window)
@@ -1611,9 +1611,18 @@ struct PairFront {
     uint32_t rec;
 };
 // steps a1-a4 of lean_wave for one wave; the rank -> window-bit table goes to job base + r
+// the push-table codes (dy << 3) | dx of window bit `lane` for the pitches P = 8, 4, 6, 5, one
+// byte each (computed once per thread; pair_front selects a byte by the window's pitch)
+__device__ __forceinline__ uint32_t push_codes(unsigned lane) {
+    uint32_t c = 0u;
+    const unsigned P[4] = {8u, 4u, 6u, 5u};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c |= (((lane / P[i]) << 3) | (lane % P[i])) << (8 * i);
+    return c;
+}
 template <bool GRAD, int FMT, class SM, bool BOX = false>
 __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 uv, uint2 gr, int base, uint8_t *bits0,
-                                                unsigned lane, unsigned lt) {
+                                                unsigned lane, unsigned lt, uint32_t cpk) {
     const unsigned lanebit = 1u << lane;
     PairFront o;
     o.s = o.t = 0.f;
@@ -1633,11 +1642,11 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     // row-major order of U for every shape); 6x5 / 5x6 take the 5x5..6x6 AABBs of rotated
     // magnified waves (~10 % of config-5 waves) off the 64-bit path
     int K = 0;
-    uint32_t P = 8u, qmul = 32u;   // pitch, ceil(256 / P): t / P = (t * qmul) >> 8 for t < 32 (64 for P = 8)
+    uint32_t P = 8u, csh = 0u;   // pitch; byte of cpk holding this pitch's push code
     if (__all_sync(FULL, (dx | (dy << 1)) < 8u)) K = 1;                                // 8x4
-    else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; P = 4u; qmul = 64u; }   // 4x8
-    else if (__all_sync(FULL, dx < 6u && dy < 5u)) { K = 1; P = 6u; qmul = 43u; }      // 6x5
-    else if (__all_sync(FULL, dx < 5u && dy < 6u)) { K = 1; P = 5u; qmul = 52u; }      // 5x6
+    else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; P = 4u; csh = 8u; }     // 4x8
+    else if (__all_sync(FULL, dx < 6u && dy < 5u)) { K = 1; P = 6u; csh = 16u; }       // 6x5
+    else if (__all_sync(FULL, dx < 5u && dy < 6u)) { K = 1; P = 5u; csh = 24u; }       // 5x6
     else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                                  // 8x8
     if (K == 0) {   // a wider window: the wide-window kernel (BC1) / the general kernel (latent MLP)
         o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
@@ -1648,8 +1657,7 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     const uint32_t dxs = (uint32_t)(f.xb - f.xa);
     const uint32_t pat = 1u + dxs + dxs;
     // push table entry of window bit t: its offset (dy << 3) | dx from the window origin
-    const uint32_t qt = (lane * qmul) >> 8;
-    const uint32_t code = (qt << 3) | (lane - qt * P);
+    const uint32_t code = (cpk >> csh) & 63u;   // = ((lane / P) << 3) | (lane % P)
     uint8_t *bits = bits0 + base;
     int n, r0, r2;
     if (K == 1) {
@@ -1657,7 +1665,9 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
         n = __popc(wm);
         r0 = __popc(wm & ((1u << t0) - 1u));
         r2 = __popc(wm & ((1u << t2) - 1u));
-        if (!BOX) st_shared_u8_if(bits + __popc(wm & lt), code, wm & lanebit);
+        // push (no predicate): the owner of window bit `lane` writes its code at its rank, every
+        // other lane into its own scratch slot 64 + lane (no divergent store region)
+        if (!BOX) bits0[(wm & lanebit) ? base + __popc(wm & lt) : 64 + (int)lane] = (uint8_t)code;
     } else {
         const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
         const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
@@ -1667,9 +1677,9 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
         r0 = rank64(wl, wh, t0);
         r2 = rank64(wl, wh, t2);
         if (!BOX) {
-            st_shared_u8_if(bits + __popc(wl & lt), lane, wl & lanebit);
+            bits0[(wl & lanebit) ? base + __popc(wl & lt) : 64 + (int)lane] = (uint8_t)lane;
             const int rh = nl + __popc(wh & lt);
-            st_shared_u8_if(bits + (rh & 31), 32u + lane, (wh & lanebit) && rh < 32);
+            bits0[((wh & lanebit) && rh < 32) ? base + (rh & 31) : 64 + (int)lane] = (uint8_t)(32u + lane);
         }
     }
     int evals = n;   // jobs: n (List), the AABB area (Box, see lean_wave)
@@ -2305,20 +2315,21 @@ __global__ void __launch_bounds__(kWarps * 32, FUSED ? CTF_FUSED_MINB
             // pairs (A, B) = waves (wx, wx + 1); A's next load is issued after A's front,
             // B's after B's front, so each covers about one pair of work
             const unsigned lt_mask = lanemask_lt();
+            const uint32_t cpk = push_codes(lane);
             float2 uv_b = make_float2(__int_as_float(0x7fc00000), 0.f);
             uint2 gr_b = make_uint2(0u, 0u);
             ld_stream_f2_if(uv_b, a.uv + (pix + 8u), wx0 + 1 < wx1);
             ld_stream_u2_if(gr_b, a.grad + (pix + 8u), (wx0 + 1 < wx1) & has_grad);
             for (int wx = wx0; wx < wx1; wx += 2, pix += 16u) {
               const bool hasB = wx + 1 < wx1;
-              const PairFront fa = pair_front<GRAD, FMT, SmemT, BOX>(a, fs, uv_n, gr_n, 0, fs.bit_of_rank, lane, lt_mask);
+              const PairFront fa = pair_front<GRAD, FMT, SmemT, BOX>(a, fs, uv_n, gr_n, 0, fs.bit_of_rank, lane, lt_mask, cpk);
               ld_stream_f2_if(uv_n, a.uv + (pix + 16u), wx + 2 < wx1);
               ld_stream_u2_if(gr_n, a.grad + (pix + 16u), (wx + 2 < wx1) & has_grad);
               PairFront fb;
               fb.n = 0;
               fb.rec = 0u;
               __syncwarp();   // A's push-table writes (all of them, also a rejected A's) before B's
-              if (hasB) fb = pair_front<GRAD, FMT, SmemT, BOX>(a, fs, uv_b, gr_b, fa.n, fs.bit_of_rank, lane, lt_mask);
+              if (hasB) fb = pair_front<GRAD, FMT, SmemT, BOX>(a, fs, uv_b, gr_b, fa.n, fs.bit_of_rank, lane, lt_mask, cpk);
               ld_stream_f2_if(uv_b, a.uv + (pix + 24u), wx + 3 < wx1);
               ld_stream_u2_if(gr_b, a.grad + (pix + 24u), (wx + 3 < wx1) & has_grad);
               __syncwarp();   // bit_of_rank written; the previous pair's xch reads are done
@@ -2820,8 +2831,11 @@ static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw,
     if (FMT == FMT_BC1) {
         // runs short enough that every resident warp gets work (small calls are latency-bound:
         // a warp's waves are a dependent chain), at most kChunk waves (large batches)
+        // (ceil(waves / resident warps), even: one round of runs, the longest chain as short as
+        // the call allows)
         const long long warps = (long long)sms * CTF_PAIR_MINB * kWarps;
-        long long ch = ((long long)k.nrec / (warps > 0 ? warps : 1)) & ~1LL;
+        long long ch = ((long long)k.nrec + warps - 1) / (warps > 0 ? warps : 1);
+        ch += ch & 1LL;
         ch = ch < 2 ? 2 : ch > kChunk ? kChunk : ch;
         const unsigned frames = k.nrec / (unsigned)k.wpf;
         k.chunk = (int)ch;

@@ -103,7 +103,7 @@ struct alignas(1024) CtaSmem {
     uint32_t w3h[16 * 16], w3l[16 * 16];        // B3 [16][32]: rows 4..15 zero
     float b2[32], b3[4];
     float4 xch[kMaxRows];                       // job row -> decoded RGBA
-    uint8_t bits[kWarpsT][64];                  // per warp: job -> window offset (pair_front)
+    uint8_t bits[kWarpsT][96];                  // per warp: job -> window offset (pair_front; 64..95 scratch)
     int info[kWarpsT][8];                       // per warp: jobs, nA, A.minx, A.miny, B.minx, B.miny
     unsigned long long mbar;
     uint32_t tmem;
@@ -290,9 +290,9 @@ __global__ void __launch_bounds__(tc05::kWarpsT * 32, CTF_TC05_MINB)
         fa.rec = fb.rec = 0u;
         const bool hasB = have && wx + 1 < wx1;
         if (have) {
-            fa = pair_front<GRAD, FMT_MLP, XchRef, BOX>(a, xr, uv_a, gr_a, 0, s.bits[warp], lane, lt_mask);
+            fa = pair_front<GRAD, FMT_MLP, XchRef, BOX>(a, xr, uv_a, gr_a, 0, s.bits[warp], lane, lt_mask, push_codes(lane));
             __syncwarp();
-            if (hasB) fb = pair_front<GRAD, FMT_MLP, XchRef, BOX>(a, xr, uv_b, gr_b, fa.n, s.bits[warp], lane, lt_mask);
+            if (hasB) fb = pair_front<GRAD, FMT_MLP, XchRef, BOX>(a, xr, uv_b, gr_b, fa.n, s.bits[warp], lane, lt_mask, push_codes(lane));
             // next pair's inputs
             uv_a = uv_b = make_float2(__int_as_float(0x7fc00000), 0.f);
             gr_a = gr_b = make_uint2(0u, 0u);
