@@ -1384,14 +1384,6 @@ __device__ __forceinline__ Merged merge_corners(const Foot &f) {
     return m;
 }
 
-// Corner masks (bit k = corner k of a footprint) read from a window bitmask (lo, hi):
-// corners 0 / 1 sit at t0 and t0 + dxs, corners 2 / 3 at t2 and t2 + dxs (one 64-bit
-// shift per footprint row).
-__device__ __forceinline__ unsigned corner_bits(uint32_t lo, uint32_t hi, uint32_t t0, uint32_t t2, uint32_t dxs) {
-    const uint64_t D = ((uint64_t)hi << 32) | lo;
-    const uint32_t r0 = (uint32_t)(D >> t0), r2 = (uint32_t)(D >> t2);
-    return (r0 & 1u) | (((r0 >> dxs) & 1u) << 1) | ((r2 & 1u) << 2) | (((r2 >> dxs) & 1u) << 3);
-}
 // bit k = corner k is the first occurrence of its texel and its merged weight is nonzero
 __device__ __forceinline__ unsigned contrib_bits(const Foot &f, const Merged &m) {
     const unsigned ddx = f.xb != f.xa, ddy = f.yb != f.ya;
@@ -1399,25 +1391,6 @@ __device__ __forceinline__ unsigned contrib_bits(const Foot &f, const Merged &m)
     const unsigned nz = (m.dw[0] != 0.0f ? 1u : 0u) | (m.dw[1] != 0.0f ? 2u : 0u) | (m.dw[2] != 0.0f ? 4u : 0u) |
                         (m.dw[3] != 0.0f ? 8u : 0u);
     return first & nz;
-}
-
-// C+ spare-lane pick (R-18 v) over served lane g's footprint: the distinct nonzero-weight
-// texels not planned (PL = planned corner mask), chosen ~ merged weight with u2 (first
-// cumulative sum > u2 * sum, else the last candidate); -1 when there is none.  The sums
-// run in corner order from 0 with one rounding per candidate, exactly as cplus_pick().
-__device__ __forceinline__ int cplus_pick_bits(const Foot &g, float u2, unsigned PL) {
-    const Merged m = merge_corners(g);
-    const unsigned cand = contrib_bits(g, m) & ~PL;
-    float ps[4], wsum = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        wsum = __fadd_rn(wsum, ((cand >> k) & 1u) ? m.dw[k] : 0.0f);
-        ps[k] = wsum;
-    }
-    const float target = __fmul_rn(u2, wsum);
-    const unsigned gt = cand & ((ps[0] > target ? 1u : 0u) | (ps[1] > target ? 2u : 0u) |
-                                (ps[2] > target ? 4u : 0u) | (ps[3] > target ? 8u : 0u));
-    return cand == 0u ? -1 : gt != 0u ? __ffs(gt) - 1 : 31 - __clz(cand);
 }
 
 // One-tap-free Eq. 1 / WC stand-in from the four corner values pv[k] (0 where the texel
@@ -1460,10 +1433,26 @@ __device__ __forceinline__ float4 combine_eq1_mc(const Foot &f, const Merged &m,
     if (N == 1 && !all_known) c = make_float4(a01.x, a01.y, a23.x, a23.y);
     return c;
 }
-template <bool WC>
-__device__ __forceinline__ float4 combine_eq1_bits(const Foot &f, unsigned IN, const float4 (&pv)[4]) {
-    const Merged m = merge_corners(f);
-    return combine_eq1_mc<WC>(f, m, contrib_bits(f, m), IN, pv);
+// Eq. 1 as one 4-corner blend with per-corner coefficients: a known corner k
+// contributes w_k (its duplicates too: their sum is the merged weight of the texel, R-14) plus,
+// on the first occurrence of each known nonzero-weight texel, rest = (1 - Sum_K dw) / N, so the
+// blend is Sum_K dw p + rest * Sum_K p; unknown corners get 0.  The special cases hold up to
+// fp32 rounding: all known -> rest = 0 and the blend is the exact-path chain; N = 1 ->
+// (dw + (1 - dw)) p.  pv must be finite everywhere (coefficient 0 x value).
+__device__ __forceinline__ float4 combine_eq1_coef(const Foot &f, const Merged &m, unsigned C, unsigned IN,
+                                                   const float4 (&pv)[4]) {
+    const unsigned Kn = C & IN;
+    const bool all_known = (C & ~IN) == 0u;
+    const int N = __popc(Kn);
+    float Sw = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) Sw = __fadd_rn(Sw, ((Kn >> k) & 1u) ? m.dw[k] : 0.0f);
+    const float rest = (all_known || N == 0) ? 0.0f : __fdividef(1.0f - Sw, (float)N);
+    float cf[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        cf[k] = __fadd_rn(((IN >> k) & 1u) ? f.w[k] : 0.0f, ((Kn >> k) & 1u) ? rest : 0.0f);
+    return blend4f(pv, cf);
 }
 
 // One FULL wave (32 active lanes) through the lean exact path.  Returns done = false with
@@ -1746,219 +1735,6 @@ __device__ __forceinline__ void pair_back(const KArgs &a, const SM &fs, const Pa
     }
 }
 
-// ---------------------------------------- lean fallback over windows up to 128 bits
-// Window masks as NW (2 or 4) words; the pitch 2^lgP <= 32 keeps every window row inside one
-// word.  NW = 2 covers the 8x4 / 4x8 / 8x8 windows (most fallback waves), NW = 4 the
-// 16x8 / 8x16 / 32x4 ones.
-template <int NW>
-struct WMaskN {
-    uint32_t w[NW];
-    __device__ __forceinline__ uint32_t word(uint32_t k) const {
-        if constexpr (NW == 2) return k == 0 ? w[0] : w[1];
-        else return k == 0 ? w[0] : k == 1 ? w[1] : k == 2 ? w[2] : w[3];
-    }
-    __device__ __forceinline__ int count() const {
-        int c = 0;
-#pragma unroll
-        for (int k = 0; k < NW; ++k) c += __popc(w[k]);
-        return c;
-    }
-    __device__ __forceinline__ int rank(uint32_t t) const {   // set bits below t
-        int c = 0;
-#pragma unroll
-        for (int k = 0; k < NW; ++k) {
-            const uint32_t kk = (uint32_t)k;
-            c += __popc(w[k] & ((t >> 5) > kk ? 0xFFFFFFFFu : (t >> 5) == kk ? (1u << (t & 31u)) - 1u : 0u));
-        }
-        return c;
-    }
-    // corners 0 / 1 at t0, t0 + dxs; 2 / 3 at t2, t2 + dxs
-    __device__ __forceinline__ unsigned corners(uint32_t t0, uint32_t t2, uint32_t dxs) const {
-        const uint32_t a = word(t0 >> 5) >> (t0 & 31u), b = word(t2 >> 5) >> (t2 & 31u);
-        return (a & 1u) | (((a >> dxs) & 1u) << 1) | ((b & 1u) << 2) | (((b >> dxs) & 1u) << 3);
-    }
-    // lane j holds bit j of every word: rank -> bit position for ranks < 32
-    __device__ __forceinline__ void push(uint8_t *tbl, unsigned lane, unsigned lt) const {
-        int pre = 0;
-#pragma unroll
-        for (int k = 0; k < NW; ++k) {
-            const int r = pre + __popc(w[k] & lt);
-            st_shared_u8_if(tbl + (r & 31), 32u * k + lane, ((w[k] >> lane) & 1u) && r < 32);
-            pre += __popc(w[k]);
-        }
-    }
-};
-// OR-reduce of per-lane bit patterns placed at window positions t (and t2), words < K
-template <int NW>
-__device__ __forceinline__ WMaskN<NW> reduce_wn(int K, uint32_t t, uint32_t pat, bool on, uint32_t t2 = 0xFFFFFFFFu) {
-    WMaskN<NW> r;
-#pragma unroll
-    for (int k = 0; k < NW; ++k) {
-        uint32_t m = 0u;
-        if (k < K) {   // warp-uniform
-            if (on && (t >> 5) == (uint32_t)k) m |= pat << (t & 31u);
-            if (on && (t2 >> 5) == (uint32_t)k) m |= pat << (t2 & 31u);
-            m = __reduce_or_sync(FULL, m);
-        }
-        r.w[k] = m;
-    }
-    return r;
-}
-
-struct FbSmem {
-    float4 xch[128];          // exact: rank -> value; fallback: window position -> value
-    uint4 lut[8];             // BC1 per-index constants (bc1_lut_entry), per warp
-    uint8_t bit_of_rank[32];  // rank -> window bit (0..127)
-};
-
-// One FULL wave whose window fits 128 bits, exact or fallback (STF / WC / C / C+), the
-// same results as the general path (records, producers, selections bit for bit).
-template <bool DBG, int NW>
-__device__ __forceinline__ LeanOut fb_wave_k(const KArgs &a, FbSmem &fs, const Foot &f, int minx, int miny, int K,
-                                             unsigned lgP, bool wave_mag, int px, int py, uint32_t frame, bool force) {
-    const unsigned lane = lane_id(), lt = lanemask_lt();
-    LeanOut o;
-    o.prod = INVALID_ID;
-    o.selbits = 0u;
-    o.done = true;
-    const uint32_t pmask = (1u << lgP) - 1u;
-    const uint32_t t0 = ((uint32_t)(f.ya - miny) << lgP) + (uint32_t)(f.xa - minx);
-    const uint32_t t2 = t0 + ((uint32_t)(f.yb - f.ya) << lgP);
-    const uint32_t dxs = (uint32_t)(f.xb - f.xa);
-    const WMaskN<NW> U = reduce_wn<NW>(K, t0, 1u + dxs + dxs, true, t2);   // the unique set (List)
-    const int n = U.count();
-    const bool exact = n <= 32 && !force;
-    const int fb = a.fallback;
-    bool produced;
-    int qx, qy;
-    if (exact) {
-        U.push(fs.bit_of_rank, lane, lt);
-        __syncwarp();
-        produced = (int)lane < n;
-        const uint32_t e = fs.bit_of_rank[lane];
-        qx = minx + (int)(e & pmask);
-        qy = miny + (int)(e >> lgP);
-    } else {
-        // ---- a7 plan: every lane's STF texel; C+ dedupes it and spreads the
-        // spare lanes over the wave with Eq. 2
-        const uint4 rn = philox4x32_10_rk(make_uint4((uint32_t)px, (uint32_t)(py + a.row0), frame, 0u), a.rk[0], a.rk[1]);
-        const int ksel = stf_corner(f, rn);
-        qx = corner_x(f, ksel);
-        qy = corner_y(f, ksel);
-        o.selbits = (uint32_t)ksel;
-        produced = true;
-        if (fb == FB_CPLUS) {
-            const uint32_t tp = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
-            const WMaskN<NW> P = reduce_wn<NW>(K, tp, 1u, true);   // planned set
-            const int np = P.count();
-            P.push(fs.bit_of_rank, lane, lt);
-            __syncwarp();
-            const bool spare = (int)lane >= np;
-            const int l = spare ? eq2_lane_rank((int)lane, np, 32) : (int)lane;   // h(., A) = id
-            Foot g;
-            g.xa = __shfl_sync(FULL, f.xa, l);
-            g.xb = __shfl_sync(FULL, f.xb, l);
-            g.ya = __shfl_sync(FULL, f.ya, l);
-            g.yb = __shfl_sync(FULL, f.yb, l);
-            g.s = __shfl_sync(FULL, f.s, l);
-            g.t = __shfl_sync(FULL, f.t, l);
-            make_weights(g);
-            const uint32_t tg0 = ((uint32_t)(g.ya - miny) << lgP) + (uint32_t)(g.xa - minx);
-            const uint32_t tg2 = tg0 + ((uint32_t)(g.yb - g.ya) << lgP);
-            const int pick = cplus_pick_bits(g, unit24(rn.z), P.corners(tg0, tg2, (uint32_t)(g.xb - g.xa)));
-            const uint32_t e = fs.bit_of_rank[lane];
-            if (!spare) {   // planned rank `lane` < n_p
-                qx = minx + (int)(e & pmask);
-                qy = miny + (int)(e >> lgP);
-            } else {
-                o.selbits |= (1u << 5) | ((uint32_t)l << 8);
-                produced = pick >= 0;
-                qx = produced ? corner_x(g, pick) : qx;
-                qy = produced ? corner_y(g, pick) : qy;
-                o.selbits |= produced ? (((uint32_t)pick << 2) | (1u << 4)) : 0u;
-            }
-        }
-    }
-    // ---- the single texel-production site (<= 1 evaluation per lane).  The
-    // decoder runs on every lane (SIMT: same cost), non-producers on the window origin,
-    // so no divergent region precedes the warp collectives below.
-    if (!produced) {
-        qx = minx;
-        qy = miny;
-    }
-    const float4 val = bc1_decode_unorm_lut(a.tex, qx, qy, fs.lut);
-    if (DBG) o.prod = produced ? (uint32_t)(qy * a.tex.W + qx) : INVALID_ID;
-    if (exact) {
-        if (produced) fs.xch[lane] = val;
-        __syncwarp();
-        const int r0 = U.rank(t0), r2 = U.rank(t2);
-        const float4 p[4] = {fs.xch[r0], fs.xch[r0 + (int)dxs], fs.xch[r2], fs.xch[r2 + (int)dxs]};
-        o.color = blend4f(p, f.w);
-        o.rec = (uint32_t)n * 0x101u | (32u << 16) | ((uint32_t)wave_mag << 25);
-        return o;
-    }
-    // ---- a7 finish: one-tap (STF), WC stand-in or Eq. 1 (C, C+) over the produced set D
-    const int evals = fb == FB_CPLUS ? __popc(__ballot_sync(FULL, produced)) : 32;
-    if (fb == FB_STF) {
-        o.color = val;
-    } else {
-        const uint32_t tq = ((uint32_t)(qy - miny) << lgP) + (uint32_t)(qx - minx);
-        const WMaskN<NW> D = reduce_wn<NW>(K, tq, 1u, produced);
-        // values indexed by window position, zero where nothing was produced; one
-        // publisher per produced texel (the decode is deterministic)
-#pragma unroll
-        for (int k = 0; k < NW; ++k)
-            if (k < K) fs.xch[32 * k + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const unsigned peers = __match_any_sync(FULL, produced ? tq : 0xFFFFFFFFu);
-        __syncwarp();
-        if (produced && (unsigned)(__ffs(peers) - 1) == lane) fs.xch[tq] = val;
-        __syncwarp();
-        const float4 pv[4] = {fs.xch[t0], fs.xch[t0 + dxs], fs.xch[t2], fs.xch[t2 + dxs]};
-        const unsigned IN = D.corners(t0, t2, dxs);
-        o.color = fb == FB_WC ? combine_eq1_bits<true>(f, IN, pv) : combine_eq1_bits<false>(f, IN, pv);
-    }
-    o.rec = (uint32_t)evals | ((uint32_t)(n & 0xFF) << 8) | (32u << 16) | ((uint32_t)(PATH_FB_STF + fb) << 22) |
-            ((uint32_t)wave_mag << 25);
-    return o;
-}
-
-template <bool DBG>
-__device__ __forceinline__ LeanOut fb_wave(const KArgs &a, FbSmem &fs, float2 uv, uint2 gr, int px, int py,
-                                           uint32_t frame, bool has_grad, bool force) {
-    const bool wave_mag = wave_magnified(gr, has_grad);
-    const Foot f = footprint2(uv, a);
-    const int minx = __reduce_min_sync(FULL, f.xa), miny = __reduce_min_sync(FULL, f.ya);
-    const unsigned dx = (unsigned)(f.xb - minx), dy = (unsigned)(f.yb - miny);
-    // the window shapes of wave_box(), in its order (one instantiation: small code)
-    int K = 0;
-    unsigned lgP = 3u;
-    if (__all_sync(FULL, dx < 8u && dy < 4u)) { K = 1; lgP = 3u; }
-    else if (__all_sync(FULL, dx < 4u && dy < 8u)) { K = 1; lgP = 2u; }
-    else if (__all_sync(FULL, dx < 8u && dy < 8u)) { K = 2; lgP = 3u; }
-    else if (__all_sync(FULL, dx < 16u && dy < 8u)) { K = 4; lgP = 4u; }
-    else if (__all_sync(FULL, dx < 8u && dy < 16u)) { K = 4; lgP = 3u; }
-    else if (__all_sync(FULL, dx < 32u && dy < 4u)) { K = 4; lgP = 5u; }
-    // Mask sampling: exact also needs the AABB inside the fixed grid; a wave outside
-    // it takes the fallback exactly like a forced one
-    if (a.variant >= VAR_MASK16) {
-        const unsigned lim = a.variant == VAR_MASK16 ? 16u : 11u;
-        force = force || !__all_sync(FULL, dx < lim && dy < lim);
-    } else if (a.variant == VAR_BOX) {   // Box: exact iff the AABB area <= 32 (its own producer mapping)
-        const int area = (int)(__reduce_max_sync(FULL, dx) + 1u) * (int)(__reduce_max_sync(FULL, dy) + 1u);
-        if (area <= 32) K = 0;   // -> general path
-        force = true;
-    }
-    if (K == 1 || K == 2) return fb_wave_k<DBG, 2>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
-    if (K == 4) return fb_wave_k<DBG, 4>(a, fs, f, minx, miny, K, lgP, wave_mag, px, py, frame, force);
-    LeanOut o;
-    o.done = false;   // general path
-    o.color = make_float4(0.f, 0.f, 0.f, 0.f);
-    o.rec = kSlowMark;
-    o.prod = INVALID_ID;
-    o.selbits = 0u;
-    return o;
-}
-
 // ------------------------------------------------ wide-window path (shared-memory bitmaps)
 // Every wave the lean exact kernel leaves (n > 32, windows wider than 8x8, partial waves,
 // forced fallbacks) whose footprint AABB fits 32 x 32 texels: the window is a bitmap of 32
@@ -2168,7 +1944,7 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
                 const unsigned PL = ((r0 >> gx0) & 1u) | (((r0 >> gx1) & 1u) << 1) | (((r1 >> gx0) & 1u) << 2) |
                                     (((r1 >> gx1) & 1u) << 3);
                 // candidates: l's distinct nonzero-weight texels not planned, picked ~ merged
-                // weight with u2 (the sums and the decision in fp32, as cplus_pick_bits)
+                // weight with u2 (the sums and the decision in fp32, in corner order, as cplus_pick)
                 const unsigned cand = (fp >> 20) & ~PL & 15u;
                 const float dw[4] = {gw.x, gw.y, gw.z, gw.w};
                 float ps[4], wsum = 0.0f;
@@ -2211,11 +1987,19 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
     const uint32_t d0 = ws.bmD[cy0], d1 = ws.bmD[cy1];
     const unsigned IN = ((d0 >> cx0) & 1u) | (((d0 >> cx1) & 1u) << 1) | (((d1 >> cx0) & 1u) << 2) |
                         (((d1 >> cx1) & 1u) << 3);
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     const int p0 = cy0 << 5, p2 = cy1 << 5;
-    const float4 pv[4] = {(IN & 1u) ? ws.xch[ws.lop[p0 | cx0]] : z, (IN & 2u) ? ws.xch[ws.lop[p0 | cx1]] : z,
-                          (IN & 4u) ? ws.xch[ws.lop[p2 | cx0]] : z, (IN & 8u) ? ws.xch[ws.lop[p2 | cx1]] : z};
-    if (active) o.color = fb == FB_WC ? combine_eq1_mc<true>(f, m, C, IN, pv) : combine_eq1_mc<false>(f, m, C, IN, pv);
+    if (fb == FB_WC) {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 pv[4] = {(IN & 1u) ? ws.xch[ws.lop[p0 | cx0]] : z, (IN & 2u) ? ws.xch[ws.lop[p0 | cx1]] : z,
+                              (IN & 4u) ? ws.xch[ws.lop[p2 | cx0]] : z, (IN & 8u) ? ws.xch[ws.lop[p2 | cx1]] : z};
+        if (active) o.color = combine_eq1_mc<true>(f, m, C, IN, pv);
+    } else {
+        // C / C+: every slot holds a finite value (zeroed at kernel start), unknown corners get
+        // coefficient 0, so the loads need no predicate
+        const float4 pv[4] = {ws.xch[ws.lop[p0 | cx0] & 31], ws.xch[ws.lop[p0 | cx1] & 31],
+                              ws.xch[ws.lop[p2 | cx0] & 31], ws.xch[ws.lop[p2 | cx1] & 31]};
+        if (active) o.color = combine_eq1_coef(f, m, C, IN, pv);
+    }
     __syncwarp();
     return o;
 }
@@ -2262,6 +2046,7 @@ __global__ void __launch_bounds__(kWarps * 32, FUSED ? CTF_FUSED_MINB
     if constexpr (FMT == FMT_BC1) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
         if (FUSED && lane < 8) ws.lut[lane] = bc1_lut_entry(lane);
+        if (FUSED) ws.xch[lane] = make_float4(0.f, 0.f, 0.f, 0.f);   // finite slots (combine_eq1_coef)
         __syncwarp();
     }
     __shared__ unsigned s_next;   // latent MLP: the CTA's warps claim its items dynamically
@@ -2485,6 +2270,7 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
     MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
     if (FALLBACK) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
+        fs.xch[lane] = make_float4(0.f, 0.f, 0.f, 0.f);   // finite values in every slot (combine_eq1_coef)
         __syncwarp();
     }
     if constexpr (FMT != FMT_BC1) {
