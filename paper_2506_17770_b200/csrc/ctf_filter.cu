@@ -2260,6 +2260,8 @@ template <bool DBG, bool FALLBACK, int FMT>
 __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == FMT_BC1 ? CTF_REST_MINB : CTF_MLP_COLLAB_MINB))
     ctf_collab_rest_kernel(const __grid_constant__ KArgs a, unsigned nrec, const typename WeightsOf<FMT>::type mw) {
     static_assert(FMT == FMT_BC1 || !FALLBACK, "no lean fallback for the latent-MLP format");
+    // launched as a programmatic dependent of the previous pass: wait for its results
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.lists && a.lcnt[FALLBACK ? 0 : 1] == 0u) return;   // empty work list (same value in every thread)
     __shared__ WarpSmem smem[(FALLBACK && !CTF_REST_MERGED) ? 1 : kWarps];
     __shared__ WideSmem fsm[FALLBACK ? kWarps : 1];
@@ -2601,8 +2603,20 @@ static cudaError_t launch_rest(const KArgs &k, const typename WeightsOf<FMT>::ty
         if (e != cudaSuccess) return e;
         long long g2 = (long long)sms * (per_sm > 0 ? per_sm : 1);
         if (g2 * kWarps > groups) g2 = (groups + kWarps - 1) / kWarps;
-        rest<<<(unsigned)(g2 < 1 ? 1 : g2), kWarps * 32, dyn, stream>>>(k, nrec, mw);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        // programmatic dependent launch: this pass is launched while the previous kernel runs and
+        // waits for it in-kernel (griddepcontrol.wait) — its launch latency overlaps the previous
+        // pass instead of following it
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.gridDim = dim3((unsigned)(g2 < 1 ? 1 : g2));
+        cfg.blockDim = dim3(kWarps * 32);
+        cfg.dynamicSmemBytes = dyn;
+        cfg.stream = stream;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if ((e = cudaLaunchKernelEx(&cfg, rest, k, nrec, mw)) != cudaSuccess) return e;
     }
     return cudaSuccess;
 }
