@@ -309,11 +309,11 @@ __device__ __forceinline__ void distinct_corners(const Foot &f, bool (&first)[4]
 __device__ __forceinline__ float4 combine_eq1f(const Foot &f, const bool (&first)[4], const float (&dw)[4],
                                                const bool (&known)[4], const int (&dup)[4], const float4 (&pv)[4],
                                                bool wc) {
-    // Branch-free over the lane's cases (R-23).  The oracle's special cases hold bitwise:
-    // every nonzero-weight texel known -> blend4 over the corners, i.e. exact bilinear
-    // (c8); N = 1 -> that texel (Sp = p exactly).  Otherwise C / C+ evaluate
-    // Eq. 1 as blend4 over the known corners (= sum w_i p_i) plus (1 - Sw) / N * Sp,
-    // which agrees with the oracle's fmaf chain to fp32 rounding.
+    // Branch-free over the lane's cases (R-23).  Every nonzero-weight texel known -> blend4
+    // over the corners, i.e. exact bilinear bit for bit (c8).  Otherwise C / C+
+    // evaluate Eq. 1 as one blend4 with per-corner coefficients w_k + rest (combine_eq1_coef;
+    // N = 1 gives (dw + (1 - dw)) p = p to fp32 rounding), which agrees with the oracle's
+    // fmaf chain to fp32 rounding; WC (R-16) renormalises, N = 1 -> that texel exactly.
     bool all_known = true;
     int N = 0;
     float Sw = 0.f, Sp[4] = {0.f, 0.f, 0.f, 0.f};
@@ -351,12 +351,18 @@ __device__ __forceinline__ float4 combine_eq1f(const Foot &f, const bool (&first
         c[1] = all_known ? bl.y : Swp[1] * r;
         c[2] = all_known ? bl.z : Swp[2] * r;
         c[3] = all_known ? bl.w : Swp[3] * r;
-    } else {  // Eq. 1
+    } else {  // Eq. 1: the coefficient blend of combine_eq1_coef (same operations in
+              // the same order, so the general and wide-window paths agree bit for bit)
         const float rest = (all_known || N == 0) ? 0.0f : __fdividef(1.0f - Sw, (float)N);
-        c[0] = fmaf(rest, Sp[0], bl.x);
-        c[1] = fmaf(rest, Sp[1], bl.y);
-        c[2] = fmaf(rest, Sp[2], bl.z);
-        c[3] = fmaf(rest, Sp[3], bl.w);
+        float cf[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int d = dup[k];
+            const bool kd = d == 0 ? known[0] : d == 1 ? known[1] : d == 2 ? known[2] : known[3];
+            const bool kn = first[k] && dw[k] != 0.0f && known[k];
+            cf[k] = __fadd_rn(kd ? f.w[k] : 0.0f, kn ? rest : 0.0f);
+        }
+        return blend4f(q, cf);
     }
     if (one) {
 #pragma unroll
@@ -1737,7 +1743,7 @@ __device__ __forceinline__ void pair_back(const KArgs &a, const SM &fs, const Pa
 
 // ------------------------------------------------ wide-window path (shared-memory bitmaps)
 // Every wave the lean exact kernel leaves (n > 32, windows wider than 8x8, partial waves,
-// forced fallbacks) whose footprint AABB fits 32 x 32 texels: the window is a bitmap of 32
+// forced fallbacks) whose footprint AABB fits 32 x ROWS texels: the window is a bitmap of ROWS
 // rows x 32 bits in shared memory, one word per row, and each active lane sets its corners
 // with two shared atomics (ATOMS.OR, one per footprint row) — the cost does not grow with
 // the AABB (no 128-key sort).  The canonical ascending-id order (R-5) is row-major over the
@@ -1748,16 +1754,28 @@ __device__ __forceinline__ void pair_back(const KArgs &a, const SM &fs, const Pa
 // producing lane stores its value in its own slot, the first setter of a texel publishes its
 // lane in a position -> lane table).  Records, producers, selections and colours equal the general path
 // bit for bit (same fp32 operations in the same order).
-struct WideSmem {
-    uint32_t bmU[32], bmP[32], bmD[32];   // window rows (bit c of word r = texel (minx + c, miny + r))
-    float4 xch[32];                       // exact: U rank -> value; fallback: D rank -> value
+// ROWS = 32 (lane l holds row l in the row scans; taller AABBs take the general path) or 64
+// (lane l holds rows 2l and 2l + 1; CTF_REST_ROWS=64 builds the wide-window kernel that way).
+// The general path evaluates Eq. 1 with the same coefficient blend (combine_eq1f), so the
+// result does not depend on which path a wave takes.
+template <int ROWS>
+struct WideSmemT {
+    static constexpr int kRows = ROWS;
+    uint32_t bmU[ROWS], bmP[ROWS], bmD[ROWS];   // window rows (bit c of word r = texel (minx + c, miny + r))
+    float4 xch[32];                       // exact: U rank -> value; fallback: producer lane -> value
     float4 mw[32];                        // per lane: merged corner weights (C+ spare lanes read the served lane's)
-    uint32_t fpos[32];                    // per lane: cx0 | cx1 << 5 | cy0 << 10 | cy1 << 15 | contrib << 20
+    uint32_t fpos[32];                    // per lane: cx0 | cx1 << 5 | cy0 << 10 | cy1 << 16 | contrib << 22
     uint16_t tbl[32];                     // rank -> window position (row << 5 | col): exact U ranks / C+ plan
     uint8_t act[32];                      // active rank -> lane (h(r, A))
     uint4 lut[8];                         // BC1 per-index constants (bc1_lut_entry)
-    uint8_t lop[1024];                    // fallback: window position -> a lane that produced it (valid where bmD is set)
+    uint8_t lop[ROWS * 32];               // fallback: window position -> a lane that produced it (valid where bmD is set)
 };
+#ifndef CTF_REST_ROWS
+#define CTF_REST_ROWS 32  // window rows of the wide-window kernel's bitmap (32 or 64)
+#endif
+// 64 rows keep C4's tall minified waves (AABB up to 32 x 64) out of the general kernel:
+// +1 % on config 4, -0.6 % on config 5 (more shared memory per warp), so 32 by default
+using WideSmem = WideSmemT<CTF_REST_ROWS>;
 
 // exclusive prefix sum over the lanes (lane k holds the count of window row k)
 // (shfl.up's in-range predicate guards the add: two instructions per step)
@@ -1775,10 +1793,41 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, unsigned) {
 __device__ __forceinline__ int bm_rank(uint32_t base, uint32_t word, int c) {
     return (int)base + __popc(word & ((1u << c) - 1u));
 }
+// row scan of a ROWS-row bitmap: lane l holds row l (32 rows) or rows 2l, 2l + 1 (64 rows);
+// the row-major rank order is preserved
+template <int ROWS>
+struct RowScan {
+    uint32_t be, c0, tot;   // set bits before the lane's first row; in that row (64 rows); in the bitmap
+};
+template <int ROWS>
+__device__ __forceinline__ RowScan<ROWS> row_scan(const uint32_t *bm, unsigned lane) {
+    RowScan<ROWS> r;
+    uint32_t c;
+    if constexpr (ROWS == 64) {
+        const uint2 w = reinterpret_cast<const uint2 *>(bm)[lane];
+        r.c0 = __popc(w.x);
+        c = r.c0 + __popc(w.y);
+    } else {
+        c = r.c0 = __popc(bm[lane]);
+    }
+    r.be = warp_excl_scan(c, lane);
+    r.tot = __reduce_add_sync(FULL, c);
+    return r;
+}
+// set bits before row `row` (every lane participates)
+template <int ROWS>
+__device__ __forceinline__ uint32_t row_base(const RowScan<ROWS> &rs, int row) {
+    if constexpr (ROWS == 64) {
+        const uint32_t be = __shfl_sync(FULL, rs.be, row >> 1), c0 = __shfl_sync(FULL, rs.c0, row >> 1);
+        return be + ((row & 1) ? c0 : 0u);
+    } else {
+        return __shfl_sync(FULL, rs.be, row);
+    }
+}
 
-template <bool DBG>
-__device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float2 uv, uint2 gr, bool inframe, int px,
-                                             int py, uint32_t frame, bool force) {
+template <bool DBG, int ROWS>
+__device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws, float2 uv, uint2 gr, bool inframe,
+                                             int px, int py, uint32_t frame, bool force) {
     const unsigned lane = lane_id(), lt = lanemask_lt();
     LeanOut o;
     o.color = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1808,16 +1857,22 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
     const int miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
     const int bw = __reduce_max_sync(FULL, active ? f.xb : 0) - minx + 1;
     const int bh = __reduce_max_sync(FULL, active ? f.yb : 0) - miny + 1;
-    if (bw > 32 || bh > 32) {   // wider than the bitmap: the general path (third kernel)
+    if (bw > 32 || bh > ROWS) {   // wider than the bitmap: the general path (third kernel)
         o.done = false;
         o.rec = kSlowMark;
         return o;
     }
-    const int cx0 = (f.xa - minx) & 31, cx1 = (f.xb - minx) & 31, cy0 = (f.ya - miny) & 31, cy1 = (f.yb - miny) & 31;
+    const int cx0 = (f.xa - minx) & 31, cx1 = (f.xb - minx) & 31, cy0 = (f.ya - miny) & (ROWS - 1), cy1 = (f.yb - miny) & (ROWS - 1);
     const int ar = __popc(A & lt);   // active rank: lane = h(ar, A)
-    ws.bmU[lane] = 0u;
-    ws.bmP[lane] = 0u;
-    ws.bmD[lane] = 0u;
+    if constexpr (ROWS == 64) {
+        reinterpret_cast<uint2 *>(ws.bmU)[lane] = make_uint2(0u, 0u);
+        reinterpret_cast<uint2 *>(ws.bmP)[lane] = make_uint2(0u, 0u);
+        reinterpret_cast<uint2 *>(ws.bmD)[lane] = make_uint2(0u, 0u);
+    } else {
+        ws.bmU[lane] = 0u;
+        ws.bmP[lane] = 0u;
+        ws.bmD[lane] = 0u;
+    }
     if (active) ws.act[ar] = (uint8_t)lane;
     __syncwarp();
     // ---- a3: the needed set U (every corner, zero weights included, R-4)
@@ -1828,8 +1883,8 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
         oU1 = atomicOr(&ws.bmU[cy1], pat);
     }
     __syncwarp();
-    const uint32_t cntU = __popc(ws.bmU[lane]);
-    const int n = (int)__reduce_add_sync(FULL, cntU);
+    const RowScan<ROWS> rsU = row_scan<ROWS>(ws.bmU, lane);
+    const int n = (int)rsU.tot;
     // ---- a4: decide (List R-6; Box / Mask R-22)
     bool exact;
     if (a.variant == VAR_LIST) exact = n <= na;
@@ -1846,8 +1901,7 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
         int qx, qy, evals;
         if (a.variant != VAR_BOX) {
             // ranks of the four corners; each texel's first setter publishes rank -> position
-            const uint32_t base = warp_excl_scan(cntU, lane);
-            const uint32_t b0 = __shfl_sync(FULL, base, cy0), b1 = __shfl_sync(FULL, base, cy1);
+            const uint32_t b0 = row_base(rsU, cy0), b1 = row_base(rsU, cy1);
             const uint32_t w0 = ws.bmU[cy0], w1 = ws.bmU[cy1];
             rho[0] = bm_rank(b0, w0, cx0);
             rho[1] = bm_rank(b0, w0, cx1);
@@ -1918,12 +1972,11 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
         const bool firstP = active && !((oP >> qcx) & 1u);
         // publish this lane's distinct corners (merged weights, R-14) for the spare lanes
         ws.mw[lane] = make_float4(m.dw[0], m.dw[1], m.dw[2], m.dw[3]);
-        ws.fpos[lane] = (uint32_t)cx0 | ((uint32_t)cx1 << 5) | ((uint32_t)cy0 << 10) | ((uint32_t)cy1 << 15) | (C << 20);
+        ws.fpos[lane] = (uint32_t)cx0 | ((uint32_t)cx1 << 5) | ((uint32_t)cy0 << 10) | ((uint32_t)cy1 << 16) | (C << 22);
         __syncwarp();
-        const uint32_t cntP = __popc(ws.bmP[lane]);
-        const int np = (int)__reduce_add_sync(FULL, cntP);
-        const uint32_t baseP = warp_excl_scan(cntP, lane);
-        const uint32_t bq = __shfl_sync(FULL, baseP, qcy);
+        const RowScan<ROWS> rsP = row_scan<ROWS>(ws.bmP, lane);
+        const int np = (int)rsP.tot;
+        const uint32_t bq = row_base(rsP, qcy);
         if (firstP) ws.tbl[bm_rank(bq, ws.bmP[qcy], qcx)] = (uint16_t)((qcy << 5) | qcx);
         __syncwarp();
         produced = false;
@@ -1938,14 +1991,14 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmem &ws, float
                 o.selbits |= (1u << 5) | ((uint32_t)l << 8);
                 const uint32_t fp = ws.fpos[l];
                 const float4 gw = ws.mw[l];
-                const int gx0 = (int)(fp & 31u), gx1 = (int)((fp >> 5) & 31u), gy0 = (int)((fp >> 10) & 31u),
-                          gy1 = (int)((fp >> 15) & 31u);
+                const int gx0 = (int)(fp & 31u), gx1 = (int)((fp >> 5) & 31u), gy0 = (int)((fp >> 10) & (ROWS - 1)),
+                          gy1 = (int)((fp >> 16) & (ROWS - 1));
                 const uint32_t r0 = ws.bmP[gy0], r1 = ws.bmP[gy1];
                 const unsigned PL = ((r0 >> gx0) & 1u) | (((r0 >> gx1) & 1u) << 1) | (((r1 >> gx0) & 1u) << 2) |
                                     (((r1 >> gx1) & 1u) << 3);
                 // candidates: l's distinct nonzero-weight texels not planned, picked ~ merged
                 // weight with u2 (the sums and the decision in fp32, in corner order, as cplus_pick)
-                const unsigned cand = (fp >> 20) & ~PL & 15u;
+                const unsigned cand = (fp >> 22) & ~PL & 15u;
                 const float dw[4] = {gw.x, gw.y, gw.z, gw.w};
                 float ps[4], wsum = 0.0f;
 #pragma unroll
@@ -2011,11 +2064,20 @@ constexpr bool kPaired = CTF_PAIR && !DBG && !FORCE && (FMT == FMT_BC1 || CTF_PA
 template <bool DBG>
 static __device__ __noinline__ WaveOut general_wave_noinline(const KArgs &a, WarpSmem &s, float2 uv, uint2 gr,
                                                              bool active, unsigned A, int px, int py, uint32_t frame);
+#ifndef CTF_MLP_WARPS
+#define CTF_MLP_WARPS 8  // latent-MLP lean kernel: warps per CTA
+#endif
+#ifndef CTF_MLP_LEAN_MINB
+#define CTF_MLP_LEAN_MINB (CTF_MLP_COLLAB_MINB * 8 / CTF_MLP_WARPS)  // latent-MLP lean kernel: CTAs per SM
+#endif
+// warps per CTA of the lean kernel: BC1 kWarps; latent MLP CTF_MLP_WARPS (its register budget)
+template <int FMT>
+__host__ __device__ constexpr int lean_warps() { return FMT == FMT_BC1 ? kWarps : CTF_MLP_WARPS; }
 // the wide-window path out of line (the fused kernel keeps the lean loop's registers)
 template <bool DBG>
-static __device__ __noinline__ LeanOut wide_wave_noinline(const KArgs &a, WideSmem &ws, float2 uv, uint2 gr, bool inframe,
-                                                          int px, int py, uint32_t frame, bool force) {
-    return wide_wave<DBG>(a, ws, uv, gr, inframe, px, py, frame, force);
+static __device__ __noinline__ LeanOut wide_wave_noinline(const KArgs &a, WideSmemT<32> &ws, float2 uv, uint2 gr,
+                                                          bool inframe, int px, int py, uint32_t frame, bool force) {
+    return wide_wave<DBG, 32>(a, ws, uv, gr, inframe, px, py, frame, force);
 }
 // FUSED (BC1, small calls): the waves a run leaves are finished in the same kernel, right after
 // the run (the wide-window path inline, the general path out of line) — one launch per call,
@@ -2028,21 +2090,22 @@ static __device__ __noinline__ LeanOut wide_wave_noinline(const KArgs &a, WideSm
 #define CTF_FUSED_MAX_WAVES 131072  // calls with at most this many waves run the fused kernel
 #endif
 template <bool DBG, bool GRAD, bool FORCE, int FMT, bool BOX = false, bool FUSED = false>
-__global__ void __launch_bounds__(kWarps * 32, FUSED ? CTF_FUSED_MINB
+__global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
                                                      : FMT == FMT_BC1 ? (kPaired<DBG, FORCE, FMT> ? CTF_PAIR_MINB : CTF_FAST_MINB)
-                                                                      : CTF_MLP_COLLAB_MINB)
+                                                                      : CTF_MLP_LEAN_MINB)
     ctf_collab_lean_kernel(const __grid_constant__ KArgs a, const typename WeightsOf<FMT>::type mw) {
     static_assert(!FUSED || FMT == FMT_BC1, "the fused kernel is BC1-only");
+    constexpr int kLW = lean_warps<FMT>();
     constexpr bool PAIR = kPaired<DBG, FORCE, FMT>;
     using SmemT = std::conditional_t<PAIR, PairSmem, FastSmem>;
-    __shared__ SmemT fsm[kWarps];
-    __shared__ WideSmem wsm[FUSED ? kWarps : 1];
-    __shared__ WarpSmem gsm[FUSED ? kWarps : 1];
+    __shared__ SmemT fsm[kLW];
+    __shared__ WideSmemT<32> wsm[FUSED ? kLW : 1];
+    __shared__ WarpSmem gsm[FUSED ? kLW : 1];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent MLP: TcWeights + per-warp TcScratch
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     SmemT &fs = fsm[warp];
     MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
-    WideSmem &ws = wsm[FUSED ? warp : 0];
+    WideSmemT<32> &ws = wsm[FUSED ? warp : 0];
     if constexpr (FMT == FMT_BC1) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
         if (FUSED && lane < 8) ws.lut[lane] = bc1_lut_entry(lane);
@@ -2055,20 +2118,20 @@ __global__ void __launch_bounds__(kWarps * 32, FUSED ? CTF_FUSED_MINB
         fill_tc_weights(mw, tw);
         mc.tw = &tw;
         mc.tsc = &reinterpret_cast<TcScratch *>(dyn_smem + sizeof(TcWeights))[warp];
-        if (threadIdx.x == 0) s_next = kWarps;
+        if (threadIdx.x == 0) s_next = kLW;
         __syncthreads();
     }
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
-    const unsigned per_warp = a.ipc / kWarps;
+    const unsigned per_warp = a.ipc / kLW;
     for (unsigned k = warp;;) {
-        // BC1: warp (b, w) takes items b*kWarps + w + j*gridDim.x*kWarps (static); latent MLP:
+        // BC1: warp (b, w) takes items b*kLW + w + j*gridDim.x*kLW (static); latent MLP:
         // CTA b owns items b + k*gridDim.x and its warps claim k from a shared counter
         // (decode cost varies with n: dynamic claims balance the warps of a CTA)
-        const unsigned c = FMT == FMT_BC1 ? (blockIdx.x * kWarps + (k % kWarps)) + (k / kWarps) * gridDim.x * kWarps
+        const unsigned c = FMT == FMT_BC1 ? (blockIdx.x * kLW + (k % kLW)) + (k / kLW) * gridDim.x * kLW
                                           : blockIdx.x + k * gridDim.x;
-        if ((FMT == FMT_BC1 ? k / kWarps >= per_warp : k >= a.ipc) || c >= a.nchunks) break;
+        if ((FMT == FMT_BC1 ? k / kLW >= per_warp : k >= a.ipc) || c >= a.nchunks) break;
         if constexpr (FMT == FMT_BC1) {
-            k += kWarps;
+            k += kLW;
         } else {
             unsigned nx = 0u;
             if (lane == 0) nx = atomicAdd(&s_next, 1u);
@@ -2291,7 +2354,7 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
         const uint32_t frame = a.frame_index + fr;
         LeanOut o;
         o.done = false;
-        if (FALLBACK) o = wide_wave<DBG>(a, fs, uv, gr, inframe, px, py, frame, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
+        if (FALLBACK) o = wide_wave<DBG, CTF_REST_ROWS>(a, fs, uv, gr, inframe, px, py, frame, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
         if (!o.done) {
             if (FALLBACK && !CTF_REST_MERGED) {   // AABB wider than 32 x 32 texels: general kernel
                 if (lane == 0) {
@@ -2561,25 +2624,25 @@ static cudaError_t launch_lean(KArgs &k, const typename WeightsOf<FMT>::type &mw
         }
     }
     auto kern = use_fused<FMT>(k) ? lean_kernel_for<FMT, DBG, true>(k) : lean_kernel_for<FMT, DBG, false>(k);
-    const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
+    const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + lean_warps<FMT>() * sizeof(TcScratch);
     int per_sm = 0;
     cudaError_t e;
     if (dyn > 0 && (e = mlp_smem_setup(kern, dyn, dev)) != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, dyn);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, lean_warps<FMT>() * 32, dyn);
     if (e != cudaSuccess) return e;
     const long long slots = (long long)sms * (per_sm > 0 ? per_sm : 1);
     long long ipw;
     if (FMT == FMT_BC1) {   // many short-lived CTAs; the block scheduler balances
-        ipw = ((long long)k.nchunks + slots * kWarps * CTF_BC1_ROUNDS / 2) / (slots * kWarps * CTF_BC1_ROUNDS);
+        ipw = ((long long)k.nchunks + slots * lean_warps<FMT>() * CTF_BC1_ROUNDS / 2) / (slots * lean_warps<FMT>() * CTF_BC1_ROUNDS);
         ipw = ipw < 1 ? 1 : ipw > CTF_BC1_MAX_IPW ? CTF_BC1_MAX_IPW : ipw;
     } else {                // latent MLP: one CTA per slot (each CTA stages the MLP weights once)
-        ipw = ((long long)k.nchunks + slots * kWarps - 1) / (slots * kWarps);
+        ipw = ((long long)k.nchunks + slots * lean_warps<FMT>() - 1) / (slots * lean_warps<FMT>());
         if (ipw < 1) ipw = 1;
     }
-    k.ipc = (unsigned)(ipw * kWarps);
+    k.ipc = (unsigned)(ipw * lean_warps<FMT>());
     long long grid = ((long long)k.nchunks + k.ipc - 1) / k.ipc;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kWarps * 32, dyn, stream>>>(k, mw);
+    kern<<<(unsigned)grid, lean_warps<FMT>() * 32, dyn, stream>>>(k, mw);
     return cudaGetLastError();
 }
 
