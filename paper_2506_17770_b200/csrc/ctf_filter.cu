@@ -184,14 +184,16 @@ template <int FMT>
 __device__ __forceinline__ float4 scaled(const Texel<FMT> &p) { return p.to_f4(); }
 
 // Eq. 2 generalised to a active lanes (R-18 iv), round half up.
-// floor(num / den) for 0 <= num < 2^11, 0 < den <= 62 as floor((num + 1/2) * rcp(den)):
-// the fractional part of (num + 1/2) / den lies in [1/(2 den), 1 - 1/(2 den)], a margin
-// of >= 1/124 against an fp32 error < 2^-12, so the result is the exact integer quotient.
+// floor(num / den) for 0 <= num < 2^11, 0 < den <= 62 as trunc((num + 1/2) / den) with the
+// approximate division (MUFU.RCP + FMUL, relative error < 2^-21): the fractional part of
+// (num + 1/2) / den lies in [1/(2 den), 1 - 1/(2 den)], a margin of >= 1/124 against an
+// absolute error < 32 * 2^-21, so the result is the exact integer quotient
+// (tests/test_kernel_arith.py checks the margin for every (j, np, na)).
 __device__ __forceinline__ int eq2_lane_rank(int j, int np, int na) {
     if (np >= na - 1) return 0;
     const int num = 2 * (na - 1) * (j - np) + (na - 1 - np);
     const int den = 2 * (na - 1 - np);
-    return __float2int_rz(((float)num + 0.5f) * __frcp_rn((float)den));
+    return __float2int_rz(__fdividef((float)num + 0.5f, (float)den));
 }
 
 // STF corner (R-12): dx = (u0 < s), dy = (u1 < t).
@@ -1797,21 +1799,29 @@ __device__ __forceinline__ int bm_rank(uint32_t base, uint32_t word, int c) {
 // the row-major rank order is preserved
 template <int ROWS>
 struct RowScan {
-    uint32_t be, c0, tot;   // set bits before the lane's first row; in that row (64 rows); in the bitmap
+    uint32_t be, c0, c, tot;   // set bits before the lane's first row; in that row (64 rows); in the lane's rows; in the bitmap
 };
+// the counts only (tot: n of a fallback wave needs no ranks); row_scan_ranks adds the scan
 template <int ROWS>
-__device__ __forceinline__ RowScan<ROWS> row_scan(const uint32_t *bm, unsigned lane) {
+__device__ __forceinline__ RowScan<ROWS> row_count(const uint32_t *bm, unsigned lane) {
     RowScan<ROWS> r;
-    uint32_t c;
     if constexpr (ROWS == 64) {
         const uint2 w = reinterpret_cast<const uint2 *>(bm)[lane];
         r.c0 = __popc(w.x);
-        c = r.c0 + __popc(w.y);
+        r.c = r.c0 + __popc(w.y);
     } else {
-        c = r.c0 = __popc(bm[lane]);
+        r.c = r.c0 = __popc(bm[lane]);
     }
-    r.be = warp_excl_scan(c, lane);
-    r.tot = __reduce_add_sync(FULL, c);
+    r.be = 0u;
+    r.tot = __reduce_add_sync(FULL, r.c);
+    return r;
+}
+template <int ROWS>
+__device__ __forceinline__ void row_scan_ranks(RowScan<ROWS> &r, unsigned lane) { r.be = warp_excl_scan(r.c, lane); }
+template <int ROWS>
+__device__ __forceinline__ RowScan<ROWS> row_scan(const uint32_t *bm, unsigned lane) {
+    RowScan<ROWS> r = row_count<ROWS>(bm, lane);
+    row_scan_ranks(r, lane);
     return r;
 }
 // set bits before row `row` (every lane participates)
@@ -1883,7 +1893,7 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws
         oU1 = atomicOr(&ws.bmU[cy1], pat);
     }
     __syncwarp();
-    const RowScan<ROWS> rsU = row_scan<ROWS>(ws.bmU, lane);
+    RowScan<ROWS> rsU = row_count<ROWS>(ws.bmU, lane);   // ranks only for an exact wave
     const int n = (int)rsU.tot;
     // ---- a4: decide (List R-6; Box / Mask R-22)
     bool exact;
@@ -1901,6 +1911,7 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws
         int qx, qy, evals;
         if (a.variant != VAR_BOX) {
             // ranks of the four corners; each texel's first setter publishes rank -> position
+            row_scan_ranks(rsU, lane);
             const uint32_t b0 = row_base(rsU, cy0), b1 = row_base(rsU, cy1);
             const uint32_t w0 = ws.bmU[cy0], w1 = ws.bmU[cy1];
             rho[0] = bm_rank(b0, w0, cx0);
@@ -2089,6 +2100,26 @@ static __device__ __noinline__ LeanOut wide_wave_noinline(const KArgs &a, WideSm
 #ifndef CTF_FUSED_MAX_WAVES
 #define CTF_FUSED_MAX_WAVES 131072  // calls with at most this many waves run the fused kernel
 #endif
+#ifndef CTF_VBAND
+#define CTF_VBAND 8  // wave-rows per band of the lean kernels' item order (1: row-major runs)
+#endif
+// work item rr of a frame -> (wave-row, run column).  Items run down bands of CTF_VBAND
+// wave-rows first, so the consecutive items a CTA's warps take are vertically stacked runs:
+// a BC1 block (4 x 4 texels, ~8-16 pixels tall when magnified) is shared by 2-4 of the CTA's
+// wave-rows at about the same time, so its L2 round trip is paid once per SM (L1) instead of
+// once per warp.  The last band of a frame holds the remaining nwy mod CTF_VBAND wave-rows.
+__device__ __forceinline__ void run_coords(int rr, const KArgs &a, int &wy, int &wxc) {
+    if constexpr (CTF_VBAND <= 1) {
+        wy = rr / a.cpr;
+        wxc = rr - wy * a.cpr;
+    } else {
+        const int bs = CTF_VBAND * a.cpr;
+        const int band = rr / bs, q = rr - band * bs;
+        const int h = min(CTF_VBAND, a.nwy - band * CTF_VBAND);
+        wxc = h == CTF_VBAND ? q / CTF_VBAND : q / h;
+        wy = band * CTF_VBAND + (q - wxc * h);
+    }
+}
 template <bool DBG, bool GRAD, bool FORCE, int FMT, bool BOX = false, bool FUSED = false>
 __global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
                                                      : FMT == FMT_BC1 ? (kPaired<DBG, FORCE, FMT> ? CTF_PAIR_MINB : CTF_FAST_MINB)
@@ -2139,8 +2170,9 @@ __global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
         }
         const int fr = (int)(c / (unsigned)a.cpf);
         const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
-        const int wy = rr / a.cpr;
-        const int wx0 = (rr - wy * a.cpr) * a.chunk;
+        int wy, wxc;
+        run_coords(rr, a, wy, wxc);
+        const int wx0 = wxc * a.chunk;
         const int wx1 = min(wx0 + a.chunk, a.nwx);
         const int py = wy * 4 + ly;
         const bool rowok = py < a.Hf;
@@ -2402,7 +2434,11 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
             ld_stream_f2_if(uv, a.uv + pix, inframe);
             ld_stream_u2_if(gr, a.grad + pix, inframe & (a.grad != nullptr));
         };
+        // list entries are loaded two waves ahead (the entry's load latency is not on the
+        // critical path of the next wave's input fetch), inputs one wave ahead
         unsigned wi_n = __shfl_sync(FULL, L[i], 0), fr_n, pix_n;
+        unsigned wi_nn = 0u;
+        ld_u32_if(wi_nn, L + (i + tw), lane == 0 && i + tw < n);
         float2 uv_n;
         uint2 gr_n;
         int px_n, py_n;
@@ -2415,7 +2451,8 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
             const int px = px_n, py = py_n;
             const bool inframe = in_n;
             if (i + tw < n) {
-                wi_n = __shfl_sync(FULL, L[i + tw], 0);
+                wi_n = __shfl_sync(FULL, wi_nn, 0);
+                ld_u32_if(wi_nn, L + (i + 2 * tw), lane == 0 && i + 2 * tw < n);
                 fetch_wi(wi_n, uv_n, gr_n, fr_n, px_n, py_n, in_n, pix_n);
             }
             process(wi, uv, gr, fr, px, py, inframe, pix);

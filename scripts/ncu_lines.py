@@ -12,6 +12,8 @@ rep, waves = sys.argv[1], float(sys.argv[2])
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 60
 import os
 kf = ["-k", os.environ["NCU_KERNEL"]] if os.environ.get("NCU_KERNEL") else []
+if os.environ.get("NCU_SKIP"):
+    kf += ["--launch-skip", os.environ["NCU_SKIP"], "--launch-count", "1"]
 out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
