@@ -459,3 +459,49 @@ def test_mask_and_box_variants_in_the_lean_kernels(ctf, sx, sy, theta, center):
             continue
         rejected += int(((((lst >> 22) & 7) == 0) & (((m >> 22) & 7) != 0)).sum())
     assert rejected > 0   # the scene exercises Mask's grid test on List-exact waves
+
+
+def _tie_frames():
+    """The measure-zero tie constructions of tests/test_oracle_pins.py (STF: u0 == s; C+ extra
+    pick: u2 * wsum == w_0), several seeds each, as (uv, mode, fb, flags, seed)."""
+    import oracle
+    W = H = 16
+    cases = []
+    for seed in range(1, 400):
+        r = oracle.philox4x32_10([0, 0, 0, 0], [seed, 0])
+        u0, u1 = (int(r[0]) >> 8) / 2.0 ** 24, (int(r[1]) >> 8) / 2.0 ** 24
+        if u1 < u0 < 0.5 and u1 + 2.0 ** -24 < 0.5:
+            uv = np.full((4, 8, 2), np.nan, np.float32)
+            uv[0, 0] = (np.float32((0.5 + u0) / W), np.float32((0.5 + u1 + 2.0 ** -24) / H))
+            cases.append((uv, 1, 0, 0, seed))
+            if len(cases) == 4:
+                break
+    nst = len(cases)
+    for seed in range(1, 3000):
+        u = [[(int(r[k]) >> 8) / 2.0 ** 24 for k in range(3)]
+             for r in (oracle.philox4x32_10([x, 0, 0, 0], [seed, 0]) for x in range(3))]
+        s_ = 1.0 - u[2][2]
+        if 0.0 < s_ < 0.5 and all(ui[1] < 0.5 for ui in u) and {(1 if ui[0] < s_ else 0) + 2 for ui in u} == {2, 3}:
+            uv = np.full((4, 8, 2), np.nan, np.float32)
+            uv[0, 0:3] = (np.float32((0.5 + s_) / W), np.float32(1.0 / H))
+            cases.append((uv, 3, 3, 2, seed))
+            if len(cases) == nst + 4:
+                break
+    return cases
+
+
+def test_rng_ties_match_oracle(ctf):
+    """STF and C+ decisions at exact ties of the 2^-24 uniform grid (strict comparisons,
+    P:460-461): debug kernels bitwise (records, producers, selections), release
+    kernels records + colours."""
+    tex = bc1_tex(16, 16, 2, "random")
+    cases = _tie_frames()
+    assert len(cases) == 8
+    for uv, mode, fb, fl, seed in cases:
+        o = run_oracle(tex, uv, None, mode, fb, fl, seed=seed)
+        assert_parity(run_gpu(ctf, tex, uv, None, mode, fb, fl, seed=seed), o, f"tie m{mode} s{seed}")
+        dt = to_dev_tex(ctf, tex)
+        out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), None, mode, fb, fl, seed, 0)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+        assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL

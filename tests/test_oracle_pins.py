@@ -279,10 +279,13 @@ def test_fallback_estimator_special_cases_and_convexity():
                 c = r["out"][y, x]
                 assert len(known) >= 1
                 assert np.all(c >= vals.min(0) - 1e-12) and np.all(c <= vals.max(0) + 1e-12)
+                # the special cases are the values themselves, bit for bit: N = 1 returns the
+                # one texel, an all-known footprint the exact bilinear result of
+                # the 4TAP mode — not the general formula's rounding of them
                 if len(known) == 1:
-                    np.testing.assert_allclose(c, vals[0], atol=1e-15)
+                    np.testing.assert_array_equal(c, vals[0])
                 if len(known) == len(need):
-                    np.testing.assert_allclose(c, exact[y, x], atol=1e-12)
+                    np.testing.assert_array_equal(c, exact[y, x])
                     n_exact += 1
         assert n_exact > 0
 
@@ -302,6 +305,68 @@ def test_stf_expectation_is_bilinear():
     acc /= nfr
     # 49152 draws: std of the mean <= 0.5/sqrt(49152) ~ 2.3e-3
     np.testing.assert_allclose(acc, ref, atol=1e-2)
+
+
+def test_stf_picks_with_probability_exactly_the_weight():
+    """One-tap STF picks the right texel column with probability s and the lower row with
+    probability t ('probability based on its corresponding filter weight').  The
+    uniforms lie on the 2^-24 grid (R-11), so P(pick right) = s holds exactly only for the
+    event {u < s}: it has s * 2^24 grid points, {u <= s} one more.  A pixel whose s equals its
+    own u0 exactly (constructed: uv.x = (1/2 + u0) / W with W = 16, exact in fp32) must keep
+    the left column; t = u1 + 2^-24 must take the lower row.  Choosing u0 > u1 also fixes the
+    stream convention of R-11 (u0 decides x, u1 decides y)."""
+    W = H = 16
+    tex = bc1_tex(W, H, 2, "random")
+    found = 0
+    for seed in range(1, 400):
+        r = oracle.philox4x32_10([0, 0, 0, 0], [seed & 0xFFFFFFFF, 0])
+        u0, u1 = (int(r[0]) >> 8) / 2.0 ** 24, (int(r[1]) >> 8) / 2.0 ** 24
+        if not (u1 < u0 < 0.5 and u1 + 2.0 ** -24 < 0.5):
+            continue
+        uv = np.full((4, 8, 2), np.nan, np.float32)
+        uv[0, 0] = (np.float32((0.5 + u0) / W), np.float32((0.5 + u1 + 2.0 ** -24) / H))
+        ids, st = oracle.footprint(float(uv[0, 0, 0]), float(uv[0, 0, 1]), W, H)
+        assert float(st[0]) == u0 and float(st[1]) == u1 + 2.0 ** -24   # the construction is exact
+        sel = int(filter_frame(tex, uv, None, M_STF, seed=seed)["selection"][0, 0]) & 3
+        assert sel == 2, (seed, u0, u1, sel)   # left column (u0 < s false), lower row (u1 < t)
+        found += 1
+        if found == 8:
+            break
+    assert found == 8
+
+
+def test_cplus_extra_pick_probability_is_the_merged_weight_exactly():
+    """A C+ spare lane picks an unplanned texel of its served lane with probability equal to
+    its merged weight over the candidates' sum (R-18 v).  With u2 on the 2^-24 grid
+    the first candidate's event {u2 * wsum < w_0} has exactly w_0 / wsum * 2^24 points only
+    with a strict comparison, so at a constructed tie (w_0 = u2 * wsum exactly) the pick must
+    be the second candidate.  Construction: lanes 0, 1, 2 share one footprint with t = 1/2 and
+    s = 1 - u2(lane 2) (exact in fp32); every STF pick is in the lower row and both LL and LR
+    are picked (n_p = 2), so lane 2 (active rank 2) serves lane 0 (Eq. 2 with n_p = a - 1)
+    and its candidates are UL (weight (1 - s)/2 = u2/2) and UR (s/2), wsum = 1/2."""
+    W = H = 16
+    tex = bc1_tex(W, H, 2, "random")
+    found = 0
+    for seed in range(1, 3000):
+        us = [oracle.philox4x32_10([x, 0, 0, 0], [seed, 0]) for x in range(3)]
+        u = [[(int(r[k]) >> 8) / 2.0 ** 24 for k in range(3)] for r in us]
+        s_ = 1.0 - u[2][2]
+        if not (0.0 < s_ < 0.5) or any(ui[1] >= 0.5 for ui in u):
+            continue
+        picks = {(1 if ui[0] < s_ else 0) + 2 for ui in u}
+        if picks != {2, 3}:
+            continue
+        uv = np.full((4, 8, 2), np.nan, np.float32)
+        uv[0, 0:3] = (np.float32((0.5 + s_) / W), np.float32((0.5 + 0.5) / H))
+        ids, st = oracle.footprint(float(uv[0, 0, 0]), float(uv[0, 0, 1]), W, H)
+        assert float(st[0]) == s_ and float(st[1]) == 0.5   # the construction is exact
+        r = filter_frame(tex, uv, None, M_COLLAB, FB_CPLUS, FL_FORCE_FALLBACK, seed=seed)
+        assert (int(r["selection"][0, 2]) >> 8) & 31 == 0 and int(r["selection"][0, 2]) & (1 << 5)
+        assert int(r["produced_id"][0, 2]) == int(ids[1]), (seed, s_)   # UR, not UL
+        found += 1
+        if found == 6:
+            break
+    assert found == 6
 
 
 def test_cplus_plan_and_spread():
