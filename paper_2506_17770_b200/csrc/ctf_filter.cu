@@ -1639,12 +1639,12 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     // row-major order of U for every shape); 6x5 / 5x6 take the 5x5..6x6 AABBs of rotated
     // magnified waves (~10 % of config-5 waves) off the 64-bit path
     int K = 0;
-    uint32_t P = 8u, csh = 0u;   // pitch; byte of cpk holding this pitch's push code
-    if (__all_sync(FULL, (dx | (dy << 1)) < 8u)) K = 1;                                // 8x4
-    else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; P = 4u; csh = 8u; }     // 4x8
-    else if (__all_sync(FULL, dx < 6u && dy < 5u)) { K = 1; P = 6u; csh = 16u; }       // 6x5
-    else if (__all_sync(FULL, dx < 5u && dy < 6u)) { K = 1; P = 5u; csh = 24u; }       // 5x6
-    else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                                  // 8x8
+    uint32_t P = 8u, csel = 0x4440u;   // pitch; byte_perm selector of cpk's byte holding this pitch's push code
+    if (__all_sync(FULL, (dx | (dy << 1)) < 8u)) K = 1;                                    // 8x4
+    else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; P = 4u; csel = 0x4441u; }   // 4x8
+    else if (__all_sync(FULL, dx < 6u && dy < 5u)) { K = 1; P = 6u; csel = 0x4442u; }      // 6x5
+    else if (__all_sync(FULL, dx < 5u && dy < 6u)) { K = 1; P = 5u; csel = 0x4443u; }      // 5x6
+    else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                                      // 8x8
     if (K == 0) {   // a wider window: the wide-window kernel (BC1) / the general kernel (latent MLP)
         o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
         return o;
@@ -1654,17 +1654,20 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     const uint32_t dxs = (uint32_t)(f.xb - f.xa);
     const uint32_t pat = 1u + dxs + dxs;
     // push table entry of window bit t: its offset (dy << 3) | dx from the window origin
-    const uint32_t code = (cpk >> csh) & 63u;   // = ((lane / P) << 3) | (lane % P)
+    const uint32_t code = __byte_perm(cpk, 0u, csel);   // = ((lane / P) << 3) | (lane % P)
     uint8_t *bits = bits0 + base;
     int n, r0, r2;
     if (K == 1) {
         const uint32_t wm = __reduce_or_sync(FULL, (pat << t0) | (pat << t2));
         n = __popc(wm);
-        r0 = __popc(wm & ((1u << t0) - 1u));
-        r2 = __popc(wm & ((1u << t2) - 1u));
+        // rank of window bit t = set bits below t = lane t's popc(wm & lanemask_lt): the
+        // corners' ranks are two shuffles of the push rank
+        const int myr = __popc(wm & lt);
+        r0 = __shfl_sync(FULL, myr, (int)t0);
+        r2 = __shfl_sync(FULL, myr, (int)t2);
         // push (no predicate): the owner of window bit `lane` writes its code at its rank, every
         // other lane into its own scratch slot 64 + lane (no divergent store region)
-        if (!BOX) bits0[(wm & lanebit) ? base + __popc(wm & lt) : 64 + (int)lane] = (uint8_t)code;
+        if (!BOX) bits0[(wm & lanebit) ? base + myr : 64 + (int)lane] = (uint8_t)code;
     } else {
         const uint64_t m = ((uint64_t)pat << t0) | ((uint64_t)pat << t2);
         const uint32_t wl = __reduce_or_sync(FULL, (uint32_t)m);
@@ -1704,7 +1707,9 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     o.n = evals;
     o.minx = minx;
     o.miny = miny;
-    o.rec = ((uint32_t)n << 8) | (uint32_t)evals | (32u << 16) | ((uint32_t)wave_mag << 25);
+    // (n << 8) | evals | (32 << 16) | (mag << 25); List: evals = n, so n * 257 + constant
+    o.rec = BOX ? (((uint32_t)n << 8) | (uint32_t)evals | (32u << 16) | ((uint32_t)wave_mag << 25))
+                : (uint32_t)n * 257u + (wave_mag ? (32u << 16) | (1u << 25) : (32u << 16));
     return o;
 }
 // step a5 for both waves: job j < nA decodes wave A's U[j], job nA + r wave B's U[r]
