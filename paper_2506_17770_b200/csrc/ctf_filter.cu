@@ -1765,24 +1765,27 @@ __device__ __forceinline__ void pair_back(const KArgs &a, const SM &fs, const Pa
 // (lane l holds rows 2l and 2l + 1; CTF_REST_ROWS=64 builds the wide-window kernel that way).
 // The general path evaluates Eq. 1 with the same coefficient blend (combine_eq1f), so the
 // result does not depend on which path a wave takes.
-template <int ROWS>
+template <int ROWS, int COLS = 32>
 struct WideSmemT {
-    static constexpr int kRows = ROWS;
-    uint32_t bmU[ROWS], bmP[ROWS], bmD[ROWS];   // window rows (bit c of word r = texel (minx + c, miny + r))
+    static constexpr int kRows = ROWS, kCols = COLS, kCW = COLS / 32;   // kCW words per window row
+    static_assert((ROWS == 32 || ROWS == 64) && (COLS == 32 || COLS == 64), "window shape");
+    // window rows, row-major: bit (c & 31) of word r * kCW + (c >> 5) = texel (minx + c, miny + r)
+    uint32_t bmU[ROWS * kCW], bmP[ROWS * kCW], bmD[ROWS * kCW];
     float4 xch[32];                       // exact: U rank -> value; fallback: producer lane -> value
     float4 mw[32];                        // per lane: merged corner weights (C+ spare lanes read the served lane's)
-    uint32_t fpos[32];                    // per lane: cx0 | cx1 << 5 | cy0 << 10 | cy1 << 16 | contrib << 22
-    uint16_t tbl[32];                     // rank -> window position (row << 5 | col): exact U ranks / C+ plan
+    uint32_t fpos[32];                    // per lane: cx0 | cx1 << 6 | cy0 << 12 | cy1 << 18 | contrib << 24
+    uint16_t tbl[32];                     // rank -> window position r * COLS + c: exact U ranks / C+ plan
     uint8_t act[32];                      // active rank -> lane (h(r, A))
     uint4 lut[8];                         // BC1 per-index constants (bc1_lut_entry)
-    uint8_t lop[ROWS * 32];               // fallback: window position -> a lane that produced it (valid where bmD is set)
+    uint8_t lop[ROWS * COLS];             // fallback: window position -> a lane that produced it (valid where bmD is set)
 };
 #ifndef CTF_REST_ROWS
 #define CTF_REST_ROWS 32  // window rows of the wide-window kernel's bitmap (32 or 64)
 #endif
-// 64 rows keep C4's tall minified waves (AABB up to 32 x 64) out of the general kernel:
-// +1 % on config 4, -0.6 % on config 5 (more shared memory per warp), so 32 by default
+// 64 rows in the second kernel: +1 % on config 4, -0.6 % on config 5 (more shared memory per
+// warp), so 32 by default; the third kernel's 64 x 64 window takes the taller waves
 using WideSmem = WideSmemT<CTF_REST_ROWS>;
+using WideSmemBig = WideSmemT<64, 64>;
 
 // exclusive prefix sum over the lanes (lane k holds the count of window row k)
 // (shfl.up's in-range predicate guards the add: two instructions per step)
@@ -1800,38 +1803,60 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, unsigned) {
 __device__ __forceinline__ int bm_rank(uint32_t base, uint32_t word, int c) {
     return (int)base + __popc(word & ((1u << c) - 1u));
 }
-// row scan of a ROWS-row bitmap: lane l holds row l (32 rows) or rows 2l, 2l + 1 (64 rows);
-// the row-major rank order is preserved
-template <int ROWS>
+// the same over a CW-word row: the set bits of the row's words before c's word, then c's word
+template <int CW>
+__device__ __forceinline__ int win_rank(const uint32_t *bm, uint32_t base, int r, int c) {
+    if constexpr (CW == 1) {
+        return bm_rank(base, bm[r], c);
+    } else {
+        const uint32_t w0 = bm[2 * r], w1 = bm[2 * r + 1];
+        return c < 32 ? bm_rank(base, w0, c) : bm_rank(base + (uint32_t)__popc(w0), w1, c - 32);
+    }
+}
+// word index and bit of window texel (r, c)
+template <int CW>
+__device__ __forceinline__ int win_word(int r, int c) { return r * CW + (c >> 5); }
+template <int CW>
+__device__ __forceinline__ uint32_t win_bit(const uint32_t *bm, int r, int c) {
+    return (bm[win_word<CW>(r, c)] >> (c & 31)) & 1u;
+}
+// row scan of a ROWS x (32 CW) bitmap: lane l holds row l (32 rows) or rows 2l, 2l + 1 (64
+// rows); the row-major rank order is preserved
+template <int ROWS, int CW>
 struct RowScan {
-    uint32_t be, c0, c, tot;   // set bits before the lane's first row; in that row (64 rows); in the lane's rows; in the bitmap
+    uint32_t be, c0, c, tot;   // set bits before the lane's first row; in that row; in the lane's rows; in the bitmap
 };
 // the counts only (tot: n of a fallback wave needs no ranks); row_scan_ranks adds the scan
-template <int ROWS>
-__device__ __forceinline__ RowScan<ROWS> row_count(const uint32_t *bm, unsigned lane) {
-    RowScan<ROWS> r;
-    if constexpr (ROWS == 64) {
-        const uint2 w = reinterpret_cast<const uint2 *>(bm)[lane];
-        r.c0 = __popc(w.x);
-        r.c = r.c0 + __popc(w.y);
-    } else {
+template <int ROWS, int CW>
+__device__ __forceinline__ RowScan<ROWS, CW> row_count(const uint32_t *bm, unsigned lane) {
+    constexpr int WPL = ROWS / 32 * CW;   // words per lane
+    RowScan<ROWS, CW> r;
+    if constexpr (WPL == 1) {
         r.c = r.c0 = __popc(bm[lane]);
+    } else if constexpr (WPL == 2) {
+        const uint2 w = reinterpret_cast<const uint2 *>(bm)[lane];
+        r.c0 = CW == 1 ? (uint32_t)__popc(w.x) : (uint32_t)(__popc(w.x) + __popc(w.y));
+        r.c = (uint32_t)(__popc(w.x) + __popc(w.y));
+    } else {
+        const uint4 w = reinterpret_cast<const uint4 *>(bm)[lane];
+        r.c0 = (uint32_t)(__popc(w.x) + __popc(w.y));
+        r.c = r.c0 + (uint32_t)(__popc(w.z) + __popc(w.w));
     }
     r.be = 0u;
     r.tot = __reduce_add_sync(FULL, r.c);
     return r;
 }
-template <int ROWS>
-__device__ __forceinline__ void row_scan_ranks(RowScan<ROWS> &r, unsigned lane) { r.be = warp_excl_scan(r.c, lane); }
-template <int ROWS>
-__device__ __forceinline__ RowScan<ROWS> row_scan(const uint32_t *bm, unsigned lane) {
-    RowScan<ROWS> r = row_count<ROWS>(bm, lane);
+template <int ROWS, int CW>
+__device__ __forceinline__ void row_scan_ranks(RowScan<ROWS, CW> &r, unsigned lane) { r.be = warp_excl_scan(r.c, lane); }
+template <int ROWS, int CW>
+__device__ __forceinline__ RowScan<ROWS, CW> row_scan(const uint32_t *bm, unsigned lane) {
+    RowScan<ROWS, CW> r = row_count<ROWS, CW>(bm, lane);
     row_scan_ranks(r, lane);
     return r;
 }
 // set bits before row `row` (every lane participates)
-template <int ROWS>
-__device__ __forceinline__ uint32_t row_base(const RowScan<ROWS> &rs, int row) {
+template <int ROWS, int CW>
+__device__ __forceinline__ uint32_t row_base(const RowScan<ROWS, CW> &rs, int row) {
     if constexpr (ROWS == 64) {
         const uint32_t be = __shfl_sync(FULL, rs.be, row >> 1), c0 = __shfl_sync(FULL, rs.c0, row >> 1);
         return be + ((row & 1) ? c0 : 0u);
@@ -1839,10 +1864,21 @@ __device__ __forceinline__ uint32_t row_base(const RowScan<ROWS> &rs, int row) {
         return __shfl_sync(FULL, rs.be, row);
     }
 }
+// zero the lane's words of a bitmap
+template <int ROWS, int CW>
+__device__ __forceinline__ void bm_zero(uint32_t *bm, unsigned lane) {
+    constexpr int WPL = ROWS / 32 * CW;
+    if constexpr (WPL == 1) bm[lane] = 0u;
+    else if constexpr (WPL == 2) reinterpret_cast<uint2 *>(bm)[lane] = make_uint2(0u, 0u);
+    else reinterpret_cast<uint4 *>(bm)[lane] = make_uint4(0u, 0u, 0u, 0u);
+}
 
-template <bool DBG, int ROWS>
-__device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws, float2 uv, uint2 gr, bool inframe,
+// ROWS x COLS window: (32, 32) in the second kernel, (64, 64) in the third (BC1), which keeps
+// the general (sort) path for AABBs beyond 64 x 64 only
+template <bool DBG, int ROWS, int COLS = 32>
+__device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS, COLS> &ws, float2 uv, uint2 gr, bool inframe,
                                              int px, int py, uint32_t frame, bool force) {
+    constexpr int CW = COLS / 32, LGC = COLS == 64 ? 6 : 5;
     const unsigned lane = lane_id(), lt = lanemask_lt();
     LeanOut o;
     o.color = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1872,33 +1908,42 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws
     const int miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
     const int bw = __reduce_max_sync(FULL, active ? f.xb : 0) - minx + 1;
     const int bh = __reduce_max_sync(FULL, active ? f.yb : 0) - miny + 1;
-    if (bw > 32 || bh > ROWS) {   // wider than the bitmap: the general path (third kernel)
+    if (bw > COLS || bh > ROWS) {   // wider than the bitmap: the next kernel (64 x 64 window / general path)
         o.done = false;
         o.rec = kSlowMark;
         return o;
     }
-    const int cx0 = (f.xa - minx) & 31, cx1 = (f.xb - minx) & 31, cy0 = (f.ya - miny) & (ROWS - 1), cy1 = (f.yb - miny) & (ROWS - 1);
+    const int cx0 = (f.xa - minx) & (COLS - 1), cx1 = (f.xb - minx) & (COLS - 1), cy0 = (f.ya - miny) & (ROWS - 1),
+              cy1 = (f.yb - miny) & (ROWS - 1);
     const int ar = __popc(A & lt);   // active rank: lane = h(ar, A)
-    if constexpr (ROWS == 64) {
-        reinterpret_cast<uint2 *>(ws.bmU)[lane] = make_uint2(0u, 0u);
-        reinterpret_cast<uint2 *>(ws.bmP)[lane] = make_uint2(0u, 0u);
-        reinterpret_cast<uint2 *>(ws.bmD)[lane] = make_uint2(0u, 0u);
-    } else {
-        ws.bmU[lane] = 0u;
-        ws.bmP[lane] = 0u;
-        ws.bmD[lane] = 0u;
-    }
+    bm_zero<ROWS, CW>(ws.bmU, lane);
+    bm_zero<ROWS, CW>(ws.bmP, lane);
+    bm_zero<ROWS, CW>(ws.bmD, lane);
     if (active) ws.act[ar] = (uint8_t)lane;
     __syncwarp();
-    // ---- a3: the needed set U (every corner, zero weights included, R-4)
-    const uint32_t pat = (1u << cx0) | (1u << cx1);
-    uint32_t oU0 = 0u, oU1 = 0u;
+    // ---- a3: the needed set U (every corner, zero weights included, R-4); firstU bit k: this
+    // lane set corner k's bit first (its duplicates within the lane see their own earlier bit)
+    unsigned firstU = 0u;
     if (active) {
-        oU0 = atomicOr(&ws.bmU[cy0], pat);
-        oU1 = atomicOr(&ws.bmU[cy1], pat);
+        if constexpr (CW == 1) {
+            const uint32_t pat = (1u << cx0) | (1u << cx1);
+            const uint32_t oU0 = atomicOr(&ws.bmU[cy0], pat);
+            const uint32_t oU1 = atomicOr(&ws.bmU[cy1], pat);
+            const bool dx = cx1 != cx0;
+            firstU = (((oU0 >> cx0) & 1u) ? 0u : 1u) | ((dx && !((oU0 >> cx1) & 1u)) ? 2u : 0u) |
+                     (((oU1 >> cx0) & 1u) ? 0u : 4u) | ((dx && !((oU1 >> cx1) & 1u)) ? 8u : 0u);
+        } else {
+            const int cx[2] = {cx0, cx1}, cy[2] = {cy0, cy1};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = cx[k & 1];
+                const uint32_t old = atomicOr(&ws.bmU[win_word<CW>(cy[k >> 1], c)], 1u << (c & 31));
+                firstU |= ((old >> (c & 31)) & 1u) ? 0u : (1u << k);
+            }
+        }
     }
     __syncwarp();
-    RowScan<ROWS> rsU = row_count<ROWS>(ws.bmU, lane);   // ranks only for an exact wave
+    RowScan<ROWS, CW> rsU = row_count<ROWS, CW>(ws.bmU, lane);   // ranks only for an exact wave
     const int n = (int)rsU.tot;
     // ---- a4: decide (List R-6; Box / Mask R-22)
     bool exact;
@@ -1918,31 +1963,29 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws
             // ranks of the four corners; each texel's first setter publishes rank -> position
             row_scan_ranks(rsU, lane);
             const uint32_t b0 = row_base(rsU, cy0), b1 = row_base(rsU, cy1);
-            const uint32_t w0 = ws.bmU[cy0], w1 = ws.bmU[cy1];
-            rho[0] = bm_rank(b0, w0, cx0);
-            rho[1] = bm_rank(b0, w0, cx1);
-            rho[2] = bm_rank(b1, w1, cx0);
-            rho[3] = bm_rank(b1, w1, cx1);
-            const bool dx = cx1 != cx0;
+            rho[0] = win_rank<CW>(ws.bmU, b0, cy0, cx0);
+            rho[1] = win_rank<CW>(ws.bmU, b0, cy0, cx1);
+            rho[2] = win_rank<CW>(ws.bmU, b1, cy1, cx0);
+            rho[3] = win_rank<CW>(ws.bmU, b1, cy1, cx1);
             if (active) {
-                if (!((oU0 >> cx0) & 1u)) ws.tbl[rho[0]] = (uint16_t)((cy0 << 5) | cx0);
-                if (dx && !((oU0 >> cx1) & 1u)) ws.tbl[rho[1]] = (uint16_t)((cy0 << 5) | cx1);
-                if (!((oU1 >> cx0) & 1u)) ws.tbl[rho[2]] = (uint16_t)((cy1 << 5) | cx0);
-                if (dx && !((oU1 >> cx1) & 1u)) ws.tbl[rho[3]] = (uint16_t)((cy1 << 5) | cx1);
+                if (firstU & 1u) ws.tbl[rho[0]] = (uint16_t)((cy0 << LGC) | cx0);
+                if (firstU & 2u) ws.tbl[rho[1]] = (uint16_t)((cy0 << LGC) | cx1);
+                if (firstU & 4u) ws.tbl[rho[2]] = (uint16_t)((cy1 << LGC) | cx0);
+                if (firstU & 8u) ws.tbl[rho[3]] = (uint16_t)((cy1 << LGC) | cx1);
             }
             __syncwarp();
             // ---- a5: active rank r < n produces U[r] (lane h(r, A))
             produced = active && ar < n;
             const uint32_t e = produced ? (uint32_t)ws.tbl[ar] : 0u;
-            qx = minx + (int)(e & 31u);
-            qy = miny + (int)(e >> 5);
+            qx = minx + (int)(e & (COLS - 1));
+            qy = miny + (int)(e >> LGC);
             evals = n;
         } else {
             // Box: active rank i < w*h produces AABB texel (i mod w, i div w) (LaneIdxToCoord,
             // P:1069-1076); a corner reads its AABB-local index (CoordToLaneIdx)
             const int area = bw * bh;
             produced = active && ar < area;
-            const int jq = (int)__fdividef((float)ar + 0.5f, (float)bw);   // exact for bw <= 32, ar < 32
+            const int jq = (int)__fdividef((float)ar + 0.5f, (float)bw);   // exact for bw <= 64, ar < 32
             qx = minx + (ar - jq * bw);
             qy = miny + (produced ? jq : 0);
             rho[0] = cy0 * bw + cx0;
@@ -1984,37 +2027,43 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws
     if (fb == FB_CPLUS) {
         // (1) the planned set P: STF texels deduplicated, ranked ascending (R-17)
         uint32_t oP = 0u;
-        if (active) oP = atomicOr(&ws.bmP[qcy], 1u << qcx);
-        const bool firstP = active && !((oP >> qcx) & 1u);
+        if (active) oP = atomicOr(&ws.bmP[win_word<CW>(qcy, qcx)], 1u << (qcx & 31));
+        const bool firstP = active && !((oP >> (qcx & 31)) & 1u);
         // publish this lane's distinct corners (merged weights, R-14) for the spare lanes
         ws.mw[lane] = make_float4(m.dw[0], m.dw[1], m.dw[2], m.dw[3]);
-        ws.fpos[lane] = (uint32_t)cx0 | ((uint32_t)cx1 << 5) | ((uint32_t)cy0 << 10) | ((uint32_t)cy1 << 16) | (C << 22);
+        ws.fpos[lane] = (uint32_t)cx0 | ((uint32_t)cx1 << 6) | ((uint32_t)cy0 << 12) | ((uint32_t)cy1 << 18) | (C << 24);
         __syncwarp();
-        const RowScan<ROWS> rsP = row_scan<ROWS>(ws.bmP, lane);
+        const RowScan<ROWS, CW> rsP = row_scan<ROWS, CW>(ws.bmP, lane);
         const int np = (int)rsP.tot;
         const uint32_t bq = row_base(rsP, qcy);
-        if (firstP) ws.tbl[bm_rank(bq, ws.bmP[qcy], qcx)] = (uint16_t)((qcy << 5) | qcx);
+        if (firstP) ws.tbl[win_rank<CW>(ws.bmP, bq, qcy, qcx)] = (uint16_t)((qcy << LGC) | qcx);
         __syncwarp();
         produced = false;
         if (active) {
             if (ar < np) {   // (2) active rank i < n_p produces planned texel i (lane h(i, A))
                 const uint32_t e = ws.tbl[ar];
-                qcx = (int)(e & 31u);
-                qcy = (int)(e >> 5);
+                qcx = (int)(e & (COLS - 1));
+                qcy = (int)(e >> LGC);
                 produced = true;
             } else {         // (3) spare lane: serves lane l of Eq. 2 (R-18)
                 const int l = ws.act[eq2_lane_rank(ar, np, na)];
                 o.selbits |= (1u << 5) | ((uint32_t)l << 8);
                 const uint32_t fp = ws.fpos[l];
                 const float4 gw = ws.mw[l];
-                const int gx0 = (int)(fp & 31u), gx1 = (int)((fp >> 5) & 31u), gy0 = (int)((fp >> 10) & (ROWS - 1)),
-                          gy1 = (int)((fp >> 16) & (ROWS - 1));
-                const uint32_t r0 = ws.bmP[gy0], r1 = ws.bmP[gy1];
-                const unsigned PL = ((r0 >> gx0) & 1u) | (((r0 >> gx1) & 1u) << 1) | (((r1 >> gx0) & 1u) << 2) |
-                                    (((r1 >> gx1) & 1u) << 3);
+                const int gx0 = (int)(fp & 63u), gx1 = (int)((fp >> 6) & 63u), gy0 = (int)((fp >> 12) & 63u),
+                          gy1 = (int)((fp >> 18) & 63u);
+                unsigned PL;
+                if constexpr (CW == 1) {
+                    const uint32_t r0 = ws.bmP[gy0], r1 = ws.bmP[gy1];
+                    PL = ((r0 >> gx0) & 1u) | (((r0 >> gx1) & 1u) << 1) | (((r1 >> gx0) & 1u) << 2) |
+                         (((r1 >> gx1) & 1u) << 3);
+                } else {
+                    PL = win_bit<CW>(ws.bmP, gy0, gx0) | (win_bit<CW>(ws.bmP, gy0, gx1) << 1) |
+                         (win_bit<CW>(ws.bmP, gy1, gx0) << 2) | (win_bit<CW>(ws.bmP, gy1, gx1) << 3);
+                }
                 // candidates: l's distinct nonzero-weight texels not planned, picked ~ merged
                 // weight with u2 (the sums and the decision in fp32, in corner order, as cplus_pick)
-                const unsigned cand = (fp >> 22) & ~PL & 15u;
+                const unsigned cand = (fp >> 24) & ~PL & 15u;
                 const float dw[4] = {gw.x, gw.y, gw.z, gw.w};
                 float ps[4], wsum = 0.0f;
 #pragma unroll
@@ -2047,16 +2096,21 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws
     }
     // ---- a7 finish: the produced set D (values in the producers' slots, one source lane per
     // texel), Eq. 1 / WC over the known corners
-    const int pq = ((qy - miny) << 5) | (qx - minx);
+    const int pq = ((qy - miny) << LGC) | (qx - minx);   // window position; its word is pq >> 5
     uint32_t oD = 0u;
     if (produced) oD = atomicOr(&ws.bmD[pq >> 5], 1u << (pq & 31));
     if (produced) ws.xch[lane] = val;
     if (produced && !((oD >> (pq & 31)) & 1u)) ws.lop[pq] = (uint8_t)lane;
     __syncwarp();
-    const uint32_t d0 = ws.bmD[cy0], d1 = ws.bmD[cy1];
-    const unsigned IN = ((d0 >> cx0) & 1u) | (((d0 >> cx1) & 1u) << 1) | (((d1 >> cx0) & 1u) << 2) |
-                        (((d1 >> cx1) & 1u) << 3);
-    const int p0 = cy0 << 5, p2 = cy1 << 5;
+    unsigned IN;
+    if constexpr (CW == 1) {
+        const uint32_t d0 = ws.bmD[cy0], d1 = ws.bmD[cy1];
+        IN = ((d0 >> cx0) & 1u) | (((d0 >> cx1) & 1u) << 1) | (((d1 >> cx0) & 1u) << 2) | (((d1 >> cx1) & 1u) << 3);
+    } else {
+        IN = win_bit<CW>(ws.bmD, cy0, cx0) | (win_bit<CW>(ws.bmD, cy0, cx1) << 1) | (win_bit<CW>(ws.bmD, cy1, cx0) << 2) |
+             (win_bit<CW>(ws.bmD, cy1, cx1) << 3);
+    }
+    const int p0 = cy0 << LGC, p2 = cy1 << LGC;
     if (fb == FB_WC) {
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 pv[4] = {(IN & 1u) ? ws.xch[ws.lop[p0 | cx0]] : z, (IN & 2u) ? ws.xch[ws.lop[p0 | cx1]] : z,
@@ -2072,6 +2126,7 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS> &ws
     __syncwarp();
     return o;
 }
+
 
 // GRAD: grad != NULL (magnified class); FORCE: CTF_FLAG_FORCE_FALLBACK (every live wave
 // goes to the rest kernel) — compile-time, so the hot loop tests neither.
@@ -2334,6 +2389,9 @@ __global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
 #define CTF_FB_MINB 4  // fallback kernel: resident CTAs per SM (64 registers)
 #endif
 constexpr int kScanGroups = 8;   // record groups loaded per warp step in the rest kernels
+#ifndef CTF_REST_BIG
+#define CTF_REST_BIG 1  // 1: the third kernel (BC1) tries the 64 x 64 bitmap window before the sort-based general path
+#endif
 #ifndef CTF_REST_MERGED
 #define CTF_REST_MERGED 0  // 1: the fallback kernel also runs the general path (out of line); no third kernel
 #endif
@@ -2363,6 +2421,9 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
     // launched as a programmatic dependent of the previous pass: wait for its results
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.lists && a.lcnt[FALLBACK ? 0 : 1] == 0u) return;   // empty work list (same value in every thread)
+    // BIG: the third kernel (BC1) runs the 64 x 64 window first; the sort-based general path
+    // only takes AABBs beyond it
+    constexpr bool BIG = !FALLBACK && FMT == FMT_BC1 && CTF_REST_BIG;
     __shared__ WarpSmem smem[(FALLBACK && !CTF_REST_MERGED) ? 1 : kWarps];
     __shared__ WideSmem fsm[FALLBACK ? kWarps : 1];
     extern __shared__ __align__(16) unsigned char dyn_smem[];   // latent MLP: TcWeights + per-warp TcScratch
@@ -2370,9 +2431,16 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
     WarpSmem &s = smem[(FALLBACK && !CTF_REST_MERGED) ? 0 : warp];
     WideSmem &fs = fsm[FALLBACK ? warp : 0];
     MlpCtx mc{nullptr, nullptr, nullptr, dyn_smem, warp};
+    // the 64 x 64 windows live in dynamic shared memory (kWarps x ~7 KB)
+    WideSmemBig &fb = reinterpret_cast<WideSmemBig *>(dyn_smem)[BIG ? warp : 0];
     if (FALLBACK) {
         if (lane < 8) fs.lut[lane] = bc1_lut_entry(lane);
         fs.xch[lane] = make_float4(0.f, 0.f, 0.f, 0.f);   // finite values in every slot (combine_eq1_coef)
+        __syncwarp();
+    }
+    if (BIG) {
+        if (lane < 8) fb.lut[lane] = bc1_lut_entry(lane);
+        fb.xch[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncwarp();
     }
     if constexpr (FMT != FMT_BC1) {
@@ -2392,6 +2460,7 @@ __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == 
         LeanOut o;
         o.done = false;
         if (FALLBACK) o = wide_wave<DBG, CTF_REST_ROWS>(a, fs, uv, gr, inframe, px, py, frame, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
+        else if constexpr (BIG) o = wide_wave<DBG, 64, 64>(a, fb, uv, gr, inframe, px, py, frame, (a.flags & FLAG_FORCE_FALLBACK) != 0u);
         if (!o.done) {
             if (FALLBACK && !CTF_REST_MERGED) {   // AABB wider than 32 x 32 texels: general kernel
                 if (lane == 0) {
@@ -2693,7 +2762,7 @@ static cudaError_t launch_lean(KArgs &k, const typename WeightsOf<FMT>::type &mw
 template <int FMT, bool DBG>
 static cudaError_t launch_rest(const KArgs &k, const typename WeightsOf<FMT>::type &mw, int dev, int sms,
                                cudaStream_t stream) {
-    const size_t dyn = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
+    const size_t dyn_mlp = FMT == FMT_BC1 ? 0 : sizeof(TcWeights) + kWarps * sizeof(TcScratch);
     const unsigned nrec = (unsigned)((long long)k.wpf * (k.nchunks / (unsigned)k.cpf));
     const long long groups = ((long long)nrec + 31) / 32;
     const int first = FMT == FMT_BC1 ? 0 : 1;
@@ -2702,6 +2771,8 @@ static cudaError_t launch_rest(const KArgs &k, const typename WeightsOf<FMT>::ty
         auto rest = ctf_collab_rest_kernel<DBG, false, FMT>;
         if constexpr (FMT == FMT_BC1)
             if (pass == 0) rest = ctf_collab_rest_kernel<DBG, true, FMT_BC1>;
+        // BC1 third kernel: the 64 x 64 windows (CTF_REST_BIG) in dynamic shared memory
+        const size_t dyn = FMT == FMT_BC1 ? (pass == 1 && CTF_REST_BIG ? kWarps * sizeof(WideSmemBig) : 0) : dyn_mlp;
         int per_sm = 0;
         if (dyn > 0 && (e = mlp_smem_setup(rest, dyn, dev)) != cudaSuccess) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rest, kWarps * 32, dyn);

@@ -505,3 +505,22 @@ def test_rng_ties_match_oracle(ctf):
         torch.cuda.synchronize()
         np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
         assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
+
+
+@pytest.mark.parametrize("jac", [[[6.0, 0.0], [0.0, 1.0]], [[1.0, 0.5], [0.0, 12.0]], [[7.5, 0.0], [0.0, 15.0]],
+                                 [[4.0, 3.0], [3.0, 4.0]], [[9.0, 0.0], [0.0, 3.0]], [[2.0, 0.0], [0.0, 23.0]]])
+def test_big_window_waves(ctf, jac):
+    """Minified waves whose footprint AABB exceeds the second kernel's 32 x 32 window: the third
+    kernel's 64 x 64 window (AABBs up to 64 x 64) and, beyond it, the sort-based general path
+    (9 x 3 and 2 x 23 texels per pixel: 65 texels wide / 71 tall).  Every mode and fallback,
+    debug kernels bitwise, release kernels records + colours."""
+    tex = bc1_tex(256, 256, 5, "image")
+    uv, g = synthetic.affine_quad(48, 20, 256, 256, jac)
+    for mode, fb, fl in MODES:
+        o = run_oracle(tex, uv, g, mode, fb, fl, seed=9)
+        assert_parity(run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=9), o, f"jac={jac} mode={mode} fb={fb} fl={fl}")
+        dt = to_dev_tex(ctf, tex)
+        out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, fl, 9, 0)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+        assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
