@@ -16,6 +16,9 @@ enum { FMT_BC1 = 1, FMT_MLP = 2 };
 enum { MODE_4TAP = 0, MODE_STF = 1, MODE_WC = 2, MODE_COLLAB = 3 };
 enum { FB_STF = 0, FB_WC = 1, FB_C = 2, FB_CPLUS = 3 };
 enum { FLAG_DEBUG = 1u, FLAG_FORCE_FALLBACK = 2u, FLAG_SEPARATE_PASSES = 4u };
+// internal (set by the launcher, never by callers): the lean kernel's grid is one wave of
+// resident CTAs, so it lets the next kernel on the stream launch at once (PDL)
+enum : uint32_t { FLAG_PDL_EARLY = 1u << 30 };
 enum { PATH_EXACT = 0, PATH_FB_STF = 1, PATH_FB_WC = 2, PATH_FB_C = 3, PATH_FB_CPLUS = 4,
        PATH_4TAP = 5, PATH_STF = 6, PATH_WC = 7 };
 

@@ -2212,6 +2212,11 @@ __global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
         if (threadIdx.x == 0) s_next = kLW;
         __syncthreads();
     }
+    // programmatic dependent launch: a one-wave grid lets the next kernel on the stream launch
+    // now (its CTAs take the free slots and wait for this grid); every grid waits for the
+    // previous kernel's results before its first global access (the prologue above overlaps it)
+    if (a.flags & FLAG_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned per_warp = a.ipc / kLW;
     for (unsigned k = warp;;) {
@@ -2753,8 +2758,23 @@ static cudaError_t launch_lean(KArgs &k, const typename WeightsOf<FMT>::type &mw
     k.ipc = (unsigned)(ipw * lean_warps<FMT>());
     long long grid = ((long long)k.nchunks + k.ipc - 1) / k.ipc;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, lean_warps<FMT>() * 32, dyn, stream>>>(k, mw);
-    return cudaGetLastError();
+#ifndef CTF_PDL_EARLY_DIV
+#define CTF_PDL_EARLY_DIV 2  // early trigger when the grid fills at most 1/DIV of the resident CTA slots
+#endif
+    if (grid * CTF_PDL_EARLY_DIV <= slots) k.flags |= FLAG_PDL_EARLY;
+    // launched as a programmatic dependent of the previous kernel on the stream (it waits for
+    // it in-kernel, after its shared-memory prologue)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(lean_warps<FMT>() * 32);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, k, mw);
 }
 
 // the marked waves of k's frames: pass 0 lean fallback (BC1), pass 1 general; each pass at
