@@ -63,6 +63,8 @@ struct KArgs {
     int Wf, Hf, nwx, nwy, wpf;
     int cpr, cpf;                   // work items (runs of `chunk` waves) per wave-row / per frame
     int chunk;                      // waves per work item (a run in one wave-row; <= 32, host-chosen)
+    uint32_t cpr_m;                 // lean kernels: run j of a wave-row spans waves [j nwx / cpr, (j+1) nwx / cpr)
+    int cpr_s;                      // (magic pair of the division by cpr, udiv_magic)
     unsigned nchunks;
     unsigned ipc;                   // work items per CTA (claimed dynamically by its warps)
     float Wflt, Hflt;
@@ -2237,8 +2239,9 @@ __global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
         const int rr = (int)(c - (unsigned)fr * (unsigned)a.cpf);
         int wy, wxc;
         run_coords(rr, a, wy, wxc);
-        const int wx0 = wxc * a.chunk;
-        const int wx1 = min(wx0 + a.chunk, a.nwx);
+        // run wxc of the wave-row: lengths differ by at most one wave (<= chunk)
+        const int wx0 = (int)udiv_magic((unsigned)(wxc * a.nwx), a.cpr_m, a.cpr_s);
+        const int wx1 = (int)udiv_magic((unsigned)((wxc + 1) * a.nwx), a.cpr_m, a.cpr_s);
         const int py = wy * 4 + ly;
         const bool rowok = py < a.Hf;
         const bool rowok_all = wy * 4 + 4 <= a.Hf;   // warp-uniform: all 4 rows in the frame
@@ -2825,17 +2828,20 @@ static cudaError_t launch_fast(KArgs k, const typename WeightsOf<FMT>::type &mw,
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
     if (FMT == FMT_BC1) {
-        // runs short enough that every resident warp gets work (small calls are latency-bound:
-        // a warp's waves are a dependent chain), at most kChunk waves (large batches)
-        // (ceil(waves / resident warps), even: one round of runs, the longest chain as short as
-        // the call allows)
+        // as many runs per wave-row as fill every resident warp once (small calls are
+        // latency-bound: a warp's waves are a dependent chain; equal-length runs keep the SMs
+        // evenly loaded), between ceil(nwx / kChunk) (runs of <= kChunk waves, large batches)
+        // and nwx / 2 (runs of >= 2 waves: pairs)
         const long long warps = (long long)sms * CTF_PAIR_MINB * kWarps;
-        long long ch = ((long long)k.nrec + warps - 1) / (warps > 0 ? warps : 1);
-        ch += ch & 1LL;
-        ch = ch < 2 ? 2 : ch > kChunk ? kChunk : ch;
         const unsigned frames = k.nrec / (unsigned)k.wpf;
-        k.chunk = (int)ch;
-        k.cpr = (k.nwx + k.chunk - 1) / k.chunk;
+        const long long rows = (long long)k.nwy * frames;
+        const long long rmin = (k.nwx + kChunk - 1) / kChunk;
+        const long long rmax = k.nwx / 2 > rmin ? k.nwx / 2 : rmin;
+        long long R = warps / (rows > 0 ? rows : 1);
+        R = R < rmin ? rmin : R > rmax ? rmax : R;
+        k.cpr = (int)R;
+        k.chunk = (int)((k.nwx + R - 1) / R);
+        udiv_magic_host((unsigned)k.cpr, k.cpr_m, k.cpr_s);
         k.cpf = k.cpr * k.nwy;
         k.nchunks = (unsigned)((long long)k.cpf * frames);
     }
@@ -2916,6 +2922,7 @@ cudaError_t launch_filter_mlp(const LaunchArgs &a, cudaStream_t stream) {
     k.nrec = (unsigned)((long long)k.wpf * a.frames);
     udiv_magic_host((unsigned)k.wpf, k.wpf_m, k.wpf_s);
     udiv_magic_host((unsigned)k.nwx, k.nwx_m, k.nwx_s);
+    udiv_magic_host((unsigned)k.cpr, k.cpr_m, k.cpr_s);
     k.Wflt = (float)a.W;
     k.Hflt = (float)a.H;
     k.Wm1 = a.W - 1;
