@@ -44,9 +44,9 @@ if str(ROOT) not in sys.path:
 
 METRIC = "4K filtered Gpix/s per B200 (1/2/4/8 GPUs); texel evals/pixel; error vs bilinear"
 UNIT = "Gpix/s"
-# the timed ABI call: BC1 COLLAB runs the lean exact kernel, then the lean fallback kernel and
-# the general kernel over the waves it marked (fallback / partial or wider windows); the
-# roofline times the whole call
+# the timed ABI call: BC1 COLLAB runs the lean exact kernel, then the wide-window kernel (32 x 32
+# bitmap windows) and the third kernel (64 x 64 windows, the sort-based general path beyond)
+# over the waves it marked (fallback / partial or wider windows); the roofline times the whole call
 KERNEL_NAME = "ctf_collab_lean_kernel + 2 x ctf_collab_rest_kernel (one ctf_filter_batch call)"
 MODES = {"collab": 3, "4tap": 0, "stf": 1, "wc": 2}
 FALLBACKS = {"stf": 0, "wc": 1, "c": 2, "cplus": 3}
