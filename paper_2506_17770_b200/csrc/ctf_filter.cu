@@ -1335,6 +1335,25 @@ __global__ void __launch_bounds__(kWarps * 32, (FMT == FMT_BC1 ? CTF_BC1_MINB : 
 // divergence check).
 constexpr uint32_t kSlowMark = 0xFFFFFFFFu;   // neither is a COLLAB record (path <= 4, n <= 128)
 constexpr uint32_t kFbMark = 0xFFFFFFFEu;
+#ifndef CTF_REST_ROWS
+#define CTF_REST_ROWS 32  // window rows of the wide-window kernel's bitmap (32 or 64)
+#endif
+#ifndef CTF_REST_CONCURRENT
+#define CTF_REST_CONCURRENT 1  // BC1: the lean kernel routes each wave it leaves by its AABB (the wide-window
+                               // kernel's 32 x CTF_REST_ROWS window, else the third kernel), so the third kernel
+                               // runs first and the wide-window kernel alongside it (PDL, see launch_rest)
+#endif
+// BC1, a wave the lean path leaves: kFbMark when its active lanes' footprint AABB fits the
+// wide-window kernel's window, else kSlowMark (the third kernel's 64 x 64 window / general path)
+// — the same test as wide_wave's, so the wide-window kernel never re-marks a wave
+__device__ __forceinline__ uint32_t bc1_rest_mark(const Foot &f, bool active) {
+    if (!CTF_REST_CONCURRENT) return kFbMark;
+    const int minx = __reduce_min_sync(FULL, active ? f.xa : INT_MAX);
+    const int miny = __reduce_min_sync(FULL, active ? f.ya : INT_MAX);
+    const int maxx = __reduce_max_sync(FULL, active ? f.xb : INT_MIN);
+    const int maxy = __reduce_max_sync(FULL, active ? f.yb : INT_MIN);
+    return (maxx - minx >= 32 || maxy - miny >= CTF_REST_ROWS) ? kSlowMark : kFbMark;
+}
 
 struct FastSmem {
     float4 xch[32];           // rank -> produced value (exact waves, n <= 32)
@@ -1518,8 +1537,8 @@ __device__ __forceinline__ LeanOut lean_wave(const KArgs &a, SM &fs, const uint4
     if (__all_sync(FULL, (dx | (dy << 1)) < 8u)) K = 1;                      // 8x4
     else if (__all_sync(FULL, (dy | (dx << 1)) < 8u)) { K = 1; lgP = 2u; }   // 4x8
     else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                        // 8x8
-    if (K == 0) {   // a wider window: the wide-window kernel (BC1) / the general kernel (latent MLP)
-        o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
+    if (K == 0) {   // a wider window: the wide-window kernel / the third kernel (BC1), the general kernel (latent MLP)
+        o.rec = FMT == FMT_BC1 ? bc1_rest_mark(f, true) : kSlowMark;
         return o;
     }
     const uint32_t pmask = (1u << lgP) - 1u;
@@ -1629,8 +1648,8 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     o.n = 0;
     o.minx = o.miny = 0;
     const unsigned A = __ballot_sync(FULL, !isnan(uv.x));   // interior run: every pixel in the frame
-    if (A != FULL) {   // empty wave: n = 0, zero colour; partial wave: wide-window kernel (BC1)
-        o.rec = A == 0u ? (1u << 26) : (FMT == FMT_BC1 ? kFbMark : kSlowMark);
+    if (A != FULL) {   // empty wave: n = 0, zero colour; partial wave: wide-window / third kernel (BC1)
+        o.rec = A == 0u ? (1u << 26) : (FMT == FMT_BC1 ? bc1_rest_mark(footprint2(uv, a), !isnan(uv.x)) : kSlowMark);
         return o;
     }
     const bool wave_mag = wave_magnified(gr, GRAD);
@@ -1647,8 +1666,8 @@ __device__ __forceinline__ PairFront pair_front(const KArgs &a, SM &fs, float2 u
     else if (__all_sync(FULL, dx < 6u && dy < 5u)) { K = 1; P = 6u; csel = 0x4442u; }      // 6x5
     else if (__all_sync(FULL, dx < 5u && dy < 6u)) { K = 1; P = 5u; csel = 0x4443u; }      // 5x6
     else if (__all_sync(FULL, (dx | dy) < 8u)) K = 2;                                      // 8x8
-    if (K == 0) {   // a wider window: the wide-window kernel (BC1) / the general kernel (latent MLP)
-        o.rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
+    if (K == 0) {   // a wider window: the wide-window / third kernel (BC1), the general kernel (latent MLP)
+        o.rec = FMT == FMT_BC1 ? bc1_rest_mark(f, true) : kSlowMark;
         return o;
     }
     const uint32_t t0 = (uint32_t)(f.ya - miny) * P + (uint32_t)(f.xa - minx);
@@ -2320,8 +2339,9 @@ __global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
                     if (a.dbg_sel) a.dbg_sel[pix] = 0u;
                 }
             } else {
-                // partial (or, FORCE, any live) wave: the wide-window kernel (BC1) / the general kernel
-                rec = FMT == FMT_BC1 ? kFbMark : kSlowMark;
+                // partial (or, FORCE, any live) wave: the wide-window / third kernel (BC1), the general kernel
+                if constexpr (FMT == FMT_BC1) rec = bc1_rest_mark(footprint2(uv, a), active);
+                else rec = kSlowMark;
             }
             if (lane == (unsigned)(wx - wx0)) myrec = rec;
           }
@@ -2426,8 +2446,20 @@ template <bool DBG, bool FALLBACK, int FMT>
 __global__ void __launch_bounds__(kWarps * 32, FALLBACK ? CTF_FB_MINB : (FMT == FMT_BC1 ? CTF_REST_MINB : CTF_MLP_COLLAB_MINB))
     ctf_collab_rest_kernel(const __grid_constant__ KArgs a, unsigned nrec, const typename WeightsOf<FMT>::type mw) {
     static_assert(FMT == FMT_BC1 || !FALLBACK, "no lean fallback for the latent-MLP format");
-    // launched as a programmatic dependent of the previous pass: wait for its results
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // launched as a programmatic dependent of the previous pass: wait for its results.  CONC
+    // (BC1, the lean kernel routes by AABB): the third kernel runs right after the lean kernel and
+    // lets the wide-window kernel launch at once; the wide-window kernel reads only the lean
+    // kernel's results (complete and visible: every third-kernel CTA triggered after its own
+    // wait) and waits for the third kernel before it completes, so the call's stream order holds
+    constexpr bool CONC = FMT == FMT_BC1 && CTF_REST_CONCURRENT && !CTF_REST_MERGED;
+    struct EndWait {
+        bool on;
+        __device__ ~EndWait() {
+            if (on) asm volatile("griddepcontrol.wait;" ::: "memory");
+        }
+    } end_wait{CONC && FALLBACK};
+    if (!(CONC && FALLBACK)) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (CONC && !FALLBACK) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (a.lists && a.lcnt[FALLBACK ? 0 : 1] == 0u) return;   // empty work list (same value in every thread)
     // BIG: the third kernel (BC1) runs the 64 x 64 window first; the sort-based general path
     // only takes AABBs beyond it
@@ -2790,7 +2822,12 @@ static cudaError_t launch_rest(const KArgs &k, const typename WeightsOf<FMT>::ty
     const long long groups = ((long long)nrec + 31) / 32;
     const int first = FMT == FMT_BC1 ? 0 : 1;
     cudaError_t e;
-    for (int pass = first; pass < (CTF_REST_MERGED ? 1 : 2); ++pass) {
+    // BC1 with CTF_REST_CONCURRENT: the third kernel (its waves routed by the lean kernel) first,
+    // the wide-window kernel launched as its programmatic dependent right away (see the kernel)
+    constexpr bool conc = FMT == FMT_BC1 && CTF_REST_CONCURRENT && !CTF_REST_MERGED;
+    const int npass = CTF_REST_MERGED ? 1 : 2;
+    for (int pi = first; pi < npass; ++pi) {
+        const int pass = conc ? 1 - pi : pi;
         auto rest = ctf_collab_rest_kernel<DBG, false, FMT>;
         if constexpr (FMT == FMT_BC1)
             if (pass == 0) rest = ctf_collab_rest_kernel<DBG, true, FMT_BC1>;
