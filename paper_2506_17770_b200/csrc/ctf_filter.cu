@@ -2837,6 +2837,10 @@ static cudaError_t launch_rest(const KArgs &k, const typename WeightsOf<FMT>::ty
         if (dyn > 0 && (e = mlp_smem_setup(rest, dyn, dev)) != cudaSuccess) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rest, kWarps * 32, dyn);
         if (e != cudaSuccess) return e;
+#ifndef CTF_THIRD_PER_SM
+#define CTF_THIRD_PER_SM 3  // BC1 third kernel (runs alongside the wide-window kernel): CTAs per SM at most
+#endif
+        if (conc && pass == 1 && per_sm > CTF_THIRD_PER_SM) per_sm = CTF_THIRD_PER_SM;
         long long g2 = (long long)sms * (per_sm > 0 ? per_sm : 1);
         if (g2 * kWarps > groups) g2 = (groups + kWarps - 1) / kWarps;
         // programmatic dependent launch: this pass is launched while the previous kernel runs and
