@@ -251,9 +251,10 @@ size_t ctf_filter_workspace_bytes(int32_t Wf, int32_t Hf, int32_t frames);
  * CTF_LAUNCH_SEPARATE_PASSES when ctf_params.flags has CTF_FLAG_SEPARATE_PASSES;
  * CTF_LAUNCH_WORKSPACE (a workspace in ctf_params) does not change the count.  The COLLAB /
  * BOX / MASK bilinear path is, for BC1, ONE fused kernel when a pass covers at most 131072
- * waves (and separate passes are not requested), else three (the lean exact kernel; the
- * wide-window kernel over the waves it leaves; the general path over AABBs wider than 32x32
- * texels, plus an 8-byte cudaMemsetAsync of the work-list counters with a workspace, not
+ * waves (and separate passes are not requested), else three (the lean exact kernel; then,
+ * side by side, the third kernel over the waves it leaves with AABBs wider than 32x32 texels
+ * — 64x64 bitmap windows, the sort-based general path beyond — and the wide-window kernel over
+ * the others; plus an 8-byte cudaMemsetAsync of the work-list counters with a workspace, not
  * counted); two for the latent MLP (lean exact kernel + general path); every other path is
  * one.  Returns -1 for an invalid format / mode / filter / size.
  */
