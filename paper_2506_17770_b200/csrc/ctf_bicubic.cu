@@ -100,8 +100,11 @@ __device__ __forceinline__ void merge_axis(const float (&w)[4], const int (&idx)
     }
 }
 
-// fx = fma(clamp(u), W, -0.5) -> (x0, s); shared with the C+ spare-lane recomputation
-__device__ __forceinline__ Foot16 footprint16(int filter, int x0, int y0, float s, float t, int W, int H) {
+// fx = fma(clamp(u), W, -0.5) -> (x0, s); shared with the C+ spare-lane recomputation.
+// interior (warp-uniform: every lane's 4 x 4 taps inside the texture): no clamp duplicates,
+// merged weight c = 0 + w_c (the bits merge_axis adds)
+__device__ __forceinline__ Foot16 footprint16(int filter, int x0, int y0, float s, float t, int W, int H,
+                                              bool interior = false) {
     Foot16 f;
     cubic_weights(filter, s, f.wx);
     cubic_weights(filter, t, f.wy);
@@ -115,8 +118,16 @@ __device__ __forceinline__ Foot16 footprint16(int filter, int x0, int y0, float 
         f.cx[i] = min(max(x0 - 1 + i, 0), W - 1) - f.xa;
         f.ry[i] = min(max(y0 - 1 + i, 0), H - 1) - f.ya;
     }
-    merge_axis(f.wx, f.cx, f.mx);
-    merge_axis(f.wy, f.ry, f.my);
+    if (interior) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            f.mx[i] = __fadd_rn(0.0f, f.wx[i]);
+            f.my[i] = __fadd_rn(0.0f, f.wy[i]);
+        }
+    } else {
+        merge_axis(f.wx, f.cx, f.mx);
+        merge_axis(f.wy, f.ry, f.my);
+    }
     return f;
 }
 
@@ -167,12 +178,19 @@ __device__ __forceinline__ int eq2_rank(int j, int np, int na) {  // Eq. 2 (P:50
     return (2 * (na - 1) * (j - np) + (na - 1 - np)) / (2 * (na - 1 - np));
 }
 
-template <int FMT>
+// MODE (4TAP / STF / COLLAB), the filter and Box sampling are compile-time (one instantiation
+// each): the exact collaborative path compiles to straight-line code
+template <int FMT, int MODE, int FILT, bool BOX>
 __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
-    ctf_bicubic_kernel(const BArgs a, const typename WeightsOf<FMT>::type mw, const int MODE) {
+    ctf_bicubic_kernel(const BArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ BSmem smem[kBWarps];
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
     BSmem &s = smem[warp];
+    // finite values in every exchange slot: the exact gather reads cells beyond a lane's
+    // clamped footprint with weight 0 (no select)
+    s.xch[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s.xch[lane + 32] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned lt = lanemask_lt();
     const int W = a.tex.W, H = a.tex.H;
@@ -224,7 +242,8 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
             const float flx = floorf(fx), fly = floorf(fy);
             const int x0 = (int)flx, y0 = (int)fly;
             const float fs = __fsub_rn(fx, flx), ft = __fsub_rn(fy, fly);
-            const Foot16 f = footprint16(a.filter, x0, y0, fs, ft, W, H);
+            const bool interior = __all_sync(FULL, !active || (x0 >= 1 && x0 + 2 <= W - 1 && y0 >= 1 && y0 + 2 <= H - 1));
+            const Foot16 f = footprint16(FILT, x0, y0, fs, ft, W, H, interior);
             __syncwarp();
 
             float4 color = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -331,20 +350,21 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                         const uint32_t b = __shfl_sync(FULL, base, (cy + r) & 31);
                         const uint32_t word = s.bm[(cy + r) & 31];
                         rr[r] = (int)b + __popc(word & ((1u << cx) - 1u));
-                        // the first setter of each texel publishes rank -> id (ranks < E*a + 1 matter)
-                        const uint32_t fresh = active && r < f.nr ? (pat & ~old[r]) : 0u;
+                        // the first setter of each texel publishes rank -> (y << 16) | x (ranks < E*a + 1
+                        // matter; the packed coordinates order like ids, W, H <= 2^16)
+                        const uint32_t fresh = active && r < f.nr ? ((pat & ~old[r]) >> cx) : 0u;
+                        const uint32_t yy = (uint32_t)(f.ya + r) << 16;
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             const int rank = rr[r] + c;
-                            if (((fresh >> (cx + c)) & 1u) && rank < 72)
-                                s.tbl[rank] = (uint32_t)(f.ya + r) * (uint32_t)W + (uint32_t)(f.xa + c);
+                            if (((fresh >> c) & 1u) && rank < 72) s.tbl[rank] = yy | (uint32_t)(f.xa + c);
                         }
                     }
                     count = nx < limit ? nx : limit;
                 } else {
                     // wider than the bitmap: peel, one redux.sync.min per distinct texel
                     int r = 0, cc = 0;
-                    uint32_t cur = active ? (uint32_t)f.ya * (uint32_t)W + (uint32_t)f.xa : INVALID_ID;
+                    uint32_t cur = active ? ((uint32_t)f.ya << 16) | (uint32_t)f.xa : INVALID_ID;
                     while (count < limit) {
                         const uint32_t m = __reduce_min_sync(FULL, cur);
                         if (m == INVALID_ID) break;
@@ -357,7 +377,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                                 rr[3] = r == 3 ? count : rr[3];
                             }
                             if (++cc == f.nc) { cc = 0; ++r; }
-                            cur = (r < f.nr) ? (uint32_t)(f.ya + r) * (uint32_t)W + (uint32_t)(f.xa + cc) : INVALID_ID;
+                            cur = (r < f.nr) ? ((uint32_t)(f.ya + r) << 16) | (uint32_t)(f.xa + cc) : INVALID_ID;
                         }
                         ++count;
                     }
@@ -365,7 +385,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                 n = count;  // exact when <= E*a, else saturated at E*a + 1 (R-28)
                 // ---- a4: decide
                 bool ok;
-                if (a.variant == BVAR_BOX) ok = bw * bh <= E * na;
+                if (BOX) ok = bw * bh <= E * na;
                 else if (a.variant == BVAR_MASK16) ok = bw <= 16 && bh <= 16 && n <= E * na;
                 else if (a.variant == BVAR_MASK11) ok = bw <= 11 && bh <= 11 && n <= E * na;
                 else ok = n <= E * na;
@@ -374,7 +394,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                 if (ok) {
                     // ---- a5: produce (<= E per lane): rank i on lane h(i mod a, A), slot i div a;
                     // the value goes to the shared table by rank (fp32, converted once)
-                    const bool box = a.variant == BVAR_BOX;
+                    constexpr bool box = BOX;
                     const int total = box ? bw * bh : n;
 #pragma unroll 1
                     for (int slot = 0; slot < 2; ++slot) {
@@ -386,9 +406,9 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                                 ty = (uint32_t)(miny + i / bw);
                                 tx = (uint32_t)(minx + i % bw);
                             } else {
-                                const uint32_t id = s.tbl[i];
-                                ty = id / (uint32_t)W;
-                                tx = id - ty * (uint32_t)W;
+                                const uint32_t e = s.tbl[i];
+                                ty = e >> 16;
+                                tx = e & 0xFFFFu;
                             }
                             s.xch[i] = produce(a.tex, mw, tx, ty).to_f4();
                         }
@@ -399,12 +419,14 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
                         const int rq = q >> 2, cq = q & 3;
-                        const bool valid = active && rq < f.nr && cq < f.nc;
                         int rank;
                         if (box) rank = (f.ya + rq - miny) * bw + (f.xa + cq - minx);
-                        else rank = (rq == 0 ? rr[0] : rq == 1 ? rr[1] : rq == 2 ? rr[2] : rr[3]) + cq;
-                        const float4 v = valid ? s.xch[rank & 63] : make_float4(0.f, 0.f, 0.f, 0.f);
-                        acc.add(__fmul_rn(sel4(f.mx, cq), sel4(f.my, rq)), v);
+                        else rank = rr[rq] + cq;
+                        // a cell beyond the lane's clamped footprint (cq >= nc or rq >= nr) has merged
+                        // weight 0 and reads a finite slot: fma(v, 0, acc) = acc, as the full filter's
+                        // zero texel
+                        const float4 v = s.xch[rank & 63];
+                        acc.add(__fmul_rn(f.mx[cq], f.my[rq]), v);
                     }
                     color = acc.get();
                     evals = total;
@@ -453,7 +475,7 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                         const int gx0 = __shfl_sync(FULL, x0, l), gy0 = __shfl_sync(FULL, y0, l);
                         const float gs = __shfl_sync(FULL, fs, l), gt = __shfl_sync(FULL, ft, l);
                         if (spare) {
-                            const Foot16 g = footprint16(a.filter, gx0, gy0, gs, gt, W, H);
+                            const Foot16 g = footprint16(FILT, gx0, gy0, gs, gt, W, H);
                             float wsum = 0.0f;
                             float cw[16];
                             uint32_t cid[16];
@@ -550,9 +572,24 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
     }
 }
 
+template <int FMT, int MODE>
+static auto bicubic_kernel_for(int filt, bool box) {
+    if constexpr (MODE == MODE_COLLAB)
+        return filt == FILT_BSPLINE ? (box ? ctf_bicubic_kernel<FMT, MODE, FILT_BSPLINE, true>
+                                           : ctf_bicubic_kernel<FMT, MODE, FILT_BSPLINE, false>)
+                                    : (box ? ctf_bicubic_kernel<FMT, MODE, FILT_CATMULL_ROM, true>
+                                           : ctf_bicubic_kernel<FMT, MODE, FILT_CATMULL_ROM, false>);
+    else
+        return filt == FILT_BSPLINE ? ctf_bicubic_kernel<FMT, MODE, FILT_BSPLINE, false>
+                                    : ctf_bicubic_kernel<FMT, MODE, FILT_CATMULL_ROM, false>;
+}
+
 template <int FMT>
 cudaError_t launch_bicubic(BArgs k, const typename WeightsOf<FMT>::type &mw, int mode, cudaStream_t stream) {
-    auto kern = ctf_bicubic_kernel<FMT>;
+    const bool box = k.variant == BVAR_BOX;
+    auto kern = mode == MODE_4TAP ? bicubic_kernel_for<FMT, MODE_4TAP>(k.filter, box)
+              : mode == MODE_STF  ? bicubic_kernel_for<FMT, MODE_STF>(k.filter, box)
+                                  : bicubic_kernel_for<FMT, MODE_COLLAB>(k.filter, box);
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -566,7 +603,7 @@ cudaError_t launch_bicubic(BArgs k, const typename WeightsOf<FMT>::type &mw, int
     k.ipw = (unsigned)ipw;
     long long grid = ((long long)k.nchunks + ipw * kBWarps - 1) / (ipw * kBWarps);
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kBWarps * 32, 0, stream>>>(k, mw, mode <= MODE_STF ? mode : MODE_COLLAB);
+    kern<<<(unsigned)grid, kBWarps * 32, 0, stream>>>(k, mw);
     return cudaGetLastError();
 }
 

@@ -2,7 +2,7 @@
 (waves = F x 540 x 480, the 4K camera-path batch of scripts/time_libs.py)."""
 import csv, sys
 lib, F = sys.argv[1], int(sys.argv[2])
-waves = F * 540 * 480
+waves = F * 540 * 480  # (4K frames)
 rows = [r for r in csv.reader(sys.stdin) if len(r) > 10]
 hdr = rows[0]
 ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")

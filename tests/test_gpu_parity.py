@@ -519,8 +519,15 @@ def test_big_window_waves(ctf, jac):
     for mode, fb, fl in MODES:
         o = run_oracle(tex, uv, g, mode, fb, fl, seed=9)
         assert_parity(run_gpu(ctf, tex, uv, g, mode, fb, fl, seed=9), o, f"jac={jac} mode={mode} fb={fb} fl={fl}")
-        dt = to_dev_tex(ctf, tex)
-        out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, fl, 9, 0)
-        torch.cuda.synchronize()
-        np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
-        assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
+        if mode == 3:
+            assert_parity(run_gpu(ctf, tex, uv, g, mode, fb, fl | ctf.FLAG_SEPARATE_PASSES, seed=9), o,
+                          f"separate jac={jac} fb={fb} fl={fl}")
+        # the single fused launch (small call) and the separate passes (lean kernel, then the
+        # third and the wide-window kernels side by side, AABB-routed work lists)
+        for sep in (0, ctf.FLAG_SEPARATE_PASSES):
+            dt = to_dev_tex(ctf, tex)
+            out, rec = ctf.filter_frame(dt, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb,
+                                        fl | sep, 9, 0)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+            assert np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max() <= ATOL
