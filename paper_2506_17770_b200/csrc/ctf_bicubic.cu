@@ -113,18 +113,20 @@ __device__ __forceinline__ Foot16 footprint16(int filter, int x0, int y0, float 
     const int xb = min(max(x0 + 2, 0), W - 1), yb = min(max(y0 + 2, 0), H - 1);
     f.nc = xb - f.xa + 1;
     f.nr = yb - f.ya + 1;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        f.cx[i] = min(max(x0 - 1 + i, 0), W - 1) - f.xa;
-        f.ry[i] = min(max(y0 - 1 + i, 0), H - 1) - f.ya;
-    }
     if (interior) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+            f.cx[i] = i;
+            f.ry[i] = i;
             f.mx[i] = __fadd_rn(0.0f, f.wx[i]);
             f.my[i] = __fadd_rn(0.0f, f.wy[i]);
         }
     } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            f.cx[i] = min(max(x0 - 1 + i, 0), W - 1) - f.xa;
+            f.ry[i] = min(max(y0 - 1 + i, 0), H - 1) - f.ya;
+        }
         merge_axis(f.wx, f.cx, f.mx);
         merge_axis(f.wy, f.ry, f.my);
     }
@@ -181,7 +183,10 @@ __device__ __forceinline__ int eq2_rank(int j, int np, int na) {  // Eq. 2 (P:50
 // MODE (4TAP / STF / COLLAB), the filter and Box sampling are compile-time (one instantiation
 // each): the exact collaborative path compiles to straight-line code
 template <int FMT, int MODE, int FILT, bool BOX>
-__global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
+#ifndef CTF_BIC_MINB
+#define CTF_BIC_MINB 4  // BC1 bicubic kernel: resident CTAs per SM (64 registers; 3: 76 registers, -9 %)
+#endif
+__global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 1)
     ctf_bicubic_kernel(const BArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ BSmem smem[kBWarps];
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)
@@ -338,12 +343,13 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? 3 : 1)
                     __syncwarp();
                     const uint32_t cnt = __popc(s.bm[lane]);
                     const int nx = (int)__reduce_add_sync(FULL, cnt);
-                    uint32_t base = cnt;   // inclusive scan of the row counts
+                    uint32_t base = cnt;   // inclusive scan of the row counts (shfl.up's in-range
+                                           // predicate guards the add: two instructions per step)
 #pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const uint32_t u = __shfl_up_sync(FULL, base, d);
-                        base += lane >= (unsigned)d ? u : 0u;
-                    }
+                    for (int d = 1; d < 32; d <<= 1)
+                        asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 u;\n\t"
+                                     "shfl.sync.up.b32 u|p, %0, %1, 0, 0xffffffff;\n\t@p add.u32 %0, %0, u;\n\t}"
+                                     : "+r"(base) : "r"(d));
                     base -= cnt;
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
