@@ -52,7 +52,7 @@ struct BArgs {
 };
 
 struct BSmem {
-    uint32_t tbl[72];         // exact: rank -> texel id (<= 2*32 + 1); C+: sorted planned ids
+    uint32_t tbl[128];        // exact: rank -> (y << 16) | x (ranks >= 124 clamped: unused); C+: sorted planned ids
     uint32_t sorted[32];      // fallback gather: sorted (id << 5 | lane) of produced texels
     uint32_t bm[32];          // collect: AABB bitmap, one word per row
     float4 xch[64];           // exact: rank -> produced value (fp32)
@@ -336,10 +336,9 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 
                     __syncwarp();
                     const int cx = (f.xa - minx) & 31, cy = (f.ya - miny) & 31;
                     const uint32_t pat = ((1u << f.nc) - 1u) << cx;
-                    uint32_t old[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
-                        if (active && r < f.nr) old[r] = atomicOr(&s.bm[(cy + r) & 31], pat);
+                        if (active && r < f.nr) atomicOr(&s.bm[(cy + r) & 31], pat);
                     __syncwarp();
                     const uint32_t cnt = __popc(s.bm[lane]);
                     const int nx = (int)__reduce_add_sync(FULL, cnt);
@@ -356,15 +355,15 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 
                         const uint32_t b = __shfl_sync(FULL, base, (cy + r) & 31);
                         const uint32_t word = s.bm[(cy + r) & 31];
                         rr[r] = (int)b + __popc(word & ((1u << cx) - 1u));
-                        // the first setter of each texel publishes rank -> (y << 16) | x (ranks < E*a + 1
-                        // matter; the packed coordinates order like ids, W, H <= 2^16)
-                        const uint32_t fresh = active && r < f.nr ? ((pat & ~old[r]) >> cx) : 0u;
-                        const uint32_t yy = (uint32_t)(f.ya + r) << 16;
+                        // every lane publishes rank -> (y << 16) | x for each of its cells: a texel's rank
+                        // and value do not depend on the lane, so lanes sharing a texel store the same
+                        // word (ranks < E*a + 1 matter; the packed coordinates order like ids, W, H <=
+                        // 2^16; a row starting at rank >= 124 only occurs in fallback waves, clamped)
+                        const int rb = rr[r] < 124 ? rr[r] : 124;
+                        const uint32_t v0 = ((uint32_t)(f.ya + r) << 16) | (uint32_t)f.xa;
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const int rank = rr[r] + c;
-                            if (((fresh >> c) & 1u) && rank < 72) s.tbl[rank] = yy | (uint32_t)(f.xa + c);
-                        }
+                        for (int c = 0; c < 4; ++c)
+                            if (active && r < f.nr && c < f.nc) s.tbl[rb + c] = v0 + (uint32_t)c;
                     }
                     count = nx < limit ? nx : limit;
                 } else {
