@@ -358,12 +358,11 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 
                         // every lane publishes rank -> (y << 16) | x for each of its cells: a texel's rank
                         // and value do not depend on the lane, so lanes sharing a texel store the same
                         // word (ranks < E*a + 1 matter; the packed coordinates order like ids, W, H <=
-                        // 2^16; a row starting at rank >= 124 only occurs in fallback waves, clamped)
-                        const int rb = rr[r] < 124 ? rr[r] : 124;
+                        // 2^16; a row starting at rank >= 124 only occurs in fallback waves, skipped)
                         const uint32_t v0 = ((uint32_t)(f.ya + r) << 16) | (uint32_t)f.xa;
 #pragma unroll
                         for (int c = 0; c < 4; ++c)
-                            if (active && r < f.nr && c < f.nc) s.tbl[rb + c] = v0 + (uint32_t)c;
+                            if (active && r < f.nr && c < f.nc && rr[r] < 124) s.tbl[rr[r] + c] = v0 + (uint32_t)c;
                     }
                     count = nx < limit ? nx : limit;
                 } else {

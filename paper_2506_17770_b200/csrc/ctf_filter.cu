@@ -1776,11 +1776,12 @@ __device__ __forceinline__ void pair_back(const KArgs &a, const SM &fs, const Pa
 // with two shared atomics (ATOMS.OR, one per footprint row) — the cost does not grow with
 // the AABB (no 128-key sort).  The canonical ascending-id order (R-5) is row-major over the
 // window, so a texel's rank is an exclusive scan of the rows' popcounts plus a popc within
-// its row; the atomic's old value tells each lane whether it set a bit first, so every
-// texel has exactly one owner that publishes it.  Bitmaps: U (the needed set: n and the
-// exact ranks), P (the C+ plan), D (the produced set the fallbacks gather from: each
-// producing lane stores its value in its own slot, the first setter of a texel publishes its
-// lane in a position -> lane table).  Records, producers, selections and colours equal the general path
+// its row; a texel's rank and position do not depend on the lane that holds it, so every
+// lane publishes its own texels (lanes sharing one store the same value; the atomics need no
+// return value).  Bitmaps: U (the needed set: n and the exact ranks), P (the C+ plan), D (the
+// produced set the fallbacks gather from: each producing lane stores its value in its own
+// slot, the first producer of a texel — the D atomic's old value — its lane in a position ->
+// lane table).  Records, producers, selections and colours equal the general path
 // bit for bit (same fp32 operations in the same order).
 // ROWS = 32 (lane l holds row l in the row scans; taller AABBs take the general path) or 64
 // (lane l holds rows 2l and 2l + 1; CTF_REST_ROWS=64 builds the wide-window kernel that way).
@@ -1942,24 +1943,20 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS, COL
     bm_zero<ROWS, CW>(ws.bmD, lane);
     if (active) ws.act[ar] = (uint8_t)lane;
     __syncwarp();
-    // ---- a3: the needed set U (every corner, zero weights included, R-4); firstU bit k: this
-    // lane set corner k's bit first (its duplicates within the lane see their own earlier bit)
-    unsigned firstU = 0u;
+    // ---- a3: the needed set U (every corner, zero weights included, R-4); no-return atomics:
+    // the tables below are published by every lane that holds a texel (its rank and position do
+    // not depend on the lane, so those lanes store the same value)
     if (active) {
         if constexpr (CW == 1) {
             const uint32_t pat = (1u << cx0) | (1u << cx1);
-            const uint32_t oU0 = atomicOr(&ws.bmU[cy0], pat);
-            const uint32_t oU1 = atomicOr(&ws.bmU[cy1], pat);
-            const bool dx = cx1 != cx0;
-            firstU = (((oU0 >> cx0) & 1u) ? 0u : 1u) | ((dx && !((oU0 >> cx1) & 1u)) ? 2u : 0u) |
-                     (((oU1 >> cx0) & 1u) ? 0u : 4u) | ((dx && !((oU1 >> cx1) & 1u)) ? 8u : 0u);
+            atomicOr(&ws.bmU[cy0], pat);
+            atomicOr(&ws.bmU[cy1], pat);
         } else {
             const int cx[2] = {cx0, cx1}, cy[2] = {cy0, cy1};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int c = cx[k & 1];
-                const uint32_t old = atomicOr(&ws.bmU[win_word<CW>(cy[k >> 1], c)], 1u << (c & 31));
-                firstU |= ((old >> (c & 31)) & 1u) ? 0u : (1u << k);
+                atomicOr(&ws.bmU[win_word<CW>(cy[k >> 1], c)], 1u << (c & 31));
             }
         }
     }
@@ -1981,18 +1978,18 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS, COL
         bool produced;
         int qx, qy, evals;
         if (a.variant != VAR_BOX) {
-            // ranks of the four corners; each texel's first setter publishes rank -> position
+            // ranks of the four corners; every lane publishes its corners' rank -> position
             row_scan_ranks(rsU, lane);
             const uint32_t b0 = row_base(rsU, cy0), b1 = row_base(rsU, cy1);
             rho[0] = win_rank<CW>(ws.bmU, b0, cy0, cx0);
             rho[1] = win_rank<CW>(ws.bmU, b0, cy0, cx1);
             rho[2] = win_rank<CW>(ws.bmU, b1, cy1, cx0);
             rho[3] = win_rank<CW>(ws.bmU, b1, cy1, cx1);
-            if (active) {
-                if (firstU & 1u) ws.tbl[rho[0]] = (uint16_t)((cy0 << LGC) | cx0);
-                if (firstU & 2u) ws.tbl[rho[1]] = (uint16_t)((cy0 << LGC) | cx1);
-                if (firstU & 4u) ws.tbl[rho[2]] = (uint16_t)((cy1 << LGC) | cx0);
-                if (firstU & 8u) ws.tbl[rho[3]] = (uint16_t)((cy1 << LGC) | cx1);
+            if (active) {   // rank -> position (every lane holding the texel stores the same value)
+                ws.tbl[rho[0]] = (uint16_t)((cy0 << LGC) | cx0);
+                ws.tbl[rho[1]] = (uint16_t)((cy0 << LGC) | cx1);
+                ws.tbl[rho[2]] = (uint16_t)((cy1 << LGC) | cx0);
+                ws.tbl[rho[3]] = (uint16_t)((cy1 << LGC) | cx1);
             }
             __syncwarp();
             // ---- a5: active rank r < n produces U[r] (lane h(r, A))
@@ -2047,9 +2044,7 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS, COL
     const unsigned C = contrib_bits(f, m);
     if (fb == FB_CPLUS) {
         // (1) the planned set P: STF texels deduplicated, ranked ascending (R-17)
-        uint32_t oP = 0u;
-        if (active) oP = atomicOr(&ws.bmP[win_word<CW>(qcy, qcx)], 1u << (qcx & 31));
-        const bool firstP = active && !((oP >> (qcx & 31)) & 1u);
+        if (active) atomicOr(&ws.bmP[win_word<CW>(qcy, qcx)], 1u << (qcx & 31));
         // publish this lane's distinct corners (merged weights, R-14) for the spare lanes
         ws.mw[lane] = make_float4(m.dw[0], m.dw[1], m.dw[2], m.dw[3]);
         ws.fpos[lane] = (uint32_t)cx0 | ((uint32_t)cx1 << 6) | ((uint32_t)cy0 << 12) | ((uint32_t)cy1 << 18) | (C << 24);
@@ -2057,7 +2052,7 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS, COL
         const RowScan<ROWS, CW> rsP = row_scan<ROWS, CW>(ws.bmP, lane);
         const int np = (int)rsP.tot;
         const uint32_t bq = row_base(rsP, qcy);
-        if (firstP) ws.tbl[win_rank<CW>(ws.bmP, bq, qcy, qcx)] = (uint16_t)((qcy << LGC) | qcx);
+        if (active) ws.tbl[win_rank<CW>(ws.bmP, bq, qcy, qcx)] = (uint16_t)((qcy << LGC) | qcx);   // same value per texel
         __syncwarp();
         produced = false;
         if (active) {
@@ -2121,6 +2116,7 @@ __device__ __forceinline__ LeanOut wide_wave(const KArgs &a, WideSmemT<ROWS, COL
     uint32_t oD = 0u;
     if (produced) oD = atomicOr(&ws.bmD[pq >> 5], 1u << (pq & 31));
     if (produced) ws.xch[lane] = val;
+    // the first producer of each texel publishes its lane (one writer per position)
     if (produced && !((oD >> (pq & 31)) & 1u)) ws.lop[pq] = (uint8_t)lane;
     __syncwarp();
     unsigned IN;
