@@ -186,7 +186,10 @@ template <int FMT, int MODE, int FILT, bool BOX>
 #ifndef CTF_BIC_MINB
 #define CTF_BIC_MINB 4  // BC1 bicubic kernel: resident CTAs per SM (64 registers; 3: 76 registers, -9 %)
 #endif
-__global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 1)
+#ifndef CTF_BIC_MLP_MINB
+#define CTF_BIC_MLP_MINB 4  // latent-MLP bicubic kernel: resident CTAs per SM (64 registers, small spills: 2.15x over 1 CTA / 167 registers)
+#endif
+__global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : CTF_BIC_MLP_MINB)
     ctf_bicubic_kernel(const BArgs a, const typename WeightsOf<FMT>::type mw) {
     __shared__ BSmem smem[kBWarps];
     const unsigned lane = lane_id(), warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);   // provably warp-uniform (no divergence guards)

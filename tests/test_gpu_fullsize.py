@@ -125,3 +125,22 @@ def test_config5_batch_as_benchmarked(ctf):
         o1, r1 = ctf.filter_frame(tex, uv[f], g[f], 3, 3, 0, 7, f, debug=d)
         check_all(tnp, uv[f].cpu().numpy(), g[f].cpu().numpy(), o1.cpu().numpy(), r1.cpu().numpy().view(np.uint32),
                   3, 3, 7, f, dbg=_host(d))
+
+
+@pytest.mark.parametrize("filt,mode,fb,E", [(2, 3, 3, 2), (2, 3, 3, 1), (1, 3, 3, 2), (2, 4, 3, 2), (2, 1, 0, 1)])
+def test_config6_4k_bicubic(ctf, filt, mode, fb, E):
+    """The bench's bicubic entries (config 6: the 4K perspective plane of config 3, BC1 4096^2):
+    Catmull-Rom / B-spline, List and Box with C+, E = 1 / 2, and the positivized STF — every
+    wave against the oracle (records bitwise, colours <= 1e-5)."""
+    import oracle
+    W = 4096
+    blocks = synthetic.bc1_texture(W, W, 0, "image")
+    uv, g = synthetic.perspective_plane(3840, 2160, W, W, synthetic.PLANE_C2)
+    tex = ctf.Texture.bc1(blocks, W, W)
+    out, rec = ctf.filter_frame(tex, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), mode, fb, 0, 7, 0,
+                                filter=filt, max_evals=E)
+    o = oracle.filter_frame({"format": 1, "width": W, "height": W, "bc1": blocks}, uv, g, mode, fb, 0, 7, 0,
+                            filter=filt, max_evals=E)
+    np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+    err = float(np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max())
+    assert err <= ATOL, err
