@@ -31,6 +31,8 @@
 namespace ctf {
 namespace {
 
+#include "ctf_mlp_tc.cuh"
+
 constexpr int kBWarps = 8;
 constexpr int kBChunk = 16;  // waves per work item (a run in one wave-row)
 enum { FILT_BSPLINE = 1, FILT_CATMULL_ROM = 2 };
@@ -199,6 +201,18 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 
     s.xch[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     s.xch[lane + 32] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
+    // latent MLP, collaborative: the texels a wave produces are decoded together on the tensor
+    // cores (mlp_decode_tc, rows = lanes, R-29), the weights staged once per CTA
+    constexpr bool TC = FMT == FMT_MLP && MODE == MODE_COLLAB;
+    extern __shared__ __align__(16) unsigned char bic_dyn[];
+    TcWeights *tw = nullptr;
+    TcScratch *tsc = nullptr;
+    if constexpr (TC) {
+        tw = reinterpret_cast<TcWeights *>(bic_dyn);
+        tsc = &reinterpret_cast<TcScratch *>(bic_dyn + sizeof(TcWeights))[warp];
+        fill_tc_weights(mw, *tw);
+        __syncthreads();
+    }
     const int lx = (int)(lane & 7), ly = (int)(lane >> 3);
     const unsigned lt = lanemask_lt();
     const int W = a.tex.W, H = a.tex.H;
@@ -407,8 +421,9 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 
                     for (int slot = 0; slot < 2; ++slot) {
                         if (slot * na >= total) break;
                         const int i = ar + slot * na;
-                        if (active && i < total) {
-                            uint32_t tx, ty;
+                        const bool valid = active && i < total;
+                        uint32_t tx = (uint32_t)minx, ty = (uint32_t)miny;
+                        if (valid) {
                             if (box) {
                                 ty = (uint32_t)(miny + i / bw);
                                 tx = (uint32_t)(minx + i % bw);
@@ -417,7 +432,12 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 
                                 ty = e >> 16;
                                 tx = e & 0xFFFFu;
                             }
-                            s.xch[i] = produce(a.tex, mw, tx, ty).to_f4();
+                        }
+                        if constexpr (TC) {
+                            const float4 v = mlp_decode_tc(a.tex, *tw, *tsc, valid, (int)tx, (int)ty, lane);
+                            if (valid) s.xch[i] = v;
+                        } else {
+                            if (valid) s.xch[i] = produce(a.tex, mw, tx, ty).to_f4();
                         }
                     }
                     __syncwarp();
@@ -517,14 +537,22 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 
                         __syncwarp();
                     }
                     // produce (one site), then every lane gathers the wave's produced set
-                    Texel<FMT> val = Texel<FMT>::zero();
-                    if (prod != INVALID_ID) {
-                        const uint32_t ty = prod / (uint32_t)W;
-                        val = produce(a.tex, mw, prod - ty * (uint32_t)W, ty);
+                    float4 valf;
+                    {
+                        const uint32_t ty = prod != INVALID_ID ? prod / (uint32_t)W : 0u;
+                        const uint32_t tx = prod != INVALID_ID ? prod - ty * (uint32_t)W : 0u;
+                        if constexpr (TC) {
+                            valf = mlp_decode_tc(a.tex, *tw, *tsc, prod != INVALID_ID, (int)tx, (int)ty, lane);
+                            if (prod == INVALID_ID) valf = make_float4(0.f, 0.f, 0.f, 0.f);
+                        } else {
+                            Texel<FMT> val = Texel<FMT>::zero();
+                            if (prod != INVALID_ID) val = produce(a.tex, mw, tx, ty);
+                            valf = val.to_f4();
+                        }
                     }
                     evals = (run_fb == FB_CPLUS) ? __popc(__ballot_sync(FULL, prod != INVALID_ID)) : na;
                     s.sorted[lane] = warp_sort32(prod != INVALID_ID ? ((prod << 5) | lane) : INVALID_ID);
-                    s.xch[lane] = val.to_f4();   // this lane's produced value (fp32), read by lane index
+                    s.xch[lane] = valf;   // this lane's produced value (fp32), read by lane index
                     __syncwarp();
                     // Eq. 1 over the known cells (R-23 evaluation order, R-28)
                     bool all_known = true;
@@ -602,7 +630,12 @@ cudaError_t launch_bicubic(BArgs k, const typename WeightsOf<FMT>::type &mw, int
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBWarps * 32, 0);
+    // latent MLP, collaborative: the tensor-core decoder's weights (per CTA) and scratch (per warp)
+    const size_t dyn = (FMT == FMT_MLP && mode != MODE_4TAP && mode != MODE_STF)
+                           ? sizeof(TcWeights) + kBWarps * sizeof(TcScratch) : 0;
+    if (dyn > 0 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn)) != cudaSuccess)
+        return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBWarps * 32, dyn);
     if (e != cudaSuccess) return e;
     const long long slots = (long long)sms * (per_sm > 0 ? per_sm : 1);
     long long ipw = ((long long)k.nchunks + slots * kBWarps * 4 - 1) / (slots * kBWarps * 4);
@@ -610,7 +643,7 @@ cudaError_t launch_bicubic(BArgs k, const typename WeightsOf<FMT>::type &mw, int
     k.ipw = (unsigned)ipw;
     long long grid = ((long long)k.nchunks + ipw * kBWarps - 1) / (ipw * kBWarps);
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kBWarps * 32, 0, stream>>>(k, mw);
+    kern<<<(unsigned)grid, kBWarps * 32, dyn, stream>>>(k, mw);
     return cudaGetLastError();
 }
 

@@ -144,3 +144,20 @@ def test_config6_4k_bicubic(ctf, filt, mode, fb, E):
     np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
     err = float(np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max())
     assert err <= ATOL, err
+
+
+def test_config6_4k_bicubic_latent_mlp(ctf):
+    """The bench's latent-MLP bicubic entry (Catmull-Rom, List C+, E = 2; the texels each wave
+    produces decoded together on the tensor cores, R-29): every wave against the oracle."""
+    import oracle
+    W = 4096
+    lat, mlp = synthetic.latent_texture(W, W, 7), synthetic.mlp_weights(8)
+    uv, g = synthetic.perspective_plane(3840, 2160, W, W, synthetic.PLANE_C2)
+    tex = ctf.Texture.latent_mlp(lat, mlp, W, W)
+    out, rec = ctf.filter_frame(tex, torch.from_numpy(uv).cuda(), torch.from_numpy(g).cuda(), 3, 3, 0, 7, 0,
+                                filter=2, max_evals=2)
+    o = oracle.filter_frame({"format": 2, "width": W, "height": W, "latent": lat, "mlp": mlp}, uv, g, 3, 3, 0, 7, 0,
+                            filter=2, max_evals=2)
+    np.testing.assert_array_equal(rec.cpu().numpy().view(np.uint32), o["rec"])
+    err = float(np.abs(out.cpu().numpy().astype(np.float64) - o["out"]).max())
+    assert err <= ATOL, err
