@@ -377,9 +377,19 @@ __global__ void __launch_bounds__(kBWarps * 32, FMT == FMT_BC1 ? CTF_BIC_MINB : 
                         // word (ranks < E*a + 1 matter; the packed coordinates order like ids, W, H <=
                         // 2^16; a row starting at rank >= 124 only occurs in fallback waves, skipped)
                         const uint32_t v0 = ((uint32_t)(f.ya + r) << 16) | (uint32_t)f.xa;
+                        if (interior) {   // 4 x 4 cells: one predicate per row, 4 stores off one address
+                            if (active && rr[r] < 124) {
+                                uint32_t *t = s.tbl + rr[r];
+                                t[0] = v0;
+                                t[1] = v0 + 1u;
+                                t[2] = v0 + 2u;
+                                t[3] = v0 + 3u;
+                            }
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (active && r < f.nr && c < f.nc && rr[r] < 124) s.tbl[rr[r] + c] = v0 + (uint32_t)c;
+                            for (int c = 0; c < 4; ++c)
+                                if (active && r < f.nr && c < f.nc && rr[r] < 124) s.tbl[rr[r] + c] = v0 + (uint32_t)c;
+                        }
                     }
                     count = nx < limit ? nx : limit;
                 } else {
