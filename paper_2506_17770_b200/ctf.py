@@ -187,6 +187,43 @@ def _call_workspace(tex, mode, filt, wf, hf, frames, device, workspace, stream):
     return ws
 
 
+_U32_DTYPES = tuple(d for d in (torch.int32, getattr(torch, "uint32", None)) if d is not None)
+
+
+def check_buffers(uv4: torch.Tensor, grad: torch.Tensor | None, out: torch.Tensor, rec: torch.Tensor | None,
+                  debug: dict | None = None):
+    """Validate the caller's buffers against the geometry uv4 = [F][Hf][Wf][2] before the C call.
+
+    The C ABI takes plain pointers and sizes (include/ctf.h), so an undersized, mistyped or
+    foreign-device buffer would be read or written out of bounds by the kernels instead of
+    failing; this is where the binding turns that into a ValueError.  Pure host logic (no CUDA
+    call): out / rec / debug buffers may be larger than needed (flat buffers are fine)."""
+    if uv4.dim() != 4 or uv4.dtype != torch.float32 or uv4.shape[3] != 2:
+        raise ValueError("uv must be float32 [F][Hf][Wf][2] (or [Hf][Wf][2])")
+    frames, hf, wf = uv4.shape[0], uv4.shape[1], uv4.shape[2]
+    if frames <= 0 or hf <= 0 or wf <= 0:
+        raise ValueError("empty frame geometry")
+    px = frames * hf * wf
+    waves = frames * ((hf + 3) // 4) * ((wf + 7) // 8)
+    need = [("grad", grad, (torch.float16,), 4 * px, True),
+            ("out", out, (torch.float32,), 4 * px, False),
+            ("rec", rec, _U32_DTYPES, waves, False)]
+    for k, n in (("produced_id", px), ("selection", px), ("unread", 1)):
+        if debug is not None and debug.get(k) is not None:
+            need.append((k, debug[k], _U32_DTYPES, n, False))
+    for name, t, dtypes, numel, exact in need:
+        if t is None:
+            continue
+        if t.dtype not in dtypes:
+            raise ValueError(f"{name} must be {' or '.join(str(d) for d in dtypes)}, got {t.dtype}")
+        if (t.numel() != numel) if exact else (t.numel() < numel):
+            raise ValueError(f"{name} holds {t.numel()} elements, the geometry needs {'' if exact else '>= '}{numel}")
+        if t.device != uv4.device:
+            raise ValueError(f"{name} is on {t.device}, uv on {uv4.device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+
+
 def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode: int, fallback: int = FB_CPLUS,
                  flags: int = 0, seed: int = 0, frame_index: int = 0, out: torch.Tensor | None = None,
                  rec: torch.Tensor | None = None, debug: dict | None = None,
@@ -201,15 +238,14 @@ def filter_batch(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
     lib = load_library()
     single = uv.dim() == 3
     uv4 = uv.unsqueeze(0) if single else uv
+    if uv4.dim() != 4:
+        raise ValueError("uv must be float32 [F][Hf][Wf][2] (or [Hf][Wf][2])")
     frames, hf, wf = uv4.shape[0], uv4.shape[1], uv4.shape[2]
-    if uv4.dtype != torch.float32 or uv4.shape[3] != 2:
-        raise ValueError("uv must be float32 [..., 2]")
-    if grad is not None and (grad.dtype != torch.float16 or grad.shape[-1] != 4):
-        raise ValueError("grad must be float16 [..., 4]")
     if out is None:
         out = torch.empty((frames, hf, wf, 4), device=uv.device, dtype=torch.float32)
     if rec is None:
         rec = torch.empty((frames, (hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
+    check_buffers(uv4, grad, out, rec, debug)
     p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
     p.row0 = row0
     _set_workspace(p, _call_workspace(tex, mode, filter, wf, hf, frames, uv.device, workspace, stream))
@@ -233,11 +269,14 @@ def filter_frame(tex: Texture, uv: torch.Tensor, grad: torch.Tensor | None, mode
                  workspace: torch.Tensor | bool | None = True, row0: int = 0):
     """One frame through ctf_filter_frame.  uv float32 [Hf][Wf][2]; workspace and row0 as filter_batch."""
     lib = load_library()
+    if uv.dim() != 3:
+        raise ValueError("filter_frame: uv must be float32 [Hf][Wf][2]")
     hf, wf = uv.shape[0], uv.shape[1]
     if out is None:
         out = torch.empty((hf, wf, 4), device=uv.device, dtype=torch.float32)
     if rec is None:
         rec = torch.empty(((hf + 3) // 4, (wf + 7) // 8), device=uv.device, dtype=torch.int32)
+    check_buffers(uv.unsqueeze(0), grad, out, rec, debug)
     p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
     p.row0 = row0
     _set_workspace(p, _call_workspace(tex, mode, filter, wf, hf, 1, uv.device, workspace, stream))
@@ -280,6 +319,9 @@ class HostPipeline:
         for t in (uv_host, grad_host, out_host, rec_host):
             if t is not None and (t.is_cuda or not t.is_contiguous()):
                 raise ValueError("host pipeline expects contiguous CPU (ideally pinned) tensors")
+        if uv_host.dim() != 4 or tuple(uv_host.shape[1:3]) != (self.hf, self.wf):
+            raise ValueError(f"uv_host must be [F][{self.hf}][{self.wf}][2] (the pipeline's geometry)")
+        check_buffers(uv_host, grad_host, out_host, rec_host)   # rec_host may be None (records not copied back)
         frames = uv_host.shape[0]
         p = ctf_params(mode, fallback, flags, frame_index, seed, filter, max_evals)
         p.row0 = row0

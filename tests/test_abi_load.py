@@ -116,3 +116,40 @@ def test_workspace_and_launch_accounting_per_mode():
         assert ctf.launches_per_call(ctf.FMT_BC1, mode, 0, 1, wf=64, hf=64) == 1, mode   # fused when lean
         assert ctf.launches_per_call(ctf.FMT_LATENT_MLP, mode, 0, 1) == (2 if lean_mlp else 1), mode
         assert ctf.workspace_for(bc1, mode, 1, 64, 32, 2, "cpu") is None   # bicubic: no work lists
+
+
+def test_binding_rejects_mismatched_buffers():
+    """ctf.check_buffers (called by filter_frame / filter_batch / HostPipeline.run before the C
+    call): an undersized, mistyped or foreign-device buffer raises instead of reaching the
+    kernels, which take plain pointers and would read or write past its end."""
+    torch = pytest.importorskip("torch")
+    import paper_2506_17770_b200.ctf as c
+    F, H, W = 2, 9, 13   # ragged: 3 wave-rows x 2 wave-columns per frame
+    uv = torch.zeros((F, H, W, 2), dtype=torch.float32)
+    g = torch.zeros((F, H, W, 4), dtype=torch.float16)
+    out = torch.zeros((F, H, W, 4), dtype=torch.float32)
+    rec = torch.zeros((F, 3, 2), dtype=torch.int32)
+    c.check_buffers(uv, g, out, rec)                                          # exact sizes
+    c.check_buffers(uv, None, out.flatten(), torch.zeros(100, dtype=torch.int32))   # flat, larger
+    c.check_buffers(uv, g, out, None)                                        # host pipeline: no records
+    dbg = {"produced_id": torch.zeros(F * H * W, dtype=torch.int32),
+           "selection": torch.zeros(F * H * W, dtype=torch.int32), "unread": torch.zeros(1, dtype=torch.int32)}
+    c.check_buffers(uv, g, out, rec, dbg)
+    bad = [
+        (uv.double(), g, out, rec, None),                       # uv dtype
+        (uv[..., :1].contiguous(), g, out, rec, None),          # uv last dim
+        (uv[0], g, out, rec, None),                             # uv rank
+        (uv, g.float(), out, rec, None),                        # grad dtype
+        (uv, g[:1], out, rec, None),                            # grad frames
+        (uv, g, out[:, :-1], rec, None),                        # out too small
+        (uv, g, out.half(), rec, None),                         # out dtype
+        (uv, g, out, rec[:, :-1], None),                        # rec too small
+        (uv, g, out, rec.float(), None),                        # rec dtype
+        (uv, g, out.transpose(1, 2), rec, None),                # out not contiguous
+        (uv, g, out, rec, dict(dbg, produced_id=torch.zeros(F * H * W - 1, dtype=torch.int32))),
+        (uv, g, out, rec, dict(dbg, unread=torch.zeros(0, dtype=torch.int32))),
+        (uv, g, out, torch.zeros((F, 3, 2), dtype=torch.int32, device="meta"), None),   # other device
+    ]
+    for args in bad:
+        with pytest.raises(ValueError):
+            c.check_buffers(*args)
