@@ -3,7 +3,7 @@
 Each entry is a plausible mistake in `oracle/ctf_oracle.c` (a dropped term, a wrong sign,
 index or comparison, a transposed operand).  For each, the script copies oracle/, synthetic/
 and tests/ to /tmp, applies the mutation, rebuilds the oracle and runs the CPU pins
-(tests/test_oracle_pins.py, tests/test_oracle_bicubic.py).  KILLED = some pin fails.
+(tests/test_oracle_pins.py, tests/test_oracle_pins2.py, tests/test_oracle_bicubic.py).  KILLED = some pin fails.
 Expected survivors are listed in DESIGN.md §3 with the reason (equivalent mutants, or
 conventions the paper leaves free).   Usage: python scripts/oracle_mutants.py [name ...]
 """
@@ -43,6 +43,47 @@ MUTS = {
  'bf_bicubic_cap_ignores_E': ("const int cap = E * a;", "const int cap = a;"),
  'bg_tap_offset': ("L->x[i] = clampi(x0 - 1 + i, 0, W - 1);", "L->x[i] = clampi(x0 + i, 0, W - 1);"),
  'bh_stf16_sign': ("double sgn = ((L->wx[i] < 0.0f) != (L->wy[j] < 0.0f)) ? -1.0 : 1.0;", "double sgn = 1.0;"),
+ # second batch (round 2, CPU session): lane order, coverage test, BC1 decode, RNG use,
+ # Eq. 1 / C+ details, AABB / Box / Mask decisions, footprint rounding, record fields
+ 'ca_lane_colmajor': ("px[lane] = wx * 8 + (lane & 7);\n        py[lane] = wy * 4 + (lane >> 3);", "px[lane] = wx * 8 + (lane >> 2);\n        py[lane] = wy * 4 + (lane & 3);"),
+ 'cb_nan_test_on_v': ("if (isnan(uvp[0])) continue;                                   /* uncovered */", "if (isnan(uvp[1])) continue;"),
+ 'cc_bc1_g_replication': ("e0[1] = (g0 << 2) | (g0 >> 4);", "e0[1] = (g0 << 2) | (g0 >> 3);"),
+ 'cd_bc1_palette_swap': ("(code == 2) ? (2 * e0[c] + e1[c]) / 3 : (e0[c] + 2 * e1[c]) / 3;", "(code == 2) ? (e0[c] + 2 * e1[c]) / 3 : (2 * e0[c] + e1[c]) / 3;"),
+ 'ce_bc1_index_transposed': ("uint32_t code = (idx >> (2 * (4 * (y & 3) + (x & 3)))) & 3u;", "uint32_t code = (idx >> (2 * (4 * (x & 3) + (y & 3)))) & 3u;"),
+ 'cf_bc1_half_round_up': ("else out[c] = (code == 2) ? (e0[c] + e1[c]) / 2 : 0;", "else out[c] = (code == 2) ? (e0[c] + e1[c] + 1) / 2 : 0;"),
+ 'cg_unit24_shift9': ("return (double)(r >> 8) * (1.0 / 16777216.0);", "return (double)(r >> 9) * (1.0 / 16777216.0);"),
+ 'ch_stf_corner_order': ("return dx + 2 * dy;", "return 2 * dx + dy;"),
+ 'ci_cplus_candidates_keep_planned': ("if (in_list(P, np, cid[q])) continue;", ""),
+ 'cj_cplus_candidates_keep_zero_w': ("if (cw[q] == 0.0f) continue;", ""),
+ 'ck_eq1_Sp_weighted': ("Sp[ch] += p[ch]; plast[ch] = p[ch]; }", "Sp[ch] += dw[j] * p[ch]; plast[ch] = p[ch]; }"),
+ 'cl_eq1_sign': ("else c[ch] = Swp[ch] + (1.0 - Sw) * Sp[ch] / N;", "else c[ch] = Swp[ch] + (Sw - 1.0) * Sp[ch] / N;"),
+ 'cm_fallback_no_merge': ("dw[j] += L->w[k];\n    }\n    int all_known", "dw[j] = L->w[k];\n    }\n    int all_known"),
+ 'cn_partial_bit_a31': ("((uint32_t)(a < 32) << 26)", "((uint32_t)(a < 31) << 26)"),
+ 'co_aabb_from_id1': ("int xb = (int)(L[lane].id[3] % (uint32_t)tex->W), yb = (int)(L[lane].id[3] / (uint32_t)tex->W);", "int xb = (int)(L[lane].id[3] % (uint32_t)tex->W), yb = (int)(L[lane].id[1] / (uint32_t)tex->W);"),
+ 'cp_box_vs_32': ("if (F->mode == M_BOX) ok = bw * bh <= a;", "if (F->mode == M_BOX) ok = bw * bh <= 32;"),
+ 'cq_mask11_12': ("ok = bw <= 11 && bh <= 11 && n <= a;", "ok = bw <= 12 && bh <= 12 && n <= a;"),
+ 'cr_footprint_two_roundings': ("float fx = fmaf(uc, (float)W, -0.5f), fy = fmaf(vc, (float)H, -0.5f);\n    float flx = floorf(fx), fly = floorf(fy);\n    int x0 = (int)flx, y0 = (int)fly;\n    st[0]", "volatile float pxw = uc * (float)W, pyh = vc * (float)H;\n    float fx = pxw - 0.5f, fy = pyh - 0.5f;\n    float flx = floorf(fx), fly = floorf(fy);\n    int x0 = (int)flx, y0 = (int)fly;\n    st[0]"),
+ 'cs_uv_unclamped_low': ("float uc = fminf(fmaxf(u, 0.0f), 1.0f);\n    float vc = fminf(fmaxf(v, 0.0f), 1.0f);\n    float fx = fmaf", "float uc = fminf(u, 1.0f);\n    float vc = fminf(v, 1.0f);\n    float fx = fmaf"),
+ 'ct_mag_sum': ("float r2 = rx > ry ? rx : ry;\n        L->magnified", "float r2 = rx + ry;\n        L->magnified"),
+ 'cu_eq2_den': ("long den = 2L * (a - 1 - n);", "long den = 2L * (a - n);"),
+ 'cv_stf_evals_32': ("        evals = a;\n    } else if (run_fallback == FB_WC", "        evals = 32;\n    } else if (run_fallback == FB_WC"),
+ 'cw_unique_descending': ("return x < y ? -1 : (x > y);", "return x > y ? -1 : (x < y);"),
+ 'cx_4tap_evals_32': ("evals = 4 * a;", "evals = 4 * 32;"),
+ 'cy_cplus_target_u0': ("volatile float target = (float)u[c][2] * wsum;", "volatile float target = (float)u[c][0] * wsum;"),
+ 'cz_philox_ctr_frame_slot': ("uint32_t ctr[4] = { (uint32_t)px, (uint32_t)py, frame, 0u };", "uint32_t ctr[4] = { (uint32_t)px, (uint32_t)py, 0u, frame };"),
+ # third batch: the latent-MLP decode (R-10), texel addressing on non-square textures,
+ # the C+ plan / spare-lane loop, Mask's n <= a test, WC vs Eq. 1 dispatch
+ 'da_mlp_no_relu1': ("h1[j] = acc > 0 ? acc : 0;", "h1[j] = acc;"),
+ 'db_mlp_latent_offset': ("double gx = (x - 1.5) / 4.0, gy = (y - 1.5) / 4.0;", "double gx = (x - 2.0) / 4.0, gy = (y - 2.0) / 4.0;"),
+ 'dc_mlp_pos_swap': ("in[8] = ((x & 3) - 1.5) / 2.0;", "in[8] = ((y & 3) - 1.5) / 2.0;"),
+ 'dd_mlp_W2_transposed': ("acc += (double)W2[j * 32 + k] * h1[k];", "acc += (double)W2[k * 32 + j] * h1[k];"),
+ 'de_produce_row_by_H': ("int x = (int)(id % (uint32_t)t->W), y = (int)(id / (uint32_t)t->W);", "int x = (int)(id % (uint32_t)t->H), y = (int)(id / (uint32_t)t->H);"),
+ 'df_footprint_pitch_H': ("id[0] = (uint32_t)ya * (uint32_t)W + (uint32_t)xa;", "id[0] = (uint32_t)ya * (uint32_t)H + (uint32_t)xa;"),
+ 'dg_cplus_plan_unsorted': ("np = sort_unique(P, np);", ""),
+ 'dh_eq2_rank_not_lane': ("int l = act[oracle_eq2(j, np, a)];", "int l = oracle_eq2(j, np, a);"),
+ 'di_cplus_first_spare_skipped': ("for (int j = np; j < a; ++j) {", "for (int j = np + 1; j < a; ++j) {"),
+ 'dj_mask16_no_n_test': ("ok = bw <= 16 && bh <= 16 && n <= a;", "ok = bw <= 16 && bh <= 16;"),
+ 'dk_wc_as_eq1': ("if (L[lane].active) blend_fallback(tex, &L[lane], plist, np, run_fallback == FB_WC, col[lane]);", "if (L[lane].active) blend_fallback(tex, &L[lane], plist, np, 0, col[lane]);"),
 }
 sel = sys.argv[1:] or list(MUTS)
 for name in sel:
@@ -55,6 +96,6 @@ for name in sel:
     p = f'{d}/oracle/ctf_oracle.c'; s = open(p).read()
     if old not in s: print(name, 'PATTERN MISSING'); continue
     open(p,'w').write(s.replace(old, new, 1))
-    r = subprocess.run(['python','-m','pytest','tests/test_oracle_pins.py','tests/test_oracle_bicubic.py','-q','-p','no:cacheprovider','-m','not gpu','-x'], cwd=d, capture_output=True, text=True, timeout=900)
+    r = subprocess.run(['python','-m','pytest','tests/test_oracle_pins.py','tests/test_oracle_pins2.py','tests/test_oracle_bicubic.py','-q','-p','no:cacheprovider','-m','not gpu','-x'], cwd=d, capture_output=True, text=True, timeout=900)
     last = [l for l in r.stdout.splitlines() if 'passed' in l or 'failed' in l or 'error' in l.lower()]
     print(f'{name:28s}', 'KILLED' if r.returncode else 'SURVIVED', last[-1] if last else r.stdout[-300:])

@@ -1,0 +1,200 @@
+"""Pins of the CPU oracle, second batch (-m "not gpu"): the survivors of the round-2 mutation
+run (scripts/oracle_mutants.py, profiles/r02/oracle_mutants.txt) each fail one of these.
+
+Each test names the passage (P:n = PAPER.md line) or the DESIGN.md reading (R-n) it checks;
+expected values come from the paper's rules, hand-decoded texels, exact rational arithmetic
+or the Random123 generator (itself pinned by its published answers), never from the oracle's
+own arithmetic on the same quantity.
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.oracle import (FB_C, FB_CPLUS, FL_FORCE_FALLBACK, M_COLLAB, M_STF, decode_record, filter_frame)
+from tests.helpers import bc1_tex
+
+pytestmark = pytest.mark.filterwarnings("ignore::RuntimeWarning")
+INVALID = 0xFFFFFFFF
+M_MASK16, M_MASK11 = 5, 6
+
+
+def test_cplus_spare_lanes_never_produce_zero_weight_texels():
+    """P:466-468 ('the unique texels ... with nonzero filter weights') and P:503-506: a C+ spare
+    lane draws only among its served lane's texels of nonzero weight.  Every lane samples a
+    texel CENTRE (s = t = 0: weights (1, 0, 0, 0)), so its STF draw is its anchor for any
+    uniform (R-12) and its only nonzero-weight texel is planned: the 16 spare lanes have no
+    candidate and produce nothing.  The needed set still counts the zero-weight corners (R-4):
+    16 columns x 4 rows = 64 > 32, so the wave falls back."""
+    W = H = 64
+    tex = bc1_tex(W, H, 4, "image")
+    uv = np.empty((4, 8, 2), np.float32)
+    for lane in range(32):
+        lx, ly = lane % 8, lane // 8
+        x, y = 8 + 2 * lx, 8 + 2 * (ly // 2)          # two rows of lanes share each anchor
+        uv[ly, lx] = ((x + 0.5) / W, (y + 0.5) / H)   # exact in fp32: fx = x, fy = y
+    r = filter_frame(tex, uv, None, M_COLLAB, FB_CPLUS, seed=3)
+    d = decode_record(r["rec"])
+    assert (d["n"][0, 0], d["a"][0, 0], d["path"][0, 0]) == (64, 32, 4)   # C+ fallback (path 4)
+    assert d["evals"][0, 0] == 16                                           # n_p planned, no extras
+    pid = r["produced_id"].reshape(-1)
+    sel = r["selection"].reshape(-1)
+    assert sorted(int(p) for p in pid if p != INVALID) == sorted(
+        (8 + 2 * (ly // 2)) * W + 8 + 2 * lx for lx in range(8) for ly in (0, 2))
+    spares = [c for c in range(32) if (sel[c] >> 5) & 1]
+    assert len(spares) == 16 and all(pid[c] == INVALID and not (sel[c] >> 4) & 1 for c in spares)
+    # every lane knows its only nonzero-weight texel: the colour is that texel (exact)
+    for lane in range(32):
+        lx, ly = lane % 8, lane // 8
+        ref = oracle.bc1_texel(tex["bc1"], W, 8 + 2 * lx, 8 + 2 * (ly // 2)) / 255.0
+        np.testing.assert_array_equal(r["out"][ly, lx], ref)
+
+
+def test_eq1_one_known_texel_at_a_clamped_edge():
+    """Eq. 1's N = 1 case (one known texel -> its value) where clamp-to-edge makes
+    corners coincide (R-2, R-14: a texel's weight is the sum of its corners' weights).  Every
+    lane samples the last texel column at s = 0 (u = (W - 1/2) / W, fx = W - 1: the right
+    corners clamp onto the left ones with weight 0), so a lane's footprint is the two texels
+    (W-1, y0) with weight 1 - t and (W-1, y0+1) with weight t, both nonzero.  Under the forced C
+    fallback a lane that knows only one of them takes that texel's value; one that knows both is
+    the exact blend."""
+    W = H = 32
+    tex = bc1_tex(W, H, 6, "random")
+    rng = np.random.default_rng(11)
+    uv = np.empty((4, 8, 2), np.float32)
+    t = rng.uniform(0.05, 0.15, 32)                      # lanes mostly draw their upper texel
+    rows = np.arange(32) % 8 * 2 + 8                     # y0: 4 lanes per row pair
+    for lane in range(32):
+        uv[lane // 8, lane % 8] = ((W - 0.5) / W, (rows[lane] + 0.5 + t[lane]) / H)
+    r = filter_frame(tex, uv, None, M_COLLAB, FB_C, FL_FORCE_FALLBACK, seed=9)
+    known = {int(p) for p in r["produced_id"].reshape(-1) if p != INVALID}
+    ones = 0
+    for lane in range(32):
+        ids, st = oracle.footprint(float(uv[lane // 8, lane % 8, 0]), float(uv[lane // 8, lane % 8, 1]), W, H)
+        assert float(st[0]) == 0.0 and ids[0] == ids[1] and ids[2] == ids[3]
+        up, lo = int(ids[0]), int(ids[2])
+        pu = oracle.bc1_texel(tex["bc1"], W, up % W, up // W).astype(np.float64) / 255.0
+        pl = oracle.bc1_texel(tex["bc1"], W, lo % W, lo // W).astype(np.float64) / 255.0
+        got = r["out"][lane // 8, lane % 8]
+        if up in known and lo in known:
+            tt = float(st[1])
+            np.testing.assert_allclose(got, (1 - tt) * pu + tt * pl, rtol=0, atol=1e-12)
+        else:
+            ones += 1
+            np.testing.assert_array_equal(got, pu if up in known else pl)
+    assert ones >= 8   # the construction exercises the N = 1 case
+
+
+def test_partial_bit_for_one_uncovered_lane():
+    """Record layout: bit 26 'partial' is set iff the wave has an
+    inactive lane; a = popc(A).  One uncovered lane: a = 31, partial = 1."""
+    W = H = 64
+    tex = bc1_tex(W, H, 1, "image")
+    uv = np.empty((4, 16, 2), np.float32)
+    for y in range(4):
+        for x in range(16):
+            uv[y, x] = ((20.25 + 0.5 * x) / W, (20.25 + 0.5 * y) / H)
+    uv[2, 11] = (np.nan, np.nan)                        # wave 1, lane 19
+    d = decode_record(filter_frame(tex, uv, None, M_COLLAB, FB_C, seed=1)["rec"])
+    assert (d["a"][0, 0], d["partial"][0, 0]) == (32, 0)
+    assert (d["a"][0, 1], d["partial"][0, 1]) == (31, 1)
+
+
+@pytest.mark.parametrize("k,exact11,exact16", [(9, True, True), (10, False, True), (14, False, True),
+                                               (15, False, False)])
+def test_mask_grid_width_limits(k, exact11, exact16):
+    """Mask Sampling resolves a wave iff its texel AABB fits the mask (16 x 16, P:368-369;
+    11 x 11) and n <= a; List has no AABB limit.  31 lanes sample the
+    centre of texel (20, 30) (footprint columns 20-21), lane 0 the centre of (20 + k, 30)
+    (columns 20+k .. 21+k): AABB width k + 2, n = 8."""
+    W = H = 64
+    tex = bc1_tex(W, H, 3, "image")
+    uv = np.empty((4, 8, 2), np.float32)
+    uv[:, :] = (20.5 / W, 30.5 / H)
+    uv[0, 0] = ((20 + k + 0.5) / W, 30.5 / H)
+    for mode, ok in ((M_COLLAB, True), (M_MASK16, exact16), (M_MASK11, exact11)):
+        d = decode_record(filter_frame(tex, uv, None, mode, FB_C, seed=1)["rec"])
+        assert d["n"][0, 0] == 8
+        assert (d["path"][0, 0] == 0) == ok, (mode, k)
+
+
+def _round_to_f32(x: Fraction) -> float:
+    """x correctly rounded to binary32 (ties to even), by exact comparison of neighbours."""
+    f = np.float32(float(x))
+    cands = {f, np.nextafter(f, np.float32(np.inf)), np.nextafter(f, np.float32(-np.inf))}
+    def key(c):
+        return (abs(Fraction(float(c)) - x), int(np.frombuffer(np.float32(c).tobytes(), np.uint32)[0]) & 1)
+    return float(min(cands, key=key))
+
+
+def test_footprint_position_is_one_rounding_of_u_times_w_minus_half():
+    """R-2: fx = u*W - 1/2 rounded ONCE to fp32 (the listing's uv * txDim - 0.5, P:1109-1112,
+    as a fused multiply-add).  Checked against exact rational arithmetic on widths that are not
+    powers of two (where one and two roundings differ): x0 = floor(fx), s = fx - x0."""
+    rng = np.random.default_rng(5)
+    differ = 0
+    for W in (12, 20, 100, 1000, 3000):
+        us = np.concatenate([rng.uniform(1.0, 1.5, 300) / W, rng.uniform(0, 1, 300)]).astype(np.float32)
+        for u in us:
+            fx = _round_to_f32(Fraction(float(u)) * W - Fraction(1, 2))
+            x0 = int(np.floor(fx))
+            if not 0 <= x0 <= W - 2:
+                continue
+            ids, st = oracle.footprint(float(u), 0.5, W, 4)
+            assert int(ids[0]) % W == x0 and float(st[0]) == fx - x0, (W, float(u))
+            two = float(np.float32(np.float32(u) * np.float32(W)) - np.float32(0.5))
+            differ += two != fx
+    assert differ > 50   # the pin separates the two readings
+
+
+@pytest.mark.parametrize("u,edge", [(-0.3, 0.0), (-1e-3, 0.0), (-16.0, 0.0), (1.0 + 1e-3, 1.0), (3.5, 1.0)])
+def test_out_of_range_coordinates_clamp_to_the_edge(u, edge):
+    """R-2 (clamp-to-edge addressing): a coordinate outside [0, 1] samples exactly
+    as the nearest edge coordinate — same texel ids AND the same fractions s, t (so the same
+    STF / C+ corner choices), on both axes."""
+    W, H = 64, 32
+    for v in (0.37, u):
+        a = oracle.footprint(u, v, W, H)
+        b = oracle.footprint(edge, v if v != u else edge, W, H)
+        assert list(a[0]) == list(b[0]) and list(a[1]) == list(b[1]), (u, v)
+
+
+def test_rng_counter_is_pixel_row_frame():
+    """R-11: the uniforms of pixel (px, py) in frame f are Philox4x32-10 of counter
+    (px, py, f, 0) under key (seed_lo, seed_hi) — the generator itself is pinned by the Random123
+    answers (test_philox_known_answers).  Pixels sampling at s = t = 1/2 exactly reveal
+    u0 < 1/2 and u1 < 1/2 (the top bits of r0, r1) through their STF corner (R-12)."""
+    W = H = 64
+    tex = bc1_tex(W, H, 2, "random")
+    hf, wf = 8, 16
+    uv = np.empty((hf, wf, 2), np.float32)
+    for y in range(hf):
+        for x in range(wf):
+            uv[y, x] = ((x + 10 + 1.0) / W, (y + 20 + 1.0) / H)     # fx = x + 10.5: s = 1/2
+    seed, frame = 0x9E3779B97F4A7C15, 5
+    sel = filter_frame(tex, uv, None, M_STF, seed=seed, frame_index=frame)["selection"]
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    for y in range(hf):
+        for x in range(wf):
+            r = oracle.philox4x32_10([x, y, frame, 0], key)
+            k = int(r[0] < 2 ** 31) + 2 * int(r[1] < 2 ** 31)
+            assert int(sel[y, x]) & 3 == k, (x, y)
+
+
+@pytest.mark.parametrize("W,H", [(32, 8), (8, 32)])
+def test_texel_addressing_on_non_square_textures(W, H):
+    """id = y*W + x (R-3) and texel (x, y) lives in block (y>>2)*(W>>2) + (x>>2)
+    (R-9): on a non-square texture, sampling the CENTRE of texel (x, y) (weights (1, 0, 0, 0))
+    returns exactly that texel's decoded value, under 4-tap and under the collaborative path."""
+    tex = bc1_tex(W, H, 12, "random")
+    rng = np.random.default_rng(4)
+    xs, ys = rng.integers(0, W - 1, 32), rng.integers(0, H - 1, 32)
+    uv = np.empty((4, 8, 2), np.float32)
+    for lane in range(32):
+        uv[lane // 8, lane % 8] = ((xs[lane] + 0.5) / W, (ys[lane] + 0.5) / H)
+    for mode in (0, M_COLLAB):
+        out = filter_frame(tex, uv, None, mode, FB_C, seed=1)["out"]
+        for lane in range(32):
+            ref = oracle.bc1_texel(tex["bc1"], W, int(xs[lane]), int(ys[lane])).astype(np.float64) / 255.0
+            np.testing.assert_array_equal(out[lane // 8, lane % 8], ref, err_msg=f"{mode} {lane}")
