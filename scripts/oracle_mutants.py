@@ -83,6 +83,15 @@ MUTS = {
  'dh_eq2_rank_not_lane': ("int l = act[oracle_eq2(j, np, a)];", "int l = oracle_eq2(j, np, a);"),
  'di_cplus_first_spare_skipped': ("for (int j = np; j < a; ++j) {", "for (int j = np + 1; j < a; ++j) {"),
  'dj_mask16_no_n_test': ("ok = bw <= 16 && bh <= 16 && n <= a;", "ok = bw <= 16 && bh <= 16;"),
+ 'ea_bspline_w0_scale': ("w[0] = r3 / 6.0f;", "w[0] = r3 / 3.0f;"),
+ 'eb_cr_w2_sign': ("w[2] = ((4.0f * s2 - 3.0f * s3) + s) * 0.5f;", "w[2] = ((4.0f * s2 - 3.0f * s3) - s) * 0.5f;"),
+ 'ec_bicubic_clamp_no_merge': ("L->mx[L->x[i] - L->xa] = L->mx[L->x[i] - L->xa] + L->wx[i];", "L->mx[L->x[i] - L->xa] = L->wx[i];"),
+ 'ed_cubic_pick_cum_signed': ("cum = cum + fabsf(w[i]);\n        if (cum > target) return i;", "cum = cum + w[i];\n        if (cum > target) return i;"),
+ 'ee_stf16_no_scale': ("for (int ch = 0; ch < 4; ++ch) c[ch] = sgn * (double)Sx * (double)Sy * p[ch];", "for (int ch = 0; ch < 4; ++ch) c[ch] = sgn * p[ch];"),
+ 'ef_positivized_same_uniform': ("volatile float target = (float)u[lobe] * Wl;", "volatile float target = (float)u[0] * Wl;"),
+ 'eg_fallback16_weight_transposed': ("float mw = L->mx[q] * L->my[r];", "float mw = L->mx[r] * L->my[q];"),
+ 'eh_blend16_transposed': ("double w = (double)L->wx[i] * (double)L->wy[j];", "double w = (double)L->wx[j] * (double)L->wy[i];"),
+ 'ei_tap_rows_offset': ("L->y[i] = clampi(y0 - 1 + i, 0, H - 1);", "L->y[i] = clampi(y0 + i, 0, H - 1);"),
  'dk_wc_as_eq1': ("if (L[lane].active) blend_fallback(tex, &L[lane], plist, np, run_fallback == FB_WC, col[lane]);", "if (L[lane].active) blend_fallback(tex, &L[lane], plist, np, 0, col[lane]);"),
 }
 sel = sys.argv[1:] or list(MUTS)

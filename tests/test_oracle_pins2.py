@@ -198,3 +198,102 @@ def test_texel_addressing_on_non_square_textures(W, H):
         for lane in range(32):
             ref = oracle.bc1_texel(tex["bc1"], W, int(xs[lane]), int(ys[lane])).astype(np.float64) / 255.0
             np.testing.assert_array_equal(out[lane // 8, lane % 8], ref, err_msg=f"{mode} {lane}")
+
+
+def test_positivized_stf_lobes_draw_independently():
+    """R-27: the positivized STF baseline draws its positive-lobe tap with u0 and
+    its negative-lobe tap with u1 — two independent draws, so over many pixels sampling the
+    same point every (positive, negative) tap pair occurs.  With one shared uniform the pair
+    would be a monotone function of it (at most n+ + n- - 1 = 15 of the 64 pairs).  Catmull-Rom
+    at interior fractions: 8 positive and 8 negative taps.  The 4 x 4 footprint (texels 22..25
+    on both axes) straddles four BC1 blocks 2 x 2 texels each, and each block gives its four
+    texels the four distinct colours of 4-colour mode (codes 0..3), so all 16 tap values differ
+    and each (positive, negative) pair has its own colour."""
+    from tests.helpers import blocks_from, codes_word
+    W = H = 64
+    nb = (W // 4) * (H // 4)
+    rng = np.random.default_rng(8)
+    c0 = rng.integers(0x8000, 0xFFFF, nb)
+    c1 = rng.integers(0x0000, 0x7FFF, nb)             # c0 > c1: 4-colour mode
+    idx = np.zeros(nb, np.uint32)
+    for by in (5, 6):
+        for bx in (5, 6):
+            codes = [[0] * 4 for _ in range(4)]
+            xs = (2, 3) if bx == 5 else (0, 1)
+            ys = (2, 3) if by == 5 else (0, 1)
+            for k, (yy, xx) in enumerate((yy, xx) for yy in ys for xx in xs):
+                codes[yy][xx] = k
+            idx[by * (W // 4) + bx] = codes_word(codes)
+    tex = {"format": 1, "width": W, "height": H, "bc1": blocks_from(c0, c1, idx)}
+    hf, wf = 32, 64
+    uv = np.empty((hf, wf, 2), np.float32)
+    uv[:, :] = ((23 + 0.3 + 0.5) / W, (23 + 0.6 + 0.5) / H)   # x0 = y0 = 23, s ~ 0.3, t ~ 0.6
+    out = filter_frame(tex, uv, None, M_STF, seed=17, filter=2)["out"].reshape(-1, 4)
+    distinct = {tuple(np.round(c, 12)) for c in out}
+    assert len(distinct) > 30, len(distinct)
+
+
+def _cubic_pick_f32(w, u):
+    """R-26's inverse-CDF tap choice in fp32 (first cumulative |w| > u * S, else the last
+    nonzero tap) — the same decision the oracle and the kernels take in fp32."""
+    S, last = np.float32(0), 0
+    for i in range(4):
+        S = np.float32(S + np.float32(abs(w[i])))
+        if w[i] != 0:
+            last = i
+    target = np.float32(np.float32(u) * S)
+    cum = np.float32(0)
+    for i in range(4):
+        cum = np.float32(cum + np.float32(abs(w[i])))
+        if cum > target:
+            return i
+    return last
+
+
+@pytest.mark.parametrize("filt", [1, 2])
+def test_bicubic_eq1_at_a_clamped_edge_reproduces_the_filter(filt):
+    """Eq. 1 estimates each unknown texel as the unweighted mean of the known ones, so
+    it reproduces the full filter exactly when the unknown texels DO equal that mean.  At the
+    left texture edge (x0 = 0: taps -1, 0 clamp onto column 0, R-24) the known-set weights are
+    the merged sums of the coinciding taps (R-25); a wrong merge breaks the identity.
+    Four lanes sample one point under the forced C fallback; their STF taps (R-26, drawn with
+    the KAT-pinned Philox words of R-11) are the known set K.  The texture is then built so
+    that K's texels average to the value M of every other texel (BC1 3-colour mode: black,
+    colour e1 = 2M, and M = (c0 + c1) / 2, exact per channel)."""
+    from tests.helpers import blocks_from
+    W = H = 16
+    u, v = (0.3 + 0.5) / W, (7.6 + 0.5) / H          # fx ~ 0.3 (x0 = 0), fy ~ 7.6 (interior)
+    ids, st = oracle.footprint(u, v, W, H)
+    assert int(ids[0]) % W == 0 and int(ids[0]) // W == 7
+    from oracle.oracle import cubic_weights
+    wx, wy = cubic_weights(filt, float(st[0])), cubic_weights(filt, float(st[1]))
+    xs = [min(max(-1 + i, 0), W - 1) for i in range(4)]
+    ys = [6 + j for j in range(4)]
+    uv = np.full((4, 8, 2), np.nan, np.float32)
+    uv[0, :4] = (u, v)
+    for seed in range(1, 400):
+        key = [seed, 0]
+        K = set()
+        for lane in range(4):
+            r = oracle.philox4x32_10([lane, 0, 0, 0], key)
+            i = _cubic_pick_f32(wx, (int(r[0]) >> 8) / 2.0 ** 24)
+            j = _cubic_pick_f32(wy, (int(r[1]) >> 8) / 2.0 ** 24)
+            K.add((xs[i], ys[j]))
+        if len(K) >= 2 and any(x == 0 for x, _ in K) and len(K) < 12:
+            break
+    else:
+        pytest.fail("no seed with a general Eq. 1 case on the merged column")
+    nb = (W // 4) * (H // 4)
+    codes = np.full((H, W), 2, np.int64)              # every texel M ...
+    for k, (x, y) in enumerate(sorted(K)):            # ... but K: black / e1 alternating (M if odd)
+        codes[y, x] = (k % 2) if not (len(K) % 2 and k == len(K) - 1) else 2
+    idx = np.zeros(nb, np.uint32)
+    for by in range(H // 4):
+        for bx in range(W // 4):
+            idx[by * (W // 4) + bx] = sum(int(codes[by * 4 + yy, bx * 4 + xx]) << (2 * (4 * yy + xx))
+                                          for yy in range(4) for xx in range(4))
+    tex = {"format": 1, "width": W, "height": H,
+           "bc1": blocks_from(np.zeros(nb, np.int64), np.full(nb, 0xDD1B), idx)}   # c0 < c1: 3-colour mode
+    full = filter_frame(tex, uv, None, 0, filter=filt)["out"][0, :4]
+    eq1 = filter_frame(tex, uv, None, M_COLLAB, FB_C, FL_FORCE_FALLBACK, seed=seed, filter=filt)["out"][0, :4]
+    np.testing.assert_allclose(eq1, full, rtol=0, atol=2e-6)
