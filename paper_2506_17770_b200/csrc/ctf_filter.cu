@@ -2140,8 +2140,7 @@ __global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
               if (lane == (unsigned)(wx - wx0)) myrec = fa.rec;
               if (lane == (unsigned)(wx + 1 - wx0)) myrec = hasB ? fb.rec : myrec;
             }
-            return;
-          }
+          } else {
           for (int wx = wx0; wx < wx1; ++wx, pix += 8u, px += 8) {
             const bool inframe = INTERIOR || (rowok & (px < a.Wf));
             const float2 uv = uv_n;
@@ -2177,6 +2176,7 @@ __global__ void __launch_bounds__(lean_warps<FMT>() * 32, FUSED ? CTF_FUSED_MINB
                 else rec = kSlowMark;
             }
             if (lane == (unsigned)(wx - wx0)) myrec = rec;
+          }
           }
         };
         if (rowok_all && wx1 * 8 <= a.Wf) run(std::true_type{});
