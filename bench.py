@@ -72,6 +72,7 @@ def parse_args():
     ap.add_argument("--no-grad", action="store_true")
     ap.add_argument("--e2e-frames", type=int, default=32)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=1, help="frames per host-pipeline chunk (copy granularity)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the other §8 configurations")
@@ -607,7 +608,7 @@ def main():
         g_h = None if grad is None else grad[:E].cpu().pin_memory()
         out_h = torch.empty((E, Hr, Wf, 4), dtype=torch.float32).pin_memory()
         rec_h = torch.empty((E, nwy, nwx), dtype=torch.int32).pin_memory()
-        chunk = 1  # one frame per chunk: the copy engines overlap H2D(c+1), kernel(c), D2H(c-1)
+        chunk = max(1, args.e2e_chunk)  # frames per chunk: the copy engines overlap H2D(c+1), kernel(c), D2H(c-1)
         pipe = ctf.HostPipeline(Wf, Hr, chunk, grad is not None, device=dev)
         pipe.run(tex, uv_h, g_h, out_h, rec_h, mode, fb, 0, args.seed, frame_base, stream=stream, row0=row0)  # warm
         if ws > 1:
