@@ -239,6 +239,9 @@ int ctf_filter_frames_host(const ctf_texture *tex, const float *uv_host, const u
         good = good && cudaEventRecord(ev_out[b], d2h) == cudaSuccess;
         if (!good) rc = CTF_ECUDA;
     }
+    // every copy that reads or writes the caller's host buffers has finished before the call
+    // returns — also on an error path that left the loop with H2D copies still queued
+    if (h2d && cudaStreamSynchronize(h2d) != cudaSuccess) rc = CTF_ECUDA;
     if (d2h && cudaStreamSynchronize(d2h) != cudaSuccess) rc = CTF_ECUDA;
     if (cudaStreamSynchronize(comp) != cudaSuccess) rc = CTF_ECUDA;
     for (int b = 0; b < 2; ++b) {
