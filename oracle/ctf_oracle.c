@@ -776,6 +776,11 @@ static void wave_bicubic(const frame_t *F, int filter, int E, int wx, int wy)
     uint32_t *rec = &F->rec[(size_t)wy * nwx + wx];
     double col[32][4];
     for (int lane = 0; lane < 32; ++lane) for (int ch = 0; ch < 4; ++ch) col[lane][ch] = 0.0;
+    /* debug outputs of the one-evaluation paths (fallbacks): the texel a lane produced and the
+     * C+ spare-lane fields, as in the bilinear wave(); the exact path (up to E evaluations per
+     * lane) and the full / positivized filters report none */
+    uint32_t prod[32], sel[32];
+    for (int lane = 0; lane < 32; ++lane) { prod[lane] = INVALID_ID; sel[lane] = 0; }
     int magnified = 0;
     if (F->grad && a > 0) {
         magnified = 1;
@@ -836,7 +841,7 @@ static void wave_bicubic(const frame_t *F, int filter, int E, int wx, int wy)
     }
 
     if (run_fallback == FB_STF) {
-        for (int lane = 0; lane < 32; ++lane) if (L[lane].active) stf16(tex, &L[lane], u[lane], col[lane]);
+        for (int lane = 0; lane < 32; ++lane) if (L[lane].active) prod[lane] = stf16(tex, &L[lane], u[lane], col[lane]);
         evals = a;
     } else if (run_fallback == FB_C || run_fallback == FB_CPLUS) {
         /* planned texels: every lane's one-tap STF choice (R-26) */
@@ -845,14 +850,16 @@ static void wave_bicubic(const frame_t *F, int filter, int E, int wx, int wy)
         for (int lane = 0; lane < 32; ++lane)
             if (L[lane].active) P[np++] = stf16(tex, &L[lane], u[lane], NULL);
         if (run_fallback == FB_C) {
-            for (int i = 0; i < np; ++i) produced[nprod++] = P[i];      /* every lane produces */
+            for (int i = 0; i < np; ++i) { produced[nprod++] = P[i]; prod[act[i]] = P[i]; }   /* every lane produces */
             evals = a;
         } else {
             np = sort_unique(P, np);                                     /* C+ plan (R-17) */
-            for (int i = 0; i < np; ++i) produced[nprod++] = P[i];
+            for (int i = 0; i < np; ++i) { produced[nprod++] = P[i]; prod[act[i]] = P[i]; }
             for (int j = np; j < a; ++j) {                               /* Eq. 2 spare lanes */
                 int cl = act[j];
-                const lane16_t *Ll = &L[act[oracle_eq2(j, np, a)]];
+                const int sl = act[oracle_eq2(j, np, a)];
+                sel[cl] |= (1u << 5) | ((uint32_t)sl << 8);
+                const lane16_t *Ll = &L[sl];
                 uint32_t fid[16]; float fw[16]; int nf = 0;
                 for (int r = 0; r < Ll->nr; ++r)
                     for (int q = 0; q < Ll->nc; ++q) {
@@ -872,6 +879,8 @@ static void wave_bicubic(const frame_t *F, int filter, int E, int wx, int wy)
                     if (cum > target) { pick = q; break; }
                 }
                 produced[nprod++] = fid[pick];
+                prod[cl] = fid[pick];
+                sel[cl] |= 1u << 4;
             }
             evals = nprod;
         }
@@ -887,8 +896,8 @@ static void wave_bicubic(const frame_t *F, int filter, int E, int wx, int wy)
         if (!inframe[lane]) continue;
         size_t pix = (size_t)py[lane] * F->Wf + px[lane];
         for (int ch = 0; ch < 4; ++ch) F->out[4 * pix + ch] = col[lane][ch];
-        if (F->produced_id) F->produced_id[pix] = INVALID_ID;
-        if (F->selection) F->selection[pix] = 0;
+        if (F->produced_id) F->produced_id[pix] = prod[lane];
+        if (F->selection) F->selection[pix] = sel[lane];
     }
 }
 

@@ -92,6 +92,14 @@ MUTS = {
  'eg_fallback16_weight_transposed': ("float mw = L->mx[q] * L->my[r];", "float mw = L->mx[r] * L->my[q];"),
  'eh_blend16_transposed': ("double w = (double)L->wx[i] * (double)L->wy[j];", "double w = (double)L->wx[j] * (double)L->wy[i];"),
  'ei_tap_rows_offset': ("L->y[i] = clampi(y0 - 1 + i, 0, H - 1);", "L->y[i] = clampi(y0 + i, 0, H - 1);"),
+ # bicubic C+ / records (R-26 .. R-28)
+ 'fa_bic_cplus_signed_weights': ("fid[nf] = id; fw[nf] = fabsf(mw); ++nf;", "fid[nf] = id; fw[nf] = mw; ++nf;"),
+ 'fb_bic_cplus_keep_planned': ("if (mw == 0.0f || in_list(P, np, id)) continue;", "if (mw == 0.0f) continue;"),
+ 'fc_bic_cplus_serves_itself': ("const int sl = act[oracle_eq2(j, np, a)];", "const int sl = cl;"),
+ 'fd_bic_cplus_target_u0': ("volatile float target = (float)u[cl][2] * wsum;", "volatile float target = (float)u[cl][0] * wsum;"),
+ 'fe_bic_rec_evals_high_bits': ("((uint32_t)((evals >> 8) & 7) << 27);", "0u;"),
+ 'ff_bic_n_unsaturated': ("n = nu < cap + 1 ? nu : cap + 1;", "n = nu;"),
+ 'fg_bic_box_cap_a': ("if (F->mode == M_BOX) ok = bw * bh <= cap;", "if (F->mode == M_BOX) ok = bw * bh <= a;"),
  'dk_wc_as_eq1': ("if (L[lane].active) blend_fallback(tex, &L[lane], plist, np, run_fallback == FB_WC, col[lane]);", "if (L[lane].active) blend_fallback(tex, &L[lane], plist, np, 0, col[lane]);"),
 }
 sel = sys.argv[1:] or list(MUTS)

@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 import oracle
+import synthetic
 from oracle.oracle import (FB_C, FB_CPLUS, FL_FORCE_FALLBACK, M_COLLAB, M_STF, decode_record, filter_frame)
 from tests.helpers import bc1_tex
 
@@ -297,3 +298,135 @@ def test_bicubic_eq1_at_a_clamped_edge_reproduces_the_filter(filt):
     full = filter_frame(tex, uv, None, 0, filter=filt)["out"][0, :4]
     eq1 = filter_frame(tex, uv, None, M_COLLAB, FB_C, FL_FORCE_FALLBACK, seed=seed, filter=filt)["out"][0, :4]
     np.testing.assert_allclose(eq1, full, rtol=0, atol=2e-6)
+
+
+# ------------------------------------------------ bicubic records / Box / C+ (R-24 .. R-28) --
+def _taps(coord: float, dim: int):
+    """R-24: fx = coord*dim - 1/2 (dim a power of two: exact), taps x0-1 .. x0+2 clamped, and
+    the fractional position s."""
+    fx = np.float32(np.clip(np.float32(coord), 0, 1) * np.float32(dim)) - np.float32(0.5)
+    x0 = int(np.floor(fx))
+    return [min(max(x0 - 1 + i, 0), dim - 1) for i in range(4)], float(fx - np.float32(x0))
+
+
+def test_bicubic_full_filter_records_16_evaluations_per_pixel():
+    """With a bicubic filter, BILINEAR_4TAP is the full 16-tap filter: 16 evaluations per active
+    pixel (include/ctf.h; P:68-69's count for a 4 x 4 footprint), so a full wave's record holds
+    512 — beyond the low 8 bits (bits 27-29 carry bits 8-10)."""
+    W = H = 64
+    tex = bc1_tex(W, H, 2, "image")
+    uv = np.empty((8, 8, 2), np.float32)
+    for y in range(8):
+        for x in range(8):
+            uv[y, x] = ((20.3 + 0.37 * x) / W, (20.6 + 0.41 * y) / H)
+    uv[5, 3] = (np.nan, np.nan)
+    d = decode_record(filter_frame(tex, uv, None, 0, filter=2)["rec"])
+    assert (d["evals"][0, 0], d["a"][0, 0], d["path"][0, 0]) == (512, 32, 5)
+    assert (d["evals"][1, 0], d["a"][1, 0]) == (16 * 31, 31)
+
+
+def test_bicubic_box_with_two_evaluations_per_lane():
+    """Box Sampling with max_evals = 2 (Fig. 13b): the wave is exact iff its texel
+    AABB area is at most 2a, and then it evaluates the whole AABB.  A full wave at
+    magnification 1.5 whose 4 x 4 footprints span an AABB of 33..64 texels: exact with E = 2,
+    a fallback with E = 1."""
+    W = H = 64
+    tex = bc1_tex(W, H, 5, "image")
+    uv = np.empty((4, 8, 2), np.float32)
+    for y in range(4):
+        for x in range(8):
+            uv[y, x] = ((20.2 + (x + 0.5) / 1.5) / W, (24.7 + (y + 0.5) / 1.5) / H)
+    xs = [t for v in uv[..., 0].ravel() for t in _taps(float(v), W)[0]]
+    ys = [t for v in uv[..., 1].ravel() for t in _taps(float(v), H)[0]]
+    area = (max(xs) - min(xs) + 1) * (max(ys) - min(ys) + 1)
+    assert 32 < area <= 64, area
+    for filt in (1, 2):
+        d1 = decode_record(filter_frame(tex, uv, None, 4, FB_C, seed=3, filter=filt, max_evals=1)["rec"])
+        d2 = decode_record(filter_frame(tex, uv, None, 4, FB_C, seed=3, filter=filt, max_evals=2)["rec"])
+        assert d1["path"][0, 0] == 3                                    # fallback C
+        assert (d2["path"][0, 0], d2["evals"][0, 0]) == (0, area)      # exact, the whole AABB
+
+
+def test_bicubic_cplus_spares_at_texel_centres_produce_nothing():
+    """Catmull-Rom interpolates: at a texel centre (s = t = 0) its weights are (0, 1, 0, 0) per
+    axis, so the only nonzero-weight texel of a lane's 4 x 4 footprint is the sampled one, its
+    STF draw (R-26) and its plan.  A C+ spare lane then has no candidate
+    and produces nothing: evals = n_p.  (16 distinct anchors for 32 lanes; the needed set,
+    zero-weight taps included, is 22 x 10 > 32 texels, so the wave falls back.)"""
+    W = H = 64
+    tex = bc1_tex(W, H, 4, "image")
+    uv = np.empty((4, 8, 2), np.float32)
+    for lane in range(32):
+        lx, ly = lane % 8, lane // 8
+        uv[ly, lx] = ((8 + 2 * lx + 0.5) / W, (8 + 2 * (ly // 2) + 0.5) / H)
+    r = filter_frame(tex, uv, None, M_COLLAB, FB_CPLUS, seed=3, filter=2)
+    d = decode_record(r["rec"])
+    assert (d["a"][0, 0], d["path"][0, 0], d["evals"][0, 0]) == (32, 4, 16)
+    pid, sel = r["produced_id"].reshape(-1), r["selection"].reshape(-1)
+    spares = [c for c in range(32) if (sel[c] >> 5) & 1]
+    assert len(spares) == 16 and all(pid[c] == INVALID and not (sel[c] >> 4) & 1 for c in spares)
+    for lane in range(32):   # every lane's only nonzero-weight texel is known: the texel itself
+        lx, ly = lane % 8, lane // 8
+        ref = oracle.bc1_texel(tex["bc1"], W, 8 + 2 * lx, 8 + 2 * (ly // 2)).astype(np.float64) / 255.0
+        np.testing.assert_allclose(r["out"][ly, lx], ref, rtol=0, atol=1e-12)
+
+
+def test_bicubic_cplus_extras_follow_eq2_and_the_absolute_weights():
+    """C+ with a bicubic filter (R-26 / R-28): spare lane c (active rank
+    j >= n_p) serves lane l = h(Eq. 2(j), A) and draws an unplanned texel of l's 4 x 4 footprint
+    with probability |w| / sum |w| — negative-lobe texels included.  Checked on full waves of a
+    rotated quad away from the texture edges: the served lane, footprint membership with
+    nonzero weight and not planned, the draw itself from the lane's u2 (the uniform R-11 gives
+    the C+ extra pick), and the share of draws landing on negative-weight texels against its
+    expectation (sum over draws of the candidates' negative |w| share)."""
+    from oracle.oracle import cubic_weights
+    W = H = 256
+    tex = bc1_tex(W, H, 8, "image")
+    uv, _ = synthetic.rotated_quad(128, 64, W, H, 1.2, 33.0, jitter_seed=2)
+    r = filter_frame(tex, uv, None, M_COLLAB, FB_CPLUS, FL_FORCE_FALLBACK, seed=5, filter=2)
+    neg, exp_neg, n_extra = 0, 0.0, 0
+    for wy in range(16):
+        for wx in range(16):
+            sl = np.s_[wy * 4:wy * 4 + 4, wx * 8:wx * 8 + 8]
+            pid, sel = r["produced_id"][sl].reshape(-1), r["selection"][sl].reshape(-1)
+            luv = uv[sl].reshape(-1, 2)
+            spare = [(sel[c] >> 5) & 1 for c in range(32)]
+            n_p = 32 - sum(spare)
+            assert spare == [0] * n_p + [1] * (32 - n_p)
+            planned = {int(p) for p in pid[:n_p]}
+            assert len(planned) == n_p and INVALID not in planned
+            for c in range(n_p, 32):
+                l = int((sel[c] >> 8) & 31)
+                assert l == oracle.eq2(c, n_p, 32), (c, n_p, l)
+                xs, s = _taps(float(luv[l, 0]), W)
+                ys, t = _taps(float(luv[l, 1]), H)
+                assert len(set(xs)) == 4 and len(set(ys)) == 4          # interior: no clamping
+                wxs, wys = cubic_weights(2, s), cubic_weights(2, t)
+                cells = {ys[j] * W + xs[i]: np.float32(wxs[i] * wys[j]) for j in range(4) for i in range(4)}
+                cand = {k: abs(float(w)) for k, w in cells.items() if w != 0 and k not in planned}
+                if not (sel[c] >> 4) & 1:
+                    assert not cand and pid[c] == INVALID
+                    continue
+                assert int(pid[c]) in cand
+                # the draw: inverse CDF of |w| over the candidates in row-major order, decided in
+                # fp32 with the lane's third uniform u2 (R-11: r2 -> the C+ extra pick, R-18 v)
+                px, py = wx * 8 + (c & 7), wy * 4 + (c >> 3)
+                u2 = (int(oracle.philox4x32_10([px, py, 0, 0], [5, 0])[2]) >> 8) / 2.0 ** 24
+                order = [ys[j] * W + xs[i] for j in range(4) for i in range(4) if ys[j] * W + xs[i] in cand]
+                wsum = np.float32(0)
+                for k in order:
+                    wsum = np.float32(wsum + np.float32(cand[k]))
+                target, cum, pick = np.float32(np.float32(u2) * wsum), np.float32(0), order[-1]
+                for k in order:
+                    cum = np.float32(cum + np.float32(cand[k]))
+                    if cum > target:
+                        pick = k
+                        break
+                assert int(pid[c]) == pick, (wx, wy, c)
+                n_extra += 1
+                neg += cells[int(pid[c])] < 0
+                exp_neg += sum(w for k, w in cand.items() if cells[k] < 0) / sum(cand.values())
+    assert n_extra > 500
+    sd = np.sqrt(exp_neg)   # <= binomial sd
+    print(f"extras {n_extra}, on negative-weight texels {neg} (expected {exp_neg:.1f})")
+    assert neg > 0 and abs(neg - exp_neg) < 4 * sd + 5, (neg, exp_neg, n_extra)
