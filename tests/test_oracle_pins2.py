@@ -430,3 +430,26 @@ def test_bicubic_cplus_extras_follow_eq2_and_the_absolute_weights():
     sd = np.sqrt(exp_neg)   # <= binomial sd
     print(f"extras {n_extra}, on negative-weight texels {neg} (expected {exp_neg:.1f})")
     assert neg > 0 and abs(neg - exp_neg) < 4 * sd + 5, (neg, exp_neg, n_extra)
+
+
+def test_frame_stats_by_hand():
+    """oracle.frame_stats (the expected ctf_stats) on hand-packed records
+    (record layout of include/ctf.h): totals written out by hand."""
+    def rec(evals, n, a, path, mag=0, partial=0):
+        return (evals & 0xFF) | (n << 8) | (a << 16) | (path << 22) | (mag << 25) | (partial << 26) | ((evals >> 8) << 27)
+    recs = np.array([rec(12, 12, 32, 0, mag=1),           # exact, magnified
+                     rec(30, 45, 32, 4),                  # C+ fallback
+                     rec(0, 0, 0, 0, partial=1),          # empty wave (not live)
+                     rec(9, 9, 20, 0, mag=1, partial=1),  # partial exact wave
+                     rec(512, 0xFF, 32, 5)], np.uint32)   # bicubic full filter
+    st = oracle.frame_stats(recs)
+    assert (st["waves_live"], st["waves_partial"], st["waves_exact"], st["waves_fallback"],
+            st["waves_magnified"]) == (4, 1, 2, 1, 2)
+    assert (st["pixels_active"], st["pixels_in_magnified_waves"]) == (116, 52)
+    assert (st["texel_evals"], st["texel_evals_in_magnified_waves"]) == (563, 21)
+    assert (st["max_unique_per_wave"], st["max_evals_per_lane"]) == (45, 16)
+    assert {i: int(v) for i, v in enumerate(st["unique_hist"]) if v} == {9: 1, 12: 1, 45: 1}
+    out = np.zeros((2, 2, 4)); ref = np.zeros((2, 2, 4))
+    out[0, 1] = (0.5, 0.0, 0.0, 0.0); out[1, 0, 2] = -0.25
+    st = oracle.frame_stats(recs, out, ref)
+    assert (st["sum_sq_err"], st["max_abs_err"], st["err_pixels"]) == (0.3125, 0.5, 4)
